@@ -1,0 +1,536 @@
+// api.cu — the C ABI (include/atk.h).  Every entry converts library errors
+// into an atk_status + thread-local message; no exception crosses the ABI.
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "atk_driver.cuh"
+
+namespace atk {
+
+thread_local std::string g_last_error;
+std::atomic<long long> g_gemm_calls{0}, g_gemm_flops{0};
+
+void record_gemm(long long charge) {
+    g_gemm_calls.fetch_add(1, std::memory_order_relaxed);
+    g_gemm_flops.fetch_add(charge, std::memory_order_relaxed);
+}
+
+void* dev_alloc(atk_ctx* ctx, size_t bytes) {
+    void* p = nullptr;
+    if (bytes == 0) return nullptr;
+    cudaError_t e = cudaMallocAsync(&p, bytes, ctx->stream);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        // drain the pool's cached blocks and retry once
+        cudaStreamSynchronize(ctx->stream);
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, ctx->device) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+        e = cudaMallocAsync(&p, bytes, ctx->stream);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            fail(ATK_OOM, "device allocation of " + std::to_string(bytes) + " bytes failed");
+        }
+    }
+    return p;
+}
+
+void dev_free(atk_ctx* ctx, void* p) {
+    if (p) cudaFreeAsync(p, ctx->stream);
+}
+
+atk_tensor* new_tensor(atk_ctx* ctx, atk_dtype dt, int order, const uint64_t* dims) {
+    if (order < 1 || order > ATK_MAX_ORDER) fail(ATK_SHAPE_MISMATCH, "tensor order must be in [1, 8]");
+    for (int m = 0; m < order; ++m)
+        if (dims[m] == 0) fail(ATK_SHAPE_MISMATCH, "tensor dimensions must be positive");
+    auto* t = new atk_tensor();
+    t->ctx = ctx;
+    t->dtype = dt;
+    t->order = order;
+    for (int m = 0; m < order; ++m) t->dims[m] = dims[m];
+    try {
+        t->data = dev_alloc(ctx, t->bytes());
+    } catch (...) {
+        delete t;
+        throw;
+    }
+    t->owned = true;
+    return t;
+}
+
+void check_tensor(const atk_tensor* t, const char* what) {
+    if (!t || !t->ctx || (!t->data && t->numel() > 0))
+        fail(ATK_INVALID_ARGUMENT, std::string(what) + ": invalid tensor handle");
+}
+
+void check_mode(int order, int mode) {
+    if (mode < 0 || mode >= order)
+        fail(ATK_MODE_OUT_OF_RANGE, "mode " + std::to_string(mode) + " out of range for order " +
+                                        std::to_string(order));
+}
+
+StageTimer::StageTimer(atk_ctx* c) : ctx(c) {
+    ATK_CUDA(cudaEventCreate(&a));
+    ATK_CUDA(cudaEventCreate(&b));
+}
+StageTimer::~StageTimer() {
+    if (a) cudaEventDestroy(a);
+    if (b) cudaEventDestroy(b);
+}
+void StageTimer::start() { ATK_CUDA(cudaEventRecord(a, ctx->stream)); }
+double StageTimer::stop_ms() {
+    ATK_CUDA(cudaEventRecord(b, ctx->stream));
+    ATK_CUDA(cudaEventSynchronize(b));
+    float ms = 0;
+    ATK_CUDA(cudaEventElapsedTime(&ms, a, b));
+    return double(ms);
+}
+
+template <class F>
+atk_status guard(F&& f) {
+    try {
+        f();
+        return ATK_OK;
+    } catch (const Error& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "host allocation failed";
+        return ATK_OOM;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return ATK_ERROR;
+    }
+}
+
+static void bind(atk_ctx* ctx) {
+    if (!ctx) fail(ATK_INVALID_ARGUMENT, "null context");
+    ATK_CUDA(cudaSetDevice(ctx->device));
+}
+
+}  // namespace atk
+
+using namespace atk;
+
+extern "C" {
+
+const char* atk_version(void) { return "atk-b200 0.1 (sm_100a)"; }
+const char* atk_last_error(void) { return g_last_error.c_str(); }
+
+atk_status atk_ctx_create(int device, atk_ctx** out) {
+    return guard([&] {
+        if (!out) fail(ATK_INVALID_ARGUMENT, "null output");
+        int n = 0;
+        ATK_CUDA(cudaGetDeviceCount(&n));
+        if (device < 0 || device >= n) fail(ATK_CUDA_ERROR, "no such CUDA device");
+        ATK_CUDA(cudaSetDevice(device));
+        cudaDeviceProp prop;
+        ATK_CUDA(cudaGetDeviceProperties(&prop, device));
+        if (prop.major != 10)
+            fail(ATK_CUDA_ERROR, "libatk_cuda is built for sm_100a (B200); device is sm_" +
+                                     std::to_string(prop.major) + std::to_string(prop.minor));
+        auto* c = new atk_ctx();
+        c->device = device;
+        c->num_sms = prop.multiProcessorCount;
+        ATK_CUDA(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+        c->stream = c->own_stream;
+        cudaMemPool_t pool;
+        ATK_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+        uint64_t thr = ~0ULL;
+        ATK_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+        *out = c;
+    });
+}
+
+atk_status atk_ctx_destroy(atk_ctx* ctx) {
+    return guard([&] {
+        if (!ctx) return;
+        cudaSetDevice(ctx->device);
+        comm_destroy(ctx);
+        if (ctx->own_stream) {
+            cudaStreamSynchronize(ctx->own_stream);
+            cudaStreamDestroy(ctx->own_stream);
+        }
+        delete ctx;
+    });
+}
+
+atk_status atk_ctx_set_stream(atk_ctx* ctx, void* s) {
+    return guard([&] {
+        bind(ctx);
+        ctx->stream = s ? static_cast<cudaStream_t>(s) : ctx->own_stream;
+    });
+}
+
+atk_status atk_ctx_synchronize(atk_ctx* ctx) {
+    return guard([&] {
+        bind(ctx);
+        ATK_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+uint64_t atk_ctx_launch_count(const atk_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+atk_status atk_ctx_set_option(atk_ctx* ctx, const char* key, double value) {
+    return guard([&] {
+        bind(ctx);
+        const std::string k = key ? key : "";
+        if (k == "simt") ctx->force_simt = value != 0.0;
+        else if (k == "eig_method") ctx->eig_method = int(value);
+        else if (k == "chfsi_tol") ctx->chfsi_tol = value;
+        else fail(ATK_INVALID_ARGUMENT, "unknown option: " + k);
+    });
+}
+
+atk_status atk_nccl_unique_id(void* out128) {
+    return guard([&] { nccl_unique_id(out128); });
+}
+
+atk_status atk_comm_init(atk_ctx* ctx, const void* uid, int rank, int world) {
+    return guard([&] {
+        bind(ctx);
+        comm_init(ctx, uid, rank, world);
+    });
+}
+
+atk_status atk_comm_destroy(atk_ctx* ctx) {
+    return guard([&] {
+        bind(ctx);
+        comm_destroy(ctx);
+    });
+}
+
+atk_status atk_tensor_create(atk_ctx* ctx, atk_dtype dt, int order, const uint64_t* dims,
+                             atk_tensor** out) {
+    return guard([&] {
+        bind(ctx);
+        *out = new_tensor(ctx, dt, order, dims);
+    });
+}
+
+atk_status atk_tensor_wrap(atk_ctx* ctx, atk_dtype dt, int order, const uint64_t* dims, void* ptr,
+                           atk_tensor** out) {
+    return guard([&] {
+        bind(ctx);
+        if (order < 1 || order > ATK_MAX_ORDER) fail(ATK_SHAPE_MISMATCH, "tensor order must be in [1, 8]");
+        if (reinterpret_cast<uintptr_t>(ptr) % 16) fail(ATK_INVALID_ARGUMENT, "device pointer must be 16-byte aligned");
+        auto* t = new atk_tensor();
+        t->ctx = ctx;
+        t->dtype = dt;
+        t->order = order;
+        for (int m = 0; m < order; ++m) {
+            if (dims[m] == 0) {
+                delete t;
+                fail(ATK_SHAPE_MISMATCH, "tensor dimensions must be positive");
+            }
+            t->dims[m] = dims[m];
+        }
+        t->data = ptr;
+        t->owned = false;
+        *out = t;
+    });
+}
+
+atk_status atk_tensor_from_host(atk_ctx* ctx, atk_dtype dt, int order, const uint64_t* dims,
+                                const void* host, atk_tensor** out) {
+    return guard([&] {
+        bind(ctx);
+        atk_tensor* t = new_tensor(ctx, dt, order, dims);
+        cudaError_t e = cudaMemcpyAsync(t->data, host, t->bytes(), cudaMemcpyHostToDevice, ctx->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+        if (e != cudaSuccess) {
+            atk_tensor_free(t);
+            fail(ATK_CUDA_ERROR, std::string("H2D copy: ") + cudaGetErrorString(e));
+        }
+        *out = t;
+    });
+}
+
+atk_status atk_tensor_to_host(atk_ctx* ctx, const atk_tensor* t, void* host) {
+    return guard([&] {
+        bind(ctx);
+        check_tensor(t, "atk_tensor_to_host");
+        ATK_CUDA(cudaMemcpyAsync(host, t->data, t->bytes(), cudaMemcpyDeviceToHost, ctx->stream));
+        ATK_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+atk_status atk_tensor_free(atk_tensor* t) {
+    return guard([&] {
+        if (!t) return;
+        if (t->owned && t->data) {
+            cudaSetDevice(t->ctx->device);
+            dev_free(t->ctx, t->data);
+        }
+        delete t;
+    });
+}
+
+atk_status atk_tensor_info(const atk_tensor* t, atk_dtype* dt, int* order, uint64_t* dims, void** ptr) {
+    return guard([&] {
+        if (!t) fail(ATK_INVALID_ARGUMENT, "null tensor");
+        if (dt) *dt = t->dtype;
+        if (order) *order = t->order;
+        if (dims)
+            for (int m = 0; m < t->order; ++m) dims[m] = t->dims[m];
+        if (ptr) *ptr = t->data;
+    });
+}
+
+atk_status atk_fill_uniform(atk_ctx* ctx, atk_tensor* t, uint64_t seed, uint64_t offset) {
+    return guard([&] {
+        bind(ctx);
+        check_tensor(t, "atk_fill_uniform");
+        fill_uniform(ctx, t, seed, offset);
+        ATK_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+atk_status atk_axpy(atk_ctx* ctx, atk_tensor* x, double alpha, const atk_tensor* y) {
+    return guard([&] {
+        bind(ctx);
+        check_tensor(x, "atk_axpy x");
+        check_tensor(y, "atk_axpy y");
+        if (x->dtype != y->dtype || x->numel() != y->numel())
+            fail(ATK_SHAPE_MISMATCH, "axpy operands differ in shape or dtype");
+        axpy(ctx, x->data, y->data, x->dtype, x->numel(), alpha);
+        ATK_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+atk_status atk_frobenius_norm(atk_ctx* ctx, const atk_tensor* t, double* out) {
+    return guard([&] {
+        bind(ctx);
+        check_tensor(t, "atk_frobenius_norm");
+        *out = std::sqrt(norm2_sq(ctx, t->data, t->dtype, t->numel()));
+    });
+}
+
+atk_status atk_gram(atk_ctx* ctx, const atk_tensor* x, int mode, double* s_out) {
+    return guard([&] {
+        bind(ctx);
+        check_tensor(x, "atk_gram");
+        check_mode(x->order, mode);
+        const uint64_t I = x->dims[mode];
+        DevBuf<double> s(ctx, I * I);
+        contract_ttt(ctx, x, x, mode, s.get(), true);
+        record_gemm((long long)(I * I) * (long long)j_of(x, mode));
+        ATK_CUDA(cudaMemcpyAsync(s_out, s.get(), I * I * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        ATK_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+atk_status atk_ttm(atk_ctx* ctx, const atk_tensor* x, const double* u, uint64_t r, uint64_t i,
+                   int mode, atk_tensor** y_out) {
+    return guard([&] {
+        bind(ctx);
+        check_tensor(x, "atk_ttm");
+        check_mode(x->order, mode);
+        if (i != x->dims[mode])
+            fail(ATK_SHAPE_MISMATCH, "ttm matrix has " + std::to_string(i) +
+                                         " columns but mode has dimension " + std::to_string(x->dims[mode]));
+        if (r == 0) fail(ATK_SHAPE_MISMATCH, "ttm matrix has no rows");
+        DevBuf<double> ud(ctx, r * i);
+        ATK_CUDA(cudaMemcpyAsync(ud.get(), u, r * i * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        *y_out = contract_ttm(ctx, x, ud.get(), r, mode);
+        record_gemm(2LL * (long long)(r * j_of(x, mode)) * (long long)i);
+        ATK_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+atk_status atk_ttt(atk_ctx* ctx, const atk_tensor* x, const atk_tensor* y, int mode, double* z_out) {
+    return guard([&] {
+        bind(ctx);
+        check_tensor(x, "atk_ttt x");
+        check_tensor(y, "atk_ttt y");
+        check_mode(x->order, mode);
+        check_mode(y->order, mode);
+        if (x->order != y->order) fail(ATK_SHAPE_MISMATCH, "ttt_mode operands differ in order");
+        if (x->dtype != y->dtype) fail(ATK_SHAPE_MISMATCH, "ttt_mode operands differ in dtype");
+        for (int m = 0; m < x->order; ++m)
+            if (m != mode && x->dims[m] != y->dims[m])
+                fail(ATK_SHAPE_MISMATCH, "ttt_mode operands disagree on dimension " + std::to_string(m));
+        const uint64_t I = x->dims[mode], R = y->dims[mode];
+        DevBuf<double> z(ctx, I * R);
+        contract_ttt(ctx, x, y, mode, z.get(), false);
+        record_gemm(2LL * (long long)(I * R) * (long long)j_of(x, mode));
+        ATK_CUDA(cudaMemcpyAsync(z_out, z.get(), I * R * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        ATK_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+atk_status atk_sym_eig_top_r(atk_ctx* ctx, const double* s, uint64_t n, uint64_t r, double* values,
+                             double* vectors) {
+    return guard([&] {
+        bind(ctx);
+        if (r < 1 || r > n)
+            fail(ATK_RANK_TOO_LARGE, "requested " + std::to_string(r) + " eigenpairs of a " +
+                                         std::to_string(n) + "x" + std::to_string(n) + " matrix");
+        DevBuf<double> sd(ctx, n * n), vd(ctx, r), vecd(ctx, n * r);
+        ATK_CUDA(cudaMemcpyAsync(sd.get(), s, n * n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        sym_eig_top_r(ctx, sd.get(), int(n), int(r), vd.get(), vecd.get());
+        ATK_CUDA(cudaMemcpyAsync(values, vd.get(), r * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        ATK_CUDA(cudaMemcpyAsync(vectors, vecd.get(), n * r * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        ATK_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+atk_status atk_thin_qr(atk_ctx* ctx, const double* a, uint64_t rows, uint64_t cols, double* q, double* r) {
+    return guard([&] {
+        bind(ctx);
+        if (rows < cols) fail(ATK_SHAPE_MISMATCH, "thin_qr expects rows >= cols");
+        DevBuf<double> ad(ctx, rows * cols), qd(ctx, rows * cols), rd(ctx, cols * cols);
+        ATK_CUDA(cudaMemcpyAsync(ad.get(), a, rows * cols * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        double fro = 0.0;
+        for (uint64_t e = 0; e < rows * cols; ++e) fro += a[e] * a[e];
+        thin_qr_dev(ctx, ad.get(), rows, cols, qd.get(), rd.get(), std::sqrt(fro));
+        ATK_CUDA(cudaMemcpyAsync(q, qd.get(), rows * cols * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        ATK_CUDA(cudaMemcpyAsync(r, rd.get(), cols * cols * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        ATK_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+atk_status atk_spd_solve(atk_ctx* ctx, const double* a, uint64_t n, const double* b, uint64_t nrhs,
+                         double* x) {
+    return guard([&] {
+        bind(ctx);
+        DevBuf<double> l(ctx, n * n), xd(ctx, n * nrhs);
+        DevBuf<int> info(ctx, 1);
+        ATK_CUDA(cudaMemcpyAsync(l.get(), a, n * n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        ATK_CUDA(cudaMemcpyAsync(xd.get(), b, n * nrhs * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        cholesky(ctx, l.get(), int(n), info.get());
+        int h = 0;
+        ATK_CUDA(cudaMemcpyAsync(&h, info.get(), sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+        ATK_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (h != 0) fail(ATK_NOT_SPD, "Cholesky factorization hit a non-positive pivot");
+        cholesky_solve(ctx, l.get(), int(n), xd.get(), int(nrhs));
+        ATK_CUDA(cudaMemcpyAsync(x, xd.get(), n * nrhs * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        ATK_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+static void copy_times(atk_stage_times* dst, const atk_stage_times& src) {
+    if (dst) *dst = src;
+}
+
+atk_status atk_eig_mode(atk_ctx* ctx, const atk_tensor* y, int mode, uint64_t r, double* factor_out,
+                        atk_tensor** shrunk_out, atk_stage_times* times) {
+    return guard([&] {
+        bind(ctx);
+        check_tensor(y, "atk_eig_mode");
+        ModeOut mo = eig_mode(ctx, y, mode, r, ATK_SOLVER_EIG);
+        std::memcpy(factor_out, mo.factor.data(), mo.factor.size() * sizeof(double));
+        *shrunk_out = mo.shrunk;
+        copy_times(times, mo.times);
+    });
+}
+
+atk_status atk_svd_mode(atk_ctx* ctx, const atk_tensor* y, int mode, uint64_t r, double* factor_out,
+                        atk_tensor** shrunk_out, atk_stage_times* times) {
+    return guard([&] {
+        bind(ctx);
+        check_tensor(y, "atk_svd_mode");
+        ModeOut mo = eig_mode(ctx, y, mode, r, ATK_SOLVER_SVD);
+        std::memcpy(factor_out, mo.factor.data(), mo.factor.size() * sizeof(double));
+        *shrunk_out = mo.shrunk;
+        copy_times(times, mo.times);
+    });
+}
+
+atk_status atk_als_mode(atk_ctx* ctx, const atk_tensor* y, int mode, uint64_t r,
+                        const atk_als_opts* opts, const double* l0, double* factor_out,
+                        atk_tensor** shrunk_out, int* iters_run, atk_stage_times* times) {
+    return guard([&] {
+        bind(ctx);
+        check_tensor(y, "atk_als_mode");
+        atk_als_opts o = opts ? *opts : atk_als_opts{5, 0.0, 0};
+        ModeOut mo = als_mode(ctx, y, mode, r, o, l0);
+        std::memcpy(factor_out, mo.factor.data(), mo.factor.size() * sizeof(double));
+        *shrunk_out = mo.shrunk;
+        if (iters_run) *iters_run = mo.iterations;
+        copy_times(times, mo.times);
+    });
+}
+
+atk_status atk_als_iterate(atk_ctx* ctx, const atk_tensor* y, int mode, const double* l0, uint64_t r,
+                           const atk_als_opts* opts, double* l_out, atk_tensor** rfac_out,
+                           int* iters_run) {
+    return guard([&] {
+        bind(ctx);
+        check_tensor(y, "atk_als_iterate");
+        check_mode(y->order, mode);
+        atk_als_opts o = opts ? *opts : atk_als_opts{5, 0.0, 0};
+        AlsOut a = als_iterate(ctx, y, mode, l0, r, o);
+        std::memcpy(l_out, a.l.data(), a.l.size() * sizeof(double));
+        *rfac_out = a.rfac;
+        if (iters_run) *iters_run = a.iterations_run;
+    });
+}
+
+atk_status atk_sthosvd(atk_ctx* ctx, const atk_tensor* x, const uint64_t* ranks, atk_selector_fn decide,
+                       void* user, const atk_als_opts* opts, atk_tensor** core_out, double* factors_out,
+                       atk_mode_report* reports) {
+    return guard([&] {
+        bind(ctx);
+        atk_als_opts o = opts ? *opts : atk_als_opts{5, 0.0, 0};
+        *core_out = sthosvd(ctx, x, ranks, decide, user, o, factors_out, reports);
+    });
+}
+
+atk_status atk_sthosvd_host(atk_ctx* ctx, atk_dtype dt, int order, const uint64_t* dims,
+                            const void* x_host, const uint64_t* ranks, atk_selector_fn decide,
+                            void* user, const atk_als_opts* opts, void* core_out_host,
+                            double* factors_out, atk_mode_report* reports) {
+    return guard([&] {
+        bind(ctx);
+        atk_als_opts o = opts ? *opts : atk_als_opts{5, 0.0, 0};
+        atk_tensor* x = new_tensor(ctx, dt, order, dims);
+        atk_tensor* core = nullptr;
+        try {
+            ATK_CUDA(cudaMemcpyAsync(x->data, x_host, x->bytes(), cudaMemcpyHostToDevice, ctx->stream));
+            core = sthosvd(ctx, x, ranks, decide, user, o, factors_out, reports);
+            ATK_CUDA(cudaMemcpyAsync(core_out_host, core->data, core->bytes(), cudaMemcpyDeviceToHost,
+                                     ctx->stream));
+            ATK_CUDA(cudaStreamSynchronize(ctx->stream));
+        } catch (...) {
+            atk_tensor_free(x);
+            if (core) atk_tensor_free(core);
+            throw;
+        }
+        atk_tensor_free(x);
+        atk_tensor_free(core);
+    });
+}
+
+atk_status atk_reconstruct(atk_ctx* ctx, const atk_tensor* core, const double* factors,
+                           const uint64_t* odims, atk_tensor** out) {
+    return guard([&] {
+        bind(ctx);
+        *out = reconstruct(ctx, core, factors, odims);
+        ATK_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+atk_status atk_relative_error(atk_ctx* ctx, const atk_tensor* x, const atk_tensor* core,
+                              const double* factors, double* out) {
+    return guard([&] {
+        bind(ctx);
+        check_tensor(x, "atk_relative_error x");
+        check_tensor(core, "atk_relative_error core");
+        if (core->order != x->order) fail(ATK_SHAPE_MISMATCH, "decomposition has inconsistent order");
+        *out = relative_error(ctx, x, core, factors);
+    });
+}
+
+void atk_reset_gemm_counters(void) {
+    g_gemm_calls = 0;
+    g_gemm_flops = 0;
+}
+long long atk_gemm_calls(void) { return g_gemm_calls.load(); }
+long long atk_gemm_flops(void) { return g_gemm_flops.load(); }
+double atk_cost_eig(double i, double r, double j) { return cost_eig(i, r, j); }
+double atk_cost_als(double i, double r, double j, int num_iters) { return cost_als(i, r, j, num_iters); }
+
+}  // extern "C"

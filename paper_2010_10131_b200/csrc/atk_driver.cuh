@@ -1,0 +1,87 @@
+// atk_driver.cuh — declarations shared by the solver driver, the C ABI and
+// the tensor-core / distributed back ends.
+#pragma once
+
+#include <vector>
+
+#include "atk_internal.cuh"
+
+namespace atk {
+
+// tensor.hpp:33-39
+inline uint64_t mix_seed(uint64_t seed, uint64_t salt) {
+    uint64_t z = seed + 0x9e3779b97f4a7c15ULL * (salt + 1);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+// selector.hpp:36-52
+inline double f_eig(double i) { return 9.0 * i * i * i; }
+inline double f_qr(double i, double r) { return 2.0 * i * r * r - (2.0 / 3.0) * r * r * r; }
+inline double f_inv(double r) { return 2.0 * r * r * r; }
+inline double cost_eig(double i, double r, double j) { return i * i * j + 2.0 * i * r * j + f_eig(i); }
+inline double cost_als(double i, double r, double j, int num_iters) {
+    const double per_iter = 2.0 * i * j * r + 2.0 * j * r * r + 2.0 * i * j * r + 2.0 * j * r * r +
+                            4.0 * i * r * r + 2.0 * f_inv(r);
+    return per_iter * num_iters + 2.0 * j * r * r + f_qr(i, r);
+}
+
+// contract_simt.cu
+void ttt_simt(atk_ctx* ctx, const void* x, const void* y, atk_dtype dt, Split s, uint64_t R,
+              double* z_dev, bool sym);
+void ttm_simt(atk_ctx* ctx, const void* x, atk_dtype dt, Split s, const double* u_dev, uint64_t R,
+              void* y);
+
+// contract_tc.cu — tcgen05 (fp32 storage, kind::tf32) / DMMA (fp64) paths.
+bool tc_ttt_supported(atk_ctx* ctx, const atk_tensor* x, const atk_tensor* y, int mode, bool sym);
+void tc_ttt(atk_ctx* ctx, const atk_tensor* x, const atk_tensor* y, int mode, double* z_dev, bool sym);
+bool tc_ttm_supported(atk_ctx* ctx, const atk_tensor* x, uint64_t R, int mode);
+void tc_ttm(atk_ctx* ctx, const atk_tensor* x, const double* u_dev, uint64_t R, int mode,
+            atk_tensor* y);
+
+// driver.cu
+struct ModeOut {
+    std::vector<double> factor;  // I x r host
+    atk_tensor* shrunk = nullptr;
+    int iterations = 0;
+    int solver = ATK_SOLVER_EIG;
+    EigInfo eig;
+    atk_stage_times times{};
+};
+struct AlsOut {
+    std::vector<double> l;  // I x r host
+    atk_tensor* rfac = nullptr;
+    int iterations_run = 0;
+};
+void contract_ttt(atk_ctx* ctx, const atk_tensor* x, const atk_tensor* y, int mode, double* z_dev,
+                  bool sym);
+atk_tensor* contract_ttm(atk_ctx* ctx, const atk_tensor* x, const double* u_dev, uint64_t R,
+                         int mode);
+uint64_t j_of(const atk_tensor* t, int mode);
+void check_truncation(const atk_tensor* y, int mode, uint64_t r);
+ModeOut eig_mode(atk_ctx* ctx, const atk_tensor* y, int mode, uint64_t r, int solver_kind);
+ModeOut als_mode(atk_ctx* ctx, const atk_tensor* y, int mode, uint64_t r, const atk_als_opts& opts,
+                 const double* l0_host);
+AlsOut als_iterate(atk_ctx* ctx, const atk_tensor* y, int mode, const double* l0_host, uint64_t r,
+                   const atk_als_opts& opts);
+std::vector<double> als_initial_guess(uint64_t rows, uint64_t r, uint64_t seed, uint64_t mode);
+void thin_qr_dev(atk_ctx* ctx, const double* a_dev, uint64_t rows, uint64_t cols, double* q_dev,
+                 double* r_dev, double fro_a);
+atk_tensor* sthosvd(atk_ctx* ctx, const atk_tensor* x, const uint64_t* ranks, atk_selector_fn decide,
+                    void* user, const atk_als_opts& opts, double* factors_out,
+                    atk_mode_report* reports);
+atk_tensor* reconstruct(atk_ctx* ctx, const atk_tensor* core, const double* factors,
+                        const uint64_t* odims);
+double relative_error(atk_ctx* ctx, const atk_tensor* x, const atk_tensor* core,
+                      const double* factors);
+
+// dist.cu — NCCL over NVLink (one process per GPU).
+void comm_init(atk_ctx* ctx, const void* unique_id, int rank, int world);
+void comm_destroy(atk_ctx* ctx);
+void nccl_unique_id(void* out128);
+void allreduce_sum(atk_ctx* ctx, double* buf, uint64_t count, double* comm_ms);
+atk_tensor* allgather_last_mode(atk_ctx* ctx, const atk_tensor* local);
+uint64_t comm_global_last(atk_ctx* ctx, const atk_tensor* local);
+
+}  // namespace atk

@@ -1,0 +1,195 @@
+// atk_internal.cuh — shared plumbing of libatk_cuda.so: context, tensor
+// handles, error mapping, device workspace, launch accounting.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/atk.h"
+
+namespace atk {
+
+// errors.hpp:9-25 -> atk_status.  Thrown inside the library, converted to a
+// status code + thread-local message at the C boundary (api.cu).
+struct Error : std::runtime_error {
+    atk_status code;
+    Error(atk_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void fail(atk_status c, const std::string& m) { throw Error(c, m); }
+
+#define ATK_CUDA(expr)                                                                        \
+    do {                                                                                      \
+        cudaError_t _e = (expr);                                                              \
+        if (_e != cudaSuccess) {                                                              \
+            ::atk::fail(_e == cudaErrorMemoryAllocation ? ATK_OOM : ATK_CUDA_ERROR,           \
+                        std::string(#expr) + ": " + cudaGetErrorString(_e) + " at " +         \
+                            __FILE__ + ":" + std::to_string(__LINE__));                       \
+        }                                                                                     \
+    } while (0)
+
+#define ATK_LAUNCHED(ctx)                                                                     \
+    do {                                                                                      \
+        (ctx)->launches++;                                                                    \
+        cudaError_t _e = cudaGetLastError();                                                  \
+        if (_e != cudaSuccess)                                                                \
+            ::atk::fail(ATK_CUDA_ERROR, std::string("kernel launch: ") +                      \
+                                            cudaGetErrorString(_e) + " at " + __FILE__ + ":" + \
+                                            std::to_string(__LINE__));                        \
+    } while (0)
+
+struct Comm;  // dist.cu
+
+}  // namespace atk
+
+struct atk_ctx {
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t stream = nullptr;
+    cudaStream_t own_stream = nullptr;
+    uint64_t launches = 0;
+    int force_simt = 0;        // option "simt": portable CUDA-core contractions
+    int eig_method = -1;       // option "eig_method": -1 auto, 0 dense Jacobi, 1 ChFSI
+    double chfsi_tol = 1e-12;  // option "chfsi_tol": relative Ritz residual target
+    atk::Comm* comm = nullptr;
+    cudaEvent_t ev[8] = {};
+};
+
+struct atk_tensor {
+    atk_ctx* ctx = nullptr;
+    atk_dtype dtype = ATK_F64;
+    int order = 0;
+    uint64_t dims[ATK_MAX_ORDER] = {};
+    void* data = nullptr;
+    bool owned = false;
+
+    uint64_t numel() const {
+        uint64_t p = 1;
+        for (int m = 0; m < order; ++m) p *= dims[m];
+        return p;
+    }
+    size_t elem_bytes() const { return dtype == ATK_F32 ? 4 : 8; }
+    size_t bytes() const { return size_t(numel()) * elem_bytes(); }
+};
+
+namespace atk {
+
+// ------------------------------------------------------------------ memory
+// Stream-ordered allocations from the device's default pool; the pool keeps
+// freed blocks (release threshold = max) so repeated sthosvd calls reuse them.
+void* dev_alloc(atk_ctx* ctx, size_t bytes);
+void dev_free(atk_ctx* ctx, void* p);
+
+template <class T>
+struct DevBuf {
+    atk_ctx* ctx = nullptr;
+    T* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    DevBuf(atk_ctx* c, size_t count) : ctx(c), n(count) {
+        p = count ? static_cast<T*>(dev_alloc(c, count * sizeof(T))) : nullptr;
+    }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : ctx(o.ctx), p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) {
+            reset();
+            ctx = o.ctx; p = o.p; n = o.n;
+            o.p = nullptr; o.n = 0;
+        }
+        return *this;
+    }
+    ~DevBuf() { reset(); }
+    void reset() {
+        if (p) dev_free(ctx, p);
+        p = nullptr;
+        n = 0;
+    }
+    T* get() const { return p; }
+};
+
+// ------------------------------------------------------------------ tensors
+atk_tensor* new_tensor(atk_ctx* ctx, atk_dtype dt, int order, const uint64_t* dims);
+void check_tensor(const atk_tensor* t, const char* what);
+
+// LoopSplit (tensor.hpp:175-187) of a device tensor at `mode`.
+struct Split {
+    uint64_t P = 1, I = 1, O = 1;
+};
+inline Split loop_split(const uint64_t* dims, int order, int mode) {
+    Split s;
+    for (int m = 0; m < mode; ++m) s.P *= dims[m];
+    s.I = dims[mode];
+    for (int m = mode + 1; m < order; ++m) s.O *= dims[m];
+    return s;
+}
+
+void check_mode(int order, int mode);
+
+// ------------------------------------------------------------------ counters
+void record_gemm(long long charge);
+
+// ------------------------------------------------------------------ timing
+struct StageTimer {
+    atk_ctx* ctx;
+    cudaEvent_t a = nullptr, b = nullptr;
+    explicit StageTimer(atk_ctx* c);
+    ~StageTimer();
+    void start();
+    double stop_ms();  // synchronizes on the stop event
+};
+
+// ------------------------------------------------------------------ kernels
+// gen.cu
+void fill_uniform(atk_ctx* ctx, atk_tensor* t, uint64_t seed, uint64_t offset);
+double norm2_sq(atk_ctx* ctx, const void* x, atk_dtype dt, uint64_t n);  // sum of squares, fp64
+void axpy(atk_ctx* ctx, void* x, const void* y, atk_dtype dt, uint64_t n, double alpha);
+void convert(atk_ctx* ctx, void* dst, atk_dtype ddt, const void* src, atk_dtype sdt, uint64_t n);
+double diff_norm2_sq(atk_ctx* ctx, const void* x, const void* y, atk_dtype dt, uint64_t n);
+
+// contract.cu — matricization-free contractions (kernels.hpp:34-138).
+// Z (I x R, fp64, device, column-major) = X_(n) Y_(n)^T, X viewed as
+// (P, I, O), Y as (P, R, O).  `sym` = Gram (X == Y): exact symmetric output.
+void ttt(atk_ctx* ctx, const void* x, const void* y, atk_dtype dt, Split s, uint64_t R,
+         double* z_dev, bool sym);
+// Y (P, R, O) = X (P, I, O) x_n U, U R x I fp64 device (column-major).
+void ttm(atk_ctx* ctx, const void* x, atk_dtype dt, Split s, const double* u_dev, uint64_t R,
+         void* y);
+
+// dense.cu — small fp64 device linear algebra.
+// C(m x n) = alpha op(A) op(B) + beta C, column-major with leading dims.
+void dgemm(atk_ctx* ctx, bool ta, bool tb, int m, int n, int k, double alpha, const double* a,
+           int lda, const double* b, int ldb, double beta, double* c, int ldc);
+// Dense symmetric eigensolver for n <= kJacobiMax (one CTA, smem Jacobi):
+// all eigenpairs of A (n x n, lda), values descending, vectors n x n.
+constexpr int kJacobiMax = 112;
+void jacobi_eig(atk_ctx* ctx, const double* a, int n, int lda, double* values, double* vectors,
+                int ldv, int* sweeps_dev);
+// Cholesky factorization in place (lower), status written to *info_dev (0 ok, k>0 pivot k).
+void cholesky(atk_ctx* ctx, double* a, int n, int* info_dev);
+// X = A^{-1} B given the Cholesky factor L (lower) of A: B overwritten.
+void cholesky_solve(atk_ctx* ctx, const double* l, int n, double* b, int nrhs);
+// Householder thin QR of A (m x n, m >= n): Q (m x n), R (n x n), diag(R) >= 0.
+void householder_qr(atk_ctx* ctx, const double* a, int m, int n, double* q, double* r);
+// fix_signs (linalg.hpp:34-50) on the columns of V (n x r), optional coupled rows.
+void fix_signs(atk_ctx* ctx, double* v, int n, int r, int ldv);
+void symmetrize(atk_ctx* ctx, double* a, int n);
+void set_identity(atk_ctx* ctx, double* a, int n);
+void transpose(atk_ctx* ctx, const double* a, int rows, int cols, double* at);
+
+// eig.cu — sym_eig_top_r on device (linalg.hpp:101-123).
+struct EigInfo {
+    int method = 0;      // 0 dense Jacobi, 1 ChFSI
+    int iterations = 0;  // ChFSI outer iterations
+    double residual = 0;
+};
+EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* values_dev,
+                      double* vectors_dev);
+
+}  // namespace atk

@@ -1,0 +1,204 @@
+// contract_simt.cu — portable CUDA-core matricization-free contractions.
+//
+// These are the engine's general-shape path (any P, I, O, R; fp32 or fp64
+// storage, fp64 accumulation).  The hot fp32 shapes dispatch to the tcgen05
+// kernels in contract_tc.cu; everything else (and option "simt") lands here.
+//
+// Index contract (kernels.hpp:34-118, tensor.hpp:175-187): X viewed as
+// (P, I, O), element (p, i, o) at p + P*i + P*I*o.  No unfolding is ever
+// materialised: the K index of every contraction is the (p, o) pair walked in
+// place.
+#include <algorithm>
+
+#include "atk_internal.cuh"
+
+namespace atk {
+namespace {
+
+constexpr int TM = 64, TN = 64, KT = 16, NT = 256;
+
+// Z(I x R) partial over k in [k0, k1) of sum_k X(k, i) Y(k, r), k = (p, o).
+template <class T>
+__global__ void __launch_bounds__(NT) ttt_simt_kernel(const T* __restrict__ x,
+                                                      const T* __restrict__ y, uint64_t P,
+                                                      uint64_t I, uint64_t R, uint64_t K,
+                                                      uint64_t kchunk, bool sym,
+                                                      double* __restrict__ part) {
+    const int tm = blockIdx.x, tn = blockIdx.y;
+    if (sym && tn < tm) return;
+    __shared__ double As[KT][TM + 1];
+    __shared__ double Bs[KT][TN + 1];
+    const uint64_t i0 = uint64_t(tm) * TM, r0 = uint64_t(tn) * TN;
+    const uint64_t kb = uint64_t(blockIdx.z) * kchunk;
+    const uint64_t ke = min(K, kb + kchunk);
+    const int tid = threadIdx.x;
+    const int ty = tid / 16, tx = tid % 16;
+    double acc[4][4] = {};
+    for (uint64_t k0 = kb; k0 < ke; k0 += KT) {
+        // load A = X tile [KT][TM]
+        for (int e = tid; e < KT * TM; e += NT) {
+            int kk, ii;
+            if (P == 1) { ii = e % TM; kk = e / TM; } else { kk = e % KT; ii = e / KT; }
+            const uint64_t k = k0 + kk, i = i0 + ii;
+            double v = 0.0;
+            if (k < ke && i < I) {
+                const uint64_t p = k % P, o = k / P;
+                v = double(x[p + P * i + P * I * o]);
+            }
+            As[kk][ii] = v;
+        }
+        for (int e = tid; e < KT * TN; e += NT) {
+            int kk, rr;
+            if (P == 1) { rr = e % TN; kk = e / TN; } else { kk = e % KT; rr = e / KT; }
+            const uint64_t k = k0 + kk, r = r0 + rr;
+            double v = 0.0;
+            if (k < ke && r < R) {
+                const uint64_t p = k % P, o = k / P;
+                v = double(y[p + P * r + P * R * o]);
+            }
+            Bs[kk][rr] = v;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < KT; ++kk) {
+            double a[4], b[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) a[u] = As[kk][ty + 16 * u];
+#pragma unroll
+            for (int v = 0; v < 4; ++v) b[v] = Bs[kk][tx + 16 * v];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) acc[u][v] = fma(a[u], b[v], acc[u][v]);
+        }
+        __syncthreads();
+    }
+    double* out = part + uint64_t(blockIdx.z) * I * R;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const uint64_t i = i0 + ty + 16 * u, r = r0 + tx + 16 * v;
+            if (i < I && r < R) out[i + I * r] = acc[u][v];
+        }
+}
+
+// Z = sum_z part[z] in fixed order; for Gram mirror the computed upper
+// triangle (i <= r) onto the lower one => exactly symmetric (kernels.hpp:127-138).
+__global__ void reduce_partials(const double* __restrict__ part, int nsplit, uint64_t I,
+                                uint64_t R, bool sym, double* __restrict__ z) {
+    const uint64_t n = I * R;
+    for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
+         e += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t i = e % I, r = e / I;
+        uint64_t src = e;
+        if (sym && i > r) src = r + I * i;
+        double s = 0.0;
+        for (int k = 0; k < nsplit; ++k) s += part[uint64_t(k) * n + src];
+        z[e] = s;
+    }
+}
+
+// Y(m, r) = sum_i X(m, i) U(r, i), m = (p, o).
+template <class T>
+__global__ void __launch_bounds__(NT) ttm_simt_kernel(const T* __restrict__ x,
+                                                      const double* __restrict__ u, uint64_t P,
+                                                      uint64_t I, uint64_t O, uint64_t R,
+                                                      T* __restrict__ y) {
+    __shared__ double As[KT][TM + 1];
+    __shared__ double Bs[KT][TN + 1];
+    const uint64_t M = P * O;
+    const uint64_t m0 = uint64_t(blockIdx.x) * TM, r0 = uint64_t(blockIdx.y) * TN;
+    const int tid = threadIdx.x, ty = tid / 16, tx = tid % 16;
+    double acc[4][4] = {};
+    for (uint64_t k0 = 0; k0 < I; k0 += KT) {
+        for (int e = tid; e < KT * TM; e += NT) {
+            int kk, mm;
+            if (P == 1) { kk = e % KT; mm = e / KT; } else { mm = e % TM; kk = e / TM; }
+            const uint64_t i = k0 + kk, m = m0 + mm;
+            double v = 0.0;
+            if (i < I && m < M) {
+                const uint64_t p = m % P, o = m / P;
+                v = double(x[p + P * i + P * I * o]);
+            }
+            As[kk][mm] = v;
+        }
+        for (int e = tid; e < KT * TN; e += NT) {
+            const int rr = e % TN, kk = e / TN;
+            const uint64_t i = k0 + kk, r = r0 + rr;
+            Bs[kk][rr] = (i < I && r < R) ? u[r + R * i] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < KT; ++kk) {
+            double a[4], b[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) a[q] = As[kk][ty + 16 * q];
+#pragma unroll
+            for (int v = 0; v < 4; ++v) b[v] = Bs[kk][tx + 16 * v];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) acc[q][v] = fma(a[q], b[v], acc[q][v]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const uint64_t m = m0 + ty + 16 * q, r = r0 + tx + 16 * v;
+            if (m < M && r < R) {
+                const uint64_t p = m % P, o = m / P;
+                y[p + P * r + P * R * o] = T(acc[q][v]);
+            }
+        }
+}
+
+}  // namespace
+
+void ttt_simt(atk_ctx* ctx, const void* x, const void* y, atk_dtype dt, Split s, uint64_t R,
+              double* z_dev, bool sym) {
+    const uint64_t K = s.P * s.O;
+    const uint64_t gm = (s.I + TM - 1) / TM, gn = (R + TN - 1) / TN;
+    const uint64_t tiles = sym ? gm * (gm + 1) / 2 : gm * gn;
+    uint64_t splits = std::max<uint64_t>(1, (uint64_t(ctx->num_sms) * 4) / std::max<uint64_t>(1, tiles));
+    splits = std::min<uint64_t>(splits, std::max<uint64_t>(1, K / (KT * 16)));
+    splits = std::min<uint64_t>(splits, 4096);
+    uint64_t kchunk = (K + splits - 1) / splits;
+    kchunk = (kchunk + KT - 1) / KT * KT;
+    splits = (K + kchunk - 1) / kchunk;
+    if (splits == 0) splits = 1;
+    DevBuf<double> part(ctx, splits * s.I * R);
+    if (K == 0) {
+        ATK_CUDA(cudaMemsetAsync(z_dev, 0, s.I * R * sizeof(double), ctx->stream));
+        return;
+    }
+    dim3 grid{unsigned(gm), unsigned(gn), unsigned(splits)};
+    if (dt == ATK_F32)
+        ttt_simt_kernel<float><<<grid, NT, 0, ctx->stream>>>((const float*)x, (const float*)y, s.P,
+                                                             s.I, R, K, kchunk, sym, part.get());
+    else
+        ttt_simt_kernel<double><<<grid, NT, 0, ctx->stream>>>((const double*)x, (const double*)y,
+                                                              s.P, s.I, R, K, kchunk, sym, part.get());
+    ATK_LAUNCHED(ctx);
+    const uint64_t n = s.I * R;
+    const int g = int(std::min<uint64_t>((n + 255) / 256, uint64_t(ctx->num_sms) * 8));
+    reduce_partials<<<g, 256, 0, ctx->stream>>>(part.get(), int(splits), s.I, R, sym, z_dev);
+    ATK_LAUNCHED(ctx);
+}
+
+void ttm_simt(atk_ctx* ctx, const void* x, atk_dtype dt, Split s, const double* u_dev, uint64_t R,
+              void* y) {
+    const uint64_t M = s.P * s.O;
+    dim3 grid{unsigned((M + TM - 1) / TM), unsigned((R + TN - 1) / TN)};
+    if (dt == ATK_F32)
+        ttm_simt_kernel<float><<<grid, NT, 0, ctx->stream>>>((const float*)x, u_dev, s.P, s.I, s.O,
+                                                             R, (float*)y);
+    else
+        ttm_simt_kernel<double><<<grid, NT, 0, ctx->stream>>>((const double*)x, u_dev, s.P, s.I,
+                                                              s.O, R, (double*)y);
+    ATK_LAUNCHED(ctx);
+}
+
+}  // namespace atk

@@ -1,0 +1,170 @@
+// dist.cu — multi-GPU st-HOSVD plumbing: NCCL over NVLink 5 / NVSwitch, one
+// process per GPU.
+//
+// The input is sharded along the LAST mode: in column-major order each rank's
+// slab [I_1 .. I_{N-1}, I_N / g] is one contiguous block of the flat buffer,
+// so the same kernels run on a smaller O.  For modes n < N-1 the local Gram
+// is a partial sum -> ONE ncclAllReduce(sum, fp64) per mode; the replicated
+// eigensolver is deterministic, so every rank holds bit-identical factors and
+// the TTM stays local (no data-path collective).  Before the shard mode the
+// shrunk tensor is small (C5: 64 x 64 x 2048 fp32 = 33.5 MB) and is
+// all-gathered once; that mode then runs replicated.
+//
+// NCCL is loaded with dlopen("libnccl.so.2") on first use, so single-GPU
+// processes carry no NCCL dependency and share torch's copy when present.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "atk_driver.cuh"
+
+namespace atk {
+
+namespace {
+
+struct NcclApi {
+    void* h = nullptr;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+    static NcclApi api;
+    if (!api.h) {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) fail(ATK_NCCL_ERROR, std::string("cannot load libnccl.so.2: ") + dlerror());
+        auto get = [&](const char* n) {
+            void* p = dlsym(h, n);
+            if (!p) fail(ATK_NCCL_ERROR, std::string("NCCL symbol missing: ") + n);
+            return p;
+        };
+        api.GetUniqueId = (decltype(api.GetUniqueId))get("ncclGetUniqueId");
+        api.CommInitRank = (decltype(api.CommInitRank))get("ncclCommInitRank");
+        api.CommDestroy = (decltype(api.CommDestroy))get("ncclCommDestroy");
+        api.AllReduce = (decltype(api.AllReduce))get("ncclAllReduce");
+        api.Broadcast = (decltype(api.Broadcast))get("ncclBroadcast");
+        api.GroupStart = (decltype(api.GroupStart))get("ncclGroupStart");
+        api.GroupEnd = (decltype(api.GroupEnd))get("ncclGroupEnd");
+        api.GetErrorString = (decltype(api.GetErrorString))get("ncclGetErrorString");
+        api.h = h;
+    }
+    return api;
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess)
+        fail(ATK_NCCL_ERROR, std::string(what) + ": " + nccl().GetErrorString(r));
+}
+
+}  // namespace
+
+struct Comm {
+    ncclComm_t comm = nullptr;
+    int rank = 0, world = 1;
+};
+
+void nccl_unique_id(void* out128) {
+    ncclUniqueId id;
+    nccl_check(nccl().GetUniqueId(&id), "ncclGetUniqueId");
+    std::memcpy(out128, &id, sizeof(id));
+}
+
+void comm_init(atk_ctx* ctx, const void* unique_id, int rank, int world) {
+    if (world < 1 || rank < 0 || rank >= world) fail(ATK_INVALID_ARGUMENT, "bad rank/world");
+    comm_destroy(ctx);
+    auto* c = new Comm();
+    c->rank = rank;
+    c->world = world;
+    ncclUniqueId id;
+    std::memcpy(&id, unique_id, sizeof(id));
+    ATK_CUDA(cudaSetDevice(ctx->device));
+    nccl_check(nccl().CommInitRank(&c->comm, world, id, rank), "ncclCommInitRank");
+    ctx->comm = c;
+}
+
+void comm_destroy(atk_ctx* ctx) {
+    if (!ctx->comm) return;
+    if (ctx->comm->comm) nccl().CommDestroy(ctx->comm->comm);
+    delete ctx->comm;
+    ctx->comm = nullptr;
+}
+
+void allreduce_sum(atk_ctx* ctx, double* buf, uint64_t count, double* comm_ms) {
+    if (!ctx->comm || ctx->comm->world == 1) return;
+    StageTimer t(ctx);
+    t.start();
+    nccl_check(nccl().AllReduce(buf, buf, count, ncclFloat64, ncclSum, ctx->comm->comm, ctx->stream),
+               "ncclAllReduce");
+    const double ms = t.stop_ms();
+    if (comm_ms) *comm_ms += ms;
+}
+
+static std::vector<uint64_t> gather_last(atk_ctx* ctx, const atk_tensor* local) {
+    const int w = ctx->comm->world;
+    DevBuf<uint64_t> d(ctx, w);
+    ATK_CUDA(cudaMemsetAsync(d.get(), 0, w * sizeof(uint64_t), ctx->stream));
+    const uint64_t mine = local->dims[local->order - 1];
+    ATK_CUDA(cudaMemcpyAsync(d.get() + ctx->comm->rank, &mine, sizeof(uint64_t),
+                             cudaMemcpyHostToDevice, ctx->stream));
+    nccl_check(nccl().AllReduce(d.get(), d.get(), w, ncclUint64, ncclSum, ctx->comm->comm, ctx->stream),
+               "ncclAllReduce(sizes)");
+    std::vector<uint64_t> h(w);
+    ATK_CUDA(cudaMemcpyAsync(h.data(), d.get(), w * sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    ATK_CUDA(cudaStreamSynchronize(ctx->stream));
+    return h;
+}
+
+uint64_t comm_global_last(atk_ctx* ctx, const atk_tensor* local) {
+    if (!ctx->comm || ctx->comm->world == 1) return local->dims[local->order - 1];
+    uint64_t s = 0;
+    for (uint64_t v : gather_last(ctx, local)) s += v;
+    return s;
+}
+
+atk_tensor* allgather_last_mode(atk_ctx* ctx, const atk_tensor* local) {
+    const int order = local->order;
+    std::vector<uint64_t> sizes =
+        (ctx->comm && ctx->comm->world > 1) ? gather_last(ctx, local)
+                                            : std::vector<uint64_t>{local->dims[order - 1]};
+    uint64_t total = 0;
+    for (uint64_t v : sizes) total += v;
+    uint64_t dims[ATK_MAX_ORDER];
+    for (int m = 0; m < order; ++m) dims[m] = local->dims[m];
+    dims[order - 1] = total;
+    atk_tensor* out = new_tensor(ctx, local->dtype, order, dims);
+    const uint64_t slab = local->numel() / std::max<uint64_t>(1, local->dims[order - 1]);
+    if (!ctx->comm || ctx->comm->world == 1) {
+        ATK_CUDA(cudaMemcpyAsync(out->data, local->data, local->bytes(), cudaMemcpyDeviceToDevice,
+                                 ctx->stream));
+        return out;
+    }
+    const ncclDataType_t dt = local->dtype == ATK_F32 ? ncclFloat32 : ncclFloat64;
+    const size_t es = local->elem_bytes();
+    uint64_t off = 0;
+    nccl_check(nccl().GroupStart(), "ncclGroupStart");
+    for (int r = 0; r < ctx->comm->world; ++r) {
+        char* dst = static_cast<char*>(out->data) + off * slab * es;
+        const void* src = (r == ctx->comm->rank) ? local->data : dst;
+        nccl_check(nccl().Broadcast(src, dst, sizes[r] * slab, dt, r, ctx->comm->comm, ctx->stream),
+                   "ncclBroadcast");
+        off += sizes[r];
+    }
+    nccl_check(nccl().GroupEnd(), "ncclGroupEnd");
+    ATK_CUDA(cudaStreamSynchronize(ctx->stream));
+    return out;
+}
+
+}  // namespace atk

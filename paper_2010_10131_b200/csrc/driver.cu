@@ -1,0 +1,334 @@
+// driver.cu — the per-mode solvers (solvers.hpp) and the st-HOSVD mode loop
+// (sthosvd.hpp) orchestrated on the device.  Host code here only sequences
+// kernels, calls the selector hook and moves small results; every
+// contraction, factorisation and reduction runs in the CUDA kernels.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "atk_driver.cuh"
+
+namespace atk {
+
+// ------------------------------------------------------------------ contractions
+void contract_ttt(atk_ctx* ctx, const atk_tensor* x, const atk_tensor* y, int mode, double* z_dev,
+                  bool sym) {
+    const Split s = loop_split(x->dims, x->order, mode);
+    const uint64_t R = y->dims[mode];
+    if (s.P * s.O == 0 || s.I == 0 || R == 0) return;
+    if (!ctx->force_simt && tc_ttt_supported(ctx, x, y, mode, sym)) {
+        tc_ttt(ctx, x, y, mode, z_dev, sym);
+        return;
+    }
+    ttt_simt(ctx, x->data, y->data, x->dtype, s, R, z_dev, sym);
+}
+
+atk_tensor* contract_ttm(atk_ctx* ctx, const atk_tensor* x, const double* u_dev, uint64_t R,
+                         int mode) {
+    uint64_t od[ATK_MAX_ORDER];
+    for (int m = 0; m < x->order; ++m) od[m] = x->dims[m];
+    od[mode] = R;
+    atk_tensor* y = new_tensor(ctx, x->dtype, x->order, od);
+    const Split s = loop_split(x->dims, x->order, mode);
+    if (!ctx->force_simt && tc_ttm_supported(ctx, x, R, mode)) {
+        tc_ttm(ctx, x, u_dev, R, mode, y);
+    } else {
+        ttm_simt(ctx, x->data, x->dtype, s, u_dev, R, y->data);
+    }
+    return y;
+}
+
+uint64_t j_of(const atk_tensor* t, int mode) {
+    uint64_t j = 1;
+    for (int m = 0; m < t->order; ++m)
+        if (m != mode) j *= t->dims[m];
+    return j;
+}
+
+// solvers.hpp:35-41
+void check_truncation(const atk_tensor* y, int mode, uint64_t r) {
+    check_mode(y->order, mode);
+    if (r < 1 || r > y->dims[mode])
+        fail(ATK_RANK_EXCEEDS_DIM, "truncation " + std::to_string(r) + " invalid for mode " +
+                                       std::to_string(mode) + " of dimension " +
+                                       std::to_string(y->dims[mode]));
+}
+
+// ------------------------------------------------------------------ EIG / SVD
+// eig_mode_solver (solvers.hpp:64-73): gram -> sym_eig_top_r -> ttm(Y, U^T).
+ModeOut eig_mode(atk_ctx* ctx, const atk_tensor* y, int mode, uint64_t r, int solver_kind) {
+    check_truncation(y, mode, r);
+    const uint64_t I = y->dims[mode], J = j_of(y, mode);
+    if (solver_kind == ATK_SOLVER_SVD && r > std::min(I, J))
+        fail(ATK_RANK_TOO_LARGE, "truncation exceeds the rank bound of the unfolding");
+    ModeOut out;
+    out.solver = solver_kind;
+    StageTimer tm(ctx);
+    DevBuf<double> S(ctx, I * I);
+    tm.start();
+    contract_ttt(ctx, y, y, mode, S.get(), true);
+    record_gemm((long long)(I * I) * (long long)J);
+    if (ctx->comm) allreduce_sum(ctx, S.get(), I * I, &out.times.comm_ms);
+    out.times.gram_ms = tm.stop_ms();
+
+    DevBuf<double> vals(ctx, r), vecs(ctx, I * r), ut(ctx, I * r);
+    tm.start();
+    out.eig = sym_eig_top_r(ctx, S.get(), int(I), int(r), vals.get(), vecs.get());
+    out.times.eig_ms = tm.stop_ms();
+
+    tm.start();
+    transpose(ctx, vecs.get(), int(I), int(r), ut.get());  // U^T : r x I
+    out.shrunk = contract_ttm(ctx, y, ut.get(), r, mode);
+    record_gemm(2LL * (long long)(r * J) * (long long)I);
+    out.times.ttm_ms = tm.stop_ms();
+    out.factor.resize(I * r);
+    ATK_CUDA(cudaMemcpyAsync(out.factor.data(), vecs.get(), I * r * sizeof(double),
+                             cudaMemcpyDeviceToHost, ctx->stream));
+    ATK_CUDA(cudaStreamSynchronize(ctx->stream));
+    out.times.total_ms = out.times.gram_ms + out.times.eig_ms + out.times.ttm_ms;
+    return out;
+}
+
+// ------------------------------------------------------------------ ALS
+// spd_solve(A, I) (linalg.hpp:169-177) on the device: returns A^{-1}.
+static void spd_inverse(atk_ctx* ctx, const double* a, int n, double* inv) {
+    DevBuf<double> l(ctx, size_t(n) * n);
+    DevBuf<int> info(ctx, 1);
+    ATK_CUDA(cudaMemcpyAsync(l.get(), a, size_t(n) * n * sizeof(double), cudaMemcpyDeviceToDevice,
+                             ctx->stream));
+    cholesky(ctx, l.get(), n, info.get());
+    int h = 0;
+    ATK_CUDA(cudaMemcpyAsync(&h, info.get(), sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    ATK_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (h != 0) fail(ATK_NOT_SPD, "Cholesky factorization hit a non-positive pivot");
+    set_identity(ctx, inv, n);
+    cholesky_solve(ctx, l.get(), n, inv, n);
+}
+
+std::vector<double> als_initial_guess(uint64_t rows, uint64_t r, uint64_t seed, uint64_t mode) {
+    // solvers.hpp:125-128 — same libstdc++ engine + distribution as the reference.
+    std::vector<double> l0(rows * r);
+    std::mt19937_64 rng(mix_seed(seed, mode));
+    std::normal_distribution<double> gauss(0.0, 1.0);
+    for (auto& v : l0) v = gauss(rng);
+    return l0;
+}
+
+// als_iterate (solvers.hpp:88-118).  L stays on the device; rfac is returned.
+AlsOut als_iterate(atk_ctx* ctx, const atk_tensor* y, int mode, const double* l0_host, uint64_t r,
+                   const atk_als_opts& opts) {
+    check_mode(y->order, mode);
+    if (opts.num_iters < 1) fail(ATK_ERROR, "num_iters must be at least 1");
+    const uint64_t I = y->dims[mode], J = j_of(y, mode);
+    AlsOut out;
+    DevBuf<double> L(ctx, I * r), Lt(ctx, I * r), GL(ctx, r * r), GLi(ctx, r * r), YR(ctx, I * r),
+        GR(ctx, r * r), GRi(ctx, r * r), nxt(ctx, I * r);
+    ATK_CUDA(cudaMemcpyAsync(L.get(), l0_host, I * r * sizeof(double), cudaMemcpyHostToDevice,
+                             ctx->stream));
+    for (int k = 0; k < opts.num_iters; ++k) {
+        transpose(ctx, L.get(), int(I), int(r), Lt.get());
+        atk_tensor* w = contract_ttm(ctx, y, Lt.get(), r, mode);  // W = Y x_n L^T
+        record_gemm(2LL * (long long)(r * J) * (long long)I);
+        dgemm(ctx, true, false, int(r), int(r), int(I), 1.0, L.get(), int(I), L.get(), int(I), 0.0,
+              GL.get(), int(r));
+        record_gemm(2LL * (long long)(r * r) * (long long)I);
+        spd_inverse(ctx, GL.get(), int(r), GLi.get());
+        if (out.rfac) atk_tensor_free(out.rfac);
+        out.rfac = contract_ttm(ctx, w, GLi.get(), r, mode);  // rfac = W x_n (L^T L)^{-1}
+        record_gemm(2LL * (long long)(r * J) * (long long)r);
+        atk_tensor_free(w);
+        if (ctx->comm) fail(ATK_UNSUPPORTED, "ALS under a multi-GPU communicator is not wired yet");
+        contract_ttt(ctx, y, out.rfac, mode, YR.get(), false);  // YR = Y_(n) rfac_(n)^T
+        record_gemm(2LL * (long long)(I * r) * (long long)J);
+        contract_ttt(ctx, out.rfac, out.rfac, mode, GR.get(), false);
+        record_gemm(2LL * (long long)(r * r) * (long long)J);
+        spd_inverse(ctx, GR.get(), int(r), GRi.get());
+        dgemm(ctx, false, false, int(I), int(r), int(r), 1.0, YR.get(), int(I), GRi.get(), int(r),
+              0.0, nxt.get(), int(I));
+        record_gemm(2LL * (long long)(I * r) * (long long)r);
+        out.iterations_run = k + 1;
+        double change = 0.0;
+        if (opts.rel_tol > 0.0) {
+            const double diff = diff_norm2_sq(ctx, nxt.get(), L.get(), ATK_F64, I * r);
+            const double base = norm2_sq(ctx, L.get(), ATK_F64, I * r);
+            change = base > 0.0 ? std::sqrt(diff / base) : 0.0;
+        }
+        std::swap(L, nxt);
+        if (opts.rel_tol > 0.0 && change <= opts.rel_tol) break;
+    }
+    out.l.resize(I * r);
+    ATK_CUDA(cudaMemcpyAsync(out.l.data(), L.get(), I * r * sizeof(double), cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    ATK_CUDA(cudaStreamSynchronize(ctx->stream));
+    return out;
+}
+
+// thin_qr (linalg.hpp:126-149) on the device, host in/out.
+void thin_qr_dev(atk_ctx* ctx, const double* a_dev, uint64_t rows, uint64_t cols, double* q_dev,
+                 double* r_dev, double fro_a) {
+    if (rows < cols) fail(ATK_SHAPE_MISMATCH, "thin_qr expects rows >= cols");
+    householder_qr(ctx, a_dev, int(rows), int(cols), q_dev, r_dev);
+    std::vector<double> rh(cols * cols);
+    ATK_CUDA(cudaMemcpyAsync(rh.data(), r_dev, cols * cols * sizeof(double), cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    ATK_CUDA(cudaStreamSynchronize(ctx->stream));
+    const double floor = 1e-12 * fro_a;
+    for (uint64_t k = 0; k < cols; ++k)
+        if (std::fabs(rh[k + cols * k]) < floor)
+            fail(ATK_RANK_DEFICIENT, "QR diagonal " + std::to_string(k) + " below tolerance");
+}
+
+// als_mode_solver (solvers.hpp:122-138).
+ModeOut als_mode(atk_ctx* ctx, const atk_tensor* y, int mode, uint64_t r, const atk_als_opts& opts,
+                 const double* l0_host) {
+    check_truncation(y, mode, r);
+    const uint64_t I = y->dims[mode], J = j_of(y, mode);
+    std::vector<double> seeded;
+    if (!l0_host) {
+        seeded = als_initial_guess(I, r, opts.seed, uint64_t(mode));
+        l0_host = seeded.data();
+    }
+    ModeOut out;
+    out.solver = ATK_SOLVER_ALS;
+    StageTimer tm(ctx);
+    tm.start();
+    AlsOut it = als_iterate(ctx, y, mode, l0_host, r, opts);
+    DevBuf<double> L(ctx, I * r), Q(ctx, I * r), Rm(ctx, r * r);
+    ATK_CUDA(cudaMemcpyAsync(L.get(), it.l.data(), I * r * sizeof(double), cudaMemcpyHostToDevice,
+                             ctx->stream));
+    double fro = 0.0;
+    for (double v : it.l) fro += v * v;
+    thin_qr_dev(ctx, L.get(), I, r, Q.get(), Rm.get(), std::sqrt(fro));
+    out.shrunk = contract_ttm(ctx, it.rfac, Rm.get(), r, mode);  // shrunk = rfac x_n R
+    record_gemm(2LL * (long long)(r * J) * (long long)r);
+    atk_tensor_free(it.rfac);
+    out.factor.resize(I * r);
+    ATK_CUDA(cudaMemcpyAsync(out.factor.data(), Q.get(), I * r * sizeof(double),
+                             cudaMemcpyDeviceToHost, ctx->stream));
+    ATK_CUDA(cudaStreamSynchronize(ctx->stream));
+    out.times.als_ms = tm.stop_ms();
+    out.times.total_ms = out.times.als_ms;
+    out.iterations = it.iterations_run;
+    return out;
+}
+
+// ------------------------------------------------------------------ st-HOSVD
+static double seconds_since(std::chrono::steady_clock::time_point t0) {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+// sthosvd (sthosvd.hpp:126-194).  The input is never copied: mode 0 reads x
+// directly and every later mode reads the previous shrunk tensor.
+atk_tensor* sthosvd(atk_ctx* ctx, const atk_tensor* x, const uint64_t* ranks, atk_selector_fn decide,
+                    void* user, const atk_als_opts& opts, double* factors_out,
+                    atk_mode_report* reports) {
+    check_tensor(x, "sthosvd input");
+    const int order = x->order;
+    for (int n = 0; n < order; ++n)
+        if (ranks[n] < 1 || ranks[n] > x->dims[n])
+            fail(ATK_RANK_EXCEEDS_DIM, "truncation " + std::to_string(ranks[n]) +
+                                           " invalid for mode " + std::to_string(n) +
+                                           " of dimension " + std::to_string(x->dims[n]));
+    const atk_tensor* work = x;
+    atk_tensor* owned = nullptr;
+    size_t foff = 0;
+    try {
+        for (int n = 0; n < order; ++n) {
+            if (ctx->comm && n == order - 1) {
+                // the shard mode: gather the (small) shrunk tensor, finish replicated
+                atk_tensor* full = allgather_last_mode(ctx, work);
+                if (owned) atk_tensor_free(owned);
+                owned = full;
+                work = full;
+            }
+            const uint64_t I = work->dims[n], r = ranks[n];
+            uint64_t J = j_of(work, n);
+            if (ctx->comm && n < order - 1) J = J / work->dims[order - 1] * comm_global_last(ctx, work);
+            atk_mode_report rep{};
+            rep.mode = n;
+            for (int m = 0; m < order; ++m) rep.dims_before[m] = work->dims[m];
+            rep.predicted_cost_eig = cost_eig(double(I), double(r), double(J));
+            rep.predicted_cost_als = cost_als(double(I), double(r), double(J), opts.num_iters);
+            const auto td = std::chrono::steady_clock::now();
+            const int choice = decide ? decide(user, n, I, r, J) : ATK_SOLVER_EIG;
+            rep.selector_decision_time = seconds_since(td);
+            if (choice < 0 || choice > 2) fail(ATK_INVALID_ARGUMENT, "selector callback failed");
+            const auto ts = std::chrono::steady_clock::now();
+            ModeOut mo;
+            try {
+                if (choice == ATK_SOLVER_ALS)
+                    mo = als_mode(ctx, work, n, r, opts, nullptr);
+                else
+                    mo = eig_mode(ctx, work, n, r, choice);
+            } catch (const Error& e) {
+                // sthosvd.hpp:177-183: NotSPD / NoConvergence keep their type,
+                // every other library error becomes a plain Error, all prefixed.
+                atk_status code = e.code;
+                if (code != ATK_NOT_SPD && code != ATK_NO_CONVERGENCE && code != ATK_CUDA_ERROR &&
+                    code != ATK_OOM && code != ATK_NCCL_ERROR)
+                    code = ATK_ERROR;
+                fail(code, "mode " + std::to_string(n + 1) + ": " + e.what());
+            }
+            rep.solver_time = seconds_since(ts);
+            rep.solver_used = mo.solver;
+            rep.iterations_run = mo.iterations;
+            rep.eig_method = mo.eig.method;
+            rep.times = mo.times;
+            std::copy(mo.factor.begin(), mo.factor.end(), factors_out + foff);
+            foff += mo.factor.size();
+            if (owned) atk_tensor_free(owned);
+            owned = mo.shrunk;
+            work = owned;
+            for (int m = 0; m < order; ++m) rep.dims_after[m] = work->dims[m];
+            if (reports) reports[n] = rep;
+        }
+    } catch (...) {
+        if (owned) atk_tensor_free(owned);
+        throw;
+    }
+    return owned;
+}
+
+// reconstruct (sthosvd.hpp:197-209)
+atk_tensor* reconstruct(atk_ctx* ctx, const atk_tensor* core, const double* factors,
+                        const uint64_t* odims) {
+    check_tensor(core, "core");
+    const int order = core->order;
+    atk_tensor* y = nullptr;
+    const atk_tensor* cur = core;
+    size_t off = 0;
+    for (int n = 0; n < order; ++n) {
+        const uint64_t In = odims[n], Rn = core->dims[n];
+        DevBuf<double> u(ctx, In * Rn);
+        ATK_CUDA(cudaMemcpyAsync(u.get(), factors + off, In * Rn * sizeof(double),
+                                 cudaMemcpyHostToDevice, ctx->stream));
+        off += In * Rn;
+        atk_tensor* nxt = contract_ttm(ctx, cur, u.get(), In, n);  // U_n is I_n x R_n ("R x I")
+        record_gemm(2LL * (long long)(In * j_of(cur, n)) * (long long)Rn);
+        if (y) atk_tensor_free(y);
+        y = nxt;
+        cur = y;
+    }
+    return y;
+}
+
+// relative_error (sthosvd.hpp:212-223)
+double relative_error(atk_ctx* ctx, const atk_tensor* x, const atk_tensor* core,
+                      const double* factors) {
+    const double nx2 = norm2_sq(ctx, x->data, x->dtype, x->numel());
+    if (nx2 == 0.0) fail(ATK_ZERO_NORM_INPUT, "relative error is undefined for a zero tensor");
+    atk_tensor* xh = reconstruct(ctx, core, factors, x->dims);
+    for (int m = 0; m < x->order; ++m)
+        if (xh->dims[m] != x->dims[m]) {
+            atk_tensor_free(xh);
+            fail(ATK_SHAPE_MISMATCH, "reconstruction shape differs from input");
+        }
+    const double d2 = diff_norm2_sq(ctx, xh->data, x->data, x->dtype, x->numel());
+    atk_tensor_free(xh);
+    return std::sqrt(d2) / std::sqrt(nx2);
+}
+
+}  // namespace atk
