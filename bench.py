@@ -1,0 +1,368 @@
+"""st-HOSVD benchmark (BASELINE.json metric): GFLOP/s of Gram + eig + TTM.
+
+python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--impl ours|reference]
+
+One step = one full st-HOSVD of the configured tensor (default C5: 2048^3
+fp32, ranks 64^3, EIG on every mode, canonical low-rank 64^3 core + 1e-2
+noise generated on the device).  Throughput is credited with the reference's
+algorithmic flop conventions (kernels.hpp:46,102; selector.hpp:36): per EIG
+mode Gram I^2 J + TTM 2 I R J + eig 9 I^3 (ALS modes:
+5(4IJR+4JR^2+4IR^2)+2JR^2, acceptance.cpp:253-254).
+
+value : device-resident throughput (input already in HBM, > L2 so no flush
+        needed), CUDA events on the engine stream, max over ranks.
+e2e   : the same through the host-buffer C-ABI entry atk_sthosvd_host: every
+        step copies the input from pinned host memory and the core back.
+roofline : dominant kernel = the mode-1 Gram (gram_tf32_kernel + its split-K
+        reduction), I^2 J flops per launch / its event-timed duration, against
+        half the measured bf16 peak (tf32 rate).
+cpu_baseline : the CPU oracle (oracle/, reference port) on a bounded sample of
+        the same workload (first 32 slabs of the last mode), all host cores.
+Multi-GPU (torchrun): the input is sharded along the last mode, one NCCL
+allreduce of the Gram partials per mode inside the engine.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    "c1": dict(dims=(200, 200, 200), ranks=(20, 20, 20), dtype="f64", strategy="eig", input="reference"),
+    "c2": dict(dims=(1024, 1024, 1024), ranks=(32, 32, 32), dtype="f32", strategy="manual:a,e,e",
+               input="uniform"),
+    "c3": dict(dims=(128, 128, 128, 128), ranks=(16, 16, 16, 16), dtype="f64", strategy="eig",
+               input="reference"),
+    "c4": dict(dims=(48,) * 5, ranks=(8,) * 5, dtype="f32", strategy="eig", input="uniform"),
+    "c5": dict(dims=(2048, 2048, 2048), ranks=(64, 64, 64), dtype="f32", strategy="eig", input="lowrank"),
+}
+SEEDS = {"c1": 1, "c2": 2, "c3": 3, "c4": 4, "c5": 5}
+
+
+def flops_of(dims, ranks, kinds, num_iters=5):
+    """Credited flops per mode following the reference conventions."""
+    work = list(dims)
+    out = []
+    for n, (r, k) in enumerate(zip(ranks, kinds)):
+        i = work[n]
+        j = int(np.prod(work)) // i
+        if k == 1:  # ALS
+            f = {"als": 5 * (4 * i * j * r + 4 * j * r * r + 4 * i * r * r) + 2 * j * r * r}
+        else:
+            f = {"gram": i * i * j, "ttm": 2 * i * r * j, "eig": 9 * i ** 3}
+        out.append(f)
+        work[n] = r
+    return out
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm": d["hbm_gbs"], "bf16": d["bf16_tflops"], "bf16_sus": d["bf16_tflops_sustained"],
+                "src": "measured"}
+    return {"hbm": 6650.0, "bf16": 1590.0, "bf16_sus": 1400.0, "src": "fallback"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [s.strip() for s in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[3 + k] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------- inputs
+def make_input(atucker, cfg, seed, ctx, shard=(0, 1)):
+    """Build this rank's slab [.., I_N lo:hi] of the configured input on the device."""
+    dims = list(cfg["dims"])
+    rank, world = shard
+    n_last = dims[-1]
+    lo, hi = n_last * rank // world, n_last * (rank + 1) // world
+    dt = np.float32 if cfg["dtype"] == "f32" else np.float64
+    if cfg["input"] == "reference":
+        sys.path.insert(0, str(ROOT / "oracle"))
+        import oracle as o  # the reference generator restated (random_tensor, tensor.hpp:246-258)
+
+        x = o.random_tensor(dims, seed, "normal")[..., lo:hi]
+        return atucker.DeviceTensor.from_numpy(np.asfortranarray(x.astype(dt)), ctx)
+    slab = dims[:-1] + [hi - lo]
+    slab_elems = int(np.prod(dims[:-1]))
+    if cfg["input"] == "uniform":
+        return atucker.DeviceTensor.uniform(slab, seed, dt, ctx, offset=lo * slab_elems)
+    # low-rank core (uniform) expanded through orthonormal factors + 1e-2 uniform noise
+    ranks = list(cfg["ranks"])
+    rng = np.random.default_rng(seed)
+    factors = [np.linalg.qr(rng.standard_normal((d, r)))[0] for d, r in zip(dims, ranks)]
+    factors[-1] = np.asfortranarray(factors[-1][lo:hi])
+    core = atucker.DeviceTensor.uniform(ranks, seed, dt, ctx)
+    x = atucker.reconstruct(atucker.TuckerDecomposition(core, factors, tuple(slab)), ctx=ctx)
+    core.free()
+    scale = float(np.sqrt(np.prod(dims) / np.prod(ranks)))
+    x.axpy(scale - 1.0, x)
+    noise = atucker.DeviceTensor.uniform(slab, seed + 1000, dt, ctx, offset=lo * slab_elems)
+    x.axpy(1e-2, noise)
+    noise.free()
+    return x
+
+
+# ---------------------------------------------------------------- reference arm / CPU baseline
+def cpu_sample(cfg, name, threads, budget_s=20.0):
+    """Oracle st-HOSVD on a bounded sample (leading slabs of the last mode)."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle as o
+    from paper_2010_10131_b200.selector import CostModelParams, Strategy
+
+    o.load()
+    o.set_threads(threads)
+    dims, ranks = list(cfg["dims"]), list(cfg["ranks"])
+    slab = int(np.prod(dims[:-1]))
+    target_elems = 2 * 10 ** 8 if name in ("c5", "c2") else int(np.prod(dims))
+    nl = max(1, min(dims[-1], target_elems // slab))
+    sdims = dims[:-1] + [nl]
+    sranks = ranks[:-1] + [min(ranks[-1], nl)]
+    seed = SEEDS[name]
+    if cfg["input"] == "reference":
+        x = o.random_tensor(dims, seed, "normal")[..., :nl]
+    else:
+        x = o.hash_uniform(seed, int(np.prod(sdims))).astype(np.float64).reshape(sdims, order="F")
+    x = np.asfortranarray(x)
+    s = Strategy.parse(cfg["strategy"])
+    p = CostModelParams()
+    kinds = []
+
+    def decide(m, i, r, j):
+        k = int(s.decide(m, i, r, j, p))
+        kinds.append(k)
+        return k
+
+    o.reset_counters()
+    t0 = time.perf_counter()
+    o.sthosvd(x, sranks, decide)
+    dt = time.perf_counter() - t0
+    fl = sum(sum(f.values()) for f in flops_of(sdims, sranks, kinds))
+    return {"value": fl / dt / 1e9, "unit": "GFLOP/s", "cores": threads, "kind": "port",
+            "sample": f"st-HOSVD of the leading {nl} slabs: dims {sdims} ranks {sranks} "
+                      f"({cfg['strategy']}), fp64 OpenBLAS, {dt:.2f} s",
+            "seconds": dt, "stage_s": o.stage_times()}
+
+
+def run_reference(args, cfg, name):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    vals = []
+    for step in range(args.warmup + args.steps):
+        r = cpu_sample(cfg, name, threads)
+        if step >= args.warmup:
+            vals.append(r)
+    v = float(np.median([r["value"] for r in vals]))
+    ms = float(np.median([r["seconds"] for r in vals])) * 1e3
+    line = {"metric": "st-HOSVD GFLOP/s (Gram+eig+TTM)", "value": v, "unit": "GFLOP/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": f"{name.upper()} sample on host CPU", "dims": cfg["dims"],
+                       "ranks": cfg["ranks"], "strategy": cfg["strategy"]},
+            "cpu_baseline": {k: vals[-1][k] for k in ("kind", "cores", "sample")} | {"value": v, "unit": "GFLOP/s"},
+            "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c5", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg, args.config)
+
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("gloo")
+    torch.cuda.set_device(local)
+    from paper_2010_10131_b200 import atucker
+    from paper_2010_10131_b200.selector import Strategy
+
+    ctx = atucker.Context(local)
+    if world > 1:
+        uid = atucker.Context.nccl_unique_id() if rank == 0 else bytes(128)
+        t = torch.tensor(list(uid), dtype=torch.uint8)
+        dist.broadcast(t, 0)
+        ctx.comm_init(bytes(t.tolist()), rank, world)
+    strategy = Strategy.parse(cfg["strategy"])
+    x = make_input(atucker, cfg, SEEDS[args.config], ctx, (rank, world))
+    gdims = tuple(cfg["dims"])
+
+    def barrier():
+        torch.cuda.synchronize()
+        ctx.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)  # engine launches on torch's current stream => events see it
+    for _ in range(args.warmup):
+        res = atucker.sthosvd(x, cfg["ranks"], strategy, ctx=ctx, global_dims=gdims)
+        res.decomposition.core.free()
+    barrier()
+    l0 = ctx.launch_count
+    reports = []
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            res = atucker.sthosvd(x, cfg["ranks"], strategy, ctx=ctx, global_dims=gdims)
+            reports.append(res.reports)
+            res.decomposition.core.free()
+        ev1.record(stream)
+        barrier()
+    launches = (ctx.launch_count - l0) // max(1, args.steps)
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    kinds = [int(r.solver_used) for r in reports[-1]]
+    fl = flops_of(gdims, cfg["ranks"], kinds)
+    total_flops = sum(sum(f.values()) for f in fl)
+    value = total_flops / (ms * 1e-3) / 1e9
+
+    # per-stage (last step, device events inside the engine)
+    stages = []
+    for rp, f in zip(reports[-1], fl):
+        t = rp.times
+        stages.append({"mode": rp.mode, "solver": str(rp.solver_used), "eig_method": rp.eig_method,
+                       "gram_ms": round(t.gram_ms, 3), "eig_ms": round(t.eig_ms, 3), "ttm_ms": round(t.ttm_ms, 3),
+                       "als_ms": round(t.als_ms, 3), "comm_ms": round(t.comm_ms, 3),
+                       "gram_tflops": round(f.get("gram", 0) / max(t.gram_ms, 1e-9) / 1e9, 1),
+                       "ttm_gbs": round(4 * (np.prod(rp.dims_before) + np.prod(rp.dims_after)) /
+                                        max(t.ttm_ms, 1e-9) / 1e6, 1)})
+    pk = peaks()
+    tf32_peak = pk["bf16_sus"] / 2.0
+    g0 = reports[-1][0]
+    gram_flops = fl[0].get("gram", 0)
+    achieved = gram_flops / (g0.times.gram_ms * 1e-3) / 1e12 if g0.times.gram_ms > 0 else None
+    traffic = None
+    prof = ROOT / "profiles" / "gram_traffic.json"
+    if prof.exists():
+        traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+    roofline = {"kernel": "gram_tf32_kernel (+gram_reduce), mode 1",
+                "bound": "tensor", "achieved": achieved, "peak": tf32_peak, "unit": "TFLOP/s",
+                "frac": (achieved / tf32_peak) if achieved else None, "traffic": traffic,
+                "peak_note": f"tf32 = 1/2 of the {pk['src']} sustained bf16 {pk['bf16_sus']} TF/s",
+                "algorithmic_flops_per_launch": gram_flops}
+
+    # e2e through the host-buffer C ABI (pinned host input, core back)
+    e2e = None
+    if world == 1 and args.e2e_steps > 0:
+        xh = torch.empty(int(np.prod(gdims)), dtype=torch.float32 if cfg["dtype"] == "f32" else torch.float64,
+                         pin_memory=True)
+        xnp = xh.numpy()
+        ctx.synchronize()
+        src = x.to_numpy()
+        xnp[:] = src.ravel(order="F")
+        del src
+        xview = xnp.reshape(gdims, order="F")
+        atucker.sthosvd_host(xview, cfg["ranks"], strategy, ctx=ctx)  # warm
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            r2 = atucker.sthosvd_host(xview, cfg["ranks"], strategy, ctx=ctx)
+        barrier()
+        e2e_ms = (time.perf_counter() - t0) * 1e3 / args.e2e_steps
+        e2e = {"value": total_flops / (e2e_ms * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": int(xnp.nbytes), "d2h_bytes_per_step": int(r2.decomposition.core.nbytes +
+                                                                                 sum(f.nbytes for f in r2.decomposition.factors))}
+        del xh, xnp, xview
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_sample(cfg, args.config, os.cpu_count() or 1)
+        cpu.pop("stage_s", None)
+        cpu.pop("seconds", None)
+
+    if rank == 0:
+        line = {"metric": "st-HOSVD GFLOP/s (Gram+eig+TTM)", "value": value, "unit": "GFLOP/s",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+                "higher_is_better": True, "scaling": "weak" if world > 1 else "strong", "vs_baseline": None,
+                "dtype": "tf32" if cfg["dtype"] == "f32" else "f64", "data": "synthetic",
+                "config": {"workload": f"{args.config.upper()} {'x'.join(map(str, gdims))} {cfg['dtype']} "
+                                       f"ranks {'x'.join(map(str, cfg['ranks']))} {cfg['strategy']} "
+                                       f"input={cfg['input']}",
+                           "l2": "input larger than L2 (no flush needed)" if np.prod(gdims) * 4 > 126e6
+                           else "input fits L2",
+                           "parallelism": f"shard last mode x{world}" if world > 1 else "single GPU",
+                           "flops_per_step": total_flops},
+                "stages": stages, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": int(launches), "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

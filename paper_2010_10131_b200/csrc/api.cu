@@ -180,6 +180,8 @@ atk_status atk_ctx_set_option(atk_ctx* ctx, const char* key, double value) {
         if (k == "simt") ctx->force_simt = value != 0.0;
         else if (k == "eig_method") ctx->eig_method = int(value);
         else if (k == "chfsi_tol") ctx->chfsi_tol = value;
+        else if (k == "tma_tf32") ctx->tma_tf32 = value != 0.0;
+        else if (k == "gram_chunk_kb") ctx->gram_chunk_kb = int(value);
         else fail(ATK_INVALID_ARGUMENT, "unknown option: " + k);
     });
 }

@@ -56,6 +56,9 @@ struct atk_ctx {
     int force_simt = 0;        // option "simt": portable CUDA-core contractions
     int eig_method = -1;       // option "eig_method": -1 auto, 0 dense Jacobi, 1 ChFSI
     double chfsi_tol = 1e-12;  // option "chfsi_tol": relative Ritz residual target
+    int tma_tf32 = 1;          // option "tma_tf32": TMA converts fp32 -> tf32 with round-to-nearest
+                               // (the MMA itself truncates: measured 6e-4 bias vs 1e-6, test_gpu_tc.py)
+    int gram_chunk_kb = 0;     // option "gram_chunk_kb": K-blocks per fp64 drain (0 = default)
     atk::Comm* comm = nullptr;
     cudaEvent_t ev[8] = {};
 };

@@ -326,6 +326,12 @@ double relative_error(atk_ctx* ctx, const atk_tensor* x, const atk_tensor* core,
             atk_tensor_free(xh);
             fail(ATK_SHAPE_MISMATCH, "reconstruction shape differs from input");
         }
+    if (xh->dtype != x->dtype) {  // e.g. fp32 core against an fp64 copy of the input
+        atk_tensor* cv = new_tensor(ctx, x->dtype, x->order, x->dims);
+        convert(ctx, cv->data, x->dtype, xh->data, xh->dtype, x->numel());
+        atk_tensor_free(xh);
+        xh = cv;
+    }
     const double d2 = diff_norm2_sq(ctx, xh->data, x->data, x->dtype, x->numel());
     atk_tensor_free(xh);
     return std::sqrt(d2) / std::sqrt(nx2);

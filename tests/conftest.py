@@ -50,8 +50,10 @@ def principal_angle(a, b) -> float:
     """oracles.hpp:108-114 — largest principal angle between column spaces."""
     qa, _ = np.linalg.qr(a)
     qb, _ = np.linalg.qr(b)
-    s = np.linalg.svd(qa.T @ qb, compute_uv=False)
-    return float(np.arccos(min(1.0, s.min())))
+    # sine form ||(I - Qa Qa^T) Qb||_2 resolves angles down to ~1e-16 (arccos of the
+    # cosine cannot resolve below ~1e-8)
+    s = np.linalg.svd(qb - qa @ (qa.T @ qb), compute_uv=False)
+    return float(np.arcsin(min(1.0, s.max())))
 
 
 def orthonormality_defect(m) -> float:

@@ -1,0 +1,92 @@
+"""tcgen05 (kind::tf32) Gram kernel vs the fp64 oracle, all operand layouts.
+
+tf32 keeps 10 mantissa bits, so the Gram is compared with a relative bound
+of 4e-3 on max|dS| / max|S| (exactly symmetric output is still required).  The
+test also records which tf32 conversion the hardware applies (truncation vs
+round-to-nearest) by comparing against both emulations in fp64.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def tf32_trunc(x):
+    b = np.asarray(x, dtype=np.float32).view(np.uint32) & np.uint32(0xFFFFE000)
+    return b.view(np.float32).astype(np.float64)
+
+
+def tf32_rn(x):
+    u = np.asarray(x, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    u = ((u + 0x1000) & 0xFFFFE000).astype(np.uint32)
+    return u.view(np.float32).astype(np.float64)
+
+
+def gram_np(x, n):
+    m = np.moveaxis(x, n, 0).reshape(x.shape[n], -1, order="F")
+    return m @ m.T
+
+
+@pytest.mark.parametrize("dims,mode", [
+    ((256, 1000), 0), ((300, 64, 7), 0), ((1024, 2048), 0), ((128, 4096), 0),   # MN-major (mode 0)
+    ((32, 256, 40), 1), ((64, 512, 9), 1), ((4096, 300), 1), ((96, 200, 5), 1),  # K-major (P >= 32)
+])
+@pytest.mark.parametrize("tma_tf32", [0, 1])
+def test_tc_gram_vs_oracle(dims, mode, tma_tf32, capsys):
+    from paper_2010_10131_b200 import atucker
+
+    ctx = atucker.Context.default(0)
+    ctx.set_option("tma_tf32", tma_tf32)
+    xd = atucker.DeviceTensor.uniform(list(dims), 11, np.float32)
+    x = xd.to_numpy()
+    launches = ctx.launch_count
+    s = atucker.gram(xd, mode)
+    assert ctx.launch_count - launches == 2  # gram_tf32_kernel + gram_reduce
+    ref = gram_np(x.astype(np.float64), mode)
+    scale = np.abs(ref).max()
+    err = np.abs(s - ref).max() / scale
+    assert np.array_equal(s, s.T)
+    assert err <= 4e-3, err
+    et = np.abs(s - gram_np(tf32_trunc(x), mode)).max() / scale
+    er = np.abs(s - gram_np(tf32_rn(x), mode)).max() / scale
+    d = np.diag(s) / np.diag(ref) - 1.0
+    with capsys.disabled():
+        print(f"\nTF32MODE dims={dims} mode={mode} tma_tf32={tma_tf32} err={err:.2e} "
+              f"vs_trunc={et:.2e} vs_rn={er:.2e} diag_bias={d.mean():+.2e}")
+    ctx.set_option("tma_tf32", 0)
+
+
+def test_tc_gram_long_k_chunked():
+    """Long K (fp32 chains bounded by the fp64 drains): diagonal bias stays small."""
+    from paper_2010_10131_b200 import atucker
+
+    ctx = atucker.Context.default(0)
+    xd = atucker.DeviceTensor.uniform([128, 1 << 20], 3, np.float32)
+    x = xd.to_numpy().astype(np.float64)
+    s = atucker.gram(xd, 0)
+    ref = x @ x.T
+    err = np.abs(s - ref).max() / np.abs(ref).max()
+    assert err <= 4e-3
+
+
+@pytest.mark.parametrize("dims,mode,r", [
+    ((256, 1000), 0, 64), ((300, 64, 7), 0, 20), ((2048, 777), 0, 128), ((96, 40, 3), 0, 33),  # K-major A
+    ((64, 256, 9), 1, 64), ((32, 128, 5), 1, 32), ((4096, 96), 1, 16), ((64, 64, 64), 2, 64),  # MN-major A
+])
+def test_tc_ttm_vs_oracle(dims, mode, r, capsys):
+    from paper_2010_10131_b200 import atucker
+
+    ctx = atucker.Context.default(0)
+    xd = atucker.DeviceTensor.uniform(list(dims), 13, np.float32)
+    x = xd.to_numpy().astype(np.float64)
+    rng = np.random.default_rng(5)
+    u = np.linalg.qr(rng.standard_normal((dims[mode], r)))[0].T.copy(order="F")  # R x I, orthonormal rows
+    launches = ctx.launch_count
+    y = atucker.ttm(xd, u, mode).to_numpy().astype(np.float64)
+    n_launch = ctx.launch_count - launches
+    ref = np.moveaxis(np.tensordot(u, x, axes=([1], [mode])), 0, mode)
+    err = np.abs(y - ref).max() / np.abs(ref).max()
+    nrm = abs(np.linalg.norm(y) - np.linalg.norm(ref)) / np.linalg.norm(ref)
+    with capsys.disabled():
+        print(f"\nTTM dims={dims} mode={mode} r={r} launches={n_launch} maxrel={err:.2e} normrel={nrm:.2e}")
+    assert err <= 4e-3 and nrm <= 1e-4
