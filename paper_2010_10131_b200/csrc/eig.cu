@@ -13,7 +13,10 @@
 // gapped.  Spectrum bounds for the filter come from an m-step Lanczos run
 // (device), its tridiagonal solved by the same Jacobi kernel.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "atk_internal.cuh"
@@ -196,16 +199,30 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
         T(ctx, size_t(k) * k), Z(ctx, size_t(k) * k), theta(ctx, k), Rm(ctx, size_t(k) * k),
         res(ctx, k);
     DevBuf<int> sweeps(ctx, 1);
+    static const bool trace = std::getenv("ATK_TRACE") != nullptr;
+    auto t_last = std::chrono::steady_clock::now();
+    auto mark = [&](const char* what, int a = -1, double v = 0.0) {
+        if (!trace) return;
+        cudaStreamSynchronize(st);
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[atk eig n=%d r=%d k=%d] %-10s %8.3f ms  %d %.3e\n", n, r, k, what,
+                     std::chrono::duration<double, std::milli>(now - t_last).count(), a, v);
+        t_last = now;
+    };
     ATK_CUDA(cudaMemcpyAsync(S.get(), s_dev, nn * sizeof(double), cudaMemcpyDeviceToDevice, st));
     symmetrize(ctx, S.get(), n);
+    mark("prep");
     const Bounds b = lanczos_bounds(ctx, S.get(), n);
+    mark("lanczos", 0, b.lo);
 
     // random orthonormal start
     fill_normalish<<<nblk(nk), 256, 0, st>>>(Ya.get(), nk, 0xc0ffee11ULL);
     ATK_LAUNCHED(ctx);
     householder_qr(ctx, Ya.get(), n, k, V.get(), Rm.get());
+    mark("qr0");
     rayleigh_ritz(ctx, S.get(), n, k, V.get(), W.get(), T.get(), Z.get(), theta.get(), Ya.get(),
                   sweeps.get());
+    mark("rr0");
 
     const int max_outer = 100;
     std::vector<double> hth(k), hres(r);
@@ -249,10 +266,14 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
             ycur = ynext;
             ynext = spare;
         }
+        mark("filter", degree, worst / scale);
         householder_qr(ctx, ycur, n, k, V.get(), Rm.get());
+        mark("qr");
         rayleigh_ritz(ctx, S.get(), n, k, V.get(), W.get(), T.get(), Z.get(), theta.get(),
                       ynext == V.get() ? Yc.get() : ynext, sweeps.get());
+        mark("rr", it);
     }
+    mark("done", it, worst / scale);
     ATK_CUDA(cudaMemcpyAsync(values_dev, theta.get(), r * sizeof(double), cudaMemcpyDeviceToDevice, st));
     ATK_CUDA(cudaMemcpyAsync(vectors_dev, V.get(), size_t(n) * r * sizeof(double),
                              cudaMemcpyDeviceToDevice, st));
