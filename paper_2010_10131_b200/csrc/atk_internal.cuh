@@ -192,7 +192,9 @@ struct EigInfo {
     int iterations = 0;  // ChFSI outer iterations
     double residual = 0;
 };
+// `psd`: the caller guarantees S is positive semidefinite (a Gram), which
+// clamps the filter's lower spectrum bound at 0.  `tol` <= 0: ctx->chfsi_tol.
 EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* values_dev,
-                      double* vectors_dev);
+                      double* vectors_dev, bool psd = false, double tol = 0.0);
 
 }  // namespace atk

@@ -20,62 +20,6 @@
 namespace atk {
 namespace {
 
-// ------------------------------------------------------------------ GEMM
-constexpr int GT = 64, GK = 16, GNT = 256;
-
-__global__ void __launch_bounds__(GNT) dgemm_kernel(bool ta, bool tb, int m, int n, int k,
-                                                    double alpha, const double* __restrict__ a,
-                                                    int lda, const double* __restrict__ b, int ldb,
-                                                    double beta, double* __restrict__ c, int ldc) {
-    __shared__ double As[GK][GT + 1];
-    __shared__ double Bs[GK][GT + 1];
-    const int m0 = blockIdx.x * GT, n0 = blockIdx.y * GT;
-    const int tid = threadIdx.x, ty = tid / 16, tx = tid % 16;
-    double acc[4][4] = {};
-    for (int k0 = 0; k0 < k; k0 += GK) {
-        for (int e = tid; e < GK * GT; e += GNT) {
-            int kk, mm;
-            if (!ta) { mm = e % GT; kk = e / GT; } else { kk = e % GK; mm = e / GK; }
-            const int gm = m0 + mm, gk = k0 + kk;
-            double v = 0.0;
-            if (gm < m && gk < k) v = ta ? a[gk + size_t(lda) * gm] : a[gm + size_t(lda) * gk];
-            As[kk][mm] = v;
-        }
-        for (int e = tid; e < GK * GT; e += GNT) {
-            int kk, nn;
-            if (tb) { nn = e % GT; kk = e / GT; } else { kk = e % GK; nn = e / GK; }
-            const int gn = n0 + nn, gk = k0 + kk;
-            double v = 0.0;
-            if (gn < n && gk < k) v = tb ? b[gn + size_t(ldb) * gk] : b[gk + size_t(ldb) * gn];
-            Bs[kk][nn] = v;
-        }
-        __syncthreads();
-#pragma unroll
-        for (int kk = 0; kk < GK; ++kk) {
-            double av[4], bv[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) av[u] = As[kk][ty + 16 * u];
-#pragma unroll
-            for (int v = 0; v < 4; ++v) bv[v] = Bs[kk][tx + 16 * v];
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-#pragma unroll
-                for (int v = 0; v < 4; ++v) acc[u][v] = fma(av[u], bv[v], acc[u][v]);
-        }
-        __syncthreads();
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-            const int gm = m0 + ty + 16 * u, gn = n0 + tx + 16 * v;
-            if (gm < m && gn < n) {
-                double* cp = c + gm + size_t(ldc) * gn;
-                *cp = alpha * acc[u][v] + (beta == 0.0 ? 0.0 : beta * *cp);
-            }
-        }
-}
-
 // ------------------------------------------------------------------ Jacobi
 // Round-robin tournament: position k of round t holds player
 //   0                       if k == 0
@@ -99,9 +43,19 @@ __global__ void __launch_bounds__(kJacobiThreads) jacobi_kernel(const double* __
     double* V = A + size_t(ld) * n;
     double* cs = V + size_t(ld) * n;        // 2 * (N/2): c, s per pair
     int* pp = reinterpret_cast<int*>(cs + N);  // p, q per pair
+    uint16_t* tab = reinterpret_cast<uint16_t*>(pp + N);  // packed (a << 8 | b), b <= a
     __shared__ int rotated;
     __shared__ double red[33];
     const int tid = threadIdx.x, nt = blockDim.x;
+    {
+        const int np = N / 2;
+        for (int e = tid; e < np * (np + 1) / 2; e += nt) {
+            int a = int((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+            while ((a + 1) * (a + 2) / 2 <= e) ++a;
+            while (a * (a + 1) / 2 > e) --a;
+            tab[e] = uint16_t((a << 8) | (e - a * (a + 1) / 2));
+        }
+    }
 
     double fro = 0.0;
     for (int e = tid; e < n * n; e += nt) {
@@ -155,11 +109,7 @@ __global__ void __launch_bounds__(kJacobiThreads) jacobi_kernel(const double* __
             const int nblk = npairs * (npairs + 1) / 2;
             for (int e = tid; e < nblk + n * npairs; e += nt) {
                 if (e < nblk) {
-                    // decode (a, b) with a <= b from the packed upper index
-                    int a = int((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
-                    while ((a + 1) * (a + 2) / 2 <= e) ++a;
-                    while (a * (a + 1) / 2 > e) --a;
-                    const int b = e - a * (a + 1) / 2;  // b <= a
+                    const int a = tab[e] >> 8, b = tab[e] & 255;  // b <= a
                     const double ca = cs[2 * a], sa = cs[2 * a + 1];
                     const double cb = cs[2 * b], sb = cs[2 * b + 1];
                     if (sa == 0.0 && sb == 0.0) continue;
@@ -427,18 +377,11 @@ inline unsigned blocks_for(size_t n, int t) { return unsigned((n + t - 1) / t); 
 
 }  // namespace
 
-void dgemm(atk_ctx* ctx, bool ta, bool tb, int m, int n, int k, double alpha, const double* a,
-           int lda, const double* b, int ldb, double beta, double* c, int ldc) {
-    if (m <= 0 || n <= 0) return;
-    dim3 grid((m + GT - 1) / GT, (n + GT - 1) / GT);
-    dgemm_kernel<<<grid, GNT, 0, ctx->stream>>>(ta, tb, m, n, k, alpha, a, lda, b, ldb, beta, c, ldc);
-    ATK_LAUNCHED(ctx);
-}
-
 size_t jacobi_smem_bytes(int n) {
     const int N = n + (n & 1);
+    const int np = N / 2;
     return size_t(2) * (n + 1) * n * sizeof(double) + size_t(N) * sizeof(double) +
-           size_t(N) * sizeof(int) + 64;
+           size_t(N) * sizeof(int) + size_t(np) * (np + 1) / 2 * sizeof(uint16_t) + 64;
 }
 
 void jacobi_eig(atk_ctx* ctx, const double* a, int n, int lda, double* values, double* vectors,

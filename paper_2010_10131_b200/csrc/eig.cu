@@ -3,15 +3,22 @@
 // The reference computes ALL eigenpairs with Eigen's SelfAdjointEigenSolver
 // and keeps the top r.  On the device:
 //   n <= kJacobiMax : dense one-CTA Jacobi (dense.cu), all pairs, keep top r.
-//   n  > kJacobiMax : Chebyshev-filtered subspace iteration (ChFSI) on a
-//                     block of k = min(n, max(r+16, 3r/2)) vectors with a
-//                     Rayleigh-Ritz step solved by the dense Jacobi, run until
-//                     every wanted Ritz pair has relative residual
-//                     ||S v - theta v|| <= tol * max|spectrum| (fp64).
-// Both paths finish with descending order + fix_signs (linalg.hpp:34-50), so
-// factors are comparable entry-wise with the reference when the spectrum is
-// gapped.  Spectrum bounds for the filter come from an m-step Lanczos run
-// (device), its tridiagonal solved by the same Jacobi kernel.
+//   n  > kJacobiMax : Chebyshev-filtered subspace iteration (ChFSI) on a block
+//                     of k = min(n, max(r+16, 3r/2)) vectors:
+//                       bounds  : one cooperative-kernel Lanczos run (m = 64
+//                                 steps, 2 grid barriers per step) + its
+//                                 tridiagonal solved by the Jacobi kernel;
+//                       filter  : T_d on [lo, cut] (scaled recurrence, fp64
+//                                 split-K DGEMMs);
+//                       orthonormalisation : SVQB twice (Gram -> Jacobi ->
+//                                 V D Z Theta^-1/2), robust to the rank loss a
+//                                 strong filter produces;
+//                       Rayleigh-Ritz : Jacobi on V^T S V;
+//                     until every wanted Ritz pair has relative residual
+//                     ||S v - theta v|| <= tol * max|theta| (tol 1e-12 for fp64
+//                     data, 1e-10 for tf32-computed Grams).
+// Both paths finish with descending order + fix_signs (linalg.hpp:34-50) so
+// factors compare entry-wise with the reference on gapped spectra.
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -24,54 +31,122 @@
 namespace atk {
 namespace {
 
-__global__ void lanczos_step(const double* __restrict__ sq, double* __restrict__ q,
-                             double* __restrict__ qprev, int n, int j, double* __restrict__ alpha,
-                             double* __restrict__ beta) {
-    // q holds q_j, sq = S q_j.  w = sq - beta_{j-1} q_{j-1} - alpha_j q_j,
-    // beta_j = ||w||, q_{j-1} <- q_j, q_j <- w / beta_j.
-    __shared__ double red[33];
-    const int tid = threadIdx.x, nt = blockDim.x;
-    const double bprev = j > 0 ? beta[j - 1] : 0.0;
-    double d = 0.0;
-    for (int i = tid; i < n; i += nt) d += sq[i] * q[i];
-    for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-    if ((tid & 31) == 0) red[tid >> 5] = d;
+inline unsigned nblk(size_t n) { return unsigned(std::min<size_t>((n + 255) / 256, 4096)); }
+
+// ------------------------------------------------------------------ grid barrier
+__device__ __forceinline__ void grid_sync(unsigned* count, unsigned* gen, unsigned nblocks) {
     __syncthreads();
-    if (tid == 0) {
-        double t = 0;
-        for (int w = 0; w < (nt >> 5); ++w) t += red[w];
-        red[32] = t;
+    if (threadIdx.x == 0) {
+        volatile unsigned* vg = gen;
+        const unsigned g = *vg;
+        __threadfence();
+        if (atomicAdd(count, 1u) == nblocks - 1) {
+            *count = 0;
+            __threadfence();
+            atomicAdd(gen, 1u);
+        } else {
+            while (*vg == g) {
+            }
+        }
+        __threadfence();
     }
     __syncthreads();
-    const double a = red[32];
-    double ss = 0.0;
-    for (int i = tid; i < n; i += nt) {
-        const double w = sq[i] - bprev * qprev[i] - a * q[i];
-        ss += w * w;
+}
+
+__device__ double block_sum3(double& a, double& b, double& c, double* sh) {
+    for (int o = 16; o > 0; o >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        b += __shfl_xor_sync(0xffffffffu, b, o);
+        c += __shfl_xor_sync(0xffffffffu, c, o);
+    }
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+    if (l == 0) {
+        sh[w] = a;
+        sh[32 + w] = b;
+        sh[64 + w] = c;
     }
     __syncthreads();
-    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-    if ((tid & 31) == 0) red[tid >> 5] = ss;
-    __syncthreads();
-    if (tid == 0) {
-        double t = 0;
-        for (int w = 0; w < (nt >> 5); ++w) t += red[w];
-        red[32] = sqrt(t);
-        alpha[j] = a;
-        beta[j] = red[32];
+    if (threadIdx.x == 0) {
+        double x = 0, y = 0, z = 0;
+        for (int i = 0; i < nw; ++i) {
+            x += sh[i];
+            y += sh[32 + i];
+            z += sh[64 + i];
+        }
+        sh[96] = x;
+        sh[97] = y;
+        sh[98] = z;
     }
     __syncthreads();
-    const double b = red[32];
-    const double inv = b > 0 ? 1.0 / b : 0.0;
-    for (int i = tid; i < n; i += nt) {
-        const double w = sq[i] - bprev * qprev[i] - a * q[i];
-        qprev[i] = q[i];
-        q[i] = w * inv;
+    a = sh[96];
+    b = sh[97];
+    c = sh[98];
+    return a;
+}
+
+// m-step Lanczos in ONE cooperative kernel.  Block b owns rows [r0, r1).
+// Per step: w = S q (own rows; S symmetric => read column r, coalesced),
+// partial sums {w.w, w.q, w.qprev} -> barrier -> alpha, beta -> own rows of
+// q/qprev updated -> barrier.
+__global__ void __launch_bounds__(256) lanczos_coop(const double* __restrict__ S, int n, int m,
+                                                    double* __restrict__ q, double* __restrict__ qprev,
+                                                    double* __restrict__ w, double* __restrict__ part,
+                                                    double* __restrict__ alpha, double* __restrict__ beta,
+                                                    unsigned* bar) {
+    __shared__ double sh[100];
+    const unsigned G = gridDim.x;
+    const int r0 = int(int64_t(blockIdx.x) * n / G), r1 = int(int64_t(blockIdx.x + 1) * n / G);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    double bprev = 0.0;
+    for (int j = 0; j < m; ++j) {
+        for (int r = r0 + warp; r < r1; r += nw) {
+            const double* col = S + size_t(n) * r;
+            double s = 0.0;
+            for (int c = lane; c < n; c += 32) s += col[c] * q[c];
+            for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            if (lane == 0) w[r] = s;
+        }
+        __syncthreads();
+        double ww = 0, wq = 0, wp = 0;
+        for (int r = r0 + int(threadIdx.x); r < r1; r += blockDim.x) {
+            ww += w[r] * w[r];
+            wq += w[r] * q[r];
+            wp += w[r] * qprev[r];
+        }
+        block_sum3(ww, wq, wp, sh);
+        if (threadIdx.x == 0) {
+            part[3 * blockIdx.x] = ww;
+            part[3 * blockIdx.x + 1] = wq;
+            part[3 * blockIdx.x + 2] = wp;
+        }
+        grid_sync(bar, bar + 1, G);
+        double tw = 0, tq = 0, tp = 0;
+        for (unsigned i = 0; i < G; ++i) {  // fixed order => identical on every block
+            tw += part[3 * i];
+            tq += part[3 * i + 1];
+            tp += part[3 * i + 2];
+        }
+        const double a = tq;
+        // ||w - a q - bprev qprev||^2 with q, qprev orthonormal
+        double bb = tw - 2.0 * a * tq - 2.0 * bprev * tp + a * a + bprev * bprev;
+        const double b = bb > 0 ? sqrt(bb) : 0.0;
+        const double inv = b > 0 ? 1.0 / b : 0.0;
+        for (int r = r0 + int(threadIdx.x); r < r1; r += blockDim.x) {
+            const double nv = (w[r] - a * q[r] - bprev * qprev[r]) * inv;
+            qprev[r] = q[r];
+            q[r] = nv;
+        }
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            alpha[j] = a;
+            beta[j] = b;
+        }
+        bprev = b;
+        grid_sync(bar, bar + 1, G);
     }
 }
 
-__global__ void tridiag_dense(const double* __restrict__ alpha, const double* __restrict__ beta,
-                              int m, double* __restrict__ t) {
+__global__ void tridiag_dense(const double* __restrict__ alpha, const double* __restrict__ beta, int m,
+                              double* __restrict__ t) {
     for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
         const int i = e % m, j = e / m;
         double v = 0.0;
@@ -83,8 +158,7 @@ __global__ void tridiag_dense(const double* __restrict__ alpha, const double* __
 }
 
 __global__ void fill_normalish(double* __restrict__ v, size_t n, uint64_t seed) {
-    for (size_t e = size_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
-         e += size_t(gridDim.x) * blockDim.x) {
+    for (size_t e = size_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += size_t(gridDim.x) * blockDim.x) {
         uint64_t x = (e + 1) * 0x9e3779b97f4a7c15ULL ^ seed;
         x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
         x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
@@ -93,18 +167,35 @@ __global__ void fill_normalish(double* __restrict__ v, size_t n, uint64_t seed) 
     }
 }
 
+__global__ void scale_vec(double* v, int n, const double* nrm2) {
+    const double s = *nrm2 > 0 ? 1.0 / sqrt(*nrm2) : 0.0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) v[i] *= s;
+}
+
+__global__ void dot_self(const double* v, int n, double* out) {
+    __shared__ double sh[32];
+    double s = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s += v[i] * v[i];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0;
+        for (int i = 0; i < int(blockDim.x >> 5); ++i) t += sh[i];
+        *out = t;
+    }
+}
+
 // ynew = g1 * y + g2 * yprev  (elementwise; dgemm then adds a * S y)
 __global__ void cheb_combine(double* __restrict__ ynew, const double* __restrict__ y,
                              const double* __restrict__ yprev, size_t n, double g1, double g2) {
-    for (size_t e = size_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
-         e += size_t(gridDim.x) * blockDim.x)
+    for (size_t e = size_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += size_t(gridDim.x) * blockDim.x)
         ynew[e] = g1 * y[e] + (yprev ? g2 * yprev[e] : 0.0);
 }
 
 // res[j] = || W(:, j) - theta_j V(:, j) ||, j < r   (one warp per column)
 __global__ void ritz_residual(const double* __restrict__ w, const double* __restrict__ v,
-                              const double* __restrict__ theta, int n, int r,
-                              double* __restrict__ res) {
+                              const double* __restrict__ theta, int n, int r, double* __restrict__ res) {
     const int col = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     const int lane = threadIdx.x & 31;
     if (col >= r) return;
@@ -118,44 +209,109 @@ __global__ void ritz_residual(const double* __restrict__ w, const double* __rest
     if (lane == 0) res[col] = sqrt(s);
 }
 
-inline unsigned nblk(size_t n) { return unsigned(std::min<size_t>((n + 255) / 256, 4096)); }
+// SVQB step 1: d_i = 1/sqrt(G_ii); G <- D G D.
+__global__ void svqb_scale(double* g, int k, double* d) {
+    __shared__ double sd[128];
+    for (int i = threadIdx.x; i < k; i += blockDim.x) {
+        const double gi = g[i + size_t(k) * i];
+        sd[i] = gi > 0 ? 1.0 / sqrt(gi) : 0.0;
+        d[i] = sd[i];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < k * k; e += blockDim.x) g[e] *= sd[e % k] * sd[e / k];
+}
+
+// SVQB step 2: M = D Z Theta^{-1/2}, eigenvalues clamped at tau * theta_max.
+__global__ void svqb_form(const double* d, const double* z, const double* th, int k, double tau, double* mm) {
+    const double tmax = th[0];
+    for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
+        const int i = e % k, j = e / k;
+        const double t = fmax(th[j], tau * tmax);
+        mm[e] = t > 0 ? d[i] * z[e] / sqrt(t) : 0.0;
+    }
+}
 
 struct Bounds {
     double lo, hi;
 };
 
-// m-step Lanczos on S (n x n): extreme Ritz values widened by the last beta.
-Bounds lanczos_bounds(atk_ctx* ctx, const double* S, int n) {
+struct Ws {
+    DevBuf<double> G, Z, th, d, M, tmp;
+    DevBuf<int> sweeps;
+};
+
+// Orthonormal basis of span(Y) into V (n x k): SVQB twice.
+void svqb(atk_ctx* ctx, const double* Y, int n, int k, double* V, Ws& ws) {
+    const double* src = Y;
+    for (int pass = 0; pass < 2; ++pass) {
+        double* dst = (pass == 0) ? V : ws.tmp.get();
+        dgemm(ctx, true, false, k, k, n, 1.0, src, n, src, n, 0.0, ws.G.get(), k);
+        svqb_scale<<<1, 256, 0, ctx->stream>>>(ws.G.get(), k, ws.d.get());
+        ATK_LAUNCHED(ctx);
+        jacobi_eig(ctx, ws.G.get(), k, k, ws.th.get(), ws.Z.get(), k, ws.sweeps.get());
+        svqb_form<<<1, 256, 0, ctx->stream>>>(ws.d.get(), ws.Z.get(), ws.th.get(), k, 1e-13, ws.M.get());
+        ATK_LAUNCHED(ctx);
+        dgemm(ctx, false, false, n, k, k, 1.0, src, n, ws.M.get(), k, 0.0, dst, n);
+        src = dst;
+    }
+    ATK_CUDA(cudaMemcpyAsync(V, ws.tmp.get(), size_t(n) * k * sizeof(double), cudaMemcpyDeviceToDevice,
+                             ctx->stream));
+}
+
+Bounds lanczos_bounds(atk_ctx* ctx, const double* S, int n, bool psd) {
     cudaStream_t st = ctx->stream;
-    const int m = std::min(n, 40);
-    DevBuf<double> q(ctx, n), qp(ctx, n), sq(ctx, n), al(ctx, m), be(ctx, m), tm(ctx, size_t(m) * m),
-        tv(ctx, m), tz(ctx, size_t(m) * m);
+    const int m = std::min(n, 64);
+    int grid = ctx->num_sms;
+    {
+        int per_sm = 0;
+        ATK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lanczos_coop, 256, 0));
+        grid = std::max(1, std::min(grid * std::max(per_sm, 1), std::min(grid, n)));
+    }
+    DevBuf<double> q(ctx, n), qp(ctx, n), w(ctx, n), part(ctx, 3 * size_t(grid)), al(ctx, m), be(ctx, m),
+        tm(ctx, size_t(m) * m), tv(ctx, m), tz(ctx, size_t(m) * m), nrm(ctx, 1);
+    DevBuf<unsigned> bar(ctx, 2);
     DevBuf<int> sweeps(ctx, 1);
+    ATK_CUDA(cudaMemsetAsync(bar.get(), 0, 2 * sizeof(unsigned), st));
+    ATK_CUDA(cudaMemsetAsync(qp.get(), 0, n * sizeof(double), st));
     fill_normalish<<<nblk(n), 256, 0, st>>>(q.get(), n, 0x5eed1234ULL);
     ATK_LAUNCHED(ctx);
-    ATK_CUDA(cudaMemsetAsync(qp.get(), 0, n * sizeof(double), st));
-    const double nq = std::sqrt(norm2_sq(ctx, q.get(), ATK_F64, n));
-    axpy(ctx, q.get(), q.get(), ATK_F64, n, 1.0 / nq - 1.0);  // q <- q / ||q||
-    for (int j = 0; j < m; ++j) {
-        dgemm(ctx, false, false, n, 1, n, 1.0, S, n, q.get(), n, 0.0, sq.get(), n);
-        lanczos_step<<<1, 1024, 0, st>>>(sq.get(), q.get(), qp.get(), n, j, al.get(), be.get());
-        ATK_LAUNCHED(ctx);
-    }
+    dot_self<<<1, 256, 0, st>>>(q.get(), n, nrm.get());
+    ATK_LAUNCHED(ctx);
+    scale_vec<<<nblk(n), 256, 0, st>>>(q.get(), n, nrm.get());
+    ATK_LAUNCHED(ctx);
+    const double* Sp = S;
+    double* qptr = q.get();
+    double* qpptr = qp.get();
+    double* wptr = w.get();
+    double* pptr = part.get();
+    double* aptr = al.get();
+    double* bptr = be.get();
+    unsigned* barp = bar.get();
+    int nn = n, mm = m;
+    void* args[] = {&Sp, &nn, &mm, &qptr, &qpptr, &wptr, &pptr, &aptr, &bptr, &barp};
+    ATK_CUDA(cudaLaunchCooperativeKernel((void*)lanczos_coop, dim3(grid), dim3(256), args, 0, st));
+    ATK_LAUNCHED(ctx);
     tridiag_dense<<<1, 256, 0, st>>>(al.get(), be.get(), m, tm.get());
     ATK_LAUNCHED(ctx);
     jacobi_eig(ctx, tm.get(), m, m, tv.get(), tz.get(), m, sweeps.get());
-    std::vector<double> hv(m), hb(m);
+    std::vector<double> hv(m), hb(m), zlast(m);
     ATK_CUDA(cudaMemcpyAsync(hv.data(), tv.get(), m * sizeof(double), cudaMemcpyDeviceToHost, st));
     ATK_CUDA(cudaMemcpyAsync(hb.data(), be.get(), m * sizeof(double), cudaMemcpyDeviceToHost, st));
+    // last row of the eigenvector matrix: z(m-1, j) for every j
+    ATK_CUDA(cudaMemcpy2DAsync(zlast.data(), sizeof(double), tz.get() + (m - 1), size_t(m) * sizeof(double),
+                               sizeof(double), m, cudaMemcpyDeviceToHost, st));
     ATK_CUDA(cudaStreamSynchronize(st));
     const double bm = std::fabs(hb[m - 1]);
-    return {hv[m - 1] - bm, hv[0] + bm};  // hv is descending
+    Bounds b{hv[m - 1] - bm * std::fabs(zlast[m - 1]) - 1e-12 * std::fabs(hv[0]),
+             hv[0] + bm * std::fabs(zlast[0])};
+    if (psd) b.lo = std::max(b.lo, 0.0);
+    return b;
 }
 
 // Rayleigh-Ritz on the orthonormal block V (n x k): W = S V, T = V^T W,
 // T = Z diag(theta) Z^T (Jacobi, descending), V <- V Z, W <- W Z.
-void rayleigh_ritz(atk_ctx* ctx, const double* S, int n, int k, double* V, double* W, double* T,
-                   double* Z, double* theta, double* tmp, int* sweeps) {
+void rayleigh_ritz(atk_ctx* ctx, const double* S, int n, int k, double* V, double* W, double* T, double* Z,
+                   double* theta, double* tmp, int* sweeps) {
     const size_t nk = size_t(n) * k;
     dgemm(ctx, false, false, n, k, n, 1.0, S, n, V, n, 0.0, W, n);
     dgemm(ctx, true, false, k, k, n, 1.0, V, n, W, n, 0.0, T, k);
@@ -168,8 +324,8 @@ void rayleigh_ritz(atk_ctx* ctx, const double* S, int n, int k, double* V, doubl
 
 }  // namespace
 
-EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* values_dev,
-                      double* vectors_dev) {
+EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* values_dev, double* vectors_dev,
+                      bool psd, double tol) {
     EigInfo info;
     cudaStream_t st = ctx->stream;
     const bool dense = n <= kJacobiMax && ctx->eig_method != 1;
@@ -178,8 +334,8 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
         DevBuf<int> sweeps(ctx, 1);
         jacobi_eig(ctx, s_dev, n, n, vals.get(), vecs.get(), n, sweeps.get());
         ATK_CUDA(cudaMemcpyAsync(values_dev, vals.get(), r * sizeof(double), cudaMemcpyDeviceToDevice, st));
-        ATK_CUDA(cudaMemcpyAsync(vectors_dev, vecs.get(), size_t(n) * r * sizeof(double),
-                                 cudaMemcpyDeviceToDevice, st));
+        ATK_CUDA(cudaMemcpyAsync(vectors_dev, vecs.get(), size_t(n) * r * sizeof(double), cudaMemcpyDeviceToDevice,
+                                 st));
         fix_signs(ctx, vectors_dev, n, r, n);
         int sw = 0;
         ATK_CUDA(cudaMemcpyAsync(&sw, sweeps.get(), sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -191,13 +347,15 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
     }
 
     // ---------------- ChFSI
+    if (tol <= 0) tol = ctx->chfsi_tol;
     int k = std::min(n, std::max(r + 16, (3 * r + 1) / 2));
     k = std::min(k, kJacobiMax);
     if (k < r) fail(ATK_UNSUPPORTED, "sym_eig_top_r: r > 112 with n > 112 is not supported");
-    const size_t nn = size_t(n) * n, nk = size_t(n) * k;
-    DevBuf<double> S(ctx, nn), V(ctx, nk), W(ctx, nk), Ya(ctx, nk), Yb(ctx, nk), Yc(ctx, nk),
-        T(ctx, size_t(k) * k), Z(ctx, size_t(k) * k), theta(ctx, k), Rm(ctx, size_t(k) * k),
-        res(ctx, k);
+    const size_t nn = size_t(n) * n, nk = size_t(n) * k, kk = size_t(k) * k;
+    DevBuf<double> S(ctx, nn), V(ctx, nk), W(ctx, nk), Ya(ctx, nk), Yb(ctx, nk), Yc(ctx, nk), T(ctx, kk), Z(ctx, kk),
+        theta(ctx, k), res(ctx, k);
+    Ws ws{DevBuf<double>(ctx, kk), DevBuf<double>(ctx, kk), DevBuf<double>(ctx, k), DevBuf<double>(ctx, k),
+          DevBuf<double>(ctx, kk), DevBuf<double>(ctx, nk), DevBuf<int>(ctx, 1)};
     DevBuf<int> sweeps(ctx, 1);
     static const bool trace = std::getenv("ATK_TRACE") != nullptr;
     auto t_last = std::chrono::steady_clock::now();
@@ -212,16 +370,16 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
     ATK_CUDA(cudaMemcpyAsync(S.get(), s_dev, nn * sizeof(double), cudaMemcpyDeviceToDevice, st));
     symmetrize(ctx, S.get(), n);
     mark("prep");
-    const Bounds b = lanczos_bounds(ctx, S.get(), n);
+    const Bounds b = lanczos_bounds(ctx, S.get(), n, psd);
     mark("lanczos", 0, b.lo);
 
-    // random orthonormal start
-    fill_normalish<<<nblk(nk), 256, 0, st>>>(Ya.get(), nk, 0xc0ffee11ULL);
+    // start: one power step on a random block, then SVQB + Rayleigh-Ritz
+    fill_normalish<<<nblk(nk), 256, 0, st>>>(Yb.get(), nk, 0xc0ffee11ULL);
     ATK_LAUNCHED(ctx);
-    householder_qr(ctx, Ya.get(), n, k, V.get(), Rm.get());
+    dgemm(ctx, false, false, n, k, n, 1.0, S.get(), n, Yb.get(), n, 0.0, Ya.get(), n);
+    svqb(ctx, Ya.get(), n, k, V.get(), ws);
     mark("qr0");
-    rayleigh_ritz(ctx, S.get(), n, k, V.get(), W.get(), T.get(), Z.get(), theta.get(), Ya.get(),
-                  sweeps.get());
+    rayleigh_ritz(ctx, S.get(), n, k, V.get(), W.get(), T.get(), Z.get(), theta.get(), Ya.get(), sweeps.get());
     mark("rr0");
 
     const int max_outer = 100;
@@ -238,7 +396,7 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
         scale = std::max(scale, std::fabs(hth[0]));
         worst = 0.0;
         for (int j = 0; j < r; ++j) worst = std::max(worst, hres[j]);
-        if (!(scale > 0.0) || worst <= ctx->chfsi_tol * scale || it >= max_outer) break;
+        if (!(scale > 0.0) || worst <= tol * scale || it >= max_outer) break;
         // Chebyshev filter on the unwanted interval [lo, cut]
         const double cut = hth[k - 1];
         const double lo = std::min(b.lo, cut - 1e-12 * scale);
@@ -246,9 +404,9 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
         if (!(e > 0.0)) e = 1e-12 * scale;
         const double smax = std::max(1.0, (std::max(b.hi, hth[0]) - c) / e);
         const double g = 1.0 / (2.0 * smax + 1.0);  // per-step rescale, keeps the recurrence linear
-        // degree: enough to separate [lo, cut] from the top by ~1e30, capped at 16
-        const double ac = std::acosh(std::max(1.0 + 1e-12, smax));
-        const int degree = std::max(2, std::min(16, int(std::ceil(69.0 / ac))));
+        // degree: separate [lo, cut] from the wanted end by ~1e20 per pass, 2..16
+        const double ac = std::acosh(std::max(1.0 + 1e-12, (hth[r - 1] - c) / e));
+        const int degree = std::max(2, std::min(16, int(std::ceil(46.0 / std::max(ac, 1e-3)))));
         // Y1 = g (S V - c V) / e ; Y_{j+1} = g (2/e)(S Y_j - c Y_j) - g^2 Y_{j-1}
         double* yprev = V.get();
         double* ycur = Ya.get();
@@ -256,7 +414,6 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
         cheb_combine<<<nblk(nk), 256, 0, st>>>(ycur, V.get(), nullptr, nk, -g * c / e, 0.0);
         ATK_LAUNCHED(ctx);
         dgemm(ctx, false, false, n, k, n, g / e, S.get(), n, V.get(), n, 1.0, ycur, n);
-        // first Y_{j-1} is V scaled consistently: V_hat_0 = V (g^0)
         for (int j = 1; j < degree; ++j) {
             cheb_combine<<<nblk(nk), 256, 0, st>>>(ynext, ycur, yprev, nk, -2.0 * g * c / e, -g * g);
             ATK_LAUNCHED(ctx);
@@ -267,7 +424,7 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
             ynext = spare;
         }
         mark("filter", degree, worst / scale);
-        householder_qr(ctx, ycur, n, k, V.get(), Rm.get());
+        svqb(ctx, ycur, n, k, V.get(), ws);
         mark("qr");
         rayleigh_ritz(ctx, S.get(), n, k, V.get(), W.get(), T.get(), Z.get(), theta.get(),
                       ynext == V.get() ? Yc.get() : ynext, sweeps.get());
@@ -275,13 +432,12 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
     }
     mark("done", it, worst / scale);
     ATK_CUDA(cudaMemcpyAsync(values_dev, theta.get(), r * sizeof(double), cudaMemcpyDeviceToDevice, st));
-    ATK_CUDA(cudaMemcpyAsync(vectors_dev, V.get(), size_t(n) * r * sizeof(double),
-                             cudaMemcpyDeviceToDevice, st));
+    ATK_CUDA(cudaMemcpyAsync(vectors_dev, V.get(), size_t(n) * r * sizeof(double), cudaMemcpyDeviceToDevice, st));
     fix_signs(ctx, vectors_dev, n, r, n);
     info.method = 1;
     info.iterations = it;
     info.residual = scale > 0 ? worst / scale : 0.0;
-    if (it >= max_outer && worst > 1e3 * ctx->chfsi_tol * scale)
+    if (it >= max_outer && worst > 1e3 * tol * scale)
         fail(ATK_NO_CONVERGENCE, "symmetric eigendecomposition failed (ChFSI did not converge)");
     return info;
 }
