@@ -384,8 +384,9 @@ size_t jacobi_smem_bytes(int n) {
            size_t(N) * sizeof(int) + size_t(np) * (np + 1) / 2 * sizeof(uint16_t) + 64;
 }
 
-void jacobi_eig(atk_ctx* ctx, const double* a, int n, int lda, double* values, double* vectors,
-                int ldv, int* sweeps_dev) {
+// Two-sided variant kept for A/B checks (option "jacobi2s"); the default is jacobi.cu.
+void jacobi2s_eig(atk_ctx* ctx, const double* a, int n, int lda, double* values, double* vectors,
+                  int ldv, int* sweeps_dev) {
     if (n > kJacobiMax) fail(ATK_UNSUPPORTED, "jacobi_eig: n exceeds the shared-memory capacity");
     const size_t smem = jacobi_smem_bytes(n);
     ATK_CUDA(cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));

@@ -238,7 +238,37 @@ struct Bounds {
 struct Ws {
     DevBuf<double> G, Z, th, d, M, tmp;
     DevBuf<int> sweeps;
+    DevBuf<int> info;  // 3 Cholesky status words
 };
+
+// G += s I with s = 11 (m k + k (k+1)) u ||Y||_F^2  (shifted CholeskyQR, Fukaya et al.)
+__global__ void add_shift(double* g, int k, int m) {
+    __shared__ double tr;
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int i = 0; i < k; ++i) t += g[i + size_t(k) * i];
+        tr = t;
+    }
+    __syncthreads();
+    const double s = 11.0 * (double(m) * k + double(k) * (k + 1)) * 1.1102230246251565e-16 * tr;
+    for (int i = threadIdx.x; i < k; i += blockDim.x) g[i + size_t(k) * i] += s;
+}
+
+// X = L^{-T} (upper triangular) from the lower Cholesky factor L; one thread per column.
+__global__ void chol_inv_t(const double* __restrict__ l, int k, double* __restrict__ x) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= k) return;
+    double* xc = x + size_t(k) * j;
+    for (int i = k - 1; i >= 0; --i) {
+        if (i > j) {
+            xc[i] = 0.0;
+            continue;
+        }
+        double s = (i == j) ? 1.0 : 0.0;
+        for (int t = i + 1; t <= j; ++t) s -= l[t + size_t(k) * i] * xc[t];
+        xc[i] = s / l[i + size_t(k) * i];
+    }
+}
 
 // Orthonormal basis of span(Y) into V (n x k): SVQB twice.
 void svqb(atk_ctx* ctx, const double* Y, int n, int k, double* V, Ws& ws) {
@@ -256,6 +286,32 @@ void svqb(atk_ctx* ctx, const double* Y, int n, int k, double* V, Ws& ws) {
     }
     ATK_CUDA(cudaMemcpyAsync(V, ws.tmp.get(), size_t(n) * k * sizeof(double), cudaMemcpyDeviceToDevice,
                              ctx->stream));
+}
+
+// Orthonormal basis of span(Y) into V: shifted CholeskyQR3 (three GEMM-based
+// passes, the first with a diagonal shift so it never breaks down); falls
+// back to SVQB if a Cholesky pivot still fails.
+void orthonormalize(atk_ctx* ctx, const double* Y, int n, int k, double* V, Ws& ws) {
+    const double* src = Y;
+    double* bufs[2] = {V, ws.tmp.get()};
+    for (int pass = 0; pass < 3; ++pass) {
+        double* dst = bufs[pass & 1];
+        dgemm(ctx, true, false, k, k, n, 1.0, src, n, src, n, 0.0, ws.G.get(), k);
+        if (pass == 0) {
+            add_shift<<<1, 128, 0, ctx->stream>>>(ws.G.get(), k, n);
+            ATK_LAUNCHED(ctx);
+        }
+        cholesky(ctx, ws.G.get(), k, ws.info.get() + pass);
+        chol_inv_t<<<(k + 63) / 64, 64, 0, ctx->stream>>>(ws.G.get(), k, ws.M.get());
+        ATK_LAUNCHED(ctx);
+        dgemm(ctx, false, false, n, k, k, 1.0, src, n, ws.M.get(), k, 0.0, dst, n);
+        src = dst;
+    }
+    // result of pass 2 is in bufs[0] == V
+    int h[3] = {0, 0, 0};
+    ATK_CUDA(cudaMemcpyAsync(h, ws.info.get(), 3 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    ATK_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (h[0] || h[1] || h[2]) svqb(ctx, Y, n, k, V, ws);
 }
 
 Bounds lanczos_bounds(atk_ctx* ctx, const double* S, int n, bool psd) {
@@ -355,7 +411,7 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
     DevBuf<double> S(ctx, nn), V(ctx, nk), W(ctx, nk), Ya(ctx, nk), Yb(ctx, nk), Yc(ctx, nk), T(ctx, kk), Z(ctx, kk),
         theta(ctx, k), res(ctx, k);
     Ws ws{DevBuf<double>(ctx, kk), DevBuf<double>(ctx, kk), DevBuf<double>(ctx, k), DevBuf<double>(ctx, k),
-          DevBuf<double>(ctx, kk), DevBuf<double>(ctx, nk), DevBuf<int>(ctx, 1)};
+          DevBuf<double>(ctx, kk), DevBuf<double>(ctx, nk), DevBuf<int>(ctx, 1), DevBuf<int>(ctx, 3)};
     DevBuf<int> sweeps(ctx, 1);
     static const bool trace = std::getenv("ATK_TRACE") != nullptr;
     auto t_last = std::chrono::steady_clock::now();
@@ -377,7 +433,7 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
     fill_normalish<<<nblk(nk), 256, 0, st>>>(Yb.get(), nk, 0xc0ffee11ULL);
     ATK_LAUNCHED(ctx);
     dgemm(ctx, false, false, n, k, n, 1.0, S.get(), n, Yb.get(), n, 0.0, Ya.get(), n);
-    svqb(ctx, Ya.get(), n, k, V.get(), ws);
+    orthonormalize(ctx, Ya.get(), n, k, V.get(), ws);
     mark("qr0");
     rayleigh_ritz(ctx, S.get(), n, k, V.get(), W.get(), T.get(), Z.get(), theta.get(), Ya.get(), sweeps.get());
     mark("rr0");
@@ -424,7 +480,7 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
             ynext = spare;
         }
         mark("filter", degree, worst / scale);
-        svqb(ctx, ycur, n, k, V.get(), ws);
+        orthonormalize(ctx, ycur, n, k, V.get(), ws);
         mark("qr");
         rayleigh_ritz(ctx, S.get(), n, k, V.get(), W.get(), T.get(), Z.get(), theta.get(),
                       ynext == V.get() ? Yc.get() : ynext, sweeps.get());

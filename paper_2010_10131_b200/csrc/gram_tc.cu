@@ -36,6 +36,8 @@ struct GramParams {
     int kmajor;         // 0: MN-major mode-0 map, 1: permuted 3-D K-major map
     int nkb_p;          // K-major: K-blocks per o (= ceil(P / 32))
     double* acc;        // [unit][BN][BM] fp64 partial tiles
+    uint32_t* progress; // [gridDim.x] K-blocks issued per CTA (drift limiter), or null
+    int slack_kb;       // allowed lead over the slowest CTA, in K-blocks
 };
 
 __global__ void __launch_bounds__(THREADS, 1)
@@ -71,12 +73,31 @@ __global__ void __launch_bounds__(THREADS, 1)
 
     if (warp == 0) {
         // ------------------------------------------------ TMA producer
-        if (lane == 0) {
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
-                const int4 un = p.units[u];
-                for (int kb = un.z; kb < un.w; ++kb) {
+        // Drift limiter: every CTA publishes how many K-blocks it has issued;
+        // a CTA more than `slack` blocks ahead of the slowest one waits.  All
+        // CTAs then stream through X in near lockstep, so each K-block is read
+        // from HBM once and served to the other tiles from L2 (measured 4.2x
+        // HBM re-reads without it, profiles/r1).
+        uint32_t issued = 0;
+        const uint32_t slack = uint32_t(p.slack_kb);
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
+            const int4 un = p.units[u];
+            for (int kb = un.z; kb < un.w; ++kb) {
+                if (p.progress && (issued & 15u) == 0) {
+                    if (lane == 0) p.progress[blockIdx.x] = issued;
+                    uint32_t spins = 0;
+                    for (;;) {
+                        uint32_t mn = 0xffffffffu;
+                        for (int j = lane; j < int(gridDim.x); j += 32) mn = min(mn, ((volatile uint32_t*)p.progress)[j]);
+                        for (int o = 16; o > 0; o >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+                        if (mn + slack >= issued || ++spins > 200000) break;
+                        __nanosleep(256);
+                    }
+                }
+                ++issued;
+                if (lane == 0) {
                     tc::mbar_wait(&empty[stage], phase ^ 1);
                     tc::mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
                     uint8_t* a = smem + stage * STAGE_BYTES;
@@ -98,6 +119,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 }
             }
         }
+        if (p.progress && lane == 0) p.progress[blockIdx.x] = 0xffffffffu;  // never hold others back
         __syncwarp();
     } else if (warp == 1) {
         // ------------------------------------------------ MMA issuer
@@ -293,13 +315,20 @@ void tc_gram(atk_ctx* ctx, const atk_tensor* x, int mode, double* s_dev) {
     ATK_CUDA(cudaMemcpyAsync(du.get(), units.data(), units.size() * sizeof(int4), cudaMemcpyHostToDevice, ctx->stream));
     ATK_CUDA(cudaMemcpyAsync(dtu.get(), tile_unit.data(), tile_unit.size() * sizeof(int), cudaMemcpyHostToDevice,
                              ctx->stream));
-    GramParams prm{du.get(), int(units.size()), chunk_kb, kmajor ? 1 : 0, nkb_p, acc.get()};
+    const int grid = std::min<int>(int(units.size()), ctx->num_sms);
+    DevBuf<uint32_t> progress(ctx, size_t(grid));
+    ATK_CUDA(cudaMemsetAsync(progress.get(), 0, size_t(grid) * sizeof(uint32_t), ctx->stream));
+    // L2 window per in-flight K-block: I rows x 32 fp32 x (#split streams); keep the
+    // lockstep window well inside the 126 MB L2.
+    const double kb_bytes = double(I) * BK * 4.0 * splits;
+    const int slack = int(std::max(8.0, std::min(256.0, 32e6 / kb_bytes)));
+    GramParams prm{du.get(), int(units.size()), chunk_kb, kmajor ? 1 : 0, nkb_p, acc.get(),
+                   ctx->gram_lockstep ? progress.get() : nullptr, slack};
     static bool attr = false;
     if (!attr) {
         ATK_CUDA(cudaFuncSetAttribute(gram_tf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES)));
         attr = true;
     }
-    const int grid = std::min<int>(int(units.size()), ctx->num_sms);
     gram_tf32_kernel<<<grid, THREADS, SMEM_BYTES, ctx->stream>>>(ta, tb, prm);
     ATK_LAUNCHED(ctx);
     const size_t n = size_t(I) * I;

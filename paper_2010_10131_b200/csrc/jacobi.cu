@@ -1,0 +1,134 @@
+// jacobi.cu — small dense symmetric eigensolver (n <= kJacobiMax), one CTA.
+//
+// One-sided (Hestenes) Jacobi on A itself: U = A V is orthogonalised column
+// pair by column pair; at convergence A V = U with orthogonal columns, i.e.
+// A = (U Sigma^-1) Sigma V^T, and for symmetric A the eigenvalues are
+// lambda_j = v_j^T A v_j = u_j . v_j, eigenvectors v_j.  Each round rotates
+// n/2 disjoint column pairs (round-robin tournament), one warp per pair:
+// three warp-reduced dot products, then the pair's two columns of U and V are
+// updated in place — pairs touch disjoint columns, so a round needs a single
+// __syncthreads.  U and V live in shared memory (2 n^2 doubles).
+// Used for: the dense eig of small Grams (n <= 112), the Rayleigh-Ritz
+// problems of ChFSI and the Lanczos tridiagonal.  Output sorted descending
+// (linalg.hpp:101-123 keeps the top r of the full spectrum).
+#include <cmath>
+
+#include "atk_internal.cuh"
+
+namespace atk {
+namespace {
+
+constexpr int kThreads = 1024;
+
+__device__ __forceinline__ int rr_player(int t, int k, int N) {
+    return k == 0 ? 0 : (t + k - 1) % (N - 1) + 1;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__global__ void __launch_bounds__(kThreads) jacobi1s_kernel(const double* __restrict__ ain, int n, int lda,
+                                                            double* __restrict__ values,
+                                                            double* __restrict__ vout, int ldv,
+                                                            int* __restrict__ sweeps_out) {
+    extern __shared__ double sm[];
+    const int ld = n + 1;  // odd leading dimension: column accesses hit distinct banks
+    double* U = sm;
+    double* V = U + size_t(ld) * n;
+    double* lam = V + size_t(ld) * n;  // n
+    __shared__ int rotated;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+    const int N = n + (n & 1);
+
+    for (int e = tid; e < n * n; e += nt) {
+        const int i = e % n, j = e / n;
+        U[i + ld * j] = 0.5 * (ain[i + size_t(lda) * j] + ain[j + size_t(lda) * i]);
+        V[i + ld * j] = (i == j) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+
+    int sweep = 0;
+    for (; sweep < 40 && n > 1; ++sweep) {
+        if (tid == 0) rotated = 0;
+        __syncthreads();
+        for (int t = 0; t < N - 1; ++t) {
+            for (int pr = warp; pr < N / 2; pr += nw) {
+                int p = rr_player(t, pr, N), q = rr_player(t, N - 1 - pr, N);
+                if (p > q) { const int x = p; p = q; q = x; }
+                if (q >= n) continue;  // dummy player
+                double* up = U + ld * p;
+                double* uq = U + ld * q;
+                double a = 0.0, b = 0.0, g = 0.0;
+                for (int i = lane; i < n; i += 32) {
+                    const double x = up[i], y = uq[i];
+                    a = fma(x, x, a);
+                    b = fma(y, y, b);
+                    g = fma(x, y, g);
+                }
+                a = warp_sum(a);
+                b = warp_sum(b);
+                g = warp_sum(g);
+                if (g == 0.0 || fabs(g) <= 1e-15 * sqrt(a * b)) continue;
+                const double zeta = (b - a) / (2.0 * g);
+                const double tt = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+                const double c = 1.0 / sqrt(1.0 + tt * tt), s = c * tt;
+                double* vp = V + ld * p;
+                double* vq = V + ld * q;
+                for (int i = lane; i < n; i += 32) {
+                    const double x = up[i], y = uq[i];
+                    up[i] = c * x - s * y;
+                    uq[i] = s * x + c * y;
+                    const double xv = vp[i], yv = vq[i];
+                    vp[i] = c * xv - s * yv;
+                    vq[i] = s * xv + c * yv;
+                }
+                if (lane == 0) rotated = 1;
+            }
+            __syncthreads();
+        }
+        if (!rotated) break;
+    }
+    // lambda_j = u_j . v_j  (sign-correct for indefinite A)
+    for (int j = warp; j < n; j += nw) {
+        double d = 0.0;
+        for (int i = lane; i < n; i += 32) d = fma(U[i + ld * j], V[i + ld * j], d);
+        d = warp_sum(d);
+        if (lane == 0) lam[j] = d;
+    }
+    __syncthreads();
+    for (int i = warp; i < n; i += nw) {
+        const double li = lam[i];
+        int rank = 0;
+        for (int j = lane; j < n; j += 32) {
+            const double lj = lam[j];
+            rank += (lj > li) || (lj == li && j < i);
+        }
+        for (int o = 16; o > 0; o >>= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
+        if (lane == 0) values[rank] = li;
+        for (int r = lane; r < n; r += 32) vout[r + size_t(ldv) * rank] = V[r + ld * i];
+    }
+    if (tid == 0 && sweeps_out) *sweeps_out = sweep;
+}
+
+}  // namespace
+
+size_t jacobi1s_smem_bytes(int n) { return (size_t(2) * (n + 1) * n + n) * sizeof(double) + 64; }
+
+void jacobi_eig(atk_ctx* ctx, const double* a, int n, int lda, double* values, double* vectors, int ldv,
+                int* sweeps_dev) {
+    if (n > kJacobiMax) fail(ATK_UNSUPPORTED, "jacobi_eig: n exceeds the shared-memory capacity");
+    const size_t smem = jacobi1s_smem_bytes(n);
+    static bool attr = false;
+    if (!attr) {
+        ATK_CUDA(cudaFuncSetAttribute(jacobi1s_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(jacobi1s_smem_bytes(kJacobiMax))));
+        attr = true;
+    }
+    jacobi1s_kernel<<<1, kThreads, smem, ctx->stream>>>(a, n, lda, values, vectors, ldv, sweeps_dev);
+    ATK_LAUNCHED(ctx);
+}
+
+}  // namespace atk
