@@ -2,17 +2,18 @@
 //
 // The reference computes ALL eigenpairs with Eigen's SelfAdjointEigenSolver
 // and keeps the top r.  On the device:
-//   n <= kJacobiMax : dense one-CTA Jacobi (dense.cu), all pairs, keep top r.
+//   n <= kJacobiMax : dense one-CTA one-sided Jacobi (jacobi.cu), keep top r.
 //   n  > kJacobiMax : Chebyshev-filtered subspace iteration (ChFSI) on a block
 //                     of k = min(n, max(r+16, 3r/2)) vectors:
-//                       bounds  : one cooperative-kernel Lanczos run (m = 64
+//                       bounds  : one cooperative-kernel Lanczos run (m = 40
 //                                 steps, 2 grid barriers per step) + its
 //                                 tridiagonal solved by the Jacobi kernel;
 //                       filter  : T_d on [lo, cut] (scaled recurrence, fp64
 //                                 split-K DGEMMs);
-//                       orthonormalisation : SVQB twice (Gram -> Jacobi ->
-//                                 V D Z Theta^-1/2), robust to the rank loss a
-//                                 strong filter produces;
+//                       orthonormalisation : shifted CholeskyQR3 (GEMMs + one-CTA
+//                                 Cholesky); on the rank loss a strong filter
+//                                 produces it falls back to SVQB twice (Gram ->
+//                                 Jacobi -> Y D Z Theta^-1/2, clamped spectrum);
 //                       Rayleigh-Ritz : Jacobi on V^T S V;
 //                     until every wanted Ritz pair has relative residual
 //                     ||S v - theta v|| <= tol * max|theta| (tol 1e-12 for fp64
@@ -45,8 +46,7 @@ __device__ __forceinline__ void grid_sync(unsigned* count, unsigned* gen, unsign
             __threadfence();
             atomicAdd(gen, 1u);
         } else {
-            while (*vg == g) {
-            }
+            while (*vg == g) __nanosleep(64);
         }
         __threadfence();
     }
@@ -316,7 +316,7 @@ void orthonormalize(atk_ctx* ctx, const double* Y, int n, int k, double* V, Ws& 
 
 Bounds lanczos_bounds(atk_ctx* ctx, const double* S, int n, bool psd) {
     cudaStream_t st = ctx->stream;
-    const int m = std::min(n, 64);
+    const int m = std::min(n, 40);
     int grid = ctx->num_sms;
     {
         int per_sm = 0;

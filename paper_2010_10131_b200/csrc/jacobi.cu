@@ -42,6 +42,7 @@ __global__ void __launch_bounds__(kThreads) jacobi1s_kernel(const double* __rest
     const int tid = threadIdx.x, nt = blockDim.x;
     const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
     const int N = n + (n & 1);
+    const double tol = fmax(1e-15, 4.0 * n * 2.220446049250313e-16);
 
     for (int e = tid; e < n * n; e += nt) {
         const int i = e % n, j = e / n;
@@ -54,30 +55,43 @@ __global__ void __launch_bounds__(kThreads) jacobi1s_kernel(const double* __rest
     for (; sweep < 40 && n > 1; ++sweep) {
         if (tid == 0) rotated = 0;
         __syncthreads();
+        // one HALF-warp per pair: 64 half-warps cover the <= 56 pairs of a round at once
+        const int hw = tid >> 4, hl = tid & 15;
         for (int t = 0; t < N - 1; ++t) {
-            for (int pr = warp; pr < N / 2; pr += nw) {
-                int p = rr_player(t, pr, N), q = rr_player(t, N - 1 - pr, N);
-                if (p > q) { const int x = p; p = q; q = x; }
-                if (q >= n) continue;  // dummy player
+            for (int base = 0; base < N / 2; base += nt / 16) {
+                const int pr = base + hw;
+                int p = 0, q = 0;
+                bool active = pr < N / 2;
+                if (active) {
+                    p = rr_player(t, pr, N);
+                    q = rr_player(t, N - 1 - pr, N);
+                    if (p > q) { const int x = p; p = q; q = x; }
+                    active = q < n;  // dummy player when n is odd
+                }
                 double* up = U + ld * p;
                 double* uq = U + ld * q;
                 double a = 0.0, b = 0.0, g = 0.0;
-                for (int i = lane; i < n; i += 32) {
-                    const double x = up[i], y = uq[i];
-                    a = fma(x, x, a);
-                    b = fma(y, y, b);
-                    g = fma(x, y, g);
+                if (active)
+                    for (int i = hl; i < n; i += 16) {
+                        const double x = up[i], y = uq[i];
+                        a = fma(x, x, a);
+                        b = fma(y, y, b);
+                        g = fma(x, y, g);
+                    }
+                for (int o = 8; o > 0; o >>= 1) {
+                    a += __shfl_xor_sync(0xffffffffu, a, o);
+                    b += __shfl_xor_sync(0xffffffffu, b, o);
+                    g += __shfl_xor_sync(0xffffffffu, g, o);
                 }
-                a = warp_sum(a);
-                b = warp_sum(b);
-                g = warp_sum(g);
-                if (g == 0.0 || fabs(g) <= 1e-15 * sqrt(a * b)) continue;
+                // rounding in the length-n dot products is ~n eps sqrt(ab): a tighter
+                // threshold never converges (measured: 40 sweeps at n = 96 with 1e-15)
+                if (!active || g == 0.0 || fabs(g) <= tol * sqrt(a * b)) continue;
                 const double zeta = (b - a) / (2.0 * g);
                 const double tt = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
                 const double c = 1.0 / sqrt(1.0 + tt * tt), s = c * tt;
                 double* vp = V + ld * p;
                 double* vq = V + ld * q;
-                for (int i = lane; i < n; i += 32) {
+                for (int i = hl; i < n; i += 16) {
                     const double x = up[i], y = uq[i];
                     up[i] = c * x - s * y;
                     uq[i] = s * x + c * y;
@@ -85,7 +99,7 @@ __global__ void __launch_bounds__(kThreads) jacobi1s_kernel(const double* __rest
                     vp[i] = c * xv - s * yv;
                     vq[i] = s * xv + c * yv;
                 }
-                if (lane == 0) rotated = 1;
+                if (hl == 0) rotated = 1;
             }
             __syncthreads();
         }

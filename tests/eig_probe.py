@@ -24,3 +24,13 @@ for kind in ["lowrank", "flat"]:
         dt = time.perf_counter() - t0
     ref = np.sort(lam)[::-1][:r]
     print(f"{kind}: {dt*1e3:.1f} ms, max rel eigval err {np.abs(p.values - ref).max() / ref.max():.2e}", flush=True)
+
+for m in (48, 96, 112):
+    a = rng.standard_normal((m, m + 7))
+    s = a @ a.T
+    for rep in range(3):
+        t0 = time.perf_counter()
+        p = atucker.sym_eig_top_r(s, m // 2)
+        dt = time.perf_counter() - t0
+    w = np.linalg.eigvalsh(s)[::-1][: m // 2]
+    print(f"dense jacobi n={m}: {dt*1e3:.3f} ms, rel err {np.abs(p.values - w).max() / w.max():.2e}", flush=True)
