@@ -103,7 +103,9 @@ __global__ void __launch_bounds__(kThreads) jacobi1s_kernel(const double* __rest
             }
             __syncthreads();
         }
-        if (!rotated) break;
+        const bool done = !rotated;
+        __syncthreads();  // everyone has read the flag before thread 0 resets it
+        if (done) break;
     }
     // lambda_j = u_j . v_j  (sign-correct for indefinite A)
     for (int j = warp; j < n; j += nw) {
