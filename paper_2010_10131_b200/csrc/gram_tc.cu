@@ -98,22 +98,26 @@ __global__ void __launch_bounds__(THREADS, 1)
                 }
                 ++issued;
                 if (lane == 0) {
+                    // half units: only the right 128 columns of the 256-wide tile are
+                    // on/above the diagonal -> load and multiply just those
+                    const int tm = un.x & 0xffff, half = un.x >> 16;
                     tc::mbar_wait(&empty[stage], phase ^ 1);
-                    tc::mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+                    tc::mbar_arrive_expect_tx(&full[stage], half ? A_BYTES + B_BYTES / 2 : STAGE_BYTES);
                     uint8_t* a = smem + stage * STAGE_BYTES;
                     uint8_t* b = a + A_BYTES;
                     if (!p.kmajor) {
                         const int k0 = kb * BK;
 #pragma unroll
                         for (int q = 0; q < BM / 32; ++q)
-                            tc::tma_load_2d(a + q * 4096, &tma_a, &full[stage], un.x * BM + q * 32, k0);
-#pragma unroll
-                        for (int q = 0; q < BN / 32; ++q)
-                            tc::tma_load_2d(b + q * 4096, &tma_a, &full[stage], un.y * BN + q * 32, k0);
+                            tc::tma_load_2d(a + q * 4096, &tma_a, &full[stage], tm * BM + q * 32, k0);
+                        const int q0 = half ? BN / 64 : 0;
+                        for (int q = q0; q < BN / 32; ++q)
+                            tc::tma_load_2d(b + (q - q0) * 4096, &tma_a, &full[stage], un.y * BN + q * 32, k0);
                     } else {
                         const int p0 = (kb % p.nkb_p) * BK, o0 = kb / p.nkb_p;
-                        tc::tma_load_3d(a, &tma_a, &full[stage], p0, o0, un.x * BM);
-                        tc::tma_load_3d(b, &tma_b, &full[stage], p0, o0, un.y * BN);
+                        tc::tma_load_3d(a, &tma_a, &full[stage], p0, o0, tm * BM);
+                        if (half) tc::tma_load_3d(b, &tma_a, &full[stage], p0, o0, un.y * BN + BN / 2);
+                        else tc::tma_load_3d(b, &tma_b, &full[stage], p0, o0, un.y * BN);
                     }
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
@@ -124,11 +128,13 @@ __global__ void __launch_bounds__(THREADS, 1)
     } else if (warp == 1) {
         // ------------------------------------------------ MMA issuer
         if (lane == 0) {
-            const uint32_t idesc = tc::idesc_tf32(BM, BN, !p.kmajor, !p.kmajor);
+            const uint32_t idesc_full = tc::idesc_tf32(BM, BN, !p.kmajor, !p.kmajor);
+            const uint32_t idesc_half = tc::idesc_tf32(BM, BN / 2, !p.kmajor, !p.kmajor);
             int stage = 0, abuf = 0;
             uint32_t phase = 0, aphase = 0;
             for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
                 const int4 un = p.units[u];
+                const uint32_t idesc = (un.x >> 16) ? idesc_half : idesc_full;
                 for (int c0 = un.z; c0 < un.w; c0 += p.chunk_kb) {
                     const int c1 = min(un.w, c0 + p.chunk_kb);
                     tc::mbar_wait(&tempty[abuf], aphase ^ 1);
@@ -175,10 +181,12 @@ __global__ void __launch_bounds__(THREADS, 1)
                 tc::mbar_wait(&tfull[abuf], aphase);
                 tc::tc_fence_after();
                 const bool first = (c0 == un.z);
+                const int cc0 = (un.x >> 16) ? BN / 64 : 0;  // half units fill columns 128..255
 #pragma unroll 1
-                for (int cc = 0; cc < BN / 32; ++cc) {
+                for (int cc = cc0; cc < BN / 32; ++cc) {
                     uint32_t r[32];
-                    tc::tmem_ld_32x32b_x32(tmem_base + (uint32_t(q * 32) << 16) + uint32_t(abuf * BN + cc * 32), r);
+                    tc::tmem_ld_32x32b_x32(tmem_base + (uint32_t(q * 32) << 16) +
+                                               uint32_t(abuf * BN + (cc - cc0) * 32), r);
                     tc::tmem_ld_wait();
                     double* dst = tile + size_t(cc * 32) * BM + row;
                     if (first) {
@@ -305,7 +313,9 @@ void tc_gram(atk_ctx* ctx, const atk_tensor* x, int mode, double* s_dev) {
         tile_unit[size_t(tiles_m[t]) * ntn + tiles_n[t]] = int(units.size());
         for (int sp = 0; sp < splits; ++sp) {
             const int kb0 = int(nkb * sp / splits), kb1 = int(nkb * (sp + 1) / splits);
-            units.push_back(make_int4(tiles_m[t], tiles_n[t], kb0, std::max(kb0 + 1, kb1)));
+            // left 128 columns entirely below the diagonal -> half-width unit (N = 128)
+            const int half = (tiles_m[t] * BM >= tiles_n[t] * BN + BN / 2) ? 1 : 0;
+            units.push_back(make_int4(tiles_m[t] | (half << 16), tiles_n[t], kb0, std::max(kb0 + 1, kb1)));
         }
     }
     // guard: a split may be empty only when nkb < splits (excluded above)
