@@ -78,6 +78,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         // CTAs then stream through X in near lockstep, so each K-block is read
         // from HBM once and served to the other tiles from L2 (measured 4.2x
         // HBM re-reads without it, profiles/r1).
+        if (lane == 0) {
         uint32_t issued = 0;
         const uint32_t slack = uint32_t(p.slack_kb);
         int stage = 0;
@@ -86,18 +87,17 @@ __global__ void __launch_bounds__(THREADS, 1)
             const int4 un = p.units[u];
             for (int kb = un.z; kb < un.w; ++kb) {
                 if (p.progress && (issued & 15u) == 0) {
-                    if (lane == 0) p.progress[blockIdx.x] = issued;
+                    p.progress[blockIdx.x] = issued;
                     uint32_t spins = 0;
                     for (;;) {
                         uint32_t mn = 0xffffffffu;
-                        for (int j = lane; j < int(gridDim.x); j += 32) mn = min(mn, ((volatile uint32_t*)p.progress)[j]);
-                        for (int o = 16; o > 0; o >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+                        for (int j = 0; j < int(gridDim.x); ++j) mn = min(mn, ((volatile uint32_t*)p.progress)[j]);
                         if (mn + slack >= issued || ++spins > 200000) break;
                         __nanosleep(256);
                     }
                 }
                 ++issued;
-                if (lane == 0) {
+                {
                     // half units: only the right 128 columns of the 256-wide tile are
                     // on/above the diagonal -> load and multiply just those
                     const int tm = un.x & 0xffff, half = un.x >> 16;
@@ -123,7 +123,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                 }
             }
         }
-        if (p.progress && lane == 0) p.progress[blockIdx.x] = 0xffffffffu;  // never hold others back
+        if (p.progress) p.progress[blockIdx.x] = 0xffffffffu;  // never hold others back
+        }
         __syncwarp();
     } else if (warp == 1) {
         // ------------------------------------------------ MMA issuer

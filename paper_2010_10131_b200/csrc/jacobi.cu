@@ -4,13 +4,15 @@
 // pair by column pair; at convergence A V = U with orthogonal columns, i.e.
 // A = (U Sigma^-1) Sigma V^T, and for symmetric A the eigenvalues are
 // lambda_j = v_j^T A v_j = u_j . v_j, eigenvectors v_j.  Each round rotates
-// n/2 disjoint column pairs (round-robin tournament), one warp per pair:
-// three warp-reduced dot products, then the pair's two columns of U and V are
-// updated in place — pairs touch disjoint columns, so a round needs a single
-// __syncthreads.  U and V live in shared memory (2 n^2 doubles).
+// the n/2 disjoint column pairs of a round-robin tournament, one 8-lane group
+// per pair (three group-reduced dot products, then the pair's columns of U and
+// V updated in place).  Pairs touch disjoint columns, so a round costs one
+// __syncthreads; the CTA has exactly 8 * n/2 threads so no lane idles.
+// U and V live in shared memory (2 n^2 doubles).
 // Used for: the dense eig of small Grams (n <= 112), the Rayleigh-Ritz
 // problems of ChFSI and the Lanczos tridiagonal.  Output sorted descending
 // (linalg.hpp:101-123 keeps the top r of the full spectrum).
+#include <algorithm>
 #include <cmath>
 
 #include "atk_internal.cuh"
@@ -18,21 +20,16 @@
 namespace atk {
 namespace {
 
-constexpr int kThreads = 1024;
+constexpr int kGroup = 8;                         // lanes per column pair
+constexpr int kMaxThreads = kGroup * ((kJacobiMax + 1) / 2);  // 448
 
 __device__ __forceinline__ int rr_player(int t, int k, int N) {
     return k == 0 ? 0 : (t + k - 1) % (N - 1) + 1;
 }
 
-__device__ __forceinline__ double warp_sum(double v) {
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
-
-__global__ void __launch_bounds__(kThreads) jacobi1s_kernel(const double* __restrict__ ain, int n, int lda,
-                                                            double* __restrict__ values,
-                                                            double* __restrict__ vout, int ldv,
-                                                            int* __restrict__ sweeps_out) {
+__global__ void __launch_bounds__(kMaxThreads, 1)
+    jacobi1s_kernel(const double* __restrict__ ain, int n, int lda, double* __restrict__ values,
+                    double* __restrict__ vout, int ldv, int* __restrict__ sweeps_out) {
     extern __shared__ double sm[];
     const int ld = n + 1;  // odd leading dimension: column accesses hit distinct banks
     double* U = sm;
@@ -40,7 +37,6 @@ __global__ void __launch_bounds__(kThreads) jacobi1s_kernel(const double* __rest
     double* lam = V + size_t(ld) * n;  // n
     __shared__ int rotated;
     const int tid = threadIdx.x, nt = blockDim.x;
-    const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
     const int N = n + (n & 1);
     const double tol = fmax(1e-15, 4.0 * n * 2.220446049250313e-16);
 
@@ -51,55 +47,56 @@ __global__ void __launch_bounds__(kThreads) jacobi1s_kernel(const double* __rest
     }
     __syncthreads();
 
+    const int grp = tid / kGroup, gl = tid % kGroup;
     int sweep = 0;
     for (; sweep < 40 && n > 1; ++sweep) {
         if (tid == 0) rotated = 0;
         __syncthreads();
-        // one HALF-warp per pair: 64 half-warps cover the <= 56 pairs of a round at once
-        const int hw = tid >> 4, hl = tid & 15;
         for (int t = 0; t < N - 1; ++t) {
-            for (int base = 0; base < N / 2; base += nt / 16) {
-                const int pr = base + hw;
-                int p = 0, q = 0;
-                bool active = pr < N / 2;
-                if (active) {
-                    p = rr_player(t, pr, N);
-                    q = rr_player(t, N - 1 - pr, N);
-                    if (p > q) { const int x = p; p = q; q = x; }
-                    active = q < n;  // dummy player when n is odd
+            bool active = grp < N / 2;
+            int p = 0, q = 0;
+            if (active) {
+                p = rr_player(t, grp, N);
+                q = rr_player(t, N - 1 - grp, N);
+                if (p > q) { const int x = p; p = q; q = x; }
+                active = q < n;  // dummy player when n is odd
+            }
+            double* up = U + ld * p;
+            double* uq = U + ld * q;
+            double a = 0.0, b = 0.0, g = 0.0;
+            if (active) {
+#pragma unroll 4
+                for (int i = gl; i < n; i += kGroup) {
+                    const double x = up[i], y = uq[i];
+                    a = fma(x, x, a);
+                    b = fma(y, y, b);
+                    g = fma(x, y, g);
                 }
-                double* up = U + ld * p;
-                double* uq = U + ld * q;
-                double a = 0.0, b = 0.0, g = 0.0;
-                if (active)
-                    for (int i = hl; i < n; i += 16) {
-                        const double x = up[i], y = uq[i];
-                        a = fma(x, x, a);
-                        b = fma(y, y, b);
-                        g = fma(x, y, g);
-                    }
-                for (int o = 8; o > 0; o >>= 1) {
-                    a += __shfl_xor_sync(0xffffffffu, a, o);
-                    b += __shfl_xor_sync(0xffffffffu, b, o);
-                    g += __shfl_xor_sync(0xffffffffu, g, o);
-                }
-                // rounding in the length-n dot products is ~n eps sqrt(ab): a tighter
-                // threshold never converges (measured: 40 sweeps at n = 96 with 1e-15)
-                if (!active || g == 0.0 || fabs(g) <= tol * sqrt(a * b)) continue;
+            }
+#pragma unroll
+            for (int o = kGroup / 2; o > 0; o >>= 1) {
+                a += __shfl_xor_sync(0xffffffffu, a, o);
+                b += __shfl_xor_sync(0xffffffffu, b, o);
+                g += __shfl_xor_sync(0xffffffffu, g, o);
+            }
+            // rounding in the length-n dot products is ~n eps sqrt(ab): a tighter
+            // threshold never converges (measured: 40 sweeps at n = 96 with 1e-15)
+            if (active && g != 0.0 && fabs(g) > tol * sqrt(a * b)) {
                 const double zeta = (b - a) / (2.0 * g);
-                const double tt = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-                const double c = 1.0 / sqrt(1.0 + tt * tt), s = c * tt;
+                const double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+                const double c = rsqrt(fma(tt, tt, 1.0)), s = c * tt;
                 double* vp = V + ld * p;
                 double* vq = V + ld * q;
-                for (int i = hl; i < n; i += 16) {
+#pragma unroll 4
+                for (int i = gl; i < n; i += kGroup) {
                     const double x = up[i], y = uq[i];
                     up[i] = c * x - s * y;
-                    uq[i] = s * x + c * y;
+                    uq[i] = fma(s, x, c * y);
                     const double xv = vp[i], yv = vq[i];
                     vp[i] = c * xv - s * yv;
-                    vq[i] = s * xv + c * yv;
+                    vq[i] = fma(s, xv, c * yv);
                 }
-                if (hl == 0) rotated = 1;
+                if (gl == 0) rotated = 1;
             }
             __syncthreads();
         }
@@ -107,24 +104,25 @@ __global__ void __launch_bounds__(kThreads) jacobi1s_kernel(const double* __rest
         __syncthreads();  // everyone has read the flag before thread 0 resets it
         if (done) break;
     }
-    // lambda_j = u_j . v_j  (sign-correct for indefinite A)
-    for (int j = warp; j < n; j += nw) {
+    // lambda_j = u_j . v_j  (sign-correct for indefinite A), one group per column
+    for (int j0 = 0; j0 < n; j0 += nt / kGroup) {  // uniform trip count: shuffles stay converged
+        const int j = j0 + grp;
         double d = 0.0;
-        for (int i = lane; i < n; i += 32) d = fma(U[i + ld * j], V[i + ld * j], d);
-        d = warp_sum(d);
-        if (lane == 0) lam[j] = d;
+        if (j < n)
+            for (int i = gl; i < n; i += kGroup) d = fma(U[i + ld * j], V[i + ld * j], d);
+        for (int o = kGroup / 2; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+        if (j < n && gl == 0) lam[j] = d;
     }
     __syncthreads();
-    for (int i = warp; i < n; i += nw) {
+    for (int i = tid; i < n; i += nt) {
         const double li = lam[i];
         int rank = 0;
-        for (int j = lane; j < n; j += 32) {
+        for (int j = 0; j < n; ++j) {
             const double lj = lam[j];
             rank += (lj > li) || (lj == li && j < i);
         }
-        for (int o = 16; o > 0; o >>= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
-        if (lane == 0) values[rank] = li;
-        for (int r = lane; r < n; r += 32) vout[r + size_t(ldv) * rank] = V[r + ld * i];
+        values[rank] = li;
+        for (int r = 0; r < n; ++r) vout[r + size_t(ldv) * rank] = V[r + ld * i];
     }
     if (tid == 0 && sweeps_out) *sweeps_out = sweep;
 }
@@ -143,7 +141,9 @@ void jacobi_eig(atk_ctx* ctx, const double* a, int n, int lda, double* values, d
                                       int(jacobi1s_smem_bytes(kJacobiMax))));
         attr = true;
     }
-    jacobi1s_kernel<<<1, kThreads, smem, ctx->stream>>>(a, n, lda, values, vectors, ldv, sweeps_dev);
+    const int N = n + (n & 1);
+    const int threads = ((kGroup * std::max(1, N / 2)) + 31) / 32 * 32;
+    jacobi1s_kernel<<<1, threads, smem, ctx->stream>>>(a, n, lda, values, vectors, ldv, sweeps_dev);
     ATK_LAUNCHED(ctx);
 }
 
