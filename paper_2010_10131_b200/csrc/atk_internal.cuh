@@ -178,6 +178,9 @@ void jacobi_eig(atk_ctx* ctx, const double* a, int n, int lda, double* values, d
                 int ldv, int* sweeps_dev);
 // Cholesky factorization in place (lower), status written to *info_dev (0 ok, k>0 pivot k).
 void cholesky(atk_ctx* ctx, double* a, int n, int* info_dev);
+// Shared-memory Cholesky of G (k x k, k <= kJacobiMax) fused with X = L^{-T};
+// *info_dev = 0 or 1 + failing pivot.
+void cholesky_inv_t(atk_ctx* ctx, const double* g, int k, double* x, int* info_dev);
 // X = A^{-1} B given the Cholesky factor L (lower) of A: B overwritten.
 void cholesky_solve(atk_ctx* ctx, const double* l, int n, double* b, int nrhs);
 // Householder thin QR of A (m x n, m >= n): Q (m x n), R (n x n), diag(R) >= 0.

@@ -148,3 +148,82 @@ void jacobi_eig(atk_ctx* ctx, const double* a, int n, int lda, double* values, d
 }
 
 }  // namespace atk
+
+namespace atk {
+namespace {
+
+// Cholesky G = L L^T entirely in shared memory, then X = L^{-T} (upper
+// triangular) by back substitution, 4 lanes per column.  One CTA, k <= 112.
+// info = 0 on success, else 1 + the failing pivot (linalg.hpp:169-177 NotSPD).
+__global__ void __launch_bounds__(448) chol_inv_kernel(const double* __restrict__ g, int k,
+                                                       double* __restrict__ x, int* __restrict__ info) {
+    extern __shared__ double sm[];
+    const int ld = k + 1;
+    double* A = sm;                  // k x k (lower factor built in place)
+    double* X = A + size_t(ld) * k;  // k x k
+    __shared__ int bad;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    if (tid == 0) bad = 0;
+    for (int e = tid; e < k * k; e += nt) A[(e % k) + ld * (e / k)] = g[e];
+    __syncthreads();
+    for (int c = 0; c < k; ++c) {
+        const double d = A[c + ld * c];
+        if (!(d > 0.0)) {
+            if (tid == 0) bad = c + 1;
+            break;  // uniform: every thread read the same pivot
+        }
+        const double l = sqrt(d), il = 1.0 / l;
+        __syncthreads();
+        if (tid == 0) A[c + ld * c] = l;
+        for (int i = c + 1 + tid; i < k; i += nt) A[i + ld * c] *= il;
+        __syncthreads();
+        const int m = k - c - 1;
+        for (int e = tid; e < m * m; e += nt) {
+            const int i = c + 1 + e % m, j = c + 1 + e / m;
+            if (i >= j) A[i + ld * j] -= A[i + ld * c] * A[j + ld * c];
+        }
+        __syncthreads();
+    }
+    __syncthreads();
+    if (bad) {
+        if (tid == 0) *info = bad;
+        return;
+    }
+    // X(:, j) solves L^T X(:, j) = e_j, i = j .. 0; group of 4 lanes per column
+    const int grp = tid >> 2, gl = tid & 3, ngrp = nt >> 2;
+    for (int j0 = 0; j0 < k; j0 += ngrp) {
+        const int j = j0 + grp;
+        const bool act = j < k;
+        double* xc = X + ld * (act ? j : 0);
+        for (int i = k - 1; i >= 0; --i) {
+            double s = 0.0;
+            if (act && i <= j)
+                for (int t = i + 1 + gl; t <= j; t += 4) s = fma(A[t + ld * i], xc[t], s);
+            s += __shfl_xor_sync(0xffffffffu, s, 1);
+            s += __shfl_xor_sync(0xffffffffu, s, 2);
+            if (act && gl == 0) xc[i] = (i > j) ? 0.0 : (((i == j) ? 1.0 : 0.0) - s) / A[i + ld * i];
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+    for (int e = tid; e < k * k; e += nt) x[e] = X[(e % k) + ld * (e / k)];
+    if (tid == 0) *info = 0;
+}
+
+}  // namespace
+
+void cholesky_inv_t(atk_ctx* ctx, const double* g, int k, double* x, int* info_dev) {
+    if (k > kJacobiMax) fail(ATK_UNSUPPORTED, "cholesky_inv_t: k too large");
+    const size_t smem = size_t(2) * (k + 1) * k * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+        ATK_CUDA(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(size_t(2) * (kJacobiMax + 1) * kJacobiMax * sizeof(double))));
+        attr = true;
+    }
+    const int threads = std::min(448, std::max(32, (4 * k + 31) / 32 * 32));
+    chol_inv_kernel<<<1, threads, smem, ctx->stream>>>(g, k, x, info_dev);
+    ATK_LAUNCHED(ctx);
+}
+
+}  // namespace atk
