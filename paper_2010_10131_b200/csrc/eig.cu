@@ -175,7 +175,42 @@ __global__ void __cluster_dims__(kLzCluster, 1, 1) __launch_bounds__(kLzThreads)
     for (int j = 0; j < m; ++j) {
         for (int i = threadIdx.x; i < n; i += blockDim.x) qs[i] = q[i];
         __syncthreads();
-        for (int r = r0 + warp; r < r1; r += nw) {
+        // four rows per warp at a time, 4 column chunks each: 16 independent
+        // 16-byte L2 loads in flight per lane
+        int rbase = r0 + warp * 4;
+        if ((n & 3) == 0)
+            for (; rbase + 3 < r1; rbase += nw * 4) {
+                const float* c0p = S + size_t(n) * rbase;
+                double acc[4] = {0, 0, 0, 0};
+                for (int c = lane * 4; c < n; c += 4 * 128) {
+                    float4 v[4][4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+#pragma unroll
+                        for (int rr = 0; rr < 4; ++rr)
+                            v[rr][u] = (c + u * 128 < n) ? *reinterpret_cast<const float4*>(c0p + size_t(n) * rr + c + u * 128)
+                                                         : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int cc = c + u * 128;
+                        if (cc >= n) break;
+                        const double q0 = qs[cc], q1 = qs[cc + 1], q2 = qs[cc + 2], q3 = qs[cc + 3];
+#pragma unroll
+                        for (int rr = 0; rr < 4; ++rr)
+                            acc[rr] += double(v[rr][u].x) * q0 + double(v[rr][u].y) * q1 + double(v[rr][u].z) * q2 +
+                                       double(v[rr][u].w) * q3;
+                    }
+                }
+#pragma unroll
+                for (int rr = 0; rr < 4; ++rr) {
+                    double t = acc[rr];
+                    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+                    if (lane == 0) w[rbase + rr] = t;
+                }
+            }
+        // leftover rows (and n % 4 != 0): one row per warp
+        for (int r = ((n & 3) == 0 ? rbase : r0 + warp); r < r1; r += ((n & 3) == 0 ? 1 : nw)) {
+            if ((n & 3) == 0 && r >= rbase + 4) break;
             const float* col = S + size_t(n) * r;  // S symmetric: row r == column r
             double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
             int c = lane * 4;
