@@ -1041,6 +1041,82 @@ int or_sthosvd(const double* x, const uint64_t* dims, int nd, const uint64_t* ra
     });
 }
 
+// Memory-lean st-HOSVD of an fp32 tensor (BASELINE C5: 34 GB fp32 would be
+// 69 GB as fp64, plus the reference's `work = x` copy).  Same arithmetic as
+// sthosvd() with an EIG first mode: the mode-0 Gram X_(0) X_(0)^T
+// (kernels.hpp:49-53) and TTM U^T X (kernels.hpp:99-102) are accumulated over
+// column chunks converted to fp64 on the fly (dgemm with beta = 1), then the
+// remaining modes run on the (small) shrunk fp64 tensor through sthosvd().
+int or_sthosvd_f32_eig0(const float* x, const uint64_t* dims, int nd, const uint64_t* ranks,
+                        selector_fn decide, void* user, int iters, double rel_tol, uint64_t seed,
+                        double* core_out, double* factors_out, int threads) {
+    return guard([&] {
+        need_blas();
+        if (nd < 2) throw Err(E_SHAPE_MISMATCH, "or_sthosvd_f32_eig0 needs order >= 2");
+        if (threads > 0) g_blas.set_threads(threads);
+        const uint64_t I = dims[0], r0 = ranks[0];
+        uint64_t J = 1;
+        for (int m = 1; m < nd; ++m) J *= dims[m];
+        if (r0 < 1 || r0 > I) throw Err(E_RANK_EXCEEDS_DIM, "truncation invalid for mode 0");
+        const uint64_t CH = std::max<uint64_t>(1, (uint64_t(1) << 27) / I);  // ~1 GB fp64 per chunk
+        std::vector<double> buf(I * std::min(CH, J));
+        Matrix s(I, I);
+        for (uint64_t j0 = 0; j0 < J; j0 += CH) {
+            const uint64_t nc = std::min(CH, J - j0);
+            for (uint64_t e = 0; e < I * nc; ++e) buf[e] = double(x[I * j0 + e]);
+            gemm_raw(false, true, I, I, nc, buf.data(), I, buf.data(), I, s.v.data(), I, j0 ? 1.0 : 0.0);
+        }
+        record_gemm((long long)(I * I) * (long long)J);
+        for (uint64_t j = 0; j < I; ++j)
+            for (uint64_t i = j + 1; i < I; ++i) {
+                const double v = 0.5 * (s(i, j) + s(j, i));
+                s(i, j) = v;
+                s(j, i) = v;
+            }
+        EigPair e = sym_eig_top_r(s, r0);
+        Tensor work;
+        work.dims.assign(dims, dims + nd);
+        work.dims[0] = r0;
+        work.v.assign(r0 * J, 0.0);
+        for (uint64_t j0 = 0; j0 < J; j0 += CH) {
+            const uint64_t nc = std::min(CH, J - j0);
+            for (uint64_t q = 0; q < I * nc; ++q) buf[q] = double(x[I * j0 + q]);
+            // Y(:, j0:j0+nc) = U^T X(:, j0:j0+nc)
+            gemm_raw(true, false, r0, nc, I, e.vectors.v.data(), I, buf.data(), I, work.v.data() + r0 * j0, r0);
+        }
+        record_gemm(2LL * (long long)(r0 * J) * (long long)I);
+        // remaining modes: the reference loop on the shrunk tensor (mode 0 already done)
+        std::vector<uint64_t> rk(ranks, ranks + nd);
+        std::vector<Matrix> factors(nd);
+        factors[0] = std::move(e.vectors);
+        AlsOptions o{iters, rel_tol, seed};
+        for (int n = 1; n < nd; ++n) {
+            const uint64_t i = work.dim(n), r = rk[n];
+            uint64_t j = 1;
+            for (int m = 0; m < nd; ++m)
+                if (m != n) j *= work.dim(m);
+            const int choice = decide ? decide(user, n, i, r, j) : 0;
+            ModeResult mr = choice == 1 ? als_mode_solver(work, n, r, o)
+                            : choice == 2 ? svd_mode_solver(work, n, r) : eig_mode_solver(work, n, r);
+            factors[n] = std::move(mr.factor);
+            work = std::move(mr.shrunk);
+        }
+        std::memcpy(core_out, work.v.data(), work.v.size() * sizeof(double));
+        size_t off = 0;
+        for (auto& f : factors) {
+            std::memcpy(factors_out + off, f.v.data(), f.v.size() * sizeof(double));
+            off += f.v.size();
+        }
+    });
+}
+
+// ||X||^2 of an fp32 tensor in fp64 (for the projection identity at full size).
+double or_norm2_f32(const float* x, uint64_t n) {
+    double s = 0.0;
+    for (uint64_t i = 0; i < n; ++i) s += double(x[i]) * double(x[i]);
+    return s;
+}
+
 static std::vector<Matrix> unpack_factors(const double* factors, const uint64_t* odims,
                                           const uint64_t* ranks, int nd) {
     std::vector<Matrix> f;

@@ -384,3 +384,44 @@ def __getattr__(name):  # pragma: no cover
 
 
 os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+
+
+def sthosvd_f32_eig0(x32, ranks, decide=None, threads=0, num_iters=5, rel_tol=0.0, seed=0) -> SthosvdResult:
+    """Memory-lean oracle for big fp32 tensors (C5): mode 0 EIG streamed in fp64
+    chunks, later modes through the regular restatement (see atk_oracle.cpp)."""
+    x32 = np.asfortranarray(x32, dtype=np.float32)
+    ranks = [int(r) for r in ranks]
+    lib = load()
+    lib.or_sthosvd_f32_eig0.argtypes = [C.POINTER(C.c_float), _up, C.c_int, _up, SELECTOR_FN, C.c_void_p, C.c_int,
+                                        C.c_double, C.c_uint64, _dp, _dp, C.c_int]
+    box = {"err": None}
+
+    def cb(_u, mode, i, r, j):
+        try:
+            return int(decide(int(mode), int(i), int(r), int(j))) if decide else 0
+        except Exception as e:
+            box["err"] = e
+            return -1
+
+    fn = SELECTOR_FN(cb)
+    core = np.empty(ranks, order="F")
+    factors = np.empty(sum(i * r for i, r in zip(x32.shape, ranks)))
+    code = lib.or_sthosvd_f32_eig0(x32.ctypes.data_as(C.POINTER(C.c_float)), _d(x32.shape), x32.ndim, _d(ranks),
+                                   fn, None, int(num_iters), float(rel_tol), int(seed), _p(core), _p(factors),
+                                   int(threads))
+    if box["err"] is not None:
+        raise box["err"]
+    _check(code)
+    out, off = [], 0
+    for i, r in zip(x32.shape, ranks):
+        out.append(np.asfortranarray(factors[off:off + i * r].reshape((i, r), order="F")))
+        off += i * r
+    return SthosvdResult(core, out, np.zeros((x32.ndim, 5)))
+
+
+def norm2_f32(x32) -> float:
+    lib = load()
+    lib.or_norm2_f32.restype = C.c_double
+    lib.or_norm2_f32.argtypes = [C.POINTER(C.c_float), C.c_uint64]
+    x32 = np.asfortranarray(x32, dtype=np.float32)
+    return float(lib.or_norm2_f32(x32.ctypes.data_as(C.POINTER(C.c_float)), x32.size))

@@ -82,8 +82,19 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
             // rounding in the length-n dot products is ~n eps sqrt(ab): a tighter
             // threshold never converges (measured: 40 sweeps at n = 96 with 1e-15)
             if (active && g != 0.0 && fabs(g) > tol * sqrt(a * b)) {
+                // The rotation ANGLE is computed in fp32 (fast div/sqrt: the fp64 chain
+                // div -> sqrt -> div -> rsqrt dominated the round latency); (c, s) are
+                // then normalised in fp64 so the rotation stays orthogonal to fp64
+                // precision.  An angle that is off by ~1e-7 leaves g' ~ 1e-7 g, removed
+                // by the next sweep; the convergence test above is exact fp64.
                 const double zeta = (b - a) / (2.0 * g);
-                const double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+                double tt;
+                if (fabs(zeta) < 1e15) {
+                    const float zf = float(zeta);
+                    tt = double(copysignf(1.0f, zf) / (fabsf(zf) + sqrtf(fmaf(zf, zf, 1.0f))));
+                } else {
+                    tt = 0.5 / zeta;
+                }
                 const double c = rsqrt(fma(tt, tt, 1.0)), s = c * tt;
                 double* vp = V + ld * p;
                 double* vq = V + ld * q;
