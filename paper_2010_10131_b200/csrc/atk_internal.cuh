@@ -59,6 +59,7 @@ struct atk_ctx {
     int tma_tf32 = 1;          // option "tma_tf32": TMA converts fp32 -> tf32 with round-to-nearest
                                // (the MMA itself truncates: measured 6e-4 bias vs 1e-6, test_gpu_tc.py)
     int gram_chunk_kb = 0;     // option "gram_chunk_kb": K-blocks per fp64 drain (0 = default)
+    int gram_2cta = 1;         // option "gram_2cta": 256x256 Gram tiles on CTA pairs (cta_group::2)
     int gram_lockstep = 0;     // option "gram_lockstep": bound CTA drift so X streams from HBM once
                                // (off: lockstep hot-spots L2 slices, 45 ms vs 34 ms at C5, r1)
     atk::Comm* comm = nullptr;

@@ -1,0 +1,342 @@
+// gram_tc2.cu — the mode-n Gram on CTA PAIRS (tcgen05 cta_group::2).
+//
+// Same contraction as gram_tc.cu (kernels.hpp:127-138, fp32 storage,
+// kind::tf32, TMA TFLOAT32 round-to-nearest, no unfolding) but each 256x256
+// output tile is computed by a 2-CTA cluster: CTA c stages rows
+// [128c, 128c+128) of the A slab and columns [128c, 128c+128) of the B slab,
+// the leader CTA issues one M=256 x N=256 x K=8 UMMA per K-step that reads
+// both CTAs' shared memory, and each CTA holds its 128 accumulator rows in its
+// own TMEM.  Per SM that halves the operand bytes staged per flop relative to
+// the 1-CTA 128x256 tile (32 KB instead of 48 KB per 32-deep K step), which
+// moves the kernel off the shared-memory-bandwidth ceiling (TMA writes + UMMA
+// reads ~ 192 B/clk/SM > 128 B/clk/SM for 1-CTA tiles).
+//
+// Pipeline per CTA: warp 0 = TMA producer (both CTAs; the leader arms the
+// leader's full barrier with the bytes of BOTH CTAs, the peer's TMA completes
+// on it through the cluster window), warp 1 = TMEM alloc + (leader only) MMA
+// issuer, warps 2-5 = epilogue (TMEM -> fp64 partial tile, then a remote
+// arrive on the leader's tmem-empty barrier).  Commits are multicast to both
+// CTAs' barriers.
+#include <algorithm>
+#include <vector>
+
+#include "atk_driver.cuh"
+#include "tc_common.cuh"
+
+namespace atk {
+namespace {
+
+constexpr int TM2 = 256, TN2 = 256, HALF = 128, BK = 32, STAGES2 = 6, THREADS = 192;
+constexpr uint32_t A_BYTES = HALF * BK * 4, B_BYTES = HALF * BK * 4, STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr size_t SMEM2 = STAGES2 * STAGE_BYTES + 1024 + 256;
+
+struct Gram2Params {
+    const int4* units;  // {tile_m, tile_n, kb_begin, kb_end} in 256-tiles
+    int num_units;      // units are dealt to clusters round-robin
+    int chunk_kb;
+    int kmajor;
+    int nkb_p;
+    double* acc;        // [unit][TN2][TM2] fp64 partial tiles
+};
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+
+// TMA whose completion is counted on the LEADER CTA's barrier (peer bit cleared).
+__device__ __forceinline__ void tma2_load_2d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1) {
+    const uint32_t b = tc::smem_u32(bar) & 0xFEFFFFFFu;
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(tc::smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(b), "r"(c0), "r"(c1)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma2_load_3d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1,
+                                             int c2) {
+    const uint32_t b = tc::smem_u32(bar) & 0xFEFFFFFFu;
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(tc::smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(b), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+
+__device__ __forceinline__ void mma2_tf32(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                          uint32_t accumulate) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+__device__ __forceinline__ void mma2_commit_mc(uint64_t* bar) {
+    const uint16_t mask = 0x3;
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            tc::smem_u32(bar)),
+        "h"(mask)
+        : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+    gram_tf32_2cta_kernel(const __grid_constant__ CUtensorMap tma_x, const Gram2Params p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES2 * STAGE_BYTES);
+    uint64_t* empty = full + STAGES2;
+    uint64_t* tfull = empty + STAGES2;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t crank = cluster_rank();
+    const bool leader = crank == 0;
+    const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < STAGES2; ++s) {
+            tc::mbar_init(&full[s], 1);
+            tc::mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            tc::mbar_init(&tfull[b], 1);
+            tc::mbar_init(&tempty[b], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is the live one)
+        }
+        tc::fence_barrier_init();
+        tc::tma_prefetch(&tma_x);
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc::smem_u32(tmem_slot)),
+                     "r"(512u)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+    tc::tc_fence_before();
+    cluster_sync();
+    tc::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int u = pair; u < p.num_units; u += npairs) {
+                const int4 un = p.units[u];
+                const int arow = un.x * TM2 + int(crank) * HALF, brow = un.y * TN2 + int(crank) * HALF;
+                for (int kb = un.z; kb < un.w; ++kb) {
+                    tc::mbar_wait(&empty[stage], phase ^ 1);
+                    if (leader) tc::mbar_arrive_expect_tx(&full[stage], 2 * STAGE_BYTES);
+                    uint8_t* a = smem + stage * STAGE_BYTES;
+                    uint8_t* b = a + A_BYTES;
+                    if (!p.kmajor) {
+                        const int k0 = kb * BK;
+#pragma unroll
+                        for (int q = 0; q < HALF / 32; ++q) tma2_load_2d(a + q * 4096, &tma_x, &full[stage], arow + q * 32, k0);
+#pragma unroll
+                        for (int q = 0; q < HALF / 32; ++q) tma2_load_2d(b + q * 4096, &tma_x, &full[stage], brow + q * 32, k0);
+                    } else {
+                        const int p0 = (kb % p.nkb_p) * BK, o0 = kb / p.nkb_p;
+                        tma2_load_3d(a, &tma_x, &full[stage], p0, o0, arow);
+                        tma2_load_3d(b, &tma_x, &full[stage], p0, o0, brow);
+                    }
+                    if (++stage == STAGES2) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        if (leader && lane == 0) {
+            const uint32_t idesc = tc::idesc_tf32(TM2, TN2, !p.kmajor, !p.kmajor);
+            int stage = 0, abuf = 0;
+            uint32_t phase = 0, aphase = 0;
+            for (int u = pair; u < p.num_units; u += npairs) {
+                const int4 un = p.units[u];
+                for (int c0 = un.z; c0 < un.w; c0 += p.chunk_kb) {
+                    const int c1 = min(un.w, c0 + p.chunk_kb);
+                    tc::mbar_wait(&tempty[abuf], aphase ^ 1);
+                    tc::tc_fence_after();
+                    const uint32_t d = tmem_base + uint32_t(abuf * TN2);
+                    for (int kb = c0; kb < c1; ++kb) {
+                        tc::mbar_wait(&full[stage], phase);
+                        tc::tc_fence_after();
+                        const uint32_t a_base = tc::smem_u32(smem + stage * STAGE_BYTES);
+                        const uint32_t b_base = a_base + A_BYTES;
+#pragma unroll
+                        for (int k = 0; k < BK / 8; ++k) {
+                            uint64_t ad, bd;
+                            if (!p.kmajor) {
+                                ad = tc::smem_desc(a_base + k * 1024, 4096, 512, 1);
+                                bd = tc::smem_desc(b_base + k * 1024, 4096, 512, 1);
+                            } else {
+                                ad = tc::smem_desc_sw128(a_base + k * 32, 16, 1024);
+                                bd = tc::smem_desc_sw128(b_base + k * 32, 16, 1024);
+                            }
+                            mma2_tf32(d, ad, bd, idesc, (kb > c0 || k > 0) ? 1u : 0u);
+                        }
+                        mma2_commit_mc(&empty[stage]);
+                        if (++stage == STAGES2) { stage = 0; phase ^= 1; }
+                    }
+                    mma2_commit_mc(&tfull[abuf]);
+                    if (++abuf == 2) { abuf = 0; aphase ^= 1; }
+                }
+            }
+        }
+        __syncwarp();
+    } else {
+        const int q = warp & 3;
+        const int row = int(crank) * HALF + q * 32 + lane;  // row within the 256-row tile
+        const uint32_t tempty_leader0 = mapa_shared(tc::smem_u32(&tempty[0]), 0);
+        const uint32_t tempty_leader1 = mapa_shared(tc::smem_u32(&tempty[1]), 0);
+        int abuf = 0;
+        uint32_t aphase = 0;
+        for (int u = pair; u < p.num_units; u += npairs) {
+            const int4 un = p.units[u];
+            double* tile = p.acc + size_t(u) * TM2 * TN2;
+            for (int c0 = un.z; c0 < un.w; c0 += p.chunk_kb) {
+                tc::mbar_wait(&tfull[abuf], aphase);
+                tc::tc_fence_after();
+                const bool first = (c0 == un.z);
+#pragma unroll 1
+                for (int cc = 0; cc < TN2 / 32; ++cc) {
+                    uint32_t r[32];
+                    tc::tmem_ld_32x32b_x32(tmem_base + (uint32_t(q * 32) << 16) + uint32_t(abuf * TN2 + cc * 32), r);
+                    tc::tmem_ld_wait();
+                    double* dst = tile + size_t(cc * 32) * TM2 + row;
+                    if (first) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) dst[size_t(j) * TM2] = double(__uint_as_float(r[j]));
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) dst[size_t(j) * TM2] += double(__uint_as_float(r[j]));
+                    }
+                }
+                tc::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(abuf ? tempty_leader1 : tempty_leader0);
+                if (++abuf == 2) { abuf = 0; aphase ^= 1; }
+            }
+        }
+    }
+    tc::tc_fence_before();
+    cluster_sync();
+    if (warp == 1) {
+        tc::tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512u) : "memory");
+    }
+}
+
+__global__ void gram2_reduce(const double* __restrict__ acc, const int* __restrict__ tile_unit, int splits, int ntn,
+                             int I, double* __restrict__ s) {
+    const size_t n = size_t(I) * I;
+    for (size_t e = size_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += size_t(gridDim.x) * blockDim.x) {
+        const int i = int(e % I), j = int(e / I);
+        if (i > j) continue;
+        const int tm = i / TM2, tn = j / TN2;
+        const int u0 = tile_unit[tm * ntn + tn];
+        const size_t off = size_t(j % TN2) * TM2 + (i % TM2);
+        double v = 0.0;
+        for (int k = 0; k < splits; ++k) v += acc[size_t(u0 + k) * TM2 * TN2 + off];
+        s[size_t(i) + size_t(I) * j] = v;
+        s[size_t(j) + size_t(I) * i] = v;
+    }
+}
+
+}  // namespace
+
+bool tc_gram2_supported(atk_ctx* ctx, const atk_tensor* x, int mode) {
+    if (!ctx->gram_2cta || x->dtype != ATK_F32) return false;
+    const Split s = loop_split(x->dims, x->order, mode);
+    if (s.I < 512) return false;  // small Grams: the 1-CTA kernel wastes less on the diagonal
+    if (s.P == 1) return s.I % 4 == 0 && s.O < (1ull << 31) / BK;
+    return s.P >= 32 && s.P % 4 == 0 && s.P * s.I < (1ull << 40) && s.O < (1ull << 31);
+}
+
+void tc_gram2(atk_ctx* ctx, const atk_tensor* x, int mode, double* s_dev) {
+    const Split s = loop_split(x->dims, x->order, mode);
+    const int I = int(s.I);
+    const bool kmajor = s.P != 1;
+    CUtensorMap tm{};
+    const CUtensorMapDataType dt = ctx->tma_tf32 ? CU_TENSOR_MAP_DATA_TYPE_TFLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    uint64_t nkb;
+    int nkb_p = 1;
+    if (!kmajor) {
+        const uint64_t dims[2] = {s.I, s.O};
+        const uint64_t str[1] = {s.I * 4};
+        const uint32_t box[2] = {32, BK};
+        if (encode_tensor_map(&tm, dt, 2, x->data, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) != CUDA_SUCCESS)
+            fail(ATK_CUDA_ERROR, "gram2: tensor map (mode 0) encoding failed");
+        nkb = (s.O + BK - 1) / BK;
+    } else {
+        nkb_p = int((s.P + BK - 1) / BK);
+        const uint64_t dims[3] = {s.P, s.O, s.I};
+        const uint64_t str[2] = {s.P * s.I * 4, s.P * 4};
+        const uint32_t box[3] = {BK, 1, HALF};
+        if (encode_tensor_map(&tm, dt, 3, x->data, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B) != CUDA_SUCCESS)
+            fail(ATK_CUDA_ERROR, "gram2: tensor map (K-major) encoding failed");
+        nkb = uint64_t(nkb_p) * s.O;
+    }
+    const int nt = (I + TM2 - 1) / TM2;
+    std::vector<int> tiles_m, tiles_n;
+    for (int tn = 0; tn < nt; ++tn)
+        for (int tmi = 0; tmi <= tn; ++tmi) {
+            tiles_m.push_back(tmi);
+            tiles_n.push_back(tn);
+        }
+    const int ntiles = int(tiles_m.size());
+    const int pairs_avail = ctx->num_sms / 2;
+    int splits = std::max(1, (pairs_avail + ntiles / 2) / ntiles);
+    splits = int(std::min<uint64_t>(uint64_t(splits), std::max<uint64_t>(1, nkb / 8)));
+    const int chunk_kb = ctx->gram_chunk_kb > 0 ? ctx->gram_chunk_kb : 512;
+    std::vector<int4> units;
+    std::vector<int> tile_unit(size_t(nt) * nt, 0);
+    for (int t = 0; t < ntiles; ++t) {
+        tile_unit[size_t(tiles_m[t]) * nt + tiles_n[t]] = int(units.size());
+        for (int sp = 0; sp < splits; ++sp) {
+            const int kb0 = int(nkb * sp / splits), kb1 = int(nkb * (sp + 1) / splits);
+            units.push_back(make_int4(tiles_m[t], tiles_n[t], kb0, std::max(kb0 + 1, kb1)));
+        }
+    }
+    DevBuf<int4> du(ctx, units.size());
+    DevBuf<int> dtu(ctx, tile_unit.size());
+    DevBuf<double> acc(ctx, units.size() * size_t(TM2) * TN2);
+    ATK_CUDA(cudaMemcpyAsync(du.get(), units.data(), units.size() * sizeof(int4), cudaMemcpyHostToDevice, ctx->stream));
+    ATK_CUDA(cudaMemcpyAsync(dtu.get(), tile_unit.data(), tile_unit.size() * sizeof(int), cudaMemcpyHostToDevice,
+                             ctx->stream));
+    Gram2Params prm{du.get(), int(units.size()), chunk_kb, kmajor ? 1 : 0, nkb_p, acc.get()};
+    static bool attr = false;
+    if (!attr) {
+        ATK_CUDA(cudaFuncSetAttribute(gram_tf32_2cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM2)));
+        attr = true;
+    }
+    const int npairs = std::min<int>(int(units.size()), pairs_avail);
+    gram_tf32_2cta_kernel<<<2 * npairs, THREADS, SMEM2, ctx->stream>>>(tm, prm);
+    ATK_LAUNCHED(ctx);
+    const size_t n = size_t(I) * I;
+    gram2_reduce<<<unsigned(std::min<size_t>((n + 255) / 256, size_t(ctx->num_sms) * 8)), 256, 0, ctx->stream>>>(
+        acc.get(), dtu.get(), splits, nt, I, s_dev);
+    ATK_LAUNCHED(ctx);
+}
+
+}  // namespace atk

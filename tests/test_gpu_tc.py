@@ -91,3 +91,28 @@ def test_tc_ttm_vs_oracle(dims, mode, r, capsys):
         print(f"\nTTM dims={dims} mode={mode} r={r} launches={n_launch} maxrel={err:.2e} normrel={nrm:.2e}")
     assert err <= 4e-3 and nrm <= 1e-4
     assert n_launch == 2  # factor cast + ttm_tf32_kernel
+
+
+@pytest.mark.parametrize("dims,mode", [
+    ((512, 5000), 0), ((2048, 1000), 0), ((768, 33, 20), 0),   # MN-major, CTA pairs
+    ((64, 1024, 5), 1), ((32, 768, 40), 1), ((256, 2048), 1),  # K-major, CTA pairs
+])
+def test_tc_gram_2cta_matches_1cta_and_oracle(dims, mode, capsys):
+    from paper_2010_10131_b200 import atucker
+
+    ctx = atucker.Context.default(0)
+    xd = atucker.DeviceTensor.uniform(list(dims), 17, np.float32)
+    x = xd.to_numpy().astype(np.float64)
+    ctx.set_option("gram_2cta", 1)
+    s2 = atucker.gram(xd, mode)
+    ctx.set_option("gram_2cta", 0)
+    s1 = atucker.gram(xd, mode)
+    ctx.set_option("gram_2cta", 1)
+    ref = gram_np(x, mode)
+    scale = np.abs(ref).max()
+    e2 = np.abs(s2 - ref).max() / scale
+    e1 = np.abs(s1 - ref).max() / scale
+    with capsys.disabled():
+        print(f"\nGRAM2 dims={dims} mode={mode} err2={e2:.2e} err1={e1:.2e} diff={np.abs(s2 - s1).max() / scale:.2e}")
+    assert np.array_equal(s2, s2.T)
+    assert e2 <= 1e-4 and e1 <= 1e-4  # RN tf32 (TMA TFLOAT32)
