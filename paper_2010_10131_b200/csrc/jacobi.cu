@@ -20,8 +20,8 @@
 namespace atk {
 namespace {
 
-constexpr int kGroup = 8;                         // lanes per column pair
-constexpr int kMaxThreads = kGroup * ((kJacobiMax + 1) / 2);  // 448
+constexpr int kGroup = 16;                        // lanes per column pair
+constexpr int kMaxThreads = kGroup * ((kJacobiMax + 1) / 2);  // 896
 
 __device__ __forceinline__ int rr_player(int t, int k, int N) {
     return k == 0 ? 0 : (t + k - 1) % (N - 1) + 1;
@@ -39,6 +39,14 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
     const int tid = threadIdx.x, nt = blockDim.x;
     const int N = n + (n & 1);
     const double tol = fmax(1e-15, 4.0 * n * 2.220446049250313e-16);
+    // tournament schedule precomputed once: sched[t * N/2 + j] = p | q << 8 (p < q)
+    uint16_t* sched = reinterpret_cast<uint16_t*>(lam + n);
+    for (int e = tid; e < (N - 1) * (N / 2); e += nt) {
+        const int t = e / (N / 2), j = e % (N / 2);
+        int p = rr_player(t, j, N), q = rr_player(t, N - 1 - j, N);
+        if (p > q) { const int x = p; p = q; q = x; }
+        sched[e] = uint16_t(p | (q << 8));
+    }
 
     for (int e = tid; e < n * n; e += nt) {
         const int i = e % n, j = e / n;
@@ -56,9 +64,9 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
             bool active = grp < N / 2;
             int p = 0, q = 0;
             if (active) {
-                p = rr_player(t, grp, N);
-                q = rr_player(t, N - 1 - grp, N);
-                if (p > q) { const int x = p; p = q; q = x; }
+                const int pq = sched[t * (N / 2) + grp];
+                p = pq & 255;
+                q = pq >> 8;
                 active = q < n;  // dummy player when n is odd
             }
             double* up = U + ld * p;
@@ -140,7 +148,10 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
 
 }  // namespace
 
-size_t jacobi1s_smem_bytes(int n) { return (size_t(2) * (n + 1) * n + n) * sizeof(double) + 64; }
+size_t jacobi1s_smem_bytes(int n) {
+    const int N = n + (n & 1);
+    return (size_t(2) * (n + 1) * n + n) * sizeof(double) + size_t(N) * (N / 2) * sizeof(uint16_t) + 64;
+}
 
 void jacobi_eig(atk_ctx* ctx, const double* a, int n, int lda, double* values, double* vectors, int ldv,
                 int* sweeps_dev) {

@@ -30,14 +30,17 @@ def test_c5_full_2048_cubed(oracle, capsys):
     x = bench.make_input(atucker, cfg, bench.SEEDS["c5"], ctx)
     res = atucker.sthosvd(x, cfg["ranks"], Strategy.fixed_eig(), ctx=ctx)
     core = res.decomposition.core.to_numpy().astype(np.float64)
+    # engine side: the true ||X - Xhat|| / ||X|| by reconstruction on the device
+    # (the projection identity only holds for an exact fp64 projection: with the
+    # low 1e-2 noise, eps^2 ~ 1e-4 would amplify the tf32 core error 1e4-fold)
+    e_gpu = atucker.relative_error(x, res.decomposition, ctx=ctx)
     xh = x.to_numpy()
     x.free()
     ref = oracle.sthosvd_f32_eig0(xh, cfg["ranks"], threads=os.cpu_count() or 8)
     nx2 = oracle.norm2_f32(xh)
     del xh
     g, gr = np.linalg.norm(core), np.linalg.norm(ref.core)
-    e_gpu = np.sqrt(max(0.0, 1.0 - g * g / nx2))
-    e_cpu = np.sqrt(max(0.0, 1.0 - gr * gr / nx2))
+    e_cpu = np.sqrt(max(0.0, 1.0 - gr * gr / nx2))  # exact for the oracle's fp64 projections
     angles = [principal_angle(a, b) for a, b in zip(res.decomposition.factors, ref.factors)]
     with capsys.disabled():
         print(f"\nC5 full: |G| gpu {g:.9e} cpu {gr:.9e} rel {abs(g - gr) / gr:.2e}; "
