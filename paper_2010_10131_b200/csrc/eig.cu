@@ -560,21 +560,25 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
     ATK_CUDA(cudaMemcpyAsync(S.get(), s_dev, nn * sizeof(double), cudaMemcpyDeviceToDevice, st));
     symmetrize(ctx, S.get(), n);
     mark("prep");
-    const Bounds b = lanczos_bounds(ctx, S.get(), n, psd);
-    mark("lanczos", 0, b.lo);
-
-    // start: one power step on a random block, then SVQB + Rayleigh-Ritz
+    // start: two power steps on a random block (S^2 Omega: on gapped spectra this
+    // alone resolves the wanted subspace), orthonormalise, Rayleigh-Ritz
     fill_normalish<<<nblk(nk), 256, 0, st>>>(Yb.get(), nk, 0xc0ffee11ULL);
     ATK_LAUNCHED(ctx);
     dgemm(ctx, false, false, n, k, n, 1.0, S.get(), n, Yb.get(), n, 0.0, Ya.get(), n);
-    orthonormalize(ctx, Ya.get(), n, k, V.get(), ws);
+    dgemm(ctx, false, false, n, k, n, 1.0, S.get(), n, Ya.get(), n, 0.0, Yb.get(), n);
+    orthonormalize(ctx, Yb.get(), n, k, V.get(), ws);
     mark("qr0");
     rayleigh_ritz(ctx, S.get(), n, k, V.get(), W.get(), T.get(), Z.get(), theta.get(), Ya.get(), sweeps.get());
     mark("rr0");
 
     const int max_outer = 100;
     std::vector<double> hth(k), hres(r);
-    double scale = std::max(std::fabs(b.lo), std::fabs(b.hi));
+    // spectrum bounds for the filter: for a PSD matrix with a clear gap between the
+    // wanted and the block-edge Ritz values, lo = 0 already gives a strong filter;
+    // otherwise (flat spectra) a Lanczos run tightens lo (computed lazily, once)
+    Bounds b{psd ? 0.0 : 0.0, 0.0};
+    bool have_bounds = false;
+    double scale = 0.0;
     int it = 0;
     double worst = 0.0;
     for (;; ++it) {
@@ -587,6 +591,16 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
         worst = 0.0;
         for (int j = 0; j < r; ++j) worst = std::max(worst, hres[j]);
         if (!(scale > 0.0) || worst <= tol * scale || it >= max_outer) break;
+        if (!have_bounds) {
+            const bool gapped = psd && hth[k - 1] >= 0.0 && hth[r - 1] > 10.0 * hth[k - 1];
+            if (gapped) {
+                b = Bounds{0.0, hth[0]};
+            } else {
+                b = lanczos_bounds(ctx, S.get(), n, psd);
+                mark("lanczos", 0, b.lo);
+            }
+            have_bounds = true;
+        }
         // Chebyshev filter on the unwanted interval [lo, cut]
         const double cut = hth[k - 1];
         const double lo = std::min(b.lo, cut - 1e-12 * scale);
