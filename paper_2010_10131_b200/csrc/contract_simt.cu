@@ -1,41 +1,43 @@
-// contract_simt.cu — portable CUDA-core matricization-free contractions.
+// contract_simt.cu — general-shape matricization-free contractions.
 //
-// These are the engine's general-shape path (any P, I, O, R; fp32 or fp64
-// storage, fp64 accumulation).  The hot fp32 shapes dispatch to the tcgen05
-// kernels in contract_tc.cu; everything else (and option "simt") lands here.
+// fp64 storage runs on the fp64 tensor cores (DMMA m8n8k4, dmma.cuh); fp32
+// storage shapes the tcgen05 kernels do not cover (P not in {1} u 32N, tiny I,
+// R > 128) run on CUDA cores with fp64 accumulation.  Option "simt" forces
+// this file for every shape.
 //
 // Index contract (kernels.hpp:34-118, tensor.hpp:175-187): X viewed as
 // (P, I, O), element (p, i, o) at p + P*i + P*I*o.  No unfolding is ever
 // materialised: the K index of every contraction is the (p, o) pair walked in
-// place.
+// place by the tile loaders.
 #include <algorithm>
+#include <type_traits>
 
 #include "atk_internal.cuh"
+#include "dmma.cuh"
 
 namespace atk {
 namespace {
 
-constexpr int TM = 64, TN = 64, KT = 16, NT = 256;
+constexpr int TM = 64, TN = 64, KT = 16, NT = 256, LD = TM + 1;
 
 // Z(I x R) partial over k in [k0, k1) of sum_k X(k, i) Y(k, r), k = (p, o).
 template <class T>
-__global__ void __launch_bounds__(NT) ttt_simt_kernel(const T* __restrict__ x,
-                                                      const T* __restrict__ y, uint64_t P,
-                                                      uint64_t I, uint64_t R, uint64_t K,
-                                                      uint64_t kchunk, bool sym,
+__global__ void __launch_bounds__(NT) ttt_tile_kernel(const T* __restrict__ x, const T* __restrict__ y, uint64_t P,
+                                                      uint64_t I, uint64_t R, uint64_t K, uint64_t kchunk, bool sym,
                                                       double* __restrict__ part) {
     const int tm = blockIdx.x, tn = blockIdx.y;
     if (sym && tn < tm) return;
-    __shared__ double As[KT][TM + 1];
-    __shared__ double Bs[KT][TN + 1];
+    __shared__ double As[KT][LD];
+    __shared__ double Bs[KT][LD];
     const uint64_t i0 = uint64_t(tm) * TM, r0 = uint64_t(tn) * TN;
     const uint64_t kb = uint64_t(blockIdx.z) * kchunk;
     const uint64_t ke = min(K, kb + kchunk);
     const int tid = threadIdx.x;
     const int ty = tid / 16, tx = tid % 16;
     double acc[4][4] = {};
+    dmma::Acc dacc;
+    dmma::zero(dacc);
     for (uint64_t k0 = kb; k0 < ke; k0 += KT) {
-        // load A = X tile [KT][TM]
         for (int e = tid; e < KT * TM; e += NT) {
             int kk, ii;
             if (P == 1) { ii = e % TM; kk = e / TM; } else { kk = e % KT; ii = e / KT; }
@@ -59,37 +61,52 @@ __global__ void __launch_bounds__(NT) ttt_simt_kernel(const T* __restrict__ x,
             Bs[kk][rr] = v;
         }
         __syncthreads();
+        if constexpr (std::is_same_v<T, double>) {
+            dmma::tile_step<LD, LD>(dacc, &As[0][0], &Bs[0][0], KT);
+        } else {
 #pragma unroll
-        for (int kk = 0; kk < KT; ++kk) {
-            double a[4], b[4];
+            for (int kk = 0; kk < KT; ++kk) {
+                double a[4], b[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) a[u] = As[kk][ty + 16 * u];
+                for (int u = 0; u < 4; ++u) a[u] = As[kk][ty + 16 * u];
 #pragma unroll
-            for (int v = 0; v < 4; ++v) b[v] = Bs[kk][tx + 16 * v];
+                for (int v = 0; v < 4; ++v) b[v] = Bs[kk][tx + 16 * v];
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
+                for (int u = 0; u < 4; ++u)
 #pragma unroll
-                for (int v = 0; v < 4; ++v) acc[u][v] = fma(a[u], b[v], acc[u][v]);
+                    for (int v = 0; v < 4; ++v) acc[u][v] = fma(a[u], b[v], acc[u][v]);
+            }
         }
         __syncthreads();
     }
     double* out = part + uint64_t(blockIdx.z) * I * R;
+    if constexpr (std::is_same_v<T, double>) {
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+        for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int v = 0; v < 4; ++v) {
-            const uint64_t i = i0 + ty + 16 * u, r = r0 + tx + 16 * v;
-            if (i < I && r < R) out[i + I * r] = acc[u][v];
-        }
+            for (int j = 0; j < 2; ++j)
+#pragma unroll
+                for (int t = 0; t < 2; ++t) {
+                    const uint64_t ii = i0 + dmma::row_of(i), rr = r0 + dmma::col_of(j, t);
+                    if (ii < I && rr < R) out[ii + I * rr] = dacc.v[i][j][t];
+                }
+    } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                const uint64_t i = i0 + ty + 16 * u, r = r0 + tx + 16 * v;
+                if (i < I && r < R) out[i + I * r] = acc[u][v];
+            }
+    }
 }
 
 // Z = sum_z part[z] in fixed order; for Gram mirror the computed upper
 // triangle (i <= r) onto the lower one => exactly symmetric (kernels.hpp:127-138).
-__global__ void reduce_partials(const double* __restrict__ part, int nsplit, uint64_t I,
-                                uint64_t R, bool sym, double* __restrict__ z) {
+__global__ void reduce_partials(const double* __restrict__ part, int nsplit, uint64_t I, uint64_t R, bool sym,
+                                double* __restrict__ z) {
     const uint64_t n = I * R;
-    for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
-         e += uint64_t(gridDim.x) * blockDim.x) {
+    for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += uint64_t(gridDim.x) * blockDim.x) {
         const uint64_t i = e % I, r = e / I;
         uint64_t src = e;
         if (sym && i > r) src = r + I * i;
@@ -101,16 +118,16 @@ __global__ void reduce_partials(const double* __restrict__ part, int nsplit, uin
 
 // Y(m, r) = sum_i X(m, i) U(r, i), m = (p, o).
 template <class T>
-__global__ void __launch_bounds__(NT) ttm_simt_kernel(const T* __restrict__ x,
-                                                      const double* __restrict__ u, uint64_t P,
-                                                      uint64_t I, uint64_t O, uint64_t R,
-                                                      T* __restrict__ y) {
-    __shared__ double As[KT][TM + 1];
-    __shared__ double Bs[KT][TN + 1];
+__global__ void __launch_bounds__(NT) ttm_tile_kernel(const T* __restrict__ x, const double* __restrict__ u, uint64_t P,
+                                                      uint64_t I, uint64_t O, uint64_t R, T* __restrict__ y) {
+    __shared__ double As[KT][LD];
+    __shared__ double Bs[KT][LD];
     const uint64_t M = P * O;
     const uint64_t m0 = uint64_t(blockIdx.x) * TM, r0 = uint64_t(blockIdx.y) * TN;
     const int tid = threadIdx.x, ty = tid / 16, tx = tid % 16;
     double acc[4][4] = {};
+    dmma::Acc dacc;
+    dmma::zero(dacc);
     for (uint64_t k0 = 0; k0 < I; k0 += KT) {
         for (int e = tid; e < KT * TM; e += NT) {
             int kk, mm;
@@ -129,36 +146,54 @@ __global__ void __launch_bounds__(NT) ttm_simt_kernel(const T* __restrict__ x,
             Bs[kk][rr] = (i < I && r < R) ? u[r + R * i] : 0.0;
         }
         __syncthreads();
+        if constexpr (std::is_same_v<T, double>) {
+            dmma::tile_step<LD, LD>(dacc, &As[0][0], &Bs[0][0], KT);
+        } else {
 #pragma unroll
-        for (int kk = 0; kk < KT; ++kk) {
-            double a[4], b[4];
+            for (int kk = 0; kk < KT; ++kk) {
+                double a[4], b[4];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) a[q] = As[kk][ty + 16 * q];
+                for (int q = 0; q < 4; ++q) a[q] = As[kk][ty + 16 * q];
 #pragma unroll
-            for (int v = 0; v < 4; ++v) b[v] = Bs[kk][tx + 16 * v];
+                for (int v = 0; v < 4; ++v) b[v] = Bs[kk][tx + 16 * v];
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
+                for (int q = 0; q < 4; ++q)
 #pragma unroll
-                for (int v = 0; v < 4; ++v) acc[q][v] = fma(a[q], b[v], acc[q][v]);
+                    for (int v = 0; v < 4; ++v) acc[q][v] = fma(a[q], b[v], acc[q][v]);
+            }
         }
         __syncthreads();
     }
+    if constexpr (std::is_same_v<T, double>) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
+        for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int v = 0; v < 4; ++v) {
-            const uint64_t m = m0 + ty + 16 * q, r = r0 + tx + 16 * v;
-            if (m < M && r < R) {
-                const uint64_t p = m % P, o = m / P;
-                y[p + P * r + P * R * o] = T(acc[q][v]);
+            for (int j = 0; j < 2; ++j)
+#pragma unroll
+                for (int t = 0; t < 2; ++t) {
+                    const uint64_t m = m0 + dmma::row_of(i), r = r0 + dmma::col_of(j, t);
+                    if (m < M && r < R) {
+                        const uint64_t p = m % P, o = m / P;
+                        y[p + P * r + P * R * o] = dacc.v[i][j][t];
+                    }
+                }
+    } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                const uint64_t m = m0 + ty + 16 * q, r = r0 + tx + 16 * v;
+                if (m < M && r < R) {
+                    const uint64_t p = m % P, o = m / P;
+                    y[p + P * r + P * R * o] = T(acc[q][v]);
+                }
             }
-        }
+    }
 }
 
 }  // namespace
 
-void ttt_simt(atk_ctx* ctx, const void* x, const void* y, atk_dtype dt, Split s, uint64_t R,
-              double* z_dev, bool sym) {
+void ttt_simt(atk_ctx* ctx, const void* x, const void* y, atk_dtype dt, Split s, uint64_t R, double* z_dev, bool sym) {
     const uint64_t K = s.P * s.O;
     const uint64_t gm = (s.I + TM - 1) / TM, gn = (R + TN - 1) / TN;
     const uint64_t tiles = sym ? gm * (gm + 1) / 2 : gm * gn;
@@ -169,18 +204,18 @@ void ttt_simt(atk_ctx* ctx, const void* x, const void* y, atk_dtype dt, Split s,
     kchunk = (kchunk + KT - 1) / KT * KT;
     splits = (K + kchunk - 1) / kchunk;
     if (splits == 0) splits = 1;
-    DevBuf<double> part(ctx, splits * s.I * R);
     if (K == 0) {
         ATK_CUDA(cudaMemsetAsync(z_dev, 0, s.I * R * sizeof(double), ctx->stream));
         return;
     }
+    DevBuf<double> part(ctx, splits * s.I * R);
     dim3 grid{unsigned(gm), unsigned(gn), unsigned(splits)};
     if (dt == ATK_F32)
-        ttt_simt_kernel<float><<<grid, NT, 0, ctx->stream>>>((const float*)x, (const float*)y, s.P,
-                                                             s.I, R, K, kchunk, sym, part.get());
+        ttt_tile_kernel<float><<<grid, NT, 0, ctx->stream>>>((const float*)x, (const float*)y, s.P, s.I, R, K, kchunk,
+                                                             sym, part.get());
     else
-        ttt_simt_kernel<double><<<grid, NT, 0, ctx->stream>>>((const double*)x, (const double*)y,
-                                                              s.P, s.I, R, K, kchunk, sym, part.get());
+        ttt_tile_kernel<double><<<grid, NT, 0, ctx->stream>>>((const double*)x, (const double*)y, s.P, s.I, R, K,
+                                                              kchunk, sym, part.get());
     ATK_LAUNCHED(ctx);
     const uint64_t n = s.I * R;
     const int g = int(std::min<uint64_t>((n + 255) / 256, uint64_t(ctx->num_sms) * 8));
@@ -188,16 +223,13 @@ void ttt_simt(atk_ctx* ctx, const void* x, const void* y, atk_dtype dt, Split s,
     ATK_LAUNCHED(ctx);
 }
 
-void ttm_simt(atk_ctx* ctx, const void* x, atk_dtype dt, Split s, const double* u_dev, uint64_t R,
-              void* y) {
+void ttm_simt(atk_ctx* ctx, const void* x, atk_dtype dt, Split s, const double* u_dev, uint64_t R, void* y) {
     const uint64_t M = s.P * s.O;
     dim3 grid{unsigned((M + TM - 1) / TM), unsigned((R + TN - 1) / TN)};
     if (dt == ATK_F32)
-        ttm_simt_kernel<float><<<grid, NT, 0, ctx->stream>>>((const float*)x, u_dev, s.P, s.I, s.O,
-                                                             R, (float*)y);
+        ttm_tile_kernel<float><<<grid, NT, 0, ctx->stream>>>((const float*)x, u_dev, s.P, s.I, s.O, R, (float*)y);
     else
-        ttm_simt_kernel<double><<<grid, NT, 0, ctx->stream>>>((const double*)x, u_dev, s.P, s.I,
-                                                              s.O, R, (double*)y);
+        ttm_tile_kernel<double><<<grid, NT, 0, ctx->stream>>>((const double*)x, u_dev, s.P, s.I, s.O, R, (double*)y);
     ATK_LAUNCHED(ctx);
 }
 

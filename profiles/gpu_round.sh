@@ -1,0 +1,18 @@
+#!/bin/bash
+# One GPU session: tests, bench, reference arm, launch list, ncu captures.
+# Usage: bash profiles/gpu_round.sh TAG [parts...]  (parts: tests bench ref launches ncu)
+TAG=$1; shift
+PARTS=${@:-tests bench ref launches ncu}
+mkdir -p gpurun_out
+python __graft_entry__.py >/dev/null 2>&1 || true
+for p in $PARTS; do
+  case $p in
+    tests) timeout 1500 python -m pytest tests -m gpu -x -q -p no:hypothesispytest > gpurun_out/${TAG}_tests.log 2>&1; echo "tests=$? $(tail -1 gpurun_out/${TAG}_tests.log)";;
+    slow) timeout 1500 python -m pytest tests -m "gpu and slow" -x -q -s -p no:hypothesispytest > gpurun_out/${TAG}_slow.log 2>&1; echo "slow=$? $(tail -1 gpurun_out/${TAG}_slow.log)";;
+    fast) timeout 900 python -m pytest tests -m "gpu and not slow" -x -q -p no:hypothesispytest > gpurun_out/${TAG}_tests.log 2>&1; echo "fast=$? $(tail -1 gpurun_out/${TAG}_tests.log)";;
+    bench) timeout 600 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err; echo "bench=$?"; head -c 400 gpurun_out/${TAG}_bench.json; echo;;
+    ref) timeout 600 python bench.py --impl reference > gpurun_out/${TAG}_ref.json 2> gpurun_out/${TAG}_ref.err; echo "ref=$?"; head -c 300 gpurun_out/${TAG}_ref.json; echo;;
+    launches) timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv python profiles/run_step.py c5 1 > gpurun_out/${TAG}_launches.log 2>&1; echo "launches=$?";;
+    ncu) timeout 900 ncu --set full --clock-control none --import-source on -k regex:"gram_tf32_2cta|ttm_tf32" -c 2 -o gpurun_out/${TAG}_full python profiles/run_step.py c5 1 > gpurun_out/${TAG}_ncu.log 2>&1; echo "ncu=$?";;
+  esac
+done
