@@ -196,6 +196,30 @@ def cpu_sample(cfg, name, threads, budget_s=20.0):
             "seconds": dt, "stage_s": o.stage_times()}
 
 
+def planned_flops(cfg):
+    """Credited flops of the whole workload under cfg's strategy (no GPU needed)."""
+    from paper_2010_10131_b200.selector import Strategy
+
+    st = Strategy.parse(cfg["strategy"])
+    work, kinds = list(cfg["dims"]), []
+    for n, r in enumerate(cfg["ranks"]):
+        j = int(np.prod(work)) // work[n]
+        kinds.append(int(st.decide(n, work[n], r, j)))
+        work[n] = r
+    return sum(sum(f.values()) for f in flops_of(cfg["dims"], cfg["ranks"], kinds))
+
+
+def workload_config(cfg, name, world, flops):
+    """The `config` object, identical for both arms (the reference arm times a
+    bounded slab sample of this same workload, described in its cpu_baseline)."""
+    gdims = tuple(cfg["dims"])
+    return {"workload": f"{name.upper()} {'x'.join(map(str, gdims))} {cfg['dtype']} "
+                        f"ranks {'x'.join(map(str, cfg['ranks']))} {cfg['strategy']} input={cfg['input']}",
+            "l2": "input larger than L2 (no flush needed)" if np.prod(gdims) * 4 > 126e6 else "input fits L2",
+            "parallelism": f"shard last mode x{world}" if world > 1 else "single GPU",
+            "flops_per_step": flops}
+
+
 def run_reference(args, cfg, name):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -210,10 +234,9 @@ def run_reference(args, cfg, name):
     ms = float(np.median([r["seconds"] for r in vals])) * 1e3
     line = {"metric": "st-HOSVD GFLOP/s (Gram+eig+TTM)", "value": v, "unit": "GFLOP/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": f"{name.upper()} sample on host CPU", "dims": cfg["dims"],
-                       "ranks": cfg["ranks"], "strategy": cfg["strategy"]},
+            "config": workload_config(cfg, name, args.gpus, planned_flops(cfg)),
             "cpu_baseline": {k: vals[-1][k] for k in ("kind", "cores", "sample")} | {"value": v, "unit": "GFLOP/s"},
             "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -349,15 +372,9 @@ def main():
     if rank == 0:
         line = {"metric": "st-HOSVD GFLOP/s (Gram+eig+TTM)", "value": value, "unit": "GFLOP/s",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-                "higher_is_better": True, "scaling": "weak" if world > 1 else "strong", "vs_baseline": None,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                 "dtype": "tf32" if cfg["dtype"] == "f32" else "f64", "data": "synthetic",
-                "config": {"workload": f"{args.config.upper()} {'x'.join(map(str, gdims))} {cfg['dtype']} "
-                                       f"ranks {'x'.join(map(str, cfg['ranks']))} {cfg['strategy']} "
-                                       f"input={cfg['input']}",
-                           "l2": "input larger than L2 (no flush needed)" if np.prod(gdims) * 4 > 126e6
-                           else "input fits L2",
-                           "parallelism": f"shard last mode x{world}" if world > 1 else "single GPU",
-                           "flops_per_step": total_flops},
+                "config": workload_config(cfg, args.config, world, total_flops),
                 "stages": stages, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(launches), "clocks": clk.summary()}
         print(json.dumps(line), flush=True)

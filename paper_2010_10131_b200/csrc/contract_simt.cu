@@ -18,7 +18,9 @@
 namespace atk {
 namespace {
 
-constexpr int TM = 64, TN = 64, KT = 16, NT = 256, LD = TM + 1;
+// LD = 68 = 4 (mod 16): conflict-free DMMA fragment loads (dmma.cuh)
+constexpr int TM = 64, TN = 64, KT = 16, NT = 256, LD = TM + 4;
+constexpr int WM = 2, FM = 4, FN = 2;  // 8 warps: 2 x 4, each 32 x 16
 
 // Z(I x R) partial over k in [k0, k1) of sum_k X(k, i) Y(k, r), k = (p, o).
 template <class T>
@@ -35,7 +37,7 @@ __global__ void __launch_bounds__(NT) ttt_tile_kernel(const T* __restrict__ x, c
     const int tid = threadIdx.x;
     const int ty = tid / 16, tx = tid % 16;
     double acc[4][4] = {};
-    dmma::Acc dacc;
+    dmma::Acc<FM, FN> dacc;
     dmma::zero(dacc);
     for (uint64_t k0 = kb; k0 < ke; k0 += KT) {
         for (int e = tid; e < KT * TM; e += NT) {
@@ -62,7 +64,7 @@ __global__ void __launch_bounds__(NT) ttt_tile_kernel(const T* __restrict__ x, c
         }
         __syncthreads();
         if constexpr (std::is_same_v<T, double>) {
-            dmma::tile_step<LD, LD>(dacc, &As[0][0], &Bs[0][0], KT);
+            dmma::tile_step<LD, LD, WM, FM, FN>(dacc, &As[0][0], &Bs[0][0], KT);
         } else {
 #pragma unroll
             for (int kk = 0; kk < KT; ++kk) {
@@ -82,12 +84,12 @@ __global__ void __launch_bounds__(NT) ttt_tile_kernel(const T* __restrict__ x, c
     double* out = part + uint64_t(blockIdx.z) * I * R;
     if constexpr (std::is_same_v<T, double>) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < FM; ++i)
 #pragma unroll
-            for (int j = 0; j < 2; ++j)
+            for (int j = 0; j < FN; ++j)
 #pragma unroll
                 for (int t = 0; t < 2; ++t) {
-                    const uint64_t ii = i0 + dmma::row_of(i), rr = r0 + dmma::col_of(j, t);
+                    const uint64_t ii = i0 + dmma::row_of<WM, FM>(i), rr = r0 + dmma::col_of<WM, FN>(j, t);
                     if (ii < I && rr < R) out[ii + I * rr] = dacc.v[i][j][t];
                 }
     } else {
@@ -126,7 +128,7 @@ __global__ void __launch_bounds__(NT) ttm_tile_kernel(const T* __restrict__ x, c
     const uint64_t m0 = uint64_t(blockIdx.x) * TM, r0 = uint64_t(blockIdx.y) * TN;
     const int tid = threadIdx.x, ty = tid / 16, tx = tid % 16;
     double acc[4][4] = {};
-    dmma::Acc dacc;
+    dmma::Acc<FM, FN> dacc;
     dmma::zero(dacc);
     for (uint64_t k0 = 0; k0 < I; k0 += KT) {
         for (int e = tid; e < KT * TM; e += NT) {
@@ -147,7 +149,7 @@ __global__ void __launch_bounds__(NT) ttm_tile_kernel(const T* __restrict__ x, c
         }
         __syncthreads();
         if constexpr (std::is_same_v<T, double>) {
-            dmma::tile_step<LD, LD>(dacc, &As[0][0], &Bs[0][0], KT);
+            dmma::tile_step<LD, LD, WM, FM, FN>(dacc, &As[0][0], &Bs[0][0], KT);
         } else {
 #pragma unroll
             for (int kk = 0; kk < KT; ++kk) {
@@ -166,12 +168,12 @@ __global__ void __launch_bounds__(NT) ttm_tile_kernel(const T* __restrict__ x, c
     }
     if constexpr (std::is_same_v<T, double>) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < FM; ++i)
 #pragma unroll
-            for (int j = 0; j < 2; ++j)
+            for (int j = 0; j < FN; ++j)
 #pragma unroll
                 for (int t = 0; t < 2; ++t) {
-                    const uint64_t m = m0 + dmma::row_of(i), r = r0 + dmma::col_of(j, t);
+                    const uint64_t m = m0 + dmma::row_of<WM, FM>(i), r = r0 + dmma::col_of<WM, FN>(j, t);
                     if (m < M && r < R) {
                         const uint64_t p = m % P, o = m / P;
                         y[p + P * r + P * R * o] = dacc.v[i][j][t];

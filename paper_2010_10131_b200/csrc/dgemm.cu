@@ -1,29 +1,34 @@
 // dgemm.cu — fp64 GEMM for the eigensolver / ALS small dense algebra.
 //
 // C(m x n) = alpha op(A) op(B) + beta C, column-major.  128x64 block tile,
-// 8-deep K slices, 256 threads each owning an 8x4 register tile (DFMA), and a
+// 8-deep K slices double-buffered in shared memory, 8 warps each owning a
+// 32x32 block computed on the fp64 tensor cores (DMMA m8n8k4, dmma.cuh), and a
 // deterministic split-K (fixed-order fp64 partial sums) so that the skinny
 // shapes of Chebyshev filtering (2048 x 96 x 2048) still fill all 148 SMs.
 #include <algorithm>
 
 #include "atk_internal.cuh"
+#include "dmma.cuh"
 
 namespace atk {
 namespace {
 
 constexpr int BM = 128, BN = 64, BK = 8, NT = 256;
+constexpr int LDA = BM + 4, LDB = BN + 4;   // = 4 (mod 16): conflict-free fragments
+constexpr int WM = 4, FM = 4, FN = 4;       // 8 warps: 4 x 2, each 32 x 32
 
 __global__ void __launch_bounds__(NT) dgemm_tile(bool ta, bool tb, int m, int n, int k, int kchunk,
                                                  const double* __restrict__ a, int lda,
                                                  const double* __restrict__ b, int ldb,
                                                  double* __restrict__ out, size_t out_split_stride,
                                                  int ldo, double alpha, double beta, bool direct) {
-    __shared__ __align__(16) double As[2][BK][BM];
-    __shared__ __align__(16) double Bs[2][BK][BN];
+    __shared__ __align__(16) double As[2][BK][LDA];
+    __shared__ __align__(16) double Bs[2][BK][LDB];
     const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
     const int kb = blockIdx.z * kchunk, ke = min(k, kb + kchunk);
-    const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
-    double acc[8][4] = {};
+    const int tid = threadIdx.x;
+    dmma::Acc<FM, FN> acc;
+    dmma::zero(acc);
 
     auto load = [&](int buf, int k0) {
 #pragma unroll
@@ -47,43 +52,25 @@ __global__ void __launch_bounds__(NT) dgemm_tile(bool ta, bool tb, int m, int n,
     __syncthreads();
     for (int k0 = kb; k0 < ke; k0 += BK) {
         if (k0 + BK < ke) load(buf ^ 1, k0 + BK);
-#pragma unroll
-        for (int kk = 0; kk < BK; ++kk) {
-            const double2* ap = reinterpret_cast<const double2*>(&As[buf][kk][ty * 8]);
-            const double2* bp = reinterpret_cast<const double2*>(&Bs[buf][kk][tx * 4]);
-            double av[8], bv[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const double2 t = ap[u];
-                av[2 * u] = t.x;
-                av[2 * u + 1] = t.y;
-            }
-#pragma unroll
-            for (int v = 0; v < 2; ++v) {
-                const double2 t = bp[v];
-                bv[2 * v] = t.x;
-                bv[2 * v + 1] = t.y;
-            }
-#pragma unroll
-            for (int u = 0; u < 8; ++u)
-#pragma unroll
-                for (int v = 0; v < 4; ++v) acc[u][v] = fma(av[u], bv[v], acc[u][v]);
-        }
+        dmma::tile_step<LDA, LDB, WM, FM, FN>(acc, &As[buf][0][0], &Bs[buf][0][0], BK);
         __syncthreads();
         buf ^= 1;
     }
     double* o = out + size_t(blockIdx.z) * out_split_stride;
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
+    for (int i = 0; i < FM; ++i)
 #pragma unroll
-        for (int v = 0; v < 4; ++v) {
-            const int gm = m0 + ty * 8 + u, gn = n0 + tx * 4 + v;
-            if (gm < m && gn < n) {
-                double* cp = o + gm + size_t(ldo) * gn;
-                if (direct) *cp = alpha * acc[u][v] + (beta == 0.0 ? 0.0 : beta * *cp);
-                else *cp = acc[u][v];
+        for (int j = 0; j < FN; ++j)
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+                const int gm = m0 + dmma::row_of<WM, FM>(i), gn = n0 + dmma::col_of<WM, FN>(j, t);
+                if (gm < m && gn < n) {
+                    double* cp = o + gm + size_t(ldo) * gn;
+                    const double v = acc.v[i][j][t];
+                    if (direct) *cp = alpha * v + (beta == 0.0 ? 0.0 : beta * *cp);
+                    else *cp = v;
+                }
             }
-        }
 }
 
 __global__ void dgemm_splitk_reduce(const double* __restrict__ part, int splits, int m, int n,

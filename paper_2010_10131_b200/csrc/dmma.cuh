@@ -1,23 +1,30 @@
-// dmma.cuh — fp64 tensor-core (DMMA, mma.sync m8n8k4 f64) microkernel for a
-// 64 x 64 output tile computed by 8 warps (2 along M x 4 along N; each warp a
-// 32 x 16 block = 4 x 2 fragments of 8 x 8).  Operands come from shared memory
-// laid out k-major: As[k][m], Bs[k][n] with leading dimensions LDA / LDB.
-// Used by the fp64 contractions (contract_simt.cu) and the fp64 GEMM
-// (dgemm.cu).  fp64 has no tcgen05 kind; DMMA is the sm_100 fp64 tensor path.
+// dmma.cuh — fp64 tensor-core (DMMA, mma.sync m8n8k4 f64) warp microkernel.
+//
+// A CTA tile is split over its warps as WARPS_M along M x (nwarps / WARPS_M)
+// along N; each warp owns FM x FN fragments of 8 x 8.  Operands come from
+// shared memory laid out k-major: As[k][m], Bs[k][n] with leading dimensions
+// LDA / LDB.  Bank-conflict-free fragment loads need LD = 4 (mod 16): the 16
+// lanes of a half-warp read k-rows r = lane & 3 at columns c = lane >> 2, i.e.
+// doubles r * LD + c, distinct mod 16 exactly when LD = 4 (mod 16).
+// Used by the fp64 contractions (contract_simt.cu) and the fp64 GEMM of the
+// eigensolver (dgemm.cu).  fp64 has no tcgen05 kind; DMMA is sm_100's fp64
+// tensor path.
 #pragma once
 
 namespace atk {
 namespace dmma {
 
+template <int FM, int FN>
 struct Acc {
-    double v[4][2][2];  // [m-frag][n-frag][pair]
+    double v[FM][FN][2];  // [m-frag][n-frag][pair]
 };
 
-__device__ __forceinline__ void zero(Acc& a) {
+template <int FM, int FN>
+__device__ __forceinline__ void zero(Acc<FM, FN>& a) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < FM; ++i)
 #pragma unroll
-        for (int j = 0; j < 2; ++j) a.v[i][j][0] = a.v[i][j][1] = 0.0;
+        for (int j = 0; j < FN; ++j) a.v[i][j][0] = a.v[i][j][1] = 0.0;
 }
 
 __device__ __forceinline__ void mma_8x8x4(double& d0, double& d1, double a, double b) {
@@ -26,33 +33,38 @@ __device__ __forceinline__ void mma_8x8x4(double& d0, double& d1, double a, doub
                  : "d"(a), "d"(b));
 }
 
-// acc += As[k0:k0+kk, wm*32 .. +32]^T-fragments x Bs[k0:k0+kk, wn*16 .. +16]
-template <int LDA, int LDB>
-__device__ __forceinline__ void tile_step(Acc& acc, const double* As, const double* Bs, int kk_count) {
+// acc += As[0:kk_count, warp's M block]^T x Bs[0:kk_count, warp's N block]
+template <int LDA, int LDB, int WARPS_M, int FM, int FN>
+__device__ __forceinline__ void tile_step(Acc<FM, FN>& acc, const double* As, const double* Bs, int kk_count) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int wm = warp & 1, wn = warp >> 1;
+    const int wm = warp % WARPS_M, wn = warp / WARPS_M;
     const int r = lane & 3, c = lane >> 2;
+    const double* ap = As + r * LDA + wm * FM * 8 + c;
+    const double* bp = Bs + r * LDB + wn * FN * 8 + c;
+#pragma unroll 2
     for (int kk = 0; kk < kk_count; kk += 4) {
-        double a[4], b[2];
+        double a[FM], b[FN];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) a[i] = As[(kk + r) * LDA + wm * 32 + i * 8 + c];
+        for (int i = 0; i < FM; ++i) a[i] = ap[kk * LDA + i * 8];
 #pragma unroll
-        for (int j = 0; j < 2; ++j) b[j] = Bs[(kk + r) * LDB + wn * 16 + j * 8 + c];
+        for (int j = 0; j < FN; ++j) b[j] = bp[kk * LDB + j * 8];
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < FM; ++i)
 #pragma unroll
-            for (int j = 0; j < 2; ++j) mma_8x8x4(acc.v[i][j][0], acc.v[i][j][1], a[i], b[j]);
+            for (int j = 0; j < FN; ++j) mma_8x8x4(acc.v[i][j][0], acc.v[i][j][1], a[i], b[j]);
     }
 }
 
-// Output coordinates of accumulator element (i, j, t) within the 64 x 64 tile.
+// Tile coordinates of accumulator element v[i][j][t].
+template <int WARPS_M, int FM>
 __device__ __forceinline__ int row_of(int i) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    return (warp & 1) * 32 + i * 8 + (lane >> 2);
+    return (warp % WARPS_M) * FM * 8 + i * 8 + (lane >> 2);
 }
+template <int WARPS_M, int FN>
 __device__ __forceinline__ int col_of(int j, int t) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    return (warp >> 1) * 16 + j * 8 + 2 * (lane & 3) + t;
+    return (warp / WARPS_M) * FN * 8 + j * 8 + 2 * (lane & 3) + t;
 }
 
 }  // namespace dmma

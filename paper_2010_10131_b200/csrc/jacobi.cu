@@ -4,10 +4,10 @@
 // pair by column pair; at convergence A V = U with orthogonal columns, i.e.
 // A = (U Sigma^-1) Sigma V^T, and for symmetric A the eigenvalues are
 // lambda_j = v_j^T A v_j = u_j . v_j, eigenvectors v_j.  Each round rotates
-// the n/2 disjoint column pairs of a round-robin tournament, one 8-lane group
+// the n/2 disjoint column pairs of a round-robin tournament, one 16-lane group
 // per pair (three group-reduced dot products, then the pair's columns of U and
 // V updated in place).  Pairs touch disjoint columns, so a round costs one
-// __syncthreads; the CTA has exactly 8 * n/2 threads so no lane idles.
+// __syncthreads; the CTA has exactly 16 * n/2 threads so no lane idles.
 // U and V live in shared memory (2 n^2 doubles).
 // Used for: the dense eig of small Grams (n <= 112), the Rayleigh-Ritz
 // problems of ChFSI and the Lanczos tridiagonal.  Output sorted descending
@@ -90,16 +90,22 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
             // rounding in the length-n dot products is ~n eps sqrt(ab): a tighter
             // threshold never converges (measured: 40 sweeps at n = 96 with 1e-15)
             if (active && g != 0.0 && fabs(g) > tol * sqrt(a * b)) {
-                // The rotation ANGLE is computed in fp32 (fast div/sqrt: the fp64 chain
-                // div -> sqrt -> div -> rsqrt dominated the round latency); (c, s) are
-                // then normalised in fp64 so the rotation stays orthogonal to fp64
-                // precision.  An angle that is off by ~1e-7 leaves g' ~ 1e-7 g, removed
-                // by the next sweep; the convergence test above is exact fp64.
+                // t = tan(theta) is the small root of t^2 + 2 zeta t - 1 = 0.  A fast
+                // fp32 estimate (the fp64 chain div -> sqrt -> div dominated the round
+                // latency) is polished by one fp64 Newton step whose reciprocal comes
+                // from fp32 rcp: the error squares, ~1e-14.  The angle must be fp64-
+                // accurate: an error eps leaves g'/sqrt(a b) ~ eps sqrt(a/b), which for
+                // a/b ~ 1e12 (RR blocks of gapped Grams) is ~1e-1 with a bare fp32 angle
+                // (measured: 13 sweeps at n = 96 instead of ~7).  (c, s) are normalised
+                // in fp64, so the rotation stays orthogonal.
                 const double zeta = (b - a) / (2.0 * g);
                 double tt;
                 if (fabs(zeta) < 1e15) {
                     const float zf = float(zeta);
-                    tt = double(copysignf(1.0f, zf) / (fabsf(zf) + sqrtf(fmaf(zf, zf, 1.0f))));
+                    const double t0 = double(copysignf(1.0f, zf) / (fabsf(zf) + sqrtf(fmaf(zf, zf, 1.0f))));
+                    const double f = fma(t0, t0, fma(2.0 * zeta, t0, -1.0));
+                    const double fp = 2.0 * (t0 + zeta);
+                    tt = t0 - f * double(__frcp_rn(float(fp)));
                 } else {
                     tt = 0.5 / zeta;
                 }
@@ -174,61 +180,52 @@ void jacobi_eig(atk_ctx* ctx, const double* a, int n, int lda, double* values, d
 namespace atk {
 namespace {
 
-// Cholesky G = L L^T entirely in shared memory, then X = L^{-T} (upper
-// triangular) by back substitution, 4 lanes per column.  One CTA, k <= 112.
-// info = 0 on success, else 1 + the failing pivot (linalg.hpp:169-177 NotSPD).
-__global__ void __launch_bounds__(448) chol_inv_kernel(const double* __restrict__ g, int k,
-                                                       double* __restrict__ x, int* __restrict__ info) {
+// X = L^{-T} for G = L L^T, entirely in shared memory, by symmetric Gauss-Jordan
+// elimination on [G | I]: step c subtracts (A(i,c)/d_c) row_c from every row
+// i > c of both blocks (trailing upper triangle of A, columns <= c of W).  The
+// row scalings by 1/sqrt(d_c) are deferred to the output pass, so each step
+// reads only row c (final after step c-1) and writes rows > c: ONE barrier per
+// step, and no separate triangular inverse (W ends as L^{-1}, X = W^T).
+// One CTA, k <= 112.  info = 0 on success, else 1 + the failing pivot
+// (linalg.hpp:169-177 NotSPD).
+__global__ void __launch_bounds__(1024) chol_inv_kernel(const double* __restrict__ g, int k,
+                                                        double* __restrict__ x, int* __restrict__ info) {
     extern __shared__ double sm[];
     const int ld = k + 1;
-    double* A = sm;                  // k x k (lower factor built in place)
-    double* X = A + size_t(ld) * k;  // k x k
-    __shared__ int bad;
+    double* A = sm;                  // k x k, upper triangle live
+    double* W = A + size_t(ld) * k;  // k x k, becomes L^{-1} (unscaled rows)
     const int tid = threadIdx.x, nt = blockDim.x;
-    if (tid == 0) bad = 0;
-    for (int e = tid; e < k * k; e += nt) A[(e % k) + ld * (e / k)] = g[e];
+    for (int e = tid; e < k * k; e += nt) {
+        const int i = e % k, j = e / k;
+        A[i + ld * j] = g[e];
+        W[i + ld * j] = (i == j) ? 1.0 : 0.0;
+    }
     __syncthreads();
+    int bad = 0;
     for (int c = 0; c < k; ++c) {
         const double d = A[c + ld * c];
-        if (!(d > 0.0)) {
-            if (tid == 0) bad = c + 1;
-            break;  // uniform: every thread read the same pivot
+        if (!(d > 0.0)) {  // uniform: every thread read the same pivot
+            bad = c + 1;
+            break;
         }
-        const double l = sqrt(d), il = 1.0 / l;
-        __syncthreads();
-        if (tid == 0) A[c + ld * c] = l;
-        for (int i = c + 1 + tid; i < k; i += nt) A[i + ld * c] *= il;
-        __syncthreads();
+        const double inv = 1.0 / d;
         const int m = k - c - 1;
-        for (int e = tid; e < m * m; e += nt) {
-            const int i = c + 1 + e % m, j = c + 1 + e / m;
-            if (i >= j) A[i + ld * j] -= A[i + ld * c] * A[j + ld * c];
+        for (int e = tid; e < m * k; e += nt) {
+            const int i = c + 1 + e % m, j = e / m;
+            const double f = A[c + ld * i] * inv;  // A(i, c) / d_c via symmetry
+            if (j <= c) W[i + ld * j] = fma(-f, W[c + ld * j], W[i + ld * j]);
+            else if (j >= i) A[i + ld * j] = fma(-f, A[c + ld * j], A[i + ld * j]);
         }
         __syncthreads();
     }
-    __syncthreads();
     if (bad) {
         if (tid == 0) *info = bad;
         return;
     }
-    // X(:, j) solves L^T X(:, j) = e_j, i = j .. 0; group of 4 lanes per column
-    const int grp = tid >> 2, gl = tid & 3, ngrp = nt >> 2;
-    for (int j0 = 0; j0 < k; j0 += ngrp) {
-        const int j = j0 + grp;
-        const bool act = j < k;
-        double* xc = X + ld * (act ? j : 0);
-        for (int i = k - 1; i >= 0; --i) {
-            double s = 0.0;
-            if (act && i <= j)
-                for (int t = i + 1 + gl; t <= j; t += 4) s = fma(A[t + ld * i], xc[t], s);
-            s += __shfl_xor_sync(0xffffffffu, s, 1);
-            s += __shfl_xor_sync(0xffffffffu, s, 2);
-            if (act && gl == 0) xc[i] = (i > j) ? 0.0 : (((i == j) ? 1.0 : 0.0) - s) / A[i + ld * i];
-            __syncwarp();
-        }
+    for (int e = tid; e < k * k; e += nt) {
+        const int r = e % k, c = e / k;
+        x[e] = (r <= c) ? W[c + ld * r] * rsqrt(A[c + ld * c]) : 0.0;
     }
-    __syncthreads();
-    for (int e = tid; e < k * k; e += nt) x[e] = X[(e % k) + ld * (e / k)];
     if (tid == 0) *info = 0;
 }
 
@@ -243,7 +240,7 @@ void cholesky_inv_t(atk_ctx* ctx, const double* g, int k, double* x, int* info_d
                                       int(size_t(2) * (kJacobiMax + 1) * kJacobiMax * sizeof(double))));
         attr = true;
     }
-    const int threads = std::min(448, std::max(32, (4 * k + 31) / 32 * 32));
+    const int threads = std::min(1024, std::max(64, (k * k / 8 + 31) / 32 * 32));
     chol_inv_kernel<<<1, threads, smem, ctx->stream>>>(g, k, x, info_dev);
     ATK_LAUNCHED(ctx);
 }
