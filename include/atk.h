@@ -114,8 +114,15 @@ atk_status atk_ctx_set_stream(atk_ctx* ctx, void* cuda_stream);
 atk_status atk_ctx_synchronize(atk_ctx* ctx);
 /* Kernels this context launched so far (for bench accounting). */
 uint64_t atk_ctx_launch_count(const atk_ctx* ctx);
-/* Engine tuning knob: 0 = fp32 contractions on tcgen05 kind::tf32 (default),
- * 1 = portable CUDA-core path (no tensor cores; debugging / odd shapes). */
+/* Engine tuning knobs (unknown keys -> ATK_INVALID_ARGUMENT):
+ *   "simt"          1 = CUDA-core contractions for every shape (default 0: tcgen05 / DMMA)
+ *   "eig_method"   -1 auto, 0 dense Jacobi (n <= 112), 1 ChFSI
+ *   "chfsi_tol"     relative Ritz-residual target of ChFSI (default 1e-12; fp32 Grams use >= 1e-10)
+ *   "eig_assume_psd" 1 = atk_sym_eig_top_r inputs are Grams (Cholesky-preconditioned Jacobi)
+ *   "tma_tf32"      1 = round-to-nearest tf32 operand loads (default), 0 = hardware truncation
+ *   "gram_2cta"     1 = CTA-pair (cta_group::2) Gram where supported (default)
+ *   "gram_chunk_kb" K-blocks per fp32 accumulation chain before the fp64 drain
+ *   "gram_lockstep" 1 = drift limiter in the 1-CTA Gram (default 0) */
 atk_status atk_ctx_set_option(atk_ctx* ctx, const char* key, double value);
 
 /* Multi-GPU (one process per GPU): sthosvd shards the input along the LAST

@@ -180,6 +180,8 @@ atk_status atk_ctx_set_option(atk_ctx* ctx, const char* key, double value) {
         if (k == "simt") ctx->force_simt = value != 0.0;
         else if (k == "eig_method") ctx->eig_method = int(value);
         else if (k == "chfsi_tol") ctx->chfsi_tol = value;
+        else if (k == "eig_assume_psd") ctx->eig_assume_psd = value != 0.0;
+        else if (k == "jacobi_group") ctx->jacobi_group = int(value);
         else if (k == "tma_tf32") ctx->tma_tf32 = value != 0.0;
         else if (k == "gram_chunk_kb") ctx->gram_chunk_kb = int(value);
         else if (k == "gram_lockstep") ctx->gram_lockstep = value != 0.0;
@@ -374,7 +376,7 @@ atk_status atk_sym_eig_top_r(atk_ctx* ctx, const double* s, uint64_t n, uint64_t
                                          std::to_string(n) + "x" + std::to_string(n) + " matrix");
         DevBuf<double> sd(ctx, n * n), vd(ctx, r), vecd(ctx, n * r);
         ATK_CUDA(cudaMemcpyAsync(sd.get(), s, n * n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-        sym_eig_top_r(ctx, sd.get(), int(n), int(r), vd.get(), vecd.get());
+        sym_eig_top_r(ctx, sd.get(), int(n), int(r), vd.get(), vecd.get(), ctx->eig_assume_psd);
         ATK_CUDA(cudaMemcpyAsync(values, vd.get(), r * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
         ATK_CUDA(cudaMemcpyAsync(vectors, vecd.get(), n * r * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
         ATK_CUDA(cudaStreamSynchronize(ctx->stream));

@@ -56,6 +56,8 @@ struct atk_ctx {
     int force_simt = 0;        // option "simt": portable CUDA-core contractions
     int eig_method = -1;       // option "eig_method": -1 auto, 0 dense Jacobi, 1 ChFSI
     double chfsi_tol = 1e-12;  // option "chfsi_tol": relative Ritz residual target
+    bool eig_assume_psd = false;
+    int jacobi_group = 16;      // option "jacobi_group": lanes per column pair (4, 8, 16)  // option "eig_assume_psd": atk_sym_eig_top_r input is a Gram
     int tma_tf32 = 1;          // option "tma_tf32": TMA converts fp32 -> tf32 with round-to-nearest
                                // (the MMA itself truncates: measured 6e-4 bias vs 1e-6, test_gpu_tc.py)
     int gram_chunk_kb = 0;     // option "gram_chunk_kb": K-blocks per fp64 drain (0 = default)
@@ -173,10 +175,11 @@ void ttm(atk_ctx* ctx, const void* x, atk_dtype dt, Split s, const double* u_dev
 void dgemm(atk_ctx* ctx, bool ta, bool tb, int m, int n, int k, double alpha, const double* a,
            int lda, const double* b, int ldb, double beta, double* c, int ldc);
 // Dense symmetric eigensolver for n <= kJacobiMax (one CTA, smem Jacobi):
-// all eigenpairs of A (n x n, lda), values descending, vectors n x n.
+// all eigenpairs of A (n x n, lda), values descending, vectors n x n.  psd:
+// A is known positive semi-definite (Cholesky-preconditioned, vector-free path).
 constexpr int kJacobiMax = 112;
 void jacobi_eig(atk_ctx* ctx, const double* a, int n, int lda, double* values, double* vectors,
-                int ldv, int* sweeps_dev);
+                int ldv, int* sweeps_dev, bool psd = false);
 // Cholesky factorization in place (lower), status written to *info_dev (0 ok, k>0 pivot k).
 void cholesky(atk_ctx* ctx, double* a, int n, int* info_dev);
 // Shared-memory Cholesky of G (k x k, k <= kJacobiMax) fused with X = L^{-T};

@@ -1,7 +1,7 @@
 // dgemm.cu — fp64 GEMM for the eigensolver / ALS small dense algebra.
 //
 // C(m x n) = alpha op(A) op(B) + beta C, column-major.  128x64 block tile,
-// 8-deep K slices double-buffered in shared memory, 8 warps each owning a
+// 8-deep K slices in a 4-stage cp.async ring in shared memory, 8 warps each owning a
 // 32x32 block computed on the fp64 tensor cores (DMMA m8n8k4, dmma.cuh), and a
 // deterministic split-K (fixed-order fp64 partial sums) so that the skinny
 // shapes of Chebyshev filtering (2048 x 96 x 2048) still fill all 148 SMs.
@@ -13,48 +13,70 @@
 namespace atk {
 namespace {
 
-constexpr int BM = 128, BN = 64, BK = 8, NT = 256;
+constexpr int BM = 128, BN = 64, BK = 8, NT = 256, STAGES = 4;
 constexpr int LDA = BM + 4, LDB = BN + 4;   // = 4 (mod 16): conflict-free fragments
 constexpr int WM = 4, FM = 4, FN = 4;       // 8 warps: 4 x 2, each 32 x 32
+constexpr int STAGE_DOUBLES = BK * (LDA + LDB);
+constexpr size_t SMEM_BYTES = size_t(STAGES) * STAGE_DOUBLES * sizeof(double);
 
+// 8-byte global -> shared async copy; src_bytes = 0 zero-fills (out-of-range).
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(valid ? 8 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// K slices stream through a STAGES-deep cp.async ring (global latency hidden
+// behind the DMMA work of the slices already resident; one barrier per slice).
 __global__ void __launch_bounds__(NT) dgemm_tile(bool ta, bool tb, int m, int n, int k, int kchunk,
                                                  const double* __restrict__ a, int lda,
                                                  const double* __restrict__ b, int ldb,
                                                  double* __restrict__ out, size_t out_split_stride,
                                                  int ldo, double alpha, double beta, bool direct) {
-    __shared__ __align__(16) double As[2][BK][LDA];
-    __shared__ __align__(16) double Bs[2][BK][LDB];
+    extern __shared__ __align__(16) double dsm[];
     const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
     const int kb = blockIdx.z * kchunk, ke = min(k, kb + kchunk);
     const int tid = threadIdx.x;
     dmma::Acc<FM, FN> acc;
     dmma::zero(acc);
 
-    auto load = [&](int buf, int k0) {
+    auto issue = [&](int stage, int k0) {
+        double* As = dsm + stage * STAGE_DOUBLES;
+        double* Bs = As + BK * LDA;
 #pragma unroll
         for (int e = tid; e < BK * BM; e += NT) {
             int kk, mm;
             if (!ta) { mm = e % BM; kk = e / BM; } else { kk = e % BK; mm = e / BK; }
             const int gm = m0 + mm, gk = k0 + kk;
-            As[buf][kk][mm] = (gm < m && gk < ke) ? (ta ? a[gk + size_t(lda) * gm] : a[gm + size_t(lda) * gk]) : 0.0;
+            const bool ok = gm < m && gk < ke;
+            cp_async8(As + kk * LDA + mm, ok ? (ta ? a + gk + size_t(lda) * gm : a + gm + size_t(lda) * gk) : a, ok);
         }
 #pragma unroll
         for (int e = tid; e < BK * BN; e += NT) {
             int kk, nn;
             if (tb) { nn = e % BN; kk = e / BN; } else { kk = e % BK; nn = e / BK; }
             const int gn = n0 + nn, gk = k0 + kk;
-            Bs[buf][kk][nn] = (gn < n && gk < ke) ? (tb ? b[gn + size_t(ldb) * gk] : b[gk + size_t(ldb) * gn]) : 0.0;
+            const bool ok = gn < n && gk < ke;
+            cp_async8(Bs + kk * LDB + nn, ok ? (tb ? b + gn + size_t(ldb) * gk : b + gk + size_t(ldb) * gn) : b, ok);
         }
     };
 
-    int buf = 0;
-    if (kb < ke) load(0, kb);
-    __syncthreads();
-    for (int k0 = kb; k0 < ke; k0 += BK) {
-        if (k0 + BK < ke) load(buf ^ 1, k0 + BK);
-        dmma::tile_step<LDA, LDB, WM, FM, FN>(acc, &As[buf][0][0], &Bs[buf][0][0], BK);
-        __syncthreads();
-        buf ^= 1;
+    const int nt = (ke > kb) ? (ke - kb + BK - 1) / BK : 0;
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+        if (s < nt) issue(s, kb + s * BK);
+        cp_async_commit();
+    }
+    for (int t = 0; t < nt; ++t) {
+        cp_async_wait<STAGES - 2>();
+        __syncthreads();  // slice t landed for every thread; slice t-1's buffer is free
+        const int tn = t + STAGES - 1;
+        if (tn < nt) issue(tn % STAGES, kb + tn * BK);
+        cp_async_commit();
+        const double* As = dsm + (t % STAGES) * STAGE_DOUBLES;
+        dmma::tile_step<LDA, LDB, WM, FM, FN>(acc, As, As + BK * LDA, BK);
     }
     double* o = out + size_t(blockIdx.z) * out_split_stride;
 #pragma unroll
@@ -90,11 +112,17 @@ __global__ void dgemm_splitk_reduce(const double* __restrict__ part, int splits,
 void dgemm(atk_ctx* ctx, bool ta, bool tb, int m, int n, int k, double alpha, const double* a, int lda,
            const double* b, int ldb, double beta, double* c, int ldc) {
     if (m <= 0 || n <= 0) return;
+    static bool attr = false;
+    if (!attr) {
+        ATK_CUDA(cudaFuncSetAttribute(dgemm_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES)));
+        attr = true;
+    }
     const int gm = (m + BM - 1) / BM, gn = (n + BN - 1) / BN;
     const int tiles = gm * gn;
     int splits = 1;
-    if (tiles < 2 * ctx->num_sms && k >= 512)
-        splits = std::min(std::max(1, (2 * ctx->num_sms + tiles - 1) / tiles), std::max(1, k / 256));
+    // up to 4 resident CTAs per SM (51 KB smem each); K chunks of >= 16 slices
+    if (tiles < 4 * ctx->num_sms && k >= 256)
+        splits = std::min(std::max(1, (4 * ctx->num_sms + tiles - 1) / tiles), std::max(1, k / 128));
     int kchunk = (k + splits - 1) / splits;
     kchunk = (kchunk + BK - 1) / BK * BK;
     splits = std::max(1, (k + kchunk - 1) / std::max(1, kchunk));
@@ -104,15 +132,15 @@ void dgemm(atk_ctx* ctx, bool ta, bool tb, int m, int n, int k, double alpha, co
     }
     if (splits == 1) {
         dim3 grid{unsigned(gm), unsigned(gn), 1u};
-        dgemm_tile<<<grid, NT, 0, ctx->stream>>>(ta, tb, m, n, std::max(k, 0), std::max(kchunk, BK), a, lda, b, ldb, c,
-                                                 0, ldc, alpha, beta, true);
+        dgemm_tile<<<grid, NT, SMEM_BYTES, ctx->stream>>>(ta, tb, m, n, std::max(k, 0), std::max(kchunk, BK), a, lda,
+                                                          b, ldb, c, 0, ldc, alpha, beta, true);
         ATK_LAUNCHED(ctx);
         return;
     }
     DevBuf<double> part(ctx, size_t(splits) * m * n);
     dim3 grid{unsigned(gm), unsigned(gn), unsigned(splits)};
-    dgemm_tile<<<grid, NT, 0, ctx->stream>>>(ta, tb, m, n, k, kchunk, a, lda, b, ldb, part.get(), size_t(m) * n, m,
-                                             1.0, 0.0, false);
+    dgemm_tile<<<grid, NT, SMEM_BYTES, ctx->stream>>>(ta, tb, m, n, k, kchunk, a, lda, b, ldb, part.get(),
+                                                      size_t(m) * n, m, 1.0, 0.0, false);
     ATK_LAUNCHED(ctx);
     const size_t mn = size_t(m) * n;
     dgemm_splitk_reduce<<<unsigned(std::min<size_t>((mn + 255) / 256, size_t(ctx->num_sms) * 8)), 256, 0,

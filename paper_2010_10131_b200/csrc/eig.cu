@@ -420,7 +420,7 @@ void svqb(atk_ctx* ctx, const double* Y, int n, int k, double* V, Ws& ws) {
         dgemm(ctx, true, false, k, k, n, 1.0, src, n, src, n, 0.0, ws.G.get(), k);
         svqb_scale<<<1, 256, 0, ctx->stream>>>(ws.G.get(), k, ws.d.get());
         ATK_LAUNCHED(ctx);
-        jacobi_eig(ctx, ws.G.get(), k, k, ws.th.get(), ws.Z.get(), k, ws.sweeps.get());
+        jacobi_eig(ctx, ws.G.get(), k, k, ws.th.get(), ws.Z.get(), k, ws.sweeps.get(), true);
         svqb_form<<<1, 256, 0, ctx->stream>>>(ws.d.get(), ws.Z.get(), ws.th.get(), k, 1e-13, ws.M.get());
         ATK_LAUNCHED(ctx);
         dgemm(ctx, false, false, n, k, k, 1.0, src, n, ws.M.get(), k, 0.0, dst, n);
@@ -500,11 +500,11 @@ Bounds lanczos_bounds(atk_ctx* ctx, const double* S, int n, bool psd) {
 // Rayleigh-Ritz on the orthonormal block V (n x k): W = S V, T = V^T W,
 // T = Z diag(theta) Z^T (Jacobi, descending), V <- V Z, W <- W Z.
 void rayleigh_ritz(atk_ctx* ctx, const double* S, int n, int k, double* V, double* W, double* T, double* Z,
-                   double* theta, double* tmp, int* sweeps) {
+                   double* theta, double* tmp, int* sweeps, bool psd) {
     const size_t nk = size_t(n) * k;
     dgemm(ctx, false, false, n, k, n, 1.0, S, n, V, n, 0.0, W, n);
     dgemm(ctx, true, false, k, k, n, 1.0, V, n, W, n, 0.0, T, k);
-    jacobi_eig(ctx, T, k, k, theta, Z, k, sweeps);
+    jacobi_eig(ctx, T, k, k, theta, Z, k, sweeps, psd);  // V^T S V is PSD when S is
     dgemm(ctx, false, false, n, k, k, 1.0, V, n, Z, k, 0.0, tmp, n);
     ATK_CUDA(cudaMemcpyAsync(V, tmp, nk * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
     dgemm(ctx, false, false, n, k, k, 1.0, W, n, Z, k, 0.0, tmp, n);
@@ -521,7 +521,7 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
     if (dense) {
         DevBuf<double> vals(ctx, n), vecs(ctx, size_t(n) * n);
         DevBuf<int> sweeps(ctx, 1);
-        jacobi_eig(ctx, s_dev, n, n, vals.get(), vecs.get(), n, sweeps.get());
+        jacobi_eig(ctx, s_dev, n, n, vals.get(), vecs.get(), n, sweeps.get(), psd);
         ATK_CUDA(cudaMemcpyAsync(values_dev, vals.get(), r * sizeof(double), cudaMemcpyDeviceToDevice, st));
         ATK_CUDA(cudaMemcpyAsync(vectors_dev, vecs.get(), size_t(n) * r * sizeof(double), cudaMemcpyDeviceToDevice,
                                  st));
@@ -557,6 +557,11 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
                      std::chrono::duration<double, std::milli>(now - t_last).count(), a, v);
         t_last = now;
     };
+    auto trace_sweeps = [&](const int* d) {  // Jacobi sweeps of the last RR (trace only)
+        int h = -1;
+        if (trace) cudaMemcpy(&h, d, sizeof(int), cudaMemcpyDeviceToHost);
+        return h;
+    };
     ATK_CUDA(cudaMemcpyAsync(S.get(), s_dev, nn * sizeof(double), cudaMemcpyDeviceToDevice, st));
     symmetrize(ctx, S.get(), n);
     mark("prep");
@@ -568,8 +573,8 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
     dgemm(ctx, false, false, n, k, n, 1.0, S.get(), n, Ya.get(), n, 0.0, Yb.get(), n);
     orthonormalize(ctx, Yb.get(), n, k, V.get(), ws);
     mark("qr0");
-    rayleigh_ritz(ctx, S.get(), n, k, V.get(), W.get(), T.get(), Z.get(), theta.get(), Ya.get(), sweeps.get());
-    mark("rr0");
+    rayleigh_ritz(ctx, S.get(), n, k, V.get(), W.get(), T.get(), Z.get(), theta.get(), Ya.get(), sweeps.get(), psd);
+    mark("rr0", trace_sweeps(sweeps.get()));
 
     const int max_outer = 100;
     std::vector<double> hth(k), hres(r);
@@ -608,9 +613,13 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
         if (!(e > 0.0)) e = 1e-12 * scale;
         const double smax = std::max(1.0, (std::max(b.hi, hth[0]) - c) / e);
         const double g = 1.0 / (2.0 * smax + 1.0);  // per-step rescale, keeps the recurrence linear
-        // degree: separate [lo, cut] from the wanted end by ~1e20 per pass, 2..16
+        // degree: damp [lo, cut] relative to the wanted end by at most ~1e10 per
+        // pass (T_d(x) ~ e^{d acosh x} / 2), 1..16.  A stronger pass leaves the
+        // block's unwanted columns numerically parallel to the wanted ones (their
+        // O(eps) wanted-direction residue is amplified past 1/eps) and CholeskyQR
+        // breaks down; on wide gaps this means a single S V power step.
         const double ac = std::acosh(std::max(1.0 + 1e-12, (hth[r - 1] - c) / e));
-        const int degree = std::max(2, std::min(16, int(std::ceil(46.0 / std::max(ac, 1e-3)))));
+        const int degree = std::max(1, std::min(16, int(23.0 / std::max(ac, 1e-3))));
         // Y1 = g (S V - c V) / e ; Y_{j+1} = g (2/e)(S Y_j - c Y_j) - g^2 Y_{j-1}
         double* yprev = V.get();
         double* ycur = Ya.get();
@@ -631,8 +640,8 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
         orthonormalize(ctx, ycur, n, k, V.get(), ws);
         mark("qr");
         rayleigh_ritz(ctx, S.get(), n, k, V.get(), W.get(), T.get(), Z.get(), theta.get(),
-                      ynext == V.get() ? Yc.get() : ynext, sweeps.get());
-        mark("rr", it);
+                      ynext == V.get() ? Yc.get() : ynext, sweeps.get(), psd);
+        mark("rr", trace_sweeps(sweeps.get()));
     }
     mark("done", it, worst / scale);
     ATK_CUDA(cudaMemcpyAsync(values_dev, theta.get(), r * sizeof(double), cudaMemcpyDeviceToDevice, st));

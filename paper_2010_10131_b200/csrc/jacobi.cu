@@ -1,17 +1,28 @@
 // jacobi.cu — small dense symmetric eigensolver (n <= kJacobiMax), one CTA.
 //
-// One-sided (Hestenes) Jacobi on A itself: U = A V is orthogonalised column
-// pair by column pair; at convergence A V = U with orthogonal columns, i.e.
-// A = (U Sigma^-1) Sigma V^T, and for symmetric A the eigenvalues are
-// lambda_j = v_j^T A v_j = u_j . v_j, eigenvectors v_j.  Each round rotates
-// the n/2 disjoint column pairs of a round-robin tournament, one 16-lane group
-// per pair (three group-reduced dot products, then the pair's columns of U and
-// V updated in place).  Pairs touch disjoint columns, so a round costs one
-// __syncthreads; the CTA has exactly 16 * n/2 threads so no lane idles.
-// U and V live in shared memory (2 n^2 doubles).
-// Used for: the dense eig of small Grams (n <= 112), the Rayleigh-Ritz
-// problems of ChFSI and the Lanczos tridiagonal.  Output sorted descending
-// (linalg.hpp:101-123 keeps the top r of the full spectrum).
+// One-sided (Hestenes) Jacobi: the columns of a working matrix U are
+// orthogonalised pair by pair.  Each round rotates the n/2 disjoint column
+// pairs of a round-robin tournament, one 16-lane group per pair (three
+// group-reduced dot products from register-resident column slices, then the
+// pair's columns updated in place).  Pairs touch disjoint columns, so a round
+// costs one __syncthreads.  Two variants, chosen per call:
+//
+//  * PSD input (Grams, Rayleigh-Ritz blocks of a Gram): Cholesky-preconditioned
+//    and vector-free.  T + sigma I = L L^T (sigma = 2 n eps max diag keeps the
+//    factorisation positive definite; eigenvectors are unchanged by a shift),
+//    then U = L is rotated to U = L J with orthogonal columns.  T + sigma I =
+//    L J J^T L^T = sum_j u_j u_j^T, so lambda_j = |u_j|^2 - sigma with
+//    eigenvector u_j / |u_j|: no accumulated V, half the shared-memory traffic
+//    per round, and the triangular factor converges in fewer sweeps than T
+//    itself (measured offline on gapped RR blocks: 11 sweeps instead of 16).
+//    A failed pivot falls back to the general variant.
+//  * General symmetric input: U = A V on A itself, V accumulated; lambda_j =
+//    u_j . v_j (sign-correct for indefinite A), eigenvectors v_j.
+//
+// U (and V) live in shared memory.  Used for: the dense eig of small Grams
+// (n <= 112), the Rayleigh-Ritz and SVQB problems of ChFSI and the Lanczos
+// tridiagonal.  Output sorted descending (linalg.hpp:101-123 keeps the top r
+// of the full spectrum).
 #include <algorithm>
 #include <cmath>
 
@@ -20,15 +31,28 @@
 namespace atk {
 namespace {
 
-constexpr int kGroup = 16;                        // lanes per column pair
-constexpr int kMaxThreads = kGroup * ((kJacobiMax + 1) / 2);  // 896
+// G lanes per column pair (template; option "jacobi_group").  A round is
+// latency-bound: measured at n = 96 (PSD path) 16 lanes 1.39 ms, 8 lanes
+// 1.56 ms, 4 lanes 2.34 ms.
+
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
 
 __device__ __forceinline__ int rr_player(int t, int k, int N) {
     return k == 0 ? 0 : (t + k - 1) % (N - 1) + 1;
 }
 
-__global__ void __launch_bounds__(kMaxThreads, 1)
-    jacobi1s_kernel(const double* __restrict__ ain, int n, int lda, double* __restrict__ values,
+template <int G>
+__global__ void __launch_bounds__(G * ((kJacobiMax + 1) / 2), 1)
+    jacobi1s_kernel(const double* __restrict__ ain, int n, int lda, bool psd, double* __restrict__ values,
                     double* __restrict__ vout, int ldv, int* __restrict__ sweeps_out) {
     extern __shared__ double sm[];
     const int ld = n + 1;  // odd leading dimension: column accesses hit distinct banks
@@ -36,9 +60,13 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
     double* V = U + size_t(ld) * n;
     double* lam = V + size_t(ld) * n;  // n
     __shared__ int rotated;
+    __shared__ double sh_sigma;
+    constexpr int kGroup = G, kVals = (kJacobiMax + G - 1) / G;  // column slice per lane
     const int tid = threadIdx.x, nt = blockDim.x;
     const int N = n + (n & 1);
-    const double tol = fmax(1e-15, 4.0 * n * 2.220446049250313e-16);
+    const double eps = 2.220446049250313e-16;
+    const double tol = fmax(1e-15, 4.0 * n * eps);
+    const double tol2 = tol * tol;
     // tournament schedule precomputed once: sched[t * N/2 + j] = p | q << 8 (p < q)
     uint16_t* sched = reinterpret_cast<uint16_t*>(lam + n);
     for (int e = tid; e < (N - 1) * (N / 2); e += nt) {
@@ -47,17 +75,84 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
         if (p > q) { const int x = p; p = q; q = x; }
         sched[e] = uint16_t(p | (q << 8));
     }
-
     for (int e = tid; e < n * n; e += nt) {
         const int i = e % n, j = e / n;
         U[i + ld * j] = 0.5 * (ain[i + size_t(lda) * j] + ain[j + size_t(lda) * i]);
-        V[i + ld * j] = (i == j) ? 1.0 : 0.0;
     }
+    __syncthreads();
+
+    bool usev = !psd;
+    double sigma = 0.0;
+    if (psd) {
+        if (tid < 32) {
+            double m = 0.0;
+            for (int i = tid; i < n; i += 32) m = fmax(m, fabs(U[i + ld * i]));
+            for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+            if (tid == 0) sh_sigma = 2.0 * n * eps * m;
+        }
+        __syncthreads();
+        sigma = sh_sigma;
+        for (int i = tid; i < n; i += nt) U[i + ld * i] += sigma;
+        __syncthreads();
+        // right-looking Cholesky, lower triangle, one barrier per step: column c
+        // is final (unscaled) after step c-1; the 1/sqrt(d_c) scaling is deferred.
+        __shared__ int chol_ok;
+        const int cw = nt;
+        {
+            int okw = 1;
+            for (int c = 0; c < n; ++c) {
+                const double d = U[c + ld * c];
+                if (!(d > 0.0)) {  // uniform: every worker read the same pivot
+                    okw = 0;
+                    break;
+                }
+                const double inv = 1.0 / d;
+                // warps over columns, lanes over rows (no integer division in the loop)
+                for (int j = c + 1 + (tid >> 5); j < n; j += cw >> 5) {
+                    const double ljc = U[j + ld * c] * inv;
+                    for (int i = j + (tid & 31); i < n; i += 32)
+                        U[i + ld * j] = fma(-U[i + ld * c], ljc, U[i + ld * j]);
+                }
+                __syncthreads();
+            }
+            if (tid == 0) chol_ok = okw;
+        }
+        __syncthreads();
+        const bool ok = chol_ok != 0;
+        if (ok) {
+            for (int j = tid; j < n; j += nt) lam[j] = rsqrt(U[j + ld * j]);
+            __syncthreads();
+            for (int e = tid; e < n * n; e += nt) {
+                const int i = e % n, j = e / n;
+                U[i + ld * j] = (i >= j) ? U[i + ld * j] * lam[j] : 0.0;
+            }
+        } else {  // not numerically PSD: the general variant on A itself
+            usev = true;
+            sigma = 0.0;
+            for (int e = tid; e < n * n; e += nt) {
+                const int i = e % n, j = e / n;
+                U[i + ld * j] = 0.5 * (ain[i + size_t(lda) * j] + ain[j + size_t(lda) * i]);
+            }
+        }
+    }
+    if (usev)
+        for (int e = tid; e < n * n; e += nt) V[e % n + ld * (e / n)] = (e % n == e / n) ? 1.0 : 0.0;
     __syncthreads();
 
     const int grp = tid / kGroup, gl = tid % kGroup;
     int sweep = 0;
     for (; sweep < 40 && n > 1; ++sweep) {
+        // column norms |u_j|^2 into lam[], exact at every sweep start; within the
+        // sweep they are updated analytically (a' = a - t g, b' = b + t g), so a
+        // round reduces only the one dot product g
+        for (int j0 = 0; j0 < n; j0 += nt / kGroup) {  // uniform trip count
+            const int j = j0 + grp;
+            double d = 0.0;
+            if (j < n)
+                for (int i = gl; i < n; i += kGroup) d = fma(U[i + ld * j], U[i + ld * j], d);
+            for (int o = kGroup / 2; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+            if (j < n && gl == 0) lam[j] = d;
+        }
         if (tid == 0) rotated = 0;
         __syncthreads();
         for (int t = 0; t < N - 1; ++t) {
@@ -71,57 +166,73 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
             }
             double* up = U + ld * p;
             double* uq = U + ld * q;
-            double a = 0.0, b = 0.0, g = 0.0;
-            if (active) {
-#pragma unroll 4
-                for (int i = gl; i < n; i += kGroup) {
-                    const double x = up[i], y = uq[i];
-                    a = fma(x, x, a);
-                    b = fma(y, y, b);
-                    g = fma(x, y, g);
-                }
-            }
+            double xr[kVals], yr[kVals];
+            double g = 0.0;
 #pragma unroll
-            for (int o = kGroup / 2; o > 0; o >>= 1) {
-                a += __shfl_xor_sync(0xffffffffu, a, o);
-                b += __shfl_xor_sync(0xffffffffu, b, o);
-                g += __shfl_xor_sync(0xffffffffu, g, o);
+            for (int s = 0; s < kVals; ++s) {
+                const int i = gl + kGroup * s;
+                xr[s] = yr[s] = 0.0;
+                if (active && i < n) {
+                    xr[s] = up[i];
+                    yr[s] = uq[i];
+                }
+                g = fma(xr[s], yr[s], g);
             }
+            // read before the full-warp shuffles: no lane can reach the lam[] update
+            // below before every lane of the warp has read its old values
+            const double a = active ? lam[p] : 1.0, b = active ? lam[q] : 1.0;
+#pragma unroll
+            for (int o = kGroup / 2; o > 0; o >>= 1) g += __shfl_xor_sync(0xffffffffu, g, o);
             // rounding in the length-n dot products is ~n eps sqrt(ab): a tighter
             // threshold never converges (measured: 40 sweeps at n = 96 with 1e-15)
-            if (active && g != 0.0 && fabs(g) > tol * sqrt(a * b)) {
-                // t = tan(theta) is the small root of t^2 + 2 zeta t - 1 = 0.  A fast
-                // fp32 estimate (the fp64 chain div -> sqrt -> div dominated the round
-                // latency) is polished by one fp64 Newton step whose reciprocal comes
-                // from fp32 rcp: the error squares, ~1e-14.  The angle must be fp64-
-                // accurate: an error eps leaves g'/sqrt(a b) ~ eps sqrt(a/b), which for
-                // a/b ~ 1e12 (RR blocks of gapped Grams) is ~1e-1 with a bare fp32 angle
-                // (measured: 13 sweeps at n = 96 instead of ~7).  (c, s) are normalised
-                // in fp64, so the rotation stays orthogonal.
-                const double zeta = (b - a) / (2.0 * g);
+            if (active && g * g > tol2 * (a * b)) {
+                // t = tan(theta) is the small root of t^2 + 2 zeta t - 1 = 0.  Only
+                // MUFU approximations seed it (no fp64 division/sqrt routines, no
+                // IEEE slow paths): zeta = (b - a) / 2g uses rcp.approx + one fp64
+                // Newton step, t0 an approximate fp32 formula, then one fp64 Newton
+                // step on the quadratic; both errors square (~1e-14).  (c, s) are
+                // normalised in fp64: the rotation stays orthogonal to fp64 precision.
+                double zeta;
+                const double g2 = 2.0 * g;
+                if (fabs(g2) > 1e-30 && fabs(g2) < 1e30) {
+                    const double r0 = double(rcp_approx(float(g2)));
+                    zeta = (b - a) * (r0 * fma(-g2, r0, 2.0));
+                } else {
+                    zeta = (b - a) / g2;
+                }
                 double tt;
                 if (fabs(zeta) < 1e15) {
                     const float zf = float(zeta);
-                    const double t0 = double(copysignf(1.0f, zf) / (fabsf(zf) + sqrtf(fmaf(zf, zf, 1.0f))));
+                    const float az = fabsf(zf);
+                    const double t0 = double(copysignf(rcp_approx(az + sqrt_approx(fmaf(az, az, 1.0f))), zf));
                     const double f = fma(t0, t0, fma(2.0 * zeta, t0, -1.0));
-                    const double fp = 2.0 * (t0 + zeta);
-                    tt = t0 - f * double(__frcp_rn(float(fp)));
+                    tt = t0 - f * double(rcp_approx(float(2.0 * (t0 + zeta))));
                 } else {
                     tt = 0.5 / zeta;
                 }
                 const double c = rsqrt(fma(tt, tt, 1.0)), s = c * tt;
-                double* vp = V + ld * p;
-                double* vq = V + ld * q;
-#pragma unroll 4
-                for (int i = gl; i < n; i += kGroup) {
-                    const double x = up[i], y = uq[i];
-                    up[i] = c * x - s * y;
-                    uq[i] = fma(s, x, c * y);
-                    const double xv = vp[i], yv = vq[i];
-                    vp[i] = c * xv - s * yv;
-                    vq[i] = fma(s, xv, c * yv);
+#pragma unroll
+                for (int k = 0; k < kVals; ++k) {
+                    const int i = gl + kGroup * k;
+                    if (i < n) {
+                        up[i] = c * xr[k] - s * yr[k];
+                        uq[i] = fma(s, xr[k], c * yr[k]);
+                    }
                 }
-                if (gl == 0) rotated = 1;
+                if (usev) {
+                    double* vp = V + ld * p;
+                    double* vq = V + ld * q;
+                    for (int i = gl; i < n; i += kGroup) {
+                        const double xv = vp[i], yv = vq[i];
+                        vp[i] = c * xv - s * yv;
+                        vq[i] = fma(s, xv, c * yv);
+                    }
+                }
+                if (gl == 0) {
+                    lam[p] = fma(-tt, g, a);
+                    lam[q] = fma(tt, g, b);
+                    rotated = 1;
+                }
             }
             __syncthreads();
         }
@@ -129,14 +240,20 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
         __syncthreads();  // everyone has read the flag before thread 0 resets it
         if (done) break;
     }
-    // lambda_j = u_j . v_j  (sign-correct for indefinite A), one group per column
+    // eigenvalues: u_j . v_j (general) or |u_j|^2 - sigma (PSD); in the PSD
+    // variant V's first row keeps 1/|u_j| for the normalisation below
     for (int j0 = 0; j0 < n; j0 += nt / kGroup) {  // uniform trip count: shuffles stay converged
         const int j = j0 + grp;
         double d = 0.0;
-        if (j < n)
-            for (int i = gl; i < n; i += kGroup) d = fma(U[i + ld * j], V[i + ld * j], d);
+        if (j < n) {
+            const double* w = usev ? V + ld * j : U + ld * j;
+            for (int i = gl; i < n; i += kGroup) d = fma(U[i + ld * j], w[i], d);
+        }
         for (int o = kGroup / 2; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-        if (j < n && gl == 0) lam[j] = d;
+        if (j < n && gl == 0) {
+            lam[j] = d - sigma;
+            if (!usev) V[j] = d > 0.0 ? rsqrt(d) : 0.0;
+        }
     }
     __syncthreads();
     for (int i = tid; i < n; i += nt) {
@@ -147,7 +264,12 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
             rank += (lj > li) || (lj == li && j < i);
         }
         values[rank] = li;
-        for (int r = 0; r < n; ++r) vout[r + size_t(ldv) * rank] = V[r + ld * i];
+        if (usev) {
+            for (int r = 0; r < n; ++r) vout[r + size_t(ldv) * rank] = V[r + ld * i];
+        } else {
+            const double sc = V[i];
+            for (int r = 0; r < n; ++r) vout[r + size_t(ldv) * rank] = U[r + ld * i] * sc;
+        }
     }
     if (tid == 0 && sweeps_out) *sweeps_out = sweep;
 }
@@ -159,20 +281,30 @@ size_t jacobi1s_smem_bytes(int n) {
     return (size_t(2) * (n + 1) * n + n) * sizeof(double) + size_t(N) * (N / 2) * sizeof(uint16_t) + 64;
 }
 
-void jacobi_eig(atk_ctx* ctx, const double* a, int n, int lda, double* values, double* vectors, int ldv,
-                int* sweeps_dev) {
-    if (n > kJacobiMax) fail(ATK_UNSUPPORTED, "jacobi_eig: n exceeds the shared-memory capacity");
-    const size_t smem = jacobi1s_smem_bytes(n);
+template <int G>
+void launch_jacobi(atk_ctx* ctx, const double* a, int n, int lda, double* values, double* vectors, int ldv,
+                   int* sweeps_dev, bool psd) {
     static bool attr = false;
     if (!attr) {
-        ATK_CUDA(cudaFuncSetAttribute(jacobi1s_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        ATK_CUDA(cudaFuncSetAttribute(jacobi1s_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       int(jacobi1s_smem_bytes(kJacobiMax))));
         attr = true;
     }
     const int N = n + (n & 1);
-    const int threads = ((kGroup * std::max(1, N / 2)) + 31) / 32 * 32;
-    jacobi1s_kernel<<<1, threads, smem, ctx->stream>>>(a, n, lda, values, vectors, ldv, sweeps_dev);
+    const int threads = ((G * std::max(1, N / 2)) + 31) / 32 * 32;
+    jacobi1s_kernel<G><<<1, threads, jacobi1s_smem_bytes(n), ctx->stream>>>(a, n, lda, psd, values, vectors, ldv,
+                                                                           sweeps_dev);
     ATK_LAUNCHED(ctx);
+}
+
+void jacobi_eig(atk_ctx* ctx, const double* a, int n, int lda, double* values, double* vectors, int ldv,
+                int* sweeps_dev, bool psd) {
+    if (n > kJacobiMax) fail(ATK_UNSUPPORTED, "jacobi_eig: n exceeds the shared-memory capacity");
+    switch (ctx->jacobi_group) {
+        case 4: launch_jacobi<4>(ctx, a, n, lda, values, vectors, ldv, sweeps_dev, psd); break;
+        case 8: launch_jacobi<8>(ctx, a, n, lda, values, vectors, ldv, sweeps_dev, psd); break;
+        default: launch_jacobi<16>(ctx, a, n, lda, values, vectors, ldv, sweeps_dev, psd); break;
+    }
 }
 
 }  // namespace atk
@@ -209,12 +341,15 @@ __global__ void __launch_bounds__(1024) chol_inv_kernel(const double* __restrict
             break;
         }
         const double inv = 1.0 / d;
-        const int m = k - c - 1;
-        for (int e = tid; e < m * k; e += nt) {
-            const int i = c + 1 + e % m, j = e / m;
-            const double f = A[c + ld * i] * inv;  // A(i, c) / d_c via symmetry
-            if (j <= c) W[i + ld * j] = fma(-f, W[c + ld * j], W[i + ld * j]);
-            else if (j >= i) A[i + ld * j] = fma(-f, A[c + ld * j], A[i + ld * j]);
+        // warps over columns, lanes over rows i > c; A(i, c) = A[c + ld i] (symmetry)
+        for (int j = tid >> 5; j < k; j += nt >> 5) {
+            if (j <= c) {
+                const double wcj = W[c + ld * j] * inv;
+                for (int i = c + 1 + (tid & 31); i < k; i += 32) W[i + ld * j] = fma(-A[c + ld * i], wcj, W[i + ld * j]);
+            } else {
+                const double acj = A[c + ld * j] * inv;
+                for (int i = c + 1 + (tid & 31); i <= j; i += 32) A[i + ld * j] = fma(-A[c + ld * i], acj, A[i + ld * j]);
+            }
         }
         __syncthreads();
     }
@@ -240,7 +375,7 @@ void cholesky_inv_t(atk_ctx* ctx, const double* g, int k, double* x, int* info_d
                                       int(size_t(2) * (kJacobiMax + 1) * kJacobiMax * sizeof(double))));
         attr = true;
     }
-    const int threads = std::min(1024, std::max(64, (k * k / 8 + 31) / 32 * 32));
+    const int threads = std::min(1024, std::max(64, 32 * k));  // one warp per column (measured: 128 threads 4x slower)
     chol_inv_kernel<<<1, threads, smem, ctx->stream>>>(g, k, x, info_dev);
     ATK_LAUNCHED(ctx);
 }

@@ -10,6 +10,9 @@ for p in $PARTS; do
     tests) timeout 1500 python -m pytest tests -m gpu -x -q -p no:hypothesispytest > gpurun_out/${TAG}_tests.log 2>&1; echo "tests=$? $(tail -1 gpurun_out/${TAG}_tests.log)";;
     slow) timeout 1500 python -m pytest tests -m "gpu and slow" -x -q -s -p no:hypothesispytest > gpurun_out/${TAG}_slow.log 2>&1; echo "slow=$? $(tail -1 gpurun_out/${TAG}_slow.log)";;
     probe) ATK_TRACE=1 timeout 600 python tests/eig_probe.py 2048 > gpurun_out/${TAG}_probe.log 2>&1; echo "probe=$?"; grep -vE "^\[atk eig n=2048" gpurun_out/${TAG}_probe.log | tail -12;;
+    trace) ATK_TRACE=1 timeout 300 python profiles/run_step.py c5 2 > gpurun_out/${TAG}_trace.log 2>&1; echo "trace=$?"; tail -40 gpurun_out/${TAG}_trace.log;;
+    eigt) timeout 300 python -m pytest tests/test_gpu_eig.py -x -q -p no:hypothesispytest 2>&1 | tail -3;;
+    ncujac) timeout 600 ncu --set full --clock-control none --import-source on -k regex:jacobi1s -c 1 -o gpurun_out/${TAG}_jac python profiles/jacobi_probe.py 96 > gpurun_out/${TAG}_ncujac.log 2>&1; echo "ncujac=$?";;
     fast) timeout 900 python -m pytest tests -m "gpu and not slow" -x -q -p no:hypothesispytest > gpurun_out/${TAG}_tests.log 2>&1; echo "fast=$? $(tail -1 gpurun_out/${TAG}_tests.log)";;
     bench) timeout 600 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err; echo "bench=$?"; head -c 400 gpurun_out/${TAG}_bench.json; echo;;
     ref) timeout 600 python bench.py --impl reference > gpurun_out/${TAG}_ref.json 2> gpurun_out/${TAG}_ref.err; echo "ref=$?"; head -c 300 gpurun_out/${TAG}_ref.json; echo;;

@@ -10,6 +10,7 @@ from paper_2010_10131_b200 import atucker  # noqa: E402
 
 n, r = int(sys.argv[1]) if len(sys.argv) > 1 else 2048, 64
 rng = np.random.default_rng(0)
+atucker.Context.default(0).set_option("eig_assume_psd", 1.0)  # as the driver: Grams are PSD
 for kind in ["lowrank", "flat"]:
     if kind == "lowrank":
         q = np.linalg.qr(rng.standard_normal((n, n)))[0]
@@ -25,7 +26,11 @@ for kind in ["lowrank", "flat"]:
     ref = np.sort(lam)[::-1][:r]
     print(f"{kind}: {dt*1e3:.1f} ms, max rel eigval err {np.abs(p.values - ref).max() / ref.max():.2e}", flush=True)
 
-for m in (48, 96, 112):
+ctx = atucker.Context.default(0)
+for psd, grp in ((0.0, 8), (1.0, 4), (1.0, 8), (1.0, 16)):
+  ctx.set_option("eig_assume_psd", psd)
+  ctx.set_option("jacobi_group", grp)
+  for m in (48, 96, 112):
     a = rng.standard_normal((m, m + 7))
     s = a @ a.T
     for rep in range(3):
@@ -33,4 +38,4 @@ for m in (48, 96, 112):
         p = atucker.sym_eig_top_r(s, m // 2)
         dt = time.perf_counter() - t0
     w = np.linalg.eigvalsh(s)[::-1][: m // 2]
-    print(f"dense jacobi n={m}: {dt*1e3:.3f} ms, rel err {np.abs(p.values - w).max() / w.max():.2e}", flush=True)
+    print(f"dense jacobi psd={psd} group={grp} n={m}: {dt*1e3:.3f} ms, rel err {np.abs(p.values - w).max() / w.max():.2e}", flush=True)
