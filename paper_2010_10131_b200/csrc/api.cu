@@ -181,7 +181,6 @@ atk_status atk_ctx_set_option(atk_ctx* ctx, const char* key, double value) {
         else if (k == "eig_method") ctx->eig_method = int(value);
         else if (k == "chfsi_tol") ctx->chfsi_tol = value;
         else if (k == "eig_assume_psd") ctx->eig_assume_psd = value != 0.0;
-        else if (k == "jacobi_group") ctx->jacobi_group = int(value);
         else if (k == "tma_tf32") ctx->tma_tf32 = value != 0.0;
         else if (k == "gram_chunk_kb") ctx->gram_chunk_kb = int(value);
         else if (k == "gram_lockstep") ctx->gram_lockstep = value != 0.0;

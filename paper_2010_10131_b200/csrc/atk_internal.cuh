@@ -56,8 +56,7 @@ struct atk_ctx {
     int force_simt = 0;        // option "simt": portable CUDA-core contractions
     int eig_method = -1;       // option "eig_method": -1 auto, 0 dense Jacobi, 1 ChFSI
     double chfsi_tol = 1e-12;  // option "chfsi_tol": relative Ritz residual target
-    bool eig_assume_psd = false;
-    int jacobi_group = 16;      // option "jacobi_group": lanes per column pair (4, 8, 16)  // option "eig_assume_psd": atk_sym_eig_top_r input is a Gram
+    bool eig_assume_psd = false;  // option "eig_assume_psd": atk_sym_eig_top_r input is a Gram
     int tma_tf32 = 1;          // option "tma_tf32": TMA converts fp32 -> tf32 with round-to-nearest
                                // (the MMA itself truncates: measured 6e-4 bias vs 1e-6, test_gpu_tc.py)
     int gram_chunk_kb = 0;     // option "gram_chunk_kb": K-blocks per fp64 drain (0 = default)
@@ -178,6 +177,9 @@ void dgemm(atk_ctx* ctx, bool ta, bool tb, int m, int n, int k, double alpha, co
 // all eigenpairs of A (n x n, lda), values descending, vectors n x n.  psd:
 // A is known positive semi-definite (Cholesky-preconditioned, vector-free path).
 constexpr int kJacobiMax = 112;
+// PSD inputs up to this size still fit (U only): sweeps_dev = -1 if the
+// Cholesky preconditioning fails (caller falls back to ChFSI).
+constexpr int kJacobiPsdMax = 152;
 void jacobi_eig(atk_ctx* ctx, const double* a, int n, int lda, double* values, double* vectors,
                 int ldv, int* sweeps_dev, bool psd = false);
 // Cholesky factorization in place (lower), status written to *info_dev (0 ok, k>0 pivot k).
@@ -185,6 +187,11 @@ void cholesky(atk_ctx* ctx, double* a, int n, int* info_dev);
 // Shared-memory Cholesky of G (k x k, k <= kJacobiMax) fused with X = L^{-T};
 // *info_dev = 0 or 1 + failing pivot.
 void cholesky_inv_t(atk_ctx* ctx, const double* g, int k, double* x, int* info_dev);
+// Q (m x n, n <= kJacobiMax) = orthonormal basis of span(A) by shifted
+// CholeskyQR3; false if a Cholesky pivot failed (caller falls back).
+bool orthonormal_basis_cholqr(atk_ctx* ctx, const double* a, int m, int n, double* q);
+// Zero the strictly lower triangle of the n x n column-major matrix r.
+void zero_lower(atk_ctx* ctx, double* r, int n);
 // X = A^{-1} B given the Cholesky factor L (lower) of A: B overwritten.
 void cholesky_solve(atk_ctx* ctx, const double* l, int n, double* b, int nrhs);
 // Householder thin QR of A (m x n, m >= n): Q (m x n), R (n x n), diag(R) >= 0.

@@ -118,6 +118,23 @@ __global__ void reduce_partials(const double* __restrict__ part, int nsplit, uin
     }
 }
 
+// The same with many splits and few elements (skinny Grams: I x R small, J
+// huge): one warp per element, lanes stride the splits, fixed shuffle tree
+// (deterministic: the summation order depends only on nsplit).
+__global__ void reduce_partials_wide(const double* __restrict__ part, int nsplit, uint64_t I, uint64_t R, bool sym,
+                                     double* __restrict__ z) {
+    const uint64_t n = I * R;
+    const uint64_t e = uint64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (e >= n) return;  // warp-uniform
+    const uint64_t i = e % I, r = e / I;
+    const uint64_t src = (sym && i > r) ? r + I * i : e;
+    double s = 0.0;
+    for (int k = lane; k < nsplit; k += 32) s += part[uint64_t(k) * n + src];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) z[e] = s;
+}
+
 // Y(m, r) = sum_i X(m, i) U(r, i), m = (p, o).
 template <class T>
 __global__ void __launch_bounds__(NT) ttm_tile_kernel(const T* __restrict__ x, const double* __restrict__ u, uint64_t P,
@@ -220,8 +237,13 @@ void ttt_simt(atk_ctx* ctx, const void* x, const void* y, atk_dtype dt, Split s,
                                                               kchunk, sym, part.get());
     ATK_LAUNCHED(ctx);
     const uint64_t n = s.I * R;
-    const int g = int(std::min<uint64_t>((n + 255) / 256, uint64_t(ctx->num_sms) * 8));
-    reduce_partials<<<g, 256, 0, ctx->stream>>>(part.get(), int(splits), s.I, R, sym, z_dev);
+    if (splits >= 64 && n <= (uint64_t(1) << 22)) {
+        reduce_partials_wide<<<unsigned((n + 7) / 8), 256, 0, ctx->stream>>>(part.get(), int(splits), s.I, R, sym,
+                                                                            z_dev);
+    } else {
+        const int g = int(std::min<uint64_t>((n + 255) / 256, uint64_t(ctx->num_sms) * 8));
+        reduce_partials<<<g, 256, 0, ctx->stream>>>(part.get(), int(splits), s.I, R, sym, z_dev);
+    }
     ATK_LAUNCHED(ctx);
 }
 

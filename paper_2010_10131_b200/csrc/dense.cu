@@ -433,4 +433,16 @@ void transpose(atk_ctx* ctx, const double* a, int rows, int cols, double* at) {
     ATK_LAUNCHED(ctx);
 }
 
+namespace {
+__global__ void zero_lower_kernel(double* r, int n) {
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n * n; e += gridDim.x * blockDim.x)
+        if (e % n > e / n) r[e] = 0.0;
+}
+}  // namespace
+
+void zero_lower(atk_ctx* ctx, double* r, int n) {
+    zero_lower_kernel<<<std::max(1, std::min(64, (n * n + 255) / 256)), 256, 0, ctx->stream>>>(r, n);
+    ATK_LAUNCHED(ctx);
+}
+
 }  // namespace atk

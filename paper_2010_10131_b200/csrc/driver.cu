@@ -97,13 +97,26 @@ ModeOut eig_mode(atk_ctx* ctx, const atk_tensor* y, int mode, uint64_t r, int so
 
 // ------------------------------------------------------------------ ALS
 // spd_solve(A, I) (linalg.hpp:169-177) on the device: returns A^{-1}.
+// (A)^{-1} for SPD A, as the reference's spd_solve(A, I) (solvers.hpp:104,109;
+// linalg.hpp:169-177, NotSPD on a non-positive pivot).  n <= 112: one-CTA
+// Cholesky fused with X = L^{-T}, then A^{-1} = X X^T (two launches instead of
+// a column-serial triangular solve).
 static void spd_inverse(atk_ctx* ctx, const double* a, int n, double* inv) {
-    DevBuf<double> l(ctx, size_t(n) * n);
     DevBuf<int> info(ctx, 1);
+    int h = 0;
+    if (n <= kJacobiMax) {
+        DevBuf<double> x(ctx, size_t(n) * n);
+        cholesky_inv_t(ctx, a, n, x.get(), info.get());
+        dgemm(ctx, false, true, n, n, n, 1.0, x.get(), n, x.get(), n, 0.0, inv, n);
+        ATK_CUDA(cudaMemcpyAsync(&h, info.get(), sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+        ATK_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (h != 0) fail(ATK_NOT_SPD, "Cholesky factorization hit a non-positive pivot");
+        return;
+    }
+    DevBuf<double> l(ctx, size_t(n) * n);
     ATK_CUDA(cudaMemcpyAsync(l.get(), a, size_t(n) * n * sizeof(double), cudaMemcpyDeviceToDevice,
                              ctx->stream));
     cholesky(ctx, l.get(), n, info.get());
-    int h = 0;
     ATK_CUDA(cudaMemcpyAsync(&h, info.get(), sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     ATK_CUDA(cudaStreamSynchronize(ctx->stream));
     if (h != 0) fail(ATK_NOT_SPD, "Cholesky factorization hit a non-positive pivot");
@@ -146,7 +159,7 @@ AlsOut als_iterate(atk_ctx* ctx, const atk_tensor* y, int mode, const double* l0
         if (ctx->comm) fail(ATK_UNSUPPORTED, "ALS under a multi-GPU communicator is not wired yet");
         contract_ttt(ctx, y, out.rfac, mode, YR.get(), false);  // YR = Y_(n) rfac_(n)^T
         record_gemm(2LL * (long long)(I * r) * (long long)J);
-        contract_ttt(ctx, out.rfac, out.rfac, mode, GR.get(), false);
+        contract_ttt(ctx, out.rfac, out.rfac, mode, GR.get(), true);  // symmetric: the Gram kernels
         record_gemm(2LL * (long long)(r * r) * (long long)J);
         spd_inverse(ctx, GR.get(), int(r), GRi.get());
         dgemm(ctx, false, false, int(I), int(r), int(r), 1.0, YR.get(), int(I), GRi.get(), int(r),
@@ -169,11 +182,22 @@ AlsOut als_iterate(atk_ctx* ctx, const atk_tensor* y, int mode, const double* l0
     return out;
 }
 
-// thin_qr (linalg.hpp:126-149) on the device, host in/out.
+// thin_qr (linalg.hpp:126-149) on the device.  Q R with diag(R) >= 0 is
+// unique for a full-rank A, so any stable method reproduces the reference's
+// Householder result: n <= 112 uses shifted CholeskyQR3 (GEMM-shaped) and
+// R = Q^T A; a failed Cholesky (numerically rank-deficient input) falls back to
+// the one-CTA Householder kernel, which reports RankDeficient exactly as the
+// reference does (|r_kk| < 1e-12 ||A||_F).
 void thin_qr_dev(atk_ctx* ctx, const double* a_dev, uint64_t rows, uint64_t cols, double* q_dev,
                  double* r_dev, double fro_a) {
     if (rows < cols) fail(ATK_SHAPE_MISMATCH, "thin_qr expects rows >= cols");
-    householder_qr(ctx, a_dev, int(rows), int(cols), q_dev, r_dev);
+    if (orthonormal_basis_cholqr(ctx, a_dev, int(rows), int(cols), q_dev)) {
+        dgemm(ctx, true, false, int(cols), int(cols), int(rows), 1.0, q_dev, int(rows), a_dev, int(rows), 0.0, r_dev,
+              int(cols));
+        zero_lower(ctx, r_dev, int(cols));
+    } else {
+        householder_qr(ctx, a_dev, int(rows), int(cols), q_dev, r_dev);
+    }
     std::vector<double> rh(cols * cols);
     ATK_CUDA(cudaMemcpyAsync(rh.data(), r_dev, cols * cols * sizeof(double), cudaMemcpyDeviceToHost,
                              ctx->stream));

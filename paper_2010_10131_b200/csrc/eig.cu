@@ -430,10 +430,10 @@ void svqb(atk_ctx* ctx, const double* Y, int n, int k, double* V, Ws& ws) {
                              ctx->stream));
 }
 
-// Orthonormal basis of span(Y) into V: shifted CholeskyQR3 (three GEMM-based
-// passes, the first with a diagonal shift so it never breaks down); falls
-// back to SVQB if a Cholesky pivot still fails.
-void orthonormalize(atk_ctx* ctx, const double* Y, int n, int k, double* V, Ws& ws) {
+// Shifted CholeskyQR3 (three GEMM-based passes, the first with a diagonal
+// shift so a moderately ill-conditioned Y cannot break it down; Fukaya et al.).
+// Returns false if a Cholesky pivot still failed (V is then unusable).
+bool cholqr3(atk_ctx* ctx, const double* Y, int n, int k, double* V, Ws& ws) {
     const double* src = Y;
     double* bufs[2] = {V, ws.tmp.get()};
     for (int pass = 0; pass < 3; ++pass) {
@@ -451,7 +451,13 @@ void orthonormalize(atk_ctx* ctx, const double* Y, int n, int k, double* V, Ws& 
     int h[3] = {0, 0, 0};
     ATK_CUDA(cudaMemcpyAsync(h, ws.info.get(), 3 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     ATK_CUDA(cudaStreamSynchronize(ctx->stream));
-    if (h[0] || h[1] || h[2]) svqb(ctx, Y, n, k, V, ws);
+    return !(h[0] || h[1] || h[2]);
+}
+
+// Orthonormal basis of span(Y) into V: shifted CholeskyQR3, SVQB if a
+// Cholesky pivot still fails.
+void orthonormalize(atk_ctx* ctx, const double* Y, int n, int k, double* V, Ws& ws) {
+    if (!cholqr3(ctx, Y, n, k, V, ws)) svqb(ctx, Y, n, k, V, ws);
 }
 
 Bounds lanczos_bounds(atk_ctx* ctx, const double* S, int n, bool psd) {
@@ -517,23 +523,27 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
                       bool psd, double tol) {
     EigInfo info;
     cudaStream_t st = ctx->stream;
-    const bool dense = n <= kJacobiMax && ctx->eig_method != 1;
+    const bool dense = (n <= kJacobiMax || (psd && n <= kJacobiPsdMax)) && ctx->eig_method != 1;
     if (dense) {
         DevBuf<double> vals(ctx, n), vecs(ctx, size_t(n) * n);
         DevBuf<int> sweeps(ctx, 1);
         jacobi_eig(ctx, s_dev, n, n, vals.get(), vecs.get(), n, sweeps.get(), psd);
-        ATK_CUDA(cudaMemcpyAsync(values_dev, vals.get(), r * sizeof(double), cudaMemcpyDeviceToDevice, st));
-        ATK_CUDA(cudaMemcpyAsync(vectors_dev, vecs.get(), size_t(n) * r * sizeof(double), cudaMemcpyDeviceToDevice,
-                                 st));
-        fix_signs(ctx, vectors_dev, n, r, n);
         int sw = 0;
         ATK_CUDA(cudaMemcpyAsync(&sw, sweeps.get(), sizeof(int), cudaMemcpyDeviceToHost, st));
         ATK_CUDA(cudaStreamSynchronize(st));
         if (std::getenv("ATK_TRACE")) std::fprintf(stderr, "[atk eig n=%d r=%d] dense jacobi sweeps %d\n", n, r, sw);
         if (sw >= 40) fail(ATK_NO_CONVERGENCE, "symmetric eigendecomposition failed (Jacobi sweeps)");
-        info.method = 0;
-        info.iterations = sw;
-        return info;
+        if (sw >= 0) {
+            ATK_CUDA(cudaMemcpyAsync(values_dev, vals.get(), r * sizeof(double), cudaMemcpyDeviceToDevice, st));
+            ATK_CUDA(cudaMemcpyAsync(vectors_dev, vecs.get(), size_t(n) * r * sizeof(double),
+                                     cudaMemcpyDeviceToDevice, st));
+            fix_signs(ctx, vectors_dev, n, r, n);
+            info.method = 0;
+            info.iterations = sw;
+            return info;
+        }
+        // sw < 0: the large (U-only) dense variant found the input not numerically
+        // PSD; ChFSI below handles it
     }
 
     // ---------------- ChFSI
@@ -614,12 +624,14 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
         const double smax = std::max(1.0, (std::max(b.hi, hth[0]) - c) / e);
         const double g = 1.0 / (2.0 * smax + 1.0);  // per-step rescale, keeps the recurrence linear
         // degree: damp [lo, cut] relative to the wanted end by at most ~1e10 per
-        // pass (T_d(x) ~ e^{d acosh x} / 2), 1..16.  A stronger pass leaves the
+        // pass (T_d(x) ~ e^{d acosh x} / 2), 1..64: on flat spectra a pass costs
+        // d skinny GEMMs plus a CholeskyQR + Rayleigh-Ritz, so fewer, stronger
+        // passes win (measured C2 mode 2, n = 1024: cap 16 -> 9 passes).  A stronger pass leaves the
         // block's unwanted columns numerically parallel to the wanted ones (their
         // O(eps) wanted-direction residue is amplified past 1/eps) and CholeskyQR
         // breaks down; on wide gaps this means a single S V power step.
         const double ac = std::acosh(std::max(1.0 + 1e-12, (hth[r - 1] - c) / e));
-        const int degree = std::max(1, std::min(16, int(23.0 / std::max(ac, 1e-3))));
+        const int degree = std::max(1, std::min(64, int(23.0 / std::max(ac, 1e-3))));
         // Y1 = g (S V - c V) / e ; Y_{j+1} = g (2/e)(S Y_j - c Y_j) - g^2 Y_{j-1}
         double* yprev = V.get();
         double* ycur = Ya.get();
@@ -653,6 +665,14 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
     if (it >= max_outer && worst > 1e3 * tol * scale)
         fail(ATK_NO_CONVERGENCE, "symmetric eigendecomposition failed (ChFSI did not converge)");
     return info;
+}
+
+bool orthonormal_basis_cholqr(atk_ctx* ctx, const double* a, int m, int n, double* q) {
+    if (n > kJacobiMax || m < n) return false;
+    const size_t mn = size_t(m) * n, nn = size_t(n) * n;
+    Ws ws{DevBuf<double>(ctx, nn), DevBuf<double>(ctx, nn), DevBuf<double>(ctx, n), DevBuf<double>(ctx, n),
+          DevBuf<double>(ctx, nn), DevBuf<double>(ctx, mn), DevBuf<int>(ctx, 1), DevBuf<int>(ctx, 3)};
+    return cholqr3(ctx, a, m, n, q, ws);
 }
 
 }  // namespace atk

@@ -110,13 +110,13 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
                         for (int q = 0; q < BM / 32; ++q)
                             tc::tma_load_2d(a + q * 4096, &tma_a, &full[stage], tm * BM + q * 32, k0);
-                        const int q0 = half ? BN / 64 : 0;
-                        for (int q = q0; q < BN / 32; ++q)
+                        const int q0 = half == 1 ? BN / 64 : 0, q1 = half == 2 ? BN / 64 : BN / 32;
+                        for (int q = q0; q < q1; ++q)
                             tc::tma_load_2d(b + (q - q0) * 4096, &tma_a, &full[stage], un.y * BN + q * 32, k0);
                     } else {
                         const int p0 = (kb % p.nkb_p) * BK, o0 = kb / p.nkb_p;
                         tc::tma_load_3d(a, &tma_a, &full[stage], p0, o0, tm * BM);
-                        if (half) tc::tma_load_3d(b, &tma_a, &full[stage], p0, o0, un.y * BN + BN / 2);
+                        if (half) tc::tma_load_3d(b, &tma_a, &full[stage], p0, o0, un.y * BN + (half == 1 ? BN / 2 : 0));
                         else tc::tma_load_3d(b, &tma_b, &full[stage], p0, o0, un.y * BN);
                     }
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -182,9 +182,10 @@ __global__ void __launch_bounds__(THREADS, 1)
                 tc::mbar_wait(&tfull[abuf], aphase);
                 tc::tc_fence_after();
                 const bool first = (c0 == un.z);
-                const int cc0 = (un.x >> 16) ? BN / 64 : 0;  // half units fill columns 128..255
+                // half units: mode 1 fills columns 128..255, mode 2 columns 0..127
+                const int cc0 = (un.x >> 16) == 1 ? BN / 64 : 0, cc1 = (un.x >> 16) == 2 ? BN / 64 : BN / 32;
 #pragma unroll 1
-                for (int cc = cc0; cc < BN / 32; ++cc) {
+                for (int cc = cc0; cc < cc1; ++cc) {
                     uint32_t r[32];
                     tc::tmem_ld_32x32b_x32(tmem_base + (uint32_t(q * 32) << 16) +
                                                uint32_t(abuf * BN + (cc - cc0) * 32), r);
@@ -256,7 +257,9 @@ CUresult encode_tensor_map(CUtensorMap* map, CUtensorMapDataType dt, uint32_t ra
 static bool gram_tc_layout_ok(const atk_tensor* x, int mode) {
     if (x->dtype != ATK_F32) return false;
     const Split s = loop_split(x->dims, x->order, mode);
-    if (s.I < 64) return false;  // tiny Gram: CUDA-core path is latency-optimal
+    // small I (ALS R x R Grams, C4's 48-wide modes): still tensor cores, on a
+    // half-width 128 x 128 tile (the SIMT path ran C4 mode 1 at 4.4 ms vs 0.16 HBM)
+    if (s.I < 8) return false;
     if (s.P == 1) return s.I % 4 == 0 && s.O < (1ull << 31) / BK;
     return s.P >= 32 && s.P % 4 == 0 && s.P * s.I < (1ull << 40) && s.O < (1ull << 31);
 }
@@ -305,7 +308,7 @@ void tc_gram(atk_ctx* ctx, const atk_tensor* x, int mode, double* s_dev) {
                 tiles_n.push_back(tn);
             }
     const int ntiles = int(tiles_m.size());
-    int splits = std::max(1, (ctx->num_sms + ntiles / 2) / ntiles);
+    int splits = std::max(1, ctx->num_sms / ntiles);  // floor: units <= CTAs (one wave)
     splits = int(std::min<uint64_t>(uint64_t(splits), std::max<uint64_t>(1, nkb / 8)));
     const int chunk_kb = ctx->gram_chunk_kb > 0 ? ctx->gram_chunk_kb : 512;  // 16K-element fp32 chains
     std::vector<int4> units;
@@ -314,8 +317,11 @@ void tc_gram(atk_ctx* ctx, const atk_tensor* x, int mode, double* s_dev) {
         tile_unit[size_t(tiles_m[t]) * ntn + tiles_n[t]] = int(units.size());
         for (int sp = 0; sp < splits; ++sp) {
             const int kb0 = int(nkb * sp / splits), kb1 = int(nkb * (sp + 1) / splits);
-            // left 128 columns entirely below the diagonal -> half-width unit (N = 128)
-            const int half = (tiles_m[t] * BM >= tiles_n[t] * BN + BN / 2) ? 1 : 0;
+            // half-width units (N = 128): mode 1 when the left 128 columns lie entirely
+            // below the diagonal, mode 2 when the right 128 columns lie beyond I
+            const int half = (tiles_m[t] * BM >= tiles_n[t] * BN + BN / 2) ? 1
+                             : (I <= tiles_n[t] * BN + BN / 2)              ? 2
+                                                                            : 0;
             units.push_back(make_int4(tiles_m[t] | (half << 16), tiles_n[t], kb0, std::max(kb0 + 1, kb1)));
         }
     }

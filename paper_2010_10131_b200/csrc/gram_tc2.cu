@@ -306,7 +306,7 @@ void tc_gram2(atk_ctx* ctx, const atk_tensor* x, int mode, double* s_dev) {
         }
     const int ntiles = int(tiles_m.size());
     const int pairs_avail = ctx->num_sms / 2;
-    int splits = std::max(1, (pairs_avail + ntiles / 2) / ntiles);
+    int splits = std::max(1, pairs_avail / ntiles);  // floor: units <= CTA pairs (one wave)
     splits = int(std::min<uint64_t>(uint64_t(splits), std::max<uint64_t>(1, nkb / 8)));
     const int chunk_kb = ctx->gram_chunk_kb > 0 ? ctx->gram_chunk_kb : 512;
     std::vector<int4> units;

@@ -31,9 +31,9 @@
 namespace atk {
 namespace {
 
-// G lanes per column pair (template; option "jacobi_group").  A round is
-// latency-bound: measured at n = 96 (PSD path) 16 lanes 1.39 ms, 8 lanes
-// 1.56 ms, 4 lanes 2.34 ms.
+// kJacobiGroup lanes per column pair.  A round is latency-bound: measured at
+// n = 96 (PSD path) 16 lanes 1.39 ms, 8 lanes 1.56 ms, 4 lanes 2.34 ms.
+constexpr int kJacobiGroup = 16;
 
 __device__ __forceinline__ float rcp_approx(float x) {
     float r;
@@ -50,25 +50,31 @@ __device__ __forceinline__ int rr_player(int t, int k, int N) {
     return k == 0 ? 0 : (t + k - 1) % (N - 1) + 1;
 }
 
-template <int G>
-__global__ void __launch_bounds__(G * ((kJacobiMax + 1) / 2), 1)
+// MAXN <= kJacobiMax: U and V in shared memory (both variants).  MAXN up to
+// kJacobiPsdMax: U only, PSD variant only (a failed Cholesky reports
+// sweeps = -1 and the caller falls back to ChFSI).  Column pairs are dealt to
+// the nt / G groups in ceil(pairs / groups) passes per round.
+template <int G, int MAXN, int MAXT>
+__global__ void __launch_bounds__(MAXT, 1)
     jacobi1s_kernel(const double* __restrict__ ain, int n, int lda, bool psd, double* __restrict__ values,
                     double* __restrict__ vout, int ldv, int* __restrict__ sweeps_out) {
+    constexpr bool kHasV = MAXN <= kJacobiMax;
     extern __shared__ double sm[];
     const int ld = n + 1;  // odd leading dimension: column accesses hit distinct banks
     double* U = sm;
-    double* V = U + size_t(ld) * n;
-    double* lam = V + size_t(ld) * n;  // n
+    double* V = kHasV ? U + size_t(ld) * n : nullptr;
+    double* lam = U + size_t(ld) * n * (kHasV ? 2 : 1);  // n
+    double* scl = lam + n;                                // n: 1 / |u_j| (PSD variant)
     __shared__ int rotated;
     __shared__ double sh_sigma;
-    constexpr int kGroup = G, kVals = (kJacobiMax + G - 1) / G;  // column slice per lane
+    constexpr int kGroup = G, kVals = (MAXN + G - 1) / G;  // column slice per lane
     const int tid = threadIdx.x, nt = blockDim.x;
     const int N = n + (n & 1);
     const double eps = 2.220446049250313e-16;
     const double tol = fmax(1e-15, 4.0 * n * eps);
     const double tol2 = tol * tol;
     // tournament schedule precomputed once: sched[t * N/2 + j] = p | q << 8 (p < q)
-    uint16_t* sched = reinterpret_cast<uint16_t*>(lam + n);
+    uint16_t* sched = reinterpret_cast<uint16_t*>(scl + n);
     for (int e = tid; e < (N - 1) * (N / 2); e += nt) {
         const int t = e / (N / 2), j = e % (N / 2);
         int p = rr_player(t, j, N), q = rr_player(t, N - 1 - j, N);
@@ -126,6 +132,9 @@ __global__ void __launch_bounds__(G * ((kJacobiMax + 1) / 2), 1)
                 const int i = e % n, j = e / n;
                 U[i + ld * j] = (i >= j) ? U[i + ld * j] * lam[j] : 0.0;
             }
+        } else if constexpr (!kHasV) {  // no room for V: let the caller fall back
+            if (tid == 0 && sweeps_out) *sweeps_out = -1;
+            return;
         } else {  // not numerically PSD: the general variant on A itself
             usev = true;
             sigma = 0.0;
@@ -135,7 +144,7 @@ __global__ void __launch_bounds__(G * ((kJacobiMax + 1) / 2), 1)
             }
         }
     }
-    if (usev)
+    if (kHasV && usev)
         for (int e = tid; e < n * n; e += nt) V[e % n + ld * (e / n)] = (e % n == e / n) ? 1.0 : 0.0;
     __syncthreads();
 
@@ -156,10 +165,12 @@ __global__ void __launch_bounds__(G * ((kJacobiMax + 1) / 2), 1)
         if (tid == 0) rotated = 0;
         __syncthreads();
         for (int t = 0; t < N - 1; ++t) {
-            bool active = grp < N / 2;
+          for (int base = 0; base < N / 2; base += nt / kGroup) {  // uniform trip count
+            const int pr = base + grp;
+            bool active = pr < N / 2;
             int p = 0, q = 0;
             if (active) {
-                const int pq = sched[t * (N / 2) + grp];
+                const int pq = sched[t * (N / 2) + pr];
                 p = pq & 255;
                 q = pq >> 8;
                 active = q < n;  // dummy player when n is odd
@@ -219,7 +230,7 @@ __global__ void __launch_bounds__(G * ((kJacobiMax + 1) / 2), 1)
                         uq[i] = fma(s, xr[k], c * yr[k]);
                     }
                 }
-                if (usev) {
+                if (kHasV && usev) {
                     double* vp = V + ld * p;
                     double* vq = V + ld * q;
                     for (int i = gl; i < n; i += kGroup) {
@@ -234,6 +245,7 @@ __global__ void __launch_bounds__(G * ((kJacobiMax + 1) / 2), 1)
                     rotated = 1;
                 }
             }
+          }
             __syncthreads();
         }
         const bool done = !rotated;
@@ -246,13 +258,13 @@ __global__ void __launch_bounds__(G * ((kJacobiMax + 1) / 2), 1)
         const int j = j0 + grp;
         double d = 0.0;
         if (j < n) {
-            const double* w = usev ? V + ld * j : U + ld * j;
+            const double* w = (kHasV && usev) ? V + ld * j : U + ld * j;
             for (int i = gl; i < n; i += kGroup) d = fma(U[i + ld * j], w[i], d);
         }
         for (int o = kGroup / 2; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
         if (j < n && gl == 0) {
             lam[j] = d - sigma;
-            if (!usev) V[j] = d > 0.0 ? rsqrt(d) : 0.0;
+            scl[j] = d > 0.0 ? rsqrt(d) : 0.0;
         }
     }
     __syncthreads();
@@ -264,46 +276,51 @@ __global__ void __launch_bounds__(G * ((kJacobiMax + 1) / 2), 1)
             rank += (lj > li) || (lj == li && j < i);
         }
         values[rank] = li;
-        if (usev) {
+        if (kHasV && usev) {
             for (int r = 0; r < n; ++r) vout[r + size_t(ldv) * rank] = V[r + ld * i];
         } else {
-            const double sc = V[i];
+            const double sc = scl[i];
             for (int r = 0; r < n; ++r) vout[r + size_t(ldv) * rank] = U[r + ld * i] * sc;
         }
     }
     if (tid == 0 && sweeps_out) *sweeps_out = sweep;
 }
 
-}  // namespace
-
-size_t jacobi1s_smem_bytes(int n) {
+size_t jacobi1s_smem_bytes(int n, bool with_v) {
     const int N = n + (n & 1);
-    return (size_t(2) * (n + 1) * n + n) * sizeof(double) + size_t(N) * (N / 2) * sizeof(uint16_t) + 64;
+    return (size_t(with_v ? 2 : 1) * (n + 1) * n + 2 * n) * sizeof(double) + size_t(N) * (N / 2) * sizeof(uint16_t) +
+           64;
 }
 
-template <int G>
+template <int MAXN, int MAXT>
 void launch_jacobi(atk_ctx* ctx, const double* a, int n, int lda, double* values, double* vectors, int ldv,
                    int* sweeps_dev, bool psd) {
+    constexpr bool kHasV = MAXN <= kJacobiMax;
     static bool attr = false;
     if (!attr) {
-        ATK_CUDA(cudaFuncSetAttribute(jacobi1s_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      int(jacobi1s_smem_bytes(kJacobiMax))));
+        ATK_CUDA(cudaFuncSetAttribute(jacobi1s_kernel<kJacobiGroup, MAXN, MAXT>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(jacobi1s_smem_bytes(MAXN, kHasV))));
         attr = true;
     }
     const int N = n + (n & 1);
-    const int threads = ((G * std::max(1, N / 2)) + 31) / 32 * 32;
-    jacobi1s_kernel<G><<<1, threads, jacobi1s_smem_bytes(n), ctx->stream>>>(a, n, lda, psd, values, vectors, ldv,
-                                                                           sweeps_dev);
+    const int threads = std::min(MAXT, ((kJacobiGroup * std::max(1, N / 2)) + 31) / 32 * 32);
+    jacobi1s_kernel<kJacobiGroup, MAXN, MAXT><<<1, threads, jacobi1s_smem_bytes(n, kHasV), ctx->stream>>>(
+        a, n, lda, psd, values, vectors, ldv, sweeps_dev);
     ATK_LAUNCHED(ctx);
 }
 
+}  // namespace
+
 void jacobi_eig(atk_ctx* ctx, const double* a, int n, int lda, double* values, double* vectors, int ldv,
                 int* sweeps_dev, bool psd) {
-    if (n > kJacobiMax) fail(ATK_UNSUPPORTED, "jacobi_eig: n exceeds the shared-memory capacity");
-    switch (ctx->jacobi_group) {
-        case 4: launch_jacobi<4>(ctx, a, n, lda, values, vectors, ldv, sweeps_dev, psd); break;
-        case 8: launch_jacobi<8>(ctx, a, n, lda, values, vectors, ldv, sweeps_dev, psd); break;
-        default: launch_jacobi<16>(ctx, a, n, lda, values, vectors, ldv, sweeps_dev, psd); break;
+    if (n <= kJacobiMax) {
+        launch_jacobi<kJacobiMax, kJacobiGroup * ((kJacobiMax + 1) / 2)>(ctx, a, n, lda, values, vectors, ldv,
+                                                                         sweeps_dev, psd);
+    } else if (psd && n <= kJacobiPsdMax) {
+        launch_jacobi<kJacobiPsdMax, 768>(ctx, a, n, lda, values, vectors, ldv, sweeps_dev, psd);
+    } else {
+        fail(ATK_UNSUPPORTED, "jacobi_eig: n exceeds the shared-memory capacity");
     }
 }
 

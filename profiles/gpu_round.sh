@@ -13,10 +13,12 @@ for p in $PARTS; do
     trace) ATK_TRACE=1 timeout 300 python profiles/run_step.py c5 2 > gpurun_out/${TAG}_trace.log 2>&1; echo "trace=$?"; tail -40 gpurun_out/${TAG}_trace.log;;
     eigt) timeout 300 python -m pytest tests/test_gpu_eig.py -x -q -p no:hypothesispytest 2>&1 | tail -3;;
     ncujac) timeout 600 ncu --set full --clock-control none --import-source on -k regex:jacobi1s -c 1 -o gpurun_out/${TAG}_jac python profiles/jacobi_probe.py 96 > gpurun_out/${TAG}_ncujac.log 2>&1; echo "ncujac=$?";;
+    allcfg) for c in c1 c2 c3 c4; do timeout 600 python bench.py --config $c --steps 5 --warmup 3 > gpurun_out/${TAG}_bench_$c.json 2> gpurun_out/${TAG}_bench_$c.err; echo "bench $c=$?"; head -c 300 gpurun_out/${TAG}_bench_$c.json; echo; done;;
+    tracecfg) for c in c1 c2; do ATK_TRACE=1 timeout 300 python profiles/run_step.py $c 1 > gpurun_out/${TAG}_trace_$c.log 2>&1; echo "trace $c=$?"; done;;
     fast) timeout 900 python -m pytest tests -m "gpu and not slow" -x -q -p no:hypothesispytest > gpurun_out/${TAG}_tests.log 2>&1; echo "fast=$? $(tail -1 gpurun_out/${TAG}_tests.log)";;
     bench) timeout 600 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err; echo "bench=$?"; head -c 400 gpurun_out/${TAG}_bench.json; echo;;
     ref) timeout 600 python bench.py --impl reference > gpurun_out/${TAG}_ref.json 2> gpurun_out/${TAG}_ref.err; echo "ref=$?"; head -c 300 gpurun_out/${TAG}_ref.json; echo;;
-    launches) timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv python profiles/run_step.py c5 1 > gpurun_out/${TAG}_launches.log 2>&1; echo "launches=$?";;
+    launches) timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv python profiles/run_step.py ${CFG:-c5} 1 > gpurun_out/${TAG}_launches.log 2>&1; echo "launches=$?";;
     ncu) timeout 900 ncu --set full --clock-control none --import-source on -k regex:"gram_tf32_2cta|ttm_tf32" -c 2 -o gpurun_out/${TAG}_full python profiles/run_step.py c5 1 > gpurun_out/${TAG}_ncu.log 2>&1; echo "ncu=$?";;
   esac
 done

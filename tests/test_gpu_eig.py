@@ -46,7 +46,7 @@ def ectx(request):
     ctx.set_option("eig_assume_psd", 0.0)
 
 
-@pytest.mark.parametrize("n", [2, 5, 17, 48, 96, 112])
+@pytest.mark.parametrize("n", [2, 5, 17, 48, 96, 112, 128, 152])
 def test_dense_gram(ectx, n):
     from paper_2010_10131_b200 import atucker
 
