@@ -334,7 +334,7 @@ def main():
     prof = ROOT / "profiles" / "gram_traffic.json"
     if prof.exists():
         traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
-    roofline = {"kernel": "gram_tf32_kernel (+gram_reduce), mode 1",
+    roofline = {"kernel": "gram_tf32_2cta_kernel (+gram2_reduce), mode 1 (n = 0)",
                 "bound": "tensor", "achieved": achieved, "peak": tf32_peak, "unit": "TFLOP/s",
                 "frac": (achieved / tf32_peak) if achieved else None, "traffic": traffic,
                 "peak_note": f"tf32 = 1/2 of the {pk['src']} sustained bf16 {pk['bf16_sus']} TF/s",
