@@ -45,8 +45,10 @@ CONFIGS = {
                input="reference"),
     "c4": dict(dims=(48,) * 5, ranks=(8,) * 5, dtype="f32", strategy="eig", input="uniform"),
     "c5": dict(dims=(2048, 2048, 2048), ranks=(64, 64, 64), dtype="f32", strategy="eig", input="lowrank"),
+    # SURVEY 8(d) stress variant: flat spectrum (eig time reported separately)
+    "c5u": dict(dims=(2048, 2048, 2048), ranks=(64, 64, 64), dtype="f32", strategy="eig", input="uniform"),
 }
-SEEDS = {"c1": 1, "c2": 2, "c3": 3, "c4": 4, "c5": 5}
+SEEDS = {"c1": 1, "c2": 2, "c3": 3, "c4": 4, "c5": 5, "c5u": 5}
 
 
 def flops_of(dims, ranks, kinds, num_iters=5):
@@ -252,6 +254,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--opt", action="append", default=[], help="engine option key=value (atk_ctx_set_option)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
@@ -270,6 +273,9 @@ def main():
     from paper_2010_10131_b200.selector import Strategy
 
     ctx = atucker.Context(local)
+    for kv in args.opt:
+        k, v = kv.split("=", 1)
+        ctx.set_option(k, float(v))
     if world > 1:
         from paper_2010_10131_b200.dist import init_comm_from_torch
 

@@ -17,7 +17,7 @@
 //                       Rayleigh-Ritz : Jacobi on V^T S V;
 //                     until every wanted Ritz pair has relative residual
 //                     ||S v - theta v|| <= tol * max|theta| (tol 1e-12 for fp64
-//                     data, 1e-10 for tf32-computed Grams).
+//                     data, 1e-9 for tf32-computed Grams).
 // Both paths finish with descending order + fix_signs (linalg.hpp:34-50) so
 // factors compare entry-wise with the reference on gapped spectra.
 #include <algorithm>
@@ -548,7 +548,9 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
 
     // ---------------- ChFSI
     if (tol <= 0) tol = ctx->chfsi_tol;
-    int k = std::min(n, std::max(r + 16, (3 * r + 1) / 2));
+    // block size: r + max(16, r / 4) (the Rayleigh-Ritz Jacobi costs ~k^2; the
+    // S^2 Omega start makes a thin guard band enough on gapped spectra)
+    int k = std::min(n, r + std::max(16, r / 4));
     k = std::min(k, kJacobiMax);
     if (k < r) fail(ATK_UNSUPPORTED, "sym_eig_top_r: r > 112 with n > 112 is not supported");
     const size_t nn = size_t(n) * n, nk = size_t(n) * k, kk = size_t(k) * k;
@@ -608,6 +610,9 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
         if (!(scale > 0.0) || worst <= tol * scale || it >= max_outer) break;
         if (!have_bounds) {
             const bool gapped = psd && hth[k - 1] >= 0.0 && hth[r - 1] > 10.0 * hth[k - 1];
+            if (trace)
+                std::fprintf(stderr, "[atk eig n=%d r=%d k=%d] theta_1 %.6e theta_r %.6e theta_k %.6e\n", n, r, k,
+                             hth[0], hth[r - 1], hth[k - 1]);
             if (gapped) {
                 b = Bounds{0.0, hth[0]};
             } else {

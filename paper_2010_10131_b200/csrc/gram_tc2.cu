@@ -11,6 +11,11 @@
 // moves the kernel off the shared-memory-bandwidth ceiling (TMA writes + UMMA
 // reads ~ 192 B/clk/SM > 128 B/clk/SM for 1-CTA tiles).
 //
+// Pairs are not synchronised: an epoch drift bound (a leader waits until every
+// pair has issued K-epoch e - window; 8..32-block epochs, window 4) measured
+// 40-41 ms against 34-38 ms free-running at C5 mode 1, despite the 2.5x HBM
+// re-read it targets (profiles/r1/SUMMARY.md).
+//
 // Pipeline per CTA: warp 0 = TMA producer (both CTAs; the leader arms the
 // leader's full barrier with the bytes of BOTH CTAs, the peer's TMA completes
 // on it through the cluster window), warp 1 = TMEM alloc + (leader only) MMA
@@ -305,7 +310,33 @@ void tc_gram2(atk_ctx* ctx, const atk_tensor* x, int mode, double* s_dev) {
             tiles_n.push_back(tn);
         }
     const int ntiles = int(tiles_m.size());
-    const int pairs_avail = ctx->num_sms / 2;
+    static bool attr = false;
+    if (!attr) {
+        ATK_CUDA(cudaFuncSetAttribute(gram_tf32_2cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM2)));
+        attr = true;
+    }
+    // CTA pairs that are co-resident (GPCs with an odd SM count leave SMs unused)
+    static int pairs_resident = 0;
+    if (!pairs_resident) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(2 * (ctx->num_sms / 2), 1, 1);
+        cfg.blockDim = dim3(THREADS, 1, 1);
+        cfg.dynamicSmemBytes = SMEM2;
+        cudaLaunchAttribute at{};
+        at.id = cudaLaunchAttributeClusterDimension;
+        at.val.clusterDim.x = 2;
+        at.val.clusterDim.y = 1;
+        at.val.clusterDim.z = 1;
+        cfg.attrs = &at;
+        cfg.numAttrs = 1;
+        int nc = 0;
+        if (cudaOccupancyMaxActiveClusters(&nc, gram_tf32_2cta_kernel, &cfg) != cudaSuccess || nc <= 0) {
+            cudaGetLastError();
+            nc = ctx->num_sms / 2;
+        }
+        pairs_resident = std::min(nc, ctx->num_sms / 2);
+    }
+    const int pairs_avail = pairs_resident;
     int splits = std::max(1, pairs_avail / ntiles);  // floor: units <= CTA pairs (one wave)
     splits = int(std::min<uint64_t>(uint64_t(splits), std::max<uint64_t>(1, nkb / 8)));
     const int chunk_kb = ctx->gram_chunk_kb > 0 ? ctx->gram_chunk_kb : 512;
@@ -324,13 +355,8 @@ void tc_gram2(atk_ctx* ctx, const atk_tensor* x, int mode, double* s_dev) {
     ATK_CUDA(cudaMemcpyAsync(du.get(), units.data(), units.size() * sizeof(int4), cudaMemcpyHostToDevice, ctx->stream));
     ATK_CUDA(cudaMemcpyAsync(dtu.get(), tile_unit.data(), tile_unit.size() * sizeof(int), cudaMemcpyHostToDevice,
                              ctx->stream));
-    Gram2Params prm{du.get(), int(units.size()), chunk_kb, kmajor ? 1 : 0, nkb_p, acc.get()};
-    static bool attr = false;
-    if (!attr) {
-        ATK_CUDA(cudaFuncSetAttribute(gram_tf32_2cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM2)));
-        attr = true;
-    }
     const int npairs = std::min<int>(int(units.size()), pairs_avail);
+    Gram2Params prm{du.get(), int(units.size()), chunk_kb, kmajor ? 1 : 0, nkb_p, acc.get()};
     gram_tf32_2cta_kernel<<<2 * npairs, THREADS, SMEM2, ctx->stream>>>(tm, prm);
     ATK_LAUNCHED(ctx);
     const size_t n = size_t(I) * I;

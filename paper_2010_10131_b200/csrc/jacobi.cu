@@ -25,14 +25,15 @@
 // of the full spectrum).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "atk_internal.cuh"
 
 namespace atk {
 namespace {
 
-// kJacobiGroup lanes per column pair.  A round is latency-bound: measured at
-// n = 96 (PSD path) 16 lanes 1.39 ms, 8 lanes 1.56 ms, 4 lanes 2.34 ms.
+// kJacobiGroup lanes per column pair.  Measured at n = 96 (PSD path): 16 lanes
+// 1.29 ms, 8 lanes 1.55 ms, 4 lanes 2.34 ms (n = 152: 4.3 vs 5.6 ms at 8).
 constexpr int kJacobiGroup = 16;
 
 __device__ __forceinline__ float rcp_approx(float x) {
@@ -292,20 +293,20 @@ size_t jacobi1s_smem_bytes(int n, bool with_v) {
            64;
 }
 
-template <int MAXN, int MAXT>
+template <int G, int MAXN, int MAXT>
 void launch_jacobi(atk_ctx* ctx, const double* a, int n, int lda, double* values, double* vectors, int ldv,
                    int* sweeps_dev, bool psd) {
     constexpr bool kHasV = MAXN <= kJacobiMax;
     static bool attr = false;
     if (!attr) {
-        ATK_CUDA(cudaFuncSetAttribute(jacobi1s_kernel<kJacobiGroup, MAXN, MAXT>,
+        ATK_CUDA(cudaFuncSetAttribute(jacobi1s_kernel<G, MAXN, MAXT>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       int(jacobi1s_smem_bytes(MAXN, kHasV))));
         attr = true;
     }
     const int N = n + (n & 1);
-    const int threads = std::min(MAXT, ((kJacobiGroup * std::max(1, N / 2)) + 31) / 32 * 32);
-    jacobi1s_kernel<kJacobiGroup, MAXN, MAXT><<<1, threads, jacobi1s_smem_bytes(n, kHasV), ctx->stream>>>(
+    const int threads = std::min(MAXT, ((G * std::max(1, N / 2)) + 31) / 32 * 32);
+    jacobi1s_kernel<G, MAXN, MAXT><<<1, threads, jacobi1s_smem_bytes(n, kHasV), ctx->stream>>>(
         a, n, lda, psd, values, vectors, ldv, sweeps_dev);
     ATK_LAUNCHED(ctx);
 }
@@ -315,10 +316,10 @@ void launch_jacobi(atk_ctx* ctx, const double* a, int n, int lda, double* values
 void jacobi_eig(atk_ctx* ctx, const double* a, int n, int lda, double* values, double* vectors, int ldv,
                 int* sweeps_dev, bool psd) {
     if (n <= kJacobiMax) {
-        launch_jacobi<kJacobiMax, kJacobiGroup * ((kJacobiMax + 1) / 2)>(ctx, a, n, lda, values, vectors, ldv,
-                                                                         sweeps_dev, psd);
+        launch_jacobi<kJacobiGroup, kJacobiMax, kJacobiGroup * ((kJacobiMax + 1) / 2)>(ctx, a, n, lda, values,
+                                                                                       vectors, ldv, sweeps_dev, psd);
     } else if (psd && n <= kJacobiPsdMax) {
-        launch_jacobi<kJacobiPsdMax, 768>(ctx, a, n, lda, values, vectors, ldv, sweeps_dev, psd);
+        launch_jacobi<kJacobiGroup, kJacobiPsdMax, 768>(ctx, a, n, lda, values, vectors, ldv, sweeps_dev, psd);
     } else {
         fail(ATK_UNSUPPORTED, "jacobi_eig: n exceeds the shared-memory capacity");
     }
