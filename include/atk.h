@@ -104,6 +104,22 @@ typedef struct atk_mode_report {
     atk_stage_times times;
 } atk_mode_report;
 
+/* ------------------------------------------------ allocation tracking
+ * instr::AllocTracker / AllocScope (instrumentation.hpp:39-150): live device
+ * tensor payloads while enabled; `watched` counts buffers of exactly
+ * watch_elems elements (the input's size), so acceptance criterion 12
+ * (acceptance.cpp:428-458, "memory discipline") can be asserted on the engine. */
+typedef struct atk_alloc_stats {
+    int64_t alloc_count;   /* registered allocations */
+    int64_t live_elems;    /* currently live tracked elements */
+    int64_t peak_elems;    /* high-water mark of live elements */
+    int64_t live_watched;  /* live buffers with exactly watch_elems elements */
+    int64_t peak_watched;  /* high-water mark of the above */
+} atk_alloc_stats;
+void atk_alloc_tracking_enable(uint64_t watch_elems);
+void atk_alloc_tracking_disable(void);
+atk_status atk_alloc_tracking_stats(atk_alloc_stats* out);
+
 /* ------------------------------------------------------------ context */
 const char* atk_version(void);
 const char* atk_last_error(void);
@@ -117,7 +133,7 @@ uint64_t atk_ctx_launch_count(const atk_ctx* ctx);
 /* Engine tuning knobs (unknown keys -> ATK_INVALID_ARGUMENT):
  *   "simt"          1 = CUDA-core contractions for every shape (default 0: tcgen05 / DMMA)
  *   "eig_method"   -1 auto, 0 dense Jacobi (n <= 112), 1 ChFSI
- *   "chfsi_tol"     relative Ritz-residual target of ChFSI (default 1e-12; fp32 Grams use >= 1e-10)
+ *   "chfsi_tol"     relative Ritz-residual target of ChFSI (default 1e-12; fp32 Grams use >= 1e-9)
  *   "eig_assume_psd" 1 = atk_sym_eig_top_r inputs are Grams (Cholesky-preconditioned Jacobi)
  *   "tma_tf32"      1 = round-to-nearest tf32 operand loads (default), 0 = hardware truncation
  *   "gram_2cta"     1 = CTA-pair (cta_group::2) Gram where supported (default)

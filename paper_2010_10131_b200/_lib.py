@@ -40,6 +40,11 @@ class ModeReportC(C.Structure):
                 ("dims_after", C.c_uint64 * ATK_MAX_ORDER), ("times", StageTimes)]
 
 
+class AllocStats(C.Structure):
+    _fields_ = [("alloc_count", C.c_int64), ("live_elems", C.c_int64), ("peak_elems", C.c_int64),
+                ("live_watched", C.c_int64), ("peak_watched", C.c_int64)]
+
+
 # name -> (restype, argtypes); every atk_status-returning entry in atk.h.
 _SIGS = {
     "atk_version": (C.c_char_p, []),
@@ -83,6 +88,9 @@ _SIGS = {
     "atk_reset_gemm_counters": (None, []),
     "atk_gemm_calls": (C.c_longlong, []),
     "atk_gemm_flops": (C.c_longlong, []),
+    "atk_alloc_tracking_enable": (None, [C.c_uint64]),
+    "atk_alloc_tracking_disable": (None, []),
+    "atk_alloc_tracking_stats": (C.c_int, [C.POINTER(AllocStats)]),
     "atk_cost_eig": (C.c_double, [C.c_double, C.c_double, C.c_double]),
     "atk_cost_als": (C.c_double, [C.c_double, C.c_double, C.c_double, C.c_int]),
 }

@@ -617,6 +617,27 @@ def reset_gemm_counters() -> None:
     _lib.load().atk_reset_gemm_counters()
 
 
+class AllocScope:
+    """instr::AllocScope (instrumentation.hpp:144-150): tracks live device tensor
+    payloads while the `with` block runs; `watch_elems` = the size to count
+    (the input's) in live/peak_watched.  `stats()` mirrors AllocTracker::Stats."""
+
+    def __init__(self, watch_elems: int):
+        self.watch = int(watch_elems)
+
+    def __enter__(self) -> "AllocScope":
+        _lib.load().atk_alloc_tracking_enable(self.watch)
+        return self
+
+    def __exit__(self, *exc) -> None:
+        _lib.load().atk_alloc_tracking_disable()
+
+    def stats(self) -> dict:
+        st = _lib.AllocStats()
+        _lib.check(_lib.load().atk_alloc_tracking_stats(C.byref(st)))
+        return {k: int(getattr(st, k)) for k, _ in _lib.AllocStats._fields_}
+
+
 def gemm_calls() -> int:
     return int(_lib.load().atk_gemm_calls())
 

@@ -3,6 +3,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -41,6 +42,40 @@ void dev_free(atk_ctx* ctx, void* p) {
     if (p) cudaFreeAsync(p, ctx->stream);
 }
 
+// ------------------------------------------------ AllocTracker (instrumentation.hpp:39-150)
+// Live device tensor payloads (the analogue of DenseTensor/DenseMatrix buffers)
+// while enabled; allocations made before enable() are invisible, as in the
+// reference.  Engine workspaces (split-K partials, eigensolver blocks) are not
+// tensors and are not counted, matching the reference's tracking of payloads.
+namespace {
+std::mutex g_track_mu;
+bool g_track_on = false;
+uint64_t g_track_epoch = 0, g_track_watch = 0;
+atk_alloc_stats g_track{};
+
+void track_alloc(atk_tensor* t) {
+    std::lock_guard<std::mutex> lk(g_track_mu);
+    const uint64_t n = t->numel();
+    if (!g_track_on || n == 0) return;
+    t->track_epoch = g_track_epoch;
+    g_track.alloc_count += 1;
+    g_track.live_elems += int64_t(n);
+    g_track.peak_elems = std::max(g_track.peak_elems, g_track.live_elems);
+    if (n == g_track_watch) {
+        g_track.live_watched += 1;
+        g_track.peak_watched = std::max(g_track.peak_watched, g_track.live_watched);
+    }
+}
+
+void track_free(const atk_tensor* t) {
+    std::lock_guard<std::mutex> lk(g_track_mu);
+    if (t->track_epoch == 0 || t->track_epoch != g_track_epoch) return;  // outlived its scope
+    const uint64_t n = t->numel();
+    g_track.live_elems -= int64_t(n);
+    if (n == g_track_watch) g_track.live_watched -= 1;
+}
+}  // namespace
+
 atk_tensor* new_tensor(atk_ctx* ctx, atk_dtype dt, int order, const uint64_t* dims) {
     if (order < 1 || order > ATK_MAX_ORDER) fail(ATK_SHAPE_MISMATCH, "tensor order must be in [1, 8]");
     for (int m = 0; m < order; ++m)
@@ -57,6 +92,7 @@ atk_tensor* new_tensor(atk_ctx* ctx, atk_dtype dt, int order, const uint64_t* di
         throw;
     }
     t->owned = true;
+    track_alloc(t);
     return t;
 }
 
@@ -265,6 +301,7 @@ atk_status atk_tensor_to_host(atk_ctx* ctx, const atk_tensor* t, void* host) {
 atk_status atk_tensor_free(atk_tensor* t) {
     return guard([&] {
         if (!t) return;
+        if (t->owned) track_free(t);
         if (t->owned && t->data) {
             cudaSetDevice(t->ctx->device);
             dev_free(t->ctx, t->data);
@@ -537,5 +574,26 @@ long long atk_gemm_calls(void) { return g_gemm_calls.load(); }
 long long atk_gemm_flops(void) { return g_gemm_flops.load(); }
 double atk_cost_eig(double i, double r, double j) { return cost_eig(i, r, j); }
 double atk_cost_als(double i, double r, double j, int num_iters) { return cost_als(i, r, j, num_iters); }
+
+void atk_alloc_tracking_enable(uint64_t watch_elems) {
+    std::lock_guard<std::mutex> lk(g_track_mu);
+    g_track_on = true;
+    ++g_track_epoch;
+    g_track_watch = watch_elems;
+    g_track = atk_alloc_stats{};
+}
+
+void atk_alloc_tracking_disable(void) {
+    std::lock_guard<std::mutex> lk(g_track_mu);
+    g_track_on = false;
+}
+
+atk_status atk_alloc_tracking_stats(atk_alloc_stats* out) {
+    return guard([&] {
+        if (!out) fail(ATK_INVALID_ARGUMENT, "null stats pointer");
+        std::lock_guard<std::mutex> lk(g_track_mu);
+        *out = g_track;
+    });
+}
 
 }  // extern "C"

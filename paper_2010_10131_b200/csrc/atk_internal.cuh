@@ -74,6 +74,7 @@ struct atk_tensor {
     uint64_t dims[ATK_MAX_ORDER] = {};
     void* data = nullptr;
     bool owned = false;
+    uint64_t track_epoch = 0;  // AllocTracker ticket (0 = untracked)
 
     uint64_t numel() const {
         uint64_t p = 1;
