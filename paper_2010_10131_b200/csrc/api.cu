@@ -1,6 +1,7 @@
 // api.cu — the C ABI (include/atk.h).  Every entry converts library errors
 // into an atk_status + thread-local message; no exception crosses the ABI.
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <mutex>
@@ -531,8 +532,27 @@ atk_status atk_sthosvd_host(atk_ctx* ctx, atk_dtype dt, int order, const uint64_
         atk_tensor* x = new_tensor(ctx, dt, order, dims);
         atk_tensor* core = nullptr;
         try {
-            ATK_CUDA(cudaMemcpyAsync(x->data, x_host, x->bytes(), cudaMemcpyHostToDevice, ctx->stream));
-            core = sthosvd(ctx, x, ranks, decide, user, o, factors_out, reports);
+            // Large single-GPU inputs whose mode 0 is an EIG/SVD mode: stream the
+            // copy in chunks and hide the mode-0 Gram behind it.  Mode 0 is decided
+            // here (once, as in sthosvd.hpp:149-166) and handed to the driver.
+            ModeZeroPre pre;
+            DevBuf<double> s0(ctx, 0);
+            const uint64_t I0 = dims[0], J0 = x->numel() / dims[0];
+            if (!ctx->comm && order >= 2 && x->bytes() >= (uint64_t(1) << 30) && ranks[0] >= 1 &&
+                ranks[0] <= I0) {
+                const auto td = std::chrono::steady_clock::now();
+                pre.choice = decide ? decide(user, 0, I0, ranks[0], J0) : ATK_SOLVER_EIG;
+                pre.decide_time = std::chrono::duration<double>(std::chrono::steady_clock::now() - td).count();
+                if (pre.choice < 0 || pre.choice > 2) fail(ATK_INVALID_ARGUMENT, "selector callback failed");
+                if (pre.choice != ATK_SOLVER_ALS) {
+                    s0 = DevBuf<double>(ctx, I0 * I0);
+                    pre.gram = s0.get();
+                    pre.gram_ms = upload_with_gram0(ctx, x, x_host, s0.get());
+                }
+            }
+            if (!pre.gram)
+                ATK_CUDA(cudaMemcpyAsync(x->data, x_host, x->bytes(), cudaMemcpyHostToDevice, ctx->stream));
+            core = sthosvd(ctx, x, ranks, decide, user, o, factors_out, reports, pre.choice >= 0 ? &pre : nullptr);
             ATK_CUDA(cudaMemcpyAsync(core_out_host, core->data, core->bytes(), cudaMemcpyDeviceToHost,
                                      ctx->stream));
             ATK_CUDA(cudaStreamSynchronize(ctx->stream));

@@ -60,7 +60,10 @@ atk_tensor* contract_ttm(atk_ctx* ctx, const atk_tensor* x, const double* u_dev,
                          int mode);
 uint64_t j_of(const atk_tensor* t, int mode);
 void check_truncation(const atk_tensor* y, int mode, uint64_t r);
-ModeOut eig_mode(atk_ctx* ctx, const atk_tensor* y, int mode, uint64_t r, int solver_kind);
+// gram_pre: the mode's Gram already on the device (the host entry streams the
+// input and overlaps the mode-0 Gram with the copy); gram_pre_ms its device time.
+ModeOut eig_mode(atk_ctx* ctx, const atk_tensor* y, int mode, uint64_t r, int solver_kind,
+                 const double* gram_pre = nullptr, double gram_pre_ms = 0.0);
 ModeOut als_mode(atk_ctx* ctx, const atk_tensor* y, int mode, uint64_t r, const atk_als_opts& opts,
                  const double* l0_host);
 AlsOut als_iterate(atk_ctx* ctx, const atk_tensor* y, int mode, const double* l0_host, uint64_t r,
@@ -68,9 +71,21 @@ AlsOut als_iterate(atk_ctx* ctx, const atk_tensor* y, int mode, const double* l0
 std::vector<double> als_initial_guess(uint64_t rows, uint64_t r, uint64_t seed, uint64_t mode);
 void thin_qr_dev(atk_ctx* ctx, const double* a_dev, uint64_t rows, uint64_t cols, double* q_dev,
                  double* r_dev, double fro_a);
+// Mode 0 already decided (and, for EIG/SVD, its Gram computed) by the caller.
+struct ModeZeroPre {
+    int choice = -1;
+    double decide_time = 0.0;
+    const double* gram = nullptr;
+    double gram_ms = 0.0;
+};
 atk_tensor* sthosvd(atk_ctx* ctx, const atk_tensor* x, const uint64_t* ranks, atk_selector_fn decide,
                     void* user, const atk_als_opts& opts, double* factors_out,
-                    atk_mode_report* reports);
+                    atk_mode_report* reports, const ModeZeroPre* pre = nullptr);
+// H2D of the host input into x (device, allocated) in chunks along the last
+// mode on a side stream, with the mode-0 Gram of every landed chunk computed
+// on the context stream meanwhile (fp64 sum of the chunk Grams into s_dev).
+// Returns the Gram's device time (ms).
+double upload_with_gram0(atk_ctx* ctx, atk_tensor* x, const void* host, double* s_dev);
 atk_tensor* reconstruct(atk_ctx* ctx, const atk_tensor* core, const double* factors,
                         const uint64_t* odims);
 double relative_error(atk_ctx* ctx, const atk_tensor* x, const atk_tensor* core,

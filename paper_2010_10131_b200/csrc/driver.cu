@@ -59,7 +59,8 @@ void check_truncation(const atk_tensor* y, int mode, uint64_t r) {
 
 // ------------------------------------------------------------------ EIG / SVD
 // eig_mode_solver (solvers.hpp:64-73): gram -> sym_eig_top_r -> ttm(Y, U^T).
-ModeOut eig_mode(atk_ctx* ctx, const atk_tensor* y, int mode, uint64_t r, int solver_kind) {
+ModeOut eig_mode(atk_ctx* ctx, const atk_tensor* y, int mode, uint64_t r, int solver_kind,
+                 const double* gram_pre, double gram_pre_ms) {
     check_truncation(y, mode, r);
     const uint64_t I = y->dims[mode], J = j_of(y, mode);
     if (solver_kind == ATK_SOLVER_SVD && r > std::min(I, J))
@@ -67,19 +68,25 @@ ModeOut eig_mode(atk_ctx* ctx, const atk_tensor* y, int mode, uint64_t r, int so
     ModeOut out;
     out.solver = solver_kind;
     StageTimer tm(ctx);
-    DevBuf<double> S(ctx, I * I);
-    tm.start();
-    contract_ttt(ctx, y, y, mode, S.get(), true);
+    DevBuf<double> S(ctx, gram_pre ? 0 : I * I);
+    const double* Sg = gram_pre;
+    if (!gram_pre) {
+        tm.start();
+        contract_ttt(ctx, y, y, mode, S.get(), true);
+        if (ctx->comm) allreduce_sum(ctx, S.get(), I * I, &out.times.comm_ms);
+        out.times.gram_ms = tm.stop_ms();
+        Sg = S.get();
+    } else {
+        out.times.gram_ms = gram_pre_ms;
+    }
     record_gemm((long long)(I * I) * (long long)J);
-    if (ctx->comm) allreduce_sum(ctx, S.get(), I * I, &out.times.comm_ms);
-    out.times.gram_ms = tm.stop_ms();
 
     DevBuf<double> vals(ctx, r), vecs(ctx, I * r), ut(ctx, I * r);
     tm.start();
     // S is a Gram (PSD).  A tf32-computed Gram carries ~1e-6 relative error, so
     // resolving its eigenpairs beyond a 1e-9 Ritz residual buys nothing (the
     // factor error is ~residual / gap, far below the tf32 Gram error); fp64 keeps 1e-12.
-    out.eig = sym_eig_top_r(ctx, S.get(), int(I), int(r), vals.get(), vecs.get(), true,
+    out.eig = sym_eig_top_r(ctx, Sg, int(I), int(r), vals.get(), vecs.get(), true,
                             y->dtype == ATK_F32 ? std::max(1e-9, ctx->chfsi_tol) : ctx->chfsi_tol);
     out.times.eig_ms = tm.stop_ms();
 
@@ -252,7 +259,7 @@ static double seconds_since(std::chrono::steady_clock::time_point t0) {
 // directly and every later mode reads the previous shrunk tensor.
 atk_tensor* sthosvd(atk_ctx* ctx, const atk_tensor* x, const uint64_t* ranks, atk_selector_fn decide,
                     void* user, const atk_als_opts& opts, double* factors_out,
-                    atk_mode_report* reports) {
+                    atk_mode_report* reports, const ModeZeroPre* pre) {
     check_tensor(x, "sthosvd input");
     const int order = x->order;
     for (int n = 0; n < order; ++n)
@@ -280,15 +287,18 @@ atk_tensor* sthosvd(atk_ctx* ctx, const atk_tensor* x, const uint64_t* ranks, at
             for (int m = 0; m < order; ++m) rep.dims_before[m] = work->dims[m];
             rep.predicted_cost_eig = cost_eig(double(I), double(r), double(J));
             rep.predicted_cost_als = cost_als(double(I), double(r), double(J), opts.num_iters);
+            const bool use_pre = n == 0 && pre && pre->choice >= 0;
             const auto td = std::chrono::steady_clock::now();
-            const int choice = decide ? decide(user, n, I, r, J) : ATK_SOLVER_EIG;
-            rep.selector_decision_time = seconds_since(td);
+            const int choice = use_pre ? pre->choice : (decide ? decide(user, n, I, r, J) : ATK_SOLVER_EIG);
+            rep.selector_decision_time = use_pre ? pre->decide_time : seconds_since(td);
             if (choice < 0 || choice > 2) fail(ATK_INVALID_ARGUMENT, "selector callback failed");
             const auto ts = std::chrono::steady_clock::now();
             ModeOut mo;
             try {
                 if (choice == ATK_SOLVER_ALS)
                     mo = als_mode(ctx, work, n, r, opts, nullptr);
+                else if (use_pre && pre->gram)
+                    mo = eig_mode(ctx, work, n, r, choice, pre->gram, pre->gram_ms);
                 else
                     mo = eig_mode(ctx, work, n, r, choice);
             } catch (const Error& e) {
@@ -318,6 +328,73 @@ atk_tensor* sthosvd(atk_ctx* ctx, const atk_tensor* x, const uint64_t* ranks, at
         throw;
     }
     return owned;
+}
+
+double upload_with_gram0(atk_ctx* ctx, atk_tensor* x, const void* host, double* s_dev) {
+    const uint64_t I = x->dims[0], J = j_of(x, 0), esz = x->elem_bytes();
+    const uint64_t col_bytes = I * esz;
+    // ~32 chunks of >= 256 MB: the copy engine stays saturated, every chunk Gram
+    // still fills the SMs, and the last (unhidden) chunk Gram is short
+    uint64_t cols = std::max<uint64_t>(1, std::max<uint64_t>((256ull << 20) / col_bytes, (J + 31) / 32));
+    cols = std::min(cols, J);
+    const uint64_t nchunks = (J + cols - 1) / cols;
+    cudaStream_t cs = nullptr;
+    ATK_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    std::vector<cudaEvent_t> landed(nchunks, nullptr);
+    cudaEvent_t g0 = nullptr, g1 = nullptr;
+    double ms = 0.0;
+    auto cleanup = [&] {
+        for (auto& e : landed)
+            if (e) cudaEventDestroy(e);
+        if (g0) cudaEventDestroy(g0);
+        if (g1) cudaEventDestroy(g1);
+        cudaStreamDestroy(cs);
+    };
+    try {
+        for (auto& e : landed) ATK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        ATK_CUDA(cudaEventCreate(&g0));
+        ATK_CUDA(cudaEventCreate(&g1));
+        // the destination must be allocated before the side stream writes into it
+        ATK_CUDA(cudaEventRecord(landed[0], ctx->stream));
+        ATK_CUDA(cudaStreamWaitEvent(cs, landed[0], 0));
+        for (uint64_t c = 0; c < nchunks; ++c) {
+            const uint64_t j0 = c * cols, nc = std::min(cols, J - j0);
+            ATK_CUDA(cudaMemcpyAsync(static_cast<char*>(x->data) + j0 * col_bytes,
+                                     static_cast<const char*>(host) + j0 * col_bytes, nc * col_bytes,
+                                     cudaMemcpyHostToDevice, cs));
+            ATK_CUDA(cudaEventRecord(landed[c], cs));
+        }
+        DevBuf<double> part(ctx, I * I);
+        bool timing = false;
+        for (uint64_t c = 0; c < nchunks; ++c) {
+            const uint64_t j0 = c * cols, nc = std::min(cols, J - j0);
+            ATK_CUDA(cudaStreamWaitEvent(ctx->stream, landed[c], 0));
+            if (!timing) {
+                ATK_CUDA(cudaEventRecord(g0, ctx->stream));
+                timing = true;
+            }
+            atk_tensor view;  // mode-0 matricization of the chunk: I x nc, in place
+            view.ctx = ctx;
+            view.dtype = x->dtype;
+            view.order = 2;
+            view.dims[0] = I;
+            view.dims[1] = nc;
+            view.data = static_cast<char*>(x->data) + j0 * col_bytes;
+            contract_ttt(ctx, &view, &view, 0, c == 0 ? s_dev : part.get(), true);
+            if (c > 0) axpy(ctx, s_dev, part.get(), ATK_F64, I * I, 1.0);
+        }
+        ATK_CUDA(cudaEventRecord(g1, ctx->stream));
+        ATK_CUDA(cudaEventSynchronize(g1));
+        float f = 0.f;
+        ATK_CUDA(cudaEventElapsedTime(&f, g0, g1));
+        ms = f;
+    } catch (...) {
+        cudaStreamSynchronize(cs);
+        cleanup();
+        throw;
+    }
+    cleanup();
+    return ms;
 }
 
 // reconstruct (sthosvd.hpp:197-209)
