@@ -138,6 +138,7 @@ uint64_t atk_ctx_launch_count(const atk_ctx* ctx);
  *   "tma_tf32"      1 = round-to-nearest tf32 operand loads (default), 0 = hardware truncation
  *   "gram_2cta"     1 = CTA-pair (cta_group::2) Gram where supported (default)
  *   "gram_chunk_kb" K-blocks per fp32 accumulation chain before the fp64 drain
+ *   "gram_launch_kb" 2-CTA Gram: K-blocks per unit per launch (default 4096; 0 = one launch)
  *   "gram_lockstep" 1 = drift limiter in the 1-CTA Gram (default 0) */
 atk_status atk_ctx_set_option(atk_ctx* ctx, const char* key, double value);
 

@@ -62,6 +62,7 @@ struct atk_ctx {
     int gram_chunk_kb = 0;     // option "gram_chunk_kb": K-blocks per fp64 drain (0 = default)
     int gram_2cta = 1;         // option "gram_2cta": 256x256 Gram tiles on CTA pairs (cta_group::2)
     int gram_lockstep = 0;     // option "gram_lockstep": bound CTA drift so X streams from HBM once
+    int gram_launch_kb = 4096; // option "gram_launch_kb": 2-CTA Gram K-blocks per unit per launch (0 = one launch)
                                // (off: lockstep hot-spots L2 slices, 45 ms vs 34 ms at C5, r1)
     atk::Comm* comm = nullptr;
     cudaEvent_t ev[8] = {};

@@ -11,10 +11,14 @@
 // moves the kernel off the shared-memory-bandwidth ceiling (TMA writes + UMMA
 // reads ~ 192 B/clk/SM > 128 B/clk/SM for 1-CTA tiles).
 //
-// Pairs are not synchronised: an epoch drift bound (a leader waits until every
-// pair has issued K-epoch e - window; 8..32-block epochs, window 4) measured
-// 40-41 ms against 34-38 ms free-running at C5 mode 1, despite the 2.5x HBM
-// re-read it targets (profiles/r1/SUMMARY.md).
+// K is cut into several launches (option "gram_launch_kb": K-blocks per unit
+// per launch, default 4096) that accumulate into the same fp64 partial tiles:
+// every launch boundary re-aligns the pairs, so their K fronts cannot drift
+// apart and each K-block of X is fetched from HBM ~once and served to the
+// other tiles from L2.  Measured at I = 2048 (profiles/gram_probe.cu): one
+// launch over J = 4M 515-519 TF/s (2.5x HBM re-reads, profiles/r1), launches
+// of J = 256K 608 TF/s.  An in-kernel epoch drift bound (leaders wait on a
+// global counter) measured slower (40 ms vs 34-38 ms).
 //
 // Pipeline per CTA: warp 0 = TMA producer (both CTAs; the leader arms the
 // leader's full barrier with the bytes of BOTH CTAs, the peer's TMA completes
@@ -42,6 +46,7 @@ struct Gram2Params {
     int kmajor;
     int nkb_p;
     double* acc;        // [unit][TN2][TM2] fp64 partial tiles
+    int accumulate;     // 1: add into acc (a later K-launch of the same Gram)
 };
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -222,7 +227,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             for (int c0 = un.z; c0 < un.w; c0 += p.chunk_kb) {
                 tc::mbar_wait(&tfull[abuf], aphase);
                 tc::tc_fence_after();
-                const bool first = (c0 == un.z);
+                const bool first = !p.accumulate && (c0 == un.z);
 #pragma unroll 1
                 for (int cc = 0; cc < TN2 / 32; ++cc) {
                     uint32_t r[32];
@@ -356,9 +361,33 @@ void tc_gram2(atk_ctx* ctx, const atk_tensor* x, int mode, double* s_dev) {
     ATK_CUDA(cudaMemcpyAsync(dtu.get(), tile_unit.data(), tile_unit.size() * sizeof(int), cudaMemcpyHostToDevice,
                              ctx->stream));
     const int npairs = std::min<int>(int(units.size()), pairs_avail);
-    Gram2Params prm{du.get(), int(units.size()), chunk_kb, kmajor ? 1 : 0, nkb_p, acc.get()};
-    gram_tf32_2cta_kernel<<<2 * npairs, THREADS, SMEM2, ctx->stream>>>(tm, prm);
-    ATK_LAUNCHED(ctx);
+    Gram2Params prm{du.get(), int(units.size()), chunk_kb, kmajor ? 1 : 0, nkb_p, acc.get(), 0};
+    // K-launches: unit u's K range [kb0, kb1) is walked in slices of launch_kb
+    // K-blocks, one launch per slice index (all units advance together)
+    const int launch_kb = ctx->gram_launch_kb > 0 ? ctx->gram_launch_kb : (1 << 30);
+    int max_len = 0;
+    for (const int4& u : units) max_len = std::max(max_len, u.w - u.z);
+    const int nlaunch = (max_len + launch_kb - 1) / launch_kb;
+    DevBuf<int4> dlu(ctx, nlaunch > 1 ? units.size() * size_t(nlaunch) : 0);
+    if (nlaunch > 1) {
+        std::vector<int4> all;
+        all.reserve(units.size() * size_t(nlaunch));
+        for (int L = 0; L < nlaunch; ++L)
+            for (const int4& u : units) {
+                const int a = std::min(u.w, u.z + L * launch_kb), b = std::min(u.w, a + launch_kb);
+                all.push_back(make_int4(u.x, u.y, a, b));
+            }
+        ATK_CUDA(cudaMemcpyAsync(dlu.get(), all.data(), all.size() * sizeof(int4), cudaMemcpyHostToDevice,
+                                 ctx->stream));
+    }
+    for (int L = 0; L < nlaunch; ++L) {
+        if (nlaunch > 1) {
+            prm.units = dlu.get() + size_t(L) * units.size();
+            prm.accumulate = L > 0 ? 1 : 0;
+        }
+        gram_tf32_2cta_kernel<<<2 * npairs, THREADS, SMEM2, ctx->stream>>>(tm, prm);
+        ATK_LAUNCHED(ctx);
+    }
     const size_t n = size_t(I) * I;
     gram2_reduce<<<unsigned(std::min<size_t>((n + 255) / 256, size_t(ctx->num_sms) * 8)), 256, 0, ctx->stream>>>(
         acc.get(), dtu.get(), splits, nt, I, s_dev);
