@@ -150,6 +150,19 @@ atk_status atk_nccl_unique_id(void* out128);
 atk_status atk_comm_init(atk_ctx* ctx, const void* unique_id, int rank, int world);
 atk_status atk_comm_destroy(atk_ctx* ctx);
 
+/* Host-staged collectives: the same sharded schedule with the two exchange
+ * primitives supplied by the caller (e.g. torch.distributed / gloo), staged
+ * through host memory.  It lets N > 1 ranks share ONE GPU (NCCL refuses two
+ * ranks on the same device), so the multi-rank schedule — Gram allreduce per
+ * mode, the ALS YR/GR allreduce per iteration, the last-mode all-gather — is
+ * testable on a single B200.  Callbacks return 0 on success. */
+typedef struct atk_host_collectives {
+    int (*allreduce_f64)(void* user, double* host_buf, uint64_t count); /* in-place sum */
+    int (*broadcast)(void* user, void* host_buf, uint64_t bytes, int root);
+    void* user;
+} atk_host_collectives;
+atk_status atk_comm_init_host(atk_ctx* ctx, const atk_host_collectives* coll, int rank, int world);
+
 /* ------------------------------------------------------------ tensors */
 /* DenseTensor(dims) (tensor.hpp:103-107) — device allocation, NOT zero-filled. */
 atk_status atk_tensor_create(atk_ctx* ctx, atk_dtype dtype, int order, const uint64_t* dims,

@@ -23,6 +23,15 @@ u64ptr = C.POINTER(C.c_uint64)
 SELECTOR_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_uint64, C.c_uint64, C.c_uint64)
 
 
+HOST_ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_uint64)
+HOST_BROADCAST_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_int)
+
+
+class HostCollectives(C.Structure):
+    _fields_ = [("allreduce_f64", HOST_ALLREDUCE_FN), ("broadcast", HOST_BROADCAST_FN),
+                ("user", C.c_void_p)]
+
+
 class AlsOpts(C.Structure):
     _fields_ = [("num_iters", C.c_int), ("rel_tol", C.c_double), ("seed", C.c_uint64)]
 
@@ -58,6 +67,7 @@ _SIGS = {
     "atk_nccl_unique_id": (C.c_int, [C.c_void_p]),
     "atk_comm_init": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int]),
     "atk_comm_destroy": (C.c_int, [C.c_void_p]),
+    "atk_comm_init_host": (C.c_int, [C.c_void_p, C.POINTER(HostCollectives), C.c_int, C.c_int]),
     "atk_tensor_create": (C.c_int, [C.c_void_p, C.c_int, C.c_int, u64ptr, C.POINTER(C.c_void_p)]),
     "atk_tensor_wrap": (C.c_int, [C.c_void_p, C.c_int, C.c_int, u64ptr, C.c_void_p, C.POINTER(C.c_void_p)]),
     "atk_tensor_from_host": (C.c_int, [C.c_void_p, C.c_int, C.c_int, u64ptr, C.c_void_p, C.POINTER(C.c_void_p)]),

@@ -71,6 +71,32 @@ class Context:
         buf = C.create_string_buffer(bytes(unique_id), 128)
         _lib.check(self.lib.atk_comm_init(self.h, buf, int(rank), int(world)))
 
+    def comm_init_host(self, allreduce_f64, broadcast, rank: int, world: int) -> None:
+        """Host-staged collectives (atk_comm_init_host): `allreduce_f64(np.ndarray)`
+        sums a float64 array in place over the ranks; `broadcast(np.ndarray, root)`
+        broadcasts a uint8 array.  Lets several ranks share one GPU."""
+        import numpy as np
+
+        def _ar(_user, buf, count):
+            try:
+                allreduce_f64(np.ctypeslib.as_array(buf, shape=(int(count),)))
+                return 0
+            except Exception:  # noqa: BLE001 — reported as a status, never across the ABI
+                return 1
+
+        def _bc(_user, buf, nbytes, root):
+            try:
+                if nbytes:
+                    a = np.ctypeslib.as_array(C.cast(buf, C.POINTER(C.c_uint8)), shape=(int(nbytes),))
+                    broadcast(a, int(root))
+                return 0
+            except Exception:  # noqa: BLE001
+                return 1
+
+        coll = _lib.HostCollectives(_lib.HOST_ALLREDUCE_FN(_ar), _lib.HOST_BROADCAST_FN(_bc), None)
+        self._host_coll = coll  # the C side keeps raw callback pointers
+        _lib.check(self.lib.atk_comm_init_host(self.h, C.byref(coll), int(rank), int(world)))
+
     @staticmethod
     def nccl_unique_id() -> bytes:
         buf = C.create_string_buffer(128)

@@ -238,6 +238,14 @@ atk_status atk_comm_init(atk_ctx* ctx, const void* uid, int rank, int world) {
     });
 }
 
+atk_status atk_comm_init_host(atk_ctx* ctx, const atk_host_collectives* coll, int rank,
+                              int world) {
+    return guard([&] {
+        bind(ctx);
+        comm_init_host(ctx, coll, rank, world);
+    });
+}
+
 atk_status atk_comm_destroy(atk_ctx* ctx) {
     return guard([&] {
         bind(ctx);

@@ -53,6 +53,7 @@ struct AlsOut {
     std::vector<double> l;  // I x r host
     atk_tensor* rfac = nullptr;
     int iterations_run = 0;
+    double comm_ms = 0.0;  // per-iteration YR/GR allreduce (sharded runs)
 };
 void contract_ttt(atk_ctx* ctx, const atk_tensor* x, const atk_tensor* y, int mode, double* z_dev,
                   bool sym);
@@ -95,7 +96,9 @@ double relative_error(atk_ctx* ctx, const atk_tensor* x, const atk_tensor* core,
 void comm_init(atk_ctx* ctx, const void* unique_id, int rank, int world);
 void comm_destroy(atk_ctx* ctx);
 void nccl_unique_id(void* out128);
+void comm_init_host(atk_ctx* ctx, const atk_host_collectives* coll, int rank, int world);
 void allreduce_sum(atk_ctx* ctx, double* buf, uint64_t count, double* comm_ms);
+void allreduce_sum2(atk_ctx* ctx, double* a, uint64_t na, double* b, uint64_t nb, double* comm_ms);
 atk_tensor* allgather_last_mode(atk_ctx* ctx, const atk_tensor* local);
 uint64_t comm_global_last(atk_ctx* ctx, const atk_tensor* local);
 

@@ -71,9 +71,32 @@ void nccl_check(ncclResult_t r, const char* what) {
 }  // namespace
 
 struct Comm {
-    ncclComm_t comm = nullptr;
+    ncclComm_t comm = nullptr;  // NCCL backend
+    bool host = false;          // host-staged backend (atk_comm_init_host)
+    atk_host_collectives coll{};
     int rank = 0, world = 1;
 };
+
+namespace {
+
+void host_check(int rc, const char* what) {
+    if (rc != 0) fail(ATK_NCCL_ERROR, std::string("host collective ") + what + " failed (" +
+                                          std::to_string(rc) + ")");
+}
+
+// In-place sum of device doubles through host memory (host backend).
+void host_allreduce(atk_ctx* ctx, double* dev, uint64_t count) {
+    std::vector<double> h(count);
+    ATK_CUDA(cudaMemcpyAsync(h.data(), dev, count * sizeof(double), cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    ATK_CUDA(cudaStreamSynchronize(ctx->stream));
+    host_check(ctx->comm->coll.allreduce_f64(ctx->comm->coll.user, h.data(), count), "allreduce");
+    ATK_CUDA(cudaMemcpyAsync(dev, h.data(), count * sizeof(double), cudaMemcpyHostToDevice,
+                             ctx->stream));
+    ATK_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+}  // namespace
 
 void nccl_unique_id(void* out128) {
     ncclUniqueId id;
@@ -94,6 +117,19 @@ void comm_init(atk_ctx* ctx, const void* unique_id, int rank, int world) {
     ctx->comm = c;
 }
 
+void comm_init_host(atk_ctx* ctx, const atk_host_collectives* coll, int rank, int world) {
+    if (world < 1 || rank < 0 || rank >= world) fail(ATK_INVALID_ARGUMENT, "bad rank/world");
+    if (!coll || !coll->allreduce_f64 || !coll->broadcast)
+        fail(ATK_INVALID_ARGUMENT, "host collectives need allreduce_f64 and broadcast");
+    comm_destroy(ctx);
+    auto* c = new Comm();
+    c->host = true;
+    c->coll = *coll;
+    c->rank = rank;
+    c->world = world;
+    ctx->comm = c;
+}
+
 void comm_destroy(atk_ctx* ctx) {
     if (!ctx->comm) return;
     if (ctx->comm->comm) nccl().CommDestroy(ctx->comm->comm);
@@ -105,14 +141,46 @@ void allreduce_sum(atk_ctx* ctx, double* buf, uint64_t count, double* comm_ms) {
     if (!ctx->comm || ctx->comm->world == 1) return;
     StageTimer t(ctx);
     t.start();
-    nccl_check(nccl().AllReduce(buf, buf, count, ncclFloat64, ncclSum, ctx->comm->comm, ctx->stream),
-               "ncclAllReduce");
+    if (ctx->comm->host)
+        host_allreduce(ctx, buf, count);
+    else
+        nccl_check(nccl().AllReduce(buf, buf, count, ncclFloat64, ncclSum, ctx->comm->comm,
+                                    ctx->stream),
+                   "ncclAllReduce");
+    const double ms = t.stop_ms();
+    if (comm_ms) *comm_ms += ms;
+}
+
+void allreduce_sum2(atk_ctx* ctx, double* a, uint64_t na, double* b, uint64_t nb,
+                    double* comm_ms) {
+    if (!ctx->comm || ctx->comm->world == 1) return;
+    StageTimer t(ctx);
+    t.start();
+    if (ctx->comm->host) {
+        host_allreduce(ctx, a, na);
+        host_allreduce(ctx, b, nb);
+    } else {
+        nccl_check(nccl().GroupStart(), "ncclGroupStart");
+        nccl_check(nccl().AllReduce(a, a, na, ncclFloat64, ncclSum, ctx->comm->comm, ctx->stream),
+                   "ncclAllReduce");
+        nccl_check(nccl().AllReduce(b, b, nb, ncclFloat64, ncclSum, ctx->comm->comm, ctx->stream),
+                   "ncclAllReduce");
+        nccl_check(nccl().GroupEnd(), "ncclGroupEnd");
+    }
     const double ms = t.stop_ms();
     if (comm_ms) *comm_ms += ms;
 }
 
 static std::vector<uint64_t> gather_last(atk_ctx* ctx, const atk_tensor* local) {
     const int w = ctx->comm->world;
+    if (ctx->comm->host) {  // sizes are < 2^53: exact in an fp64 sum
+        std::vector<double> v(w, 0.0);
+        v[ctx->comm->rank] = double(local->dims[local->order - 1]);
+        host_check(ctx->comm->coll.allreduce_f64(ctx->comm->coll.user, v.data(), w), "allreduce");
+        std::vector<uint64_t> h(w);
+        for (int r = 0; r < w; ++r) h[r] = uint64_t(v[r]);
+        return h;
+    }
     DevBuf<uint64_t> d(ctx, w);
     ATK_CUDA(cudaMemsetAsync(d.get(), 0, w * sizeof(uint64_t), ctx->stream));
     const uint64_t mine = local->dims[local->order - 1];
@@ -149,6 +217,24 @@ atk_tensor* allgather_last_mode(atk_ctx* ctx, const atk_tensor* local) {
     if (!ctx->comm || ctx->comm->world == 1) {
         ATK_CUDA(cudaMemcpyAsync(out->data, local->data, local->bytes(), cudaMemcpyDeviceToDevice,
                                  ctx->stream));
+        return out;
+    }
+    if (ctx->comm->host) {
+        const size_t es = local->elem_bytes();
+        std::vector<char> h(out->bytes());
+        uint64_t off = 0;
+        for (int r = 0; r < ctx->comm->world; ++r) {
+            char* dst = h.data() + off * slab * es;
+            const uint64_t nb = sizes[r] * slab * es;
+            if (r == ctx->comm->rank) {
+                ATK_CUDA(cudaMemcpyAsync(dst, local->data, nb, cudaMemcpyDeviceToHost, ctx->stream));
+                ATK_CUDA(cudaStreamSynchronize(ctx->stream));
+            }
+            host_check(ctx->comm->coll.broadcast(ctx->comm->coll.user, dst, nb, r), "broadcast");
+            off += sizes[r];
+        }
+        ATK_CUDA(cudaMemcpyAsync(out->data, h.data(), h.size(), cudaMemcpyHostToDevice, ctx->stream));
+        ATK_CUDA(cudaStreamSynchronize(ctx->stream));
         return out;
     }
     const ncclDataType_t dt = local->dtype == ATK_F32 ? ncclFloat32 : ncclFloat64;

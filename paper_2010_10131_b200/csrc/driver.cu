@@ -164,11 +164,14 @@ AlsOut als_iterate(atk_ctx* ctx, const atk_tensor* y, int mode, const double* l0
         out.rfac = contract_ttm(ctx, w, GLi.get(), r, mode);  // rfac = W x_n (L^T L)^{-1}
         record_gemm(2LL * (long long)(r * J) * (long long)r);
         atk_tensor_free(w);
-        if (ctx->comm) fail(ATK_UNSUPPORTED, "ALS under a multi-GPU communicator is not wired yet");
         contract_ttt(ctx, y, out.rfac, mode, YR.get(), false);  // YR = Y_(n) rfac_(n)^T
         record_gemm(2LL * (long long)(I * r) * (long long)J);
         contract_ttt(ctx, out.rfac, out.rfac, mode, GR.get(), true);  // symmetric: the Gram kernels
         record_gemm(2LL * (long long)(r * r) * (long long)J);
+        // Sharded (SURVEY §8(e) "ALS modes"): YR and GR are sums over J, so the
+        // local partials are combined with one grouped allreduce per iteration;
+        // L, its Gram and every R x R solve are then replicated bit-identically.
+        if (ctx->comm) allreduce_sum2(ctx, YR.get(), I * r, GR.get(), r * r, &out.comm_ms);
         spd_inverse(ctx, GR.get(), int(r), GRi.get());
         dgemm(ctx, false, false, int(I), int(r), int(r), 1.0, YR.get(), int(I), GRi.get(), int(r),
               0.0, nxt.get(), int(I));
@@ -245,6 +248,7 @@ ModeOut als_mode(atk_ctx* ctx, const atk_tensor* y, int mode, uint64_t r, const 
                              cudaMemcpyDeviceToHost, ctx->stream));
     ATK_CUDA(cudaStreamSynchronize(ctx->stream));
     out.times.als_ms = tm.stop_ms();
+    out.times.comm_ms = it.comm_ms;
     out.times.total_ms = out.times.als_ms;
     out.iterations = it.iterations_run;
     return out;

@@ -27,3 +27,20 @@ def init_comm_from_torch(ctx, group=None) -> None:
     t = torch.tensor(list(uid), dtype=torch.uint8)
     dist.broadcast(t, 0, group=group)
     ctx.comm_init(bytes(t.tolist()), rank, world)
+
+
+def init_host_comm_from_torch(ctx, group=None) -> None:
+    """atk_comm_init_host over a torch.distributed group (e.g. gloo): the
+    collectives are staged through host memory, so ranks may share a GPU."""
+    import torch
+    import torch.distributed as dist
+
+    def allreduce_f64(a):
+        t = torch.from_numpy(a)  # shares memory with the engine's staging buffer
+        dist.all_reduce(t, group=group)
+
+    def broadcast(a, root):
+        t = torch.from_numpy(a)
+        dist.broadcast(t, root, group=group)
+
+    ctx.comm_init_host(allreduce_f64, broadcast, dist.get_rank(group), dist.get_world_size(group))

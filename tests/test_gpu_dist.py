@@ -34,3 +34,74 @@ def test_world1_nccl_matches_single(dtype):
     np.testing.assert_array_equal(g0, g1)
     for a, b in zip(ref.decomposition.factors, res.decomposition.factors):
         np.testing.assert_array_equal(a, b)
+
+
+def _host_comm_worker(rank, world, port, dims, ranks, kinds, dtype, out):
+    import os
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    sys.path.insert(0, str(root))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2010_10131_b200 import atucker
+    from paper_2010_10131_b200.dist import init_host_comm_from_torch, shard_range
+    from paper_2010_10131_b200.selector import SolverKind, Strategy
+
+    rng = np.random.default_rng(5)
+    x = np.asfortranarray(rng.standard_normal(dims).astype(dtype))
+    strat = Strategy.manual([SolverKind(k) for k in kinds])
+    opts = atucker.AlsOptions(seed=9)
+    ctx = atucker.Context(0)
+    init_host_comm_from_torch(ctx)
+    lo, hi = shard_range(dims[-1], rank, world)
+    xl = atucker.DeviceTensor.from_numpy(np.asfortranarray(x[..., lo:hi]), ctx=ctx)
+    res = atucker.sthosvd(xl, ranks, strat, opts, ctx=ctx, global_dims=dims)
+    core = res.decomposition.core.to_numpy().astype(np.float64)
+    facs = res.decomposition.factors
+    comm_ms = sum(r.times.comm_ms for r in res.reports)
+    if rank == 0:
+        plain = atucker.Context(0)
+        ref = atucker.sthosvd(atucker.DeviceTensor.from_numpy(x, ctx=plain), ranks, strat, opts, ctx=plain)
+        g, gr = np.linalg.norm(core), np.linalg.norm(ref.decomposition.core.to_numpy().astype(np.float64))
+        fd = max(np.abs(a - b).max() for a, b in zip(facs, ref.decomposition.factors))
+        out.put((g, gr, fd, comm_ms))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("dims,ranks,kinds,dtype,tol", [
+    ([40, 36, 30], [8, 6, 5], [1, 0, 0], np.float64, 1e-10),
+    ([24, 20, 18, 16], [5, 4, 4, 3], [0, 1, 0, 1], np.float64, 1e-10),
+    ([96, 64, 80], [12, 10, 8], [1, 1, 0], np.float32, 1e-4),
+    ([256, 64, 96], [16, 12, 8], [0, 0, 0], np.float32, 1e-4),
+])
+def test_two_ranks_one_gpu_host_collectives(dims, ranks, kinds, dtype, tol):
+    """N = 2 on the one GPU: both ranks share cuda:0 and exchange through the
+    host-staged backend (gloo).  The sharded schedule — per-mode Gram
+    allreduce, per-iteration ALS YR/GR allreduce, last-mode all-gather — must
+    reproduce the single-process st-HOSVD."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    mpc = mp.get_context("spawn")
+    q = mpc.Queue()
+    procs = [mpc.Process(target=_host_comm_worker, args=(r, 2, port, dims, ranks, kinds, dtype, q))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    g, gr, fd, comm_ms = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert abs(g - gr) / gr <= tol
+    assert fd <= (1e-8 if dtype == np.float64 else 1e-3)
+    assert comm_ms > 0.0
