@@ -94,7 +94,8 @@ typedef struct atk_mode_report {
     int mode;
     int solver_used;
     int iterations_run;
-    int eig_method;               /* 0 = Jacobi (dense), 1 = Chebyshev-filtered Rayleigh-Ritz */
+    int eig_method;               /* 0 = Jacobi (dense), 1 = Chebyshev-filtered Rayleigh-Ritz,
+                                     2 = tridiagonal (Householder + bisection + inverse iteration) */
     double selector_decision_time; /* seconds, host */
     double solver_time;            /* seconds, host wall incl. sync */
     double predicted_cost_eig;
@@ -132,7 +133,8 @@ atk_status atk_ctx_synchronize(atk_ctx* ctx);
 uint64_t atk_ctx_launch_count(const atk_ctx* ctx);
 /* Engine tuning knobs (unknown keys -> ATK_INVALID_ARGUMENT):
  *   "simt"          1 = CUDA-core contractions for every shape (default 0: tcgen05 / DMMA)
- *   "eig_method"   -1 auto, 0 dense Jacobi (n <= 112), 1 ChFSI
+ *   "eig_method"   -1 auto (tridiagonal for n <= 200, else ChFSI), 0 dense Jacobi (n <= 112;
+ *                  also the Rayleigh-Ritz solver), 1 ChFSI, 2 tridiagonal (n <= 200)
  *   "chfsi_tol"     relative Ritz-residual target of ChFSI (default 1e-12; fp32 Grams use >= 1e-9)
  *   "eig_assume_psd" 1 = atk_sym_eig_top_r inputs are Grams (Cholesky-preconditioned Jacobi)
  *   "tma_tf32"      1 = round-to-nearest tf32 operand loads (default), 0 = hardware truncation

@@ -67,7 +67,25 @@ class Context:
     def launch_count(self) -> int:
         return int(self.lib.atk_ctx_launch_count(self.h))
 
+    @staticmethod
+    def _nccl_hint() -> None:
+        """Point the engine's dlopen at torch's bundled NCCL (same copy as torch.distributed)."""
+        import os
+
+        if "ATK_NCCL_PATH" in os.environ:
+            return
+        try:
+            import nvidia.nccl
+        except ImportError:
+            return
+        for d in nvidia.nccl.__path__:
+            p = os.path.join(d, "lib", "libnccl.so.2")
+            if os.path.exists(p):
+                os.environ["ATK_NCCL_PATH"] = p
+                return
+
     def comm_init(self, unique_id: bytes, rank: int, world: int) -> None:
+        self._nccl_hint()
         buf = C.create_string_buffer(bytes(unique_id), 128)
         _lib.check(self.lib.atk_comm_init(self.h, buf, int(rank), int(world)))
 
@@ -99,6 +117,7 @@ class Context:
 
     @staticmethod
     def nccl_unique_id() -> bytes:
+        Context._nccl_hint()
         buf = C.create_string_buffer(128)
         _lib.check(_lib.load().atk_nccl_unique_id(buf))
         return buf.raw
@@ -510,7 +529,7 @@ def _reports(reps, order: int) -> list:
             predicted_cost_eig=rp.predicted_cost_eig, predicted_cost_als=rp.predicted_cost_als,
             dims_before=tuple(int(v) for v in rp.dims_before[:order]),
             dims_after=tuple(int(v) for v in rp.dims_after[:order]),
-            iterations_run=rp.iterations_run, eig_method="chfsi" if rp.eig_method == 1 else "jacobi",
+            iterations_run=rp.iterations_run, eig_method={0: "jacobi", 1: "chfsi", 2: "tridiag"}.get(rp.eig_method, "?"),
             times=StageTimes.from_c(rp.times)))
     return out
 

@@ -54,7 +54,7 @@ struct atk_ctx {
     cudaStream_t own_stream = nullptr;
     uint64_t launches = 0;
     int force_simt = 0;        // option "simt": portable CUDA-core contractions
-    int eig_method = -1;       // option "eig_method": -1 auto, 0 dense Jacobi, 1 ChFSI
+    int eig_method = -1;       // option "eig_method": -1 auto, 0 dense Jacobi, 1 ChFSI, 2 tridiagonal
     double chfsi_tol = 1e-12;  // option "chfsi_tol": relative Ritz residual target
     bool eig_assume_psd = false;  // option "eig_assume_psd": atk_sym_eig_top_r input is a Gram
     int tma_tf32 = 1;          // option "tma_tf32": TMA converts fp32 -> tf32 with round-to-nearest
@@ -184,6 +184,14 @@ constexpr int kJacobiMax = 112;
 constexpr int kJacobiPsdMax = 152;
 void jacobi_eig(atk_ctx* ctx, const double* a, int n, int lda, double* values, double* vectors,
                 int ldv, int* sweeps_dev, bool psd = false);
+// tridiag.cu — dense symmetric eigensolver by Householder tridiagonalisation,
+// bisection and inverse iteration (one CTA holds the packed lower triangle):
+// the top `nvals` (>= nwant) eigenvalues of A (n x n, lda), descending, and
+// the vectors of the top `nwant` (n x nwant, ldv), signs NOT fixed.
+// Bit-reproducible (no atomics).
+constexpr int kTridiagMax = 200;
+void tridiag_eig(atk_ctx* ctx, const double* a, int n, int lda, int nwant, double* values, double* vectors,
+                 int ldv, int nvals = 0);
 // Cholesky factorization in place (lower), status written to *info_dev (0 ok, k>0 pivot k).
 void cholesky(atk_ctx* ctx, double* a, int n, int* info_dev);
 // Shared-memory Cholesky of G (k x k, k <= kJacobiMax) fused with X = L^{-T};

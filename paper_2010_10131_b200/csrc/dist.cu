@@ -15,6 +15,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -42,7 +43,14 @@ struct NcclApi {
 NcclApi& nccl() {
     static NcclApi api;
     if (!api.h) {
-        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        // Prefer (1) an explicit ATK_NCCL_PATH (the Python layer points it at
+        // torch's bundled NCCL), (2) a libnccl already in the process, (3) the
+        // system one.  Loading an older system NCCL first would shadow the
+        // newer symbols a later `import torch` needs.
+        void* h = nullptr;
+        if (const char* env = std::getenv("ATK_NCCL_PATH")) h = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
         if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
         if (!h) fail(ATK_NCCL_ERROR, std::string("cannot load libnccl.so.2: ") + dlerror());
         auto get = [&](const char* n) {

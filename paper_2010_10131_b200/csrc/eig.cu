@@ -504,17 +504,20 @@ Bounds lanczos_bounds(atk_ctx* ctx, const double* S, int n, bool psd) {
 }
 
 // Rayleigh-Ritz on the orthonormal block V (n x k): W = S V, T = V^T W,
-// T = Z diag(theta) Z^T (Jacobi, descending), V <- V Z, W <- W Z.
-void rayleigh_ritz(atk_ctx* ctx, const double* S, int n, int k, double* V, double* W, double* T, double* Z,
-                   double* theta, double* tmp, int* sweeps, bool psd) {
-    const size_t nk = size_t(n) * k;
+// theta = all k Ritz values (descending), Z = the top r Ritz vectors of T;
+// Vr = V Z, Wr = W Z (n x r).  V itself stays unrotated: the next Chebyshev
+// filter only needs a basis of span(V), so the k - r guard-band vectors are
+// never formed (their values still set the filter's cut).
+void rayleigh_ritz(atk_ctx* ctx, const double* S, int n, int k, int r, const double* V, double* W, double* T,
+                   double* Z, double* theta, double* Vr, double* Wr, int* sweeps, bool psd) {
     dgemm(ctx, false, false, n, k, n, 1.0, S, n, V, n, 0.0, W, n);
     dgemm(ctx, true, false, k, k, n, 1.0, V, n, W, n, 0.0, T, k);
-    jacobi_eig(ctx, T, k, k, theta, Z, k, sweeps, psd);  // V^T S V is PSD when S is
-    dgemm(ctx, false, false, n, k, k, 1.0, V, n, Z, k, 0.0, tmp, n);
-    ATK_CUDA(cudaMemcpyAsync(V, tmp, nk * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
-    dgemm(ctx, false, false, n, k, k, 1.0, W, n, Z, k, 0.0, tmp, n);
-    ATK_CUDA(cudaMemcpyAsync(W, tmp, nk * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+    if (ctx->eig_method == 0)
+        jacobi_eig(ctx, T, k, k, theta, Z, k, sweeps, psd);  // V^T S V is PSD when S is; all k vectors
+    else
+        tridiag_eig(ctx, T, k, k, r, theta, Z, k, k);
+    dgemm(ctx, false, false, n, r, k, 1.0, V, n, Z, k, 0.0, Vr, n);
+    dgemm(ctx, false, false, n, r, k, 1.0, W, n, Z, k, 0.0, Wr, n);
 }
 
 }  // namespace
@@ -523,6 +526,13 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
                       bool psd, double tol) {
     EigInfo info;
     cudaStream_t st = ctx->stream;
+    if (n <= kTridiagMax && (ctx->eig_method == -1 || ctx->eig_method == 2)) {
+        tridiag_eig(ctx, s_dev, n, n, r, values_dev, vectors_dev, n);
+        fix_signs(ctx, vectors_dev, n, r, n);
+        if (std::getenv("ATK_TRACE")) std::fprintf(stderr, "[atk eig n=%d r=%d] tridiagonal\n", n, r);
+        info.method = 2;
+        return info;
+    }
     const bool dense = (n <= kJacobiMax || (psd && n <= kJacobiPsdMax)) && ctx->eig_method != 1;
     if (dense) {
         DevBuf<double> vals(ctx, n), vecs(ctx, size_t(n) * n);
@@ -554,8 +564,9 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
     k = std::min(k, kJacobiMax);
     if (k < r) fail(ATK_UNSUPPORTED, "sym_eig_top_r: r > 112 with n > 112 is not supported");
     const size_t nn = size_t(n) * n, nk = size_t(n) * k, kk = size_t(k) * k;
+    const size_t nr = size_t(n) * r;
     DevBuf<double> S(ctx, nn), V(ctx, nk), W(ctx, nk), Ya(ctx, nk), Yb(ctx, nk), Yc(ctx, nk), T(ctx, kk), Z(ctx, kk),
-        theta(ctx, k), res(ctx, k);
+        theta(ctx, k), res(ctx, k), Vr(ctx, nr), Wr(ctx, nr);
     Ws ws{DevBuf<double>(ctx, kk), DevBuf<double>(ctx, kk), DevBuf<double>(ctx, k), DevBuf<double>(ctx, k),
           DevBuf<double>(ctx, kk), DevBuf<double>(ctx, nk), DevBuf<int>(ctx, 1), DevBuf<int>(ctx, 3)};
     DevBuf<int> sweeps(ctx, 1);
@@ -585,7 +596,8 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
     dgemm(ctx, false, false, n, k, n, 1.0, S.get(), n, Ya.get(), n, 0.0, Yb.get(), n);
     orthonormalize(ctx, Yb.get(), n, k, V.get(), ws);
     mark("qr0");
-    rayleigh_ritz(ctx, S.get(), n, k, V.get(), W.get(), T.get(), Z.get(), theta.get(), Ya.get(), sweeps.get(), psd);
+    rayleigh_ritz(ctx, S.get(), n, k, r, V.get(), W.get(), T.get(), Z.get(), theta.get(), Vr.get(), Wr.get(),
+                  sweeps.get(), psd);
     mark("rr0", trace_sweeps(sweeps.get()));
 
     const int max_outer = 100;
@@ -599,7 +611,7 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
     int it = 0;
     double worst = 0.0;
     for (;; ++it) {
-        ritz_residual<<<(r + 7) / 8, 256, 0, st>>>(W.get(), V.get(), theta.get(), n, r, res.get());
+        ritz_residual<<<(r + 7) / 8, 256, 0, st>>>(Wr.get(), Vr.get(), theta.get(), n, r, res.get());
         ATK_LAUNCHED(ctx);
         ATK_CUDA(cudaMemcpyAsync(hth.data(), theta.get(), k * sizeof(double), cudaMemcpyDeviceToHost, st));
         ATK_CUDA(cudaMemcpyAsync(hres.data(), res.get(), r * sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -656,13 +668,13 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
         mark("filter", degree, worst / scale);
         orthonormalize(ctx, ycur, n, k, V.get(), ws);
         mark("qr");
-        rayleigh_ritz(ctx, S.get(), n, k, V.get(), W.get(), T.get(), Z.get(), theta.get(),
-                      ynext == V.get() ? Yc.get() : ynext, sweeps.get(), psd);
+        rayleigh_ritz(ctx, S.get(), n, k, r, V.get(), W.get(), T.get(), Z.get(), theta.get(), Vr.get(), Wr.get(),
+                      sweeps.get(), psd);
         mark("rr", trace_sweeps(sweeps.get()));
     }
     mark("done", it, worst / scale);
     ATK_CUDA(cudaMemcpyAsync(values_dev, theta.get(), r * sizeof(double), cudaMemcpyDeviceToDevice, st));
-    ATK_CUDA(cudaMemcpyAsync(vectors_dev, V.get(), size_t(n) * r * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    ATK_CUDA(cudaMemcpyAsync(vectors_dev, Vr.get(), nr * sizeof(double), cudaMemcpyDeviceToDevice, st));
     fix_signs(ctx, vectors_dev, n, r, n);
     info.method = 1;
     info.iterations = it;

@@ -1,0 +1,553 @@
+// tridiag.cu — dense symmetric eigensolver for n <= kTridiagMax by reduction
+// to tridiagonal form (the structure of LAPACK dsytrd + dstebz + dstein +
+// dormtr; the reference's Eigen SelfAdjointEigenSolver, linalg.hpp:101-123,
+// also tridiagonalises first, then runs implicit QR).  Four launches:
+//
+//  1. trd_kernel (one CTA, 1024 threads): Householder reduction A = Q T Q^T
+//     of the symmetrised input, packed lower triangle resident in shared memory
+//     (n <= 200: 160.8 KB).  Warps own columns (j = w mod 32), lanes own rows
+//     (i = lane mod 32) so the symmetric matvec reads each stored element once
+//     and the rank-2 update touches it once; the matvec's row partials go
+//     through a per-warp buffer summed in a fixed order (no atomics: results
+//     are bit-reproducible, which the sharded multi-GPU path relies on).
+//     Three barriers per Householder step.
+//  2. bisect_kernel (one warp per wanted eigenvalue): Sturm-count
+//     multisection, 32 shifts per pass (each pass narrows the bracket 33x).
+//  3. invit_kernel (one warp per cluster): inverse iteration on T - lambda I
+//     (tridiagonal LU with partial pivoting, dgttrf/dgttrs), 3 iterations from
+//     a fixed pseudo-random start.  Eigenvalues closer than 1e-3 ||T||_1 form a
+//     cluster (dstein's criterion): the cluster's members are solved in
+//     parallel, one lane each, and Gram-Schmidt-orthogonalised in order after
+//     every iteration.
+//  4. backtr_kernel (one warp per vector): x <- H_0 ... H_{n-3} x with the
+//     Householder vectors staged in shared memory.
+//
+// Only the wanted top `nwant` pairs are formed (the reference computes all n
+// and discards n - r).  Values descending; signs are fixed by the caller.
+#include <algorithm>
+#include <cfloat>
+#include <cmath>
+
+#include "atk_internal.cuh"
+
+namespace atk {
+namespace {
+
+constexpr int kTrdThreads = 1024;
+constexpr int kTrdWarps = kTrdThreads / 32;
+constexpr int kRowSlots = (kTridiagMax + 31) / 32;  // rows per lane
+
+__device__ __forceinline__ int pk(int i, int j, int n) {  // A(i, j), i >= j, packed lower
+    return j * n - (j * (j - 1)) / 2 + (i - j);
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Publish reflector c (c + 2 < n) from the current column c: every lane of
+// the calling warp; writes T's d[c], e[c], tau[c], scal[c] and the dense v
+// (zero outside rows c+1..n-1) into vb.  dsytd2 / dlarfg conventions.
+template <int S>
+__device__ __forceinline__ void publish_reflector(const double* AP, int n, int c, double* vb, double* sh_tau,
+                                                  double* d, double* e, double* tau_out, double* scal_out) {
+    const int lane = threadIdx.x & 31;
+    const int cc = pk(c, c, n) - c;
+    const double alpha = AP[cc + c + 1];
+    double x[S], xn = 0.0;
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        const int i = lane + 32 * s;
+        x[s] = (i >= c + 2 && i < n) ? AP[cc + i] : 0.0;
+        xn = fma(x[s], x[s], xn);
+    }
+    xn = warp_sum(xn);
+    double tau = 0.0, scal = 0.0, beta = alpha;
+    if (xn > 0.0) {
+        beta = -copysign(sqrt(fma(alpha, alpha, xn)), alpha);
+        scal = 1.0 / (alpha - beta);
+        tau = (beta - alpha) / beta;
+    }
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        const int i = lane + 32 * s;
+        vb[i] = (i == c + 1) ? 1.0 : x[s] * scal;
+    }
+    if (lane == 0) {
+        d[c] = AP[cc + c];
+        e[c] = beta;
+        tau_out[c] = tau;
+        scal_out[c] = scal;
+        *sh_tau = tau;
+    }
+}
+
+// hh: packed lower triangle after the reduction (column k below the diagonal =
+// the unscaled Householder vector k); d, e: T; tau, scal: reflector k is
+// H_k = I - tau_k v v^T with v_{k+1} = 1, v_i = hh(i, k) * scal_k (i > k + 1).
+// S = ceil(n / 32) row slots per lane (a template: no dead slots for small n).
+template <int S>
+__global__ void __launch_bounds__(kTrdThreads, 1)
+    trd_kernel(const double* __restrict__ a, int n, int lda, double* __restrict__ hh, double* __restrict__ d,
+               double* __restrict__ e, double* __restrict__ tau_out, double* __restrict__ scal_out) {
+    extern __shared__ double sm[];
+    constexpr int NR = 32 * S;             // padded rows
+    const int np = n * (n + 1) / 2;
+    double* AP = sm;                       // np + NR zero pad (reads past the end stay finite)
+    double* part = AP + np + NR;           // kTrdWarps x n row partials of the matvec
+    double* dots = part + kTrdWarps * n;   // n: column dots of the matvec
+    double* p = dots + n;                  // NR
+    double* vbuf = p + NR;                 // 2 x NR (reflector k in vbuf[k & 1])
+    double* vav = vbuf + 2 * NR;           // kTrdWarps partials of v^T A v
+    double* sc = vav + kTrdWarps;          // tau[2], K
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    for (int j = 0; j < n; ++j)
+        for (int i = j + tid; i < n; i += kTrdThreads)
+            AP[pk(i, j, n)] = 0.5 * (a[i + size_t(lda) * j] + a[j + size_t(lda) * i]);
+    for (int q = tid; q < NR; q += kTrdThreads) {
+        AP[np + q] = 0.0;
+        p[q] = 0.0;
+    }
+    for (int q = tid; q < kTrdWarps * n; q += kTrdThreads) part[q] = 0.0;
+    __syncthreads();
+    if (n > 2 && w == 0) publish_reflector<S>(AP, n, 0, vbuf, sc, d, e, tau_out, scal_out);
+    __syncthreads();
+
+    for (int k = 0; k + 2 < n; ++k) {
+        const double tau = sc[k & 1];
+        const double* vk = vbuf + (k & 1) * NR;
+        const int j0 = k + 1 + ((w - (k + 1)) % kTrdWarps + kTrdWarps) % kTrdWarps;
+        const bool next = k + 3 < n;  // reflector k+1 exists
+        if (tau != 0.0) {  // uniform
+            double v[S], acc[S];
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                v[s] = vk[lane + 32 * s];
+                acc[s] = 0.0;
+            }
+            // ---- B: symmetric matvec A22 v (warp w: columns j = w mod 32), v^T A v partial
+            double vav_l = 0.0;
+            for (int j = j0; j < n; j += kTrdWarps) {
+                const double vj = vk[j];
+                const int cj = pk(j, j, n) - j;
+                const int s0 = j >> 5;
+                double dt = 0.0;
+#pragma unroll
+                for (int s = 0; s < S; ++s) {
+                    if (s >= s0) {  // warp-uniform
+                        const int i = lane + 32 * s;
+                        double aij = AP[cj + i];
+                        if (s == s0) aij = (i >= j) ? aij : 0.0;
+                        dt = fma(aij, v[s], dt);
+                        acc[s] = fma(i > j ? aij : 0.0, vj, acc[s]);
+                    }
+                }
+                dt = warp_sum(dt);
+                if (lane == 0) {
+                    dots[j] = dt;
+                    vav_l = fma(vj, dt, vav_l);
+                }
+            }
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                const int i = lane + 32 * s;
+                vav_l = fma(v[s], acc[s], vav_l);
+                if (i > k && i < n) part[w * n + i] = acc[s];
+            }
+            vav_l = warp_sum(vav_l);
+            if (lane == 0) vav[w] = vav_l;
+            __syncthreads();
+            // ---- B2: p = tau (dots + sum_w part[w]) in a fixed order, 4 threads per row;
+            //      K = (tau / 2) p^T v = (tau^2 / 2) v^T A v
+            {
+                const int row = k + 1 + (tid >> 2), q0 = tid & 3;
+                double s0 = 0.0;
+                if (row < n)
+#pragma unroll
+                    for (int q = q0; q < kTrdWarps; q += 4) s0 += part[q * n + row];
+                s0 += __shfl_xor_sync(0xffffffffu, s0, 1);
+                s0 += __shfl_xor_sync(0xffffffffu, s0, 2);
+                if (row < n && q0 == 0) p[row] = tau * (dots[row] + s0);
+                if (tid == kTrdThreads - 1) {
+                    double t = 0.0;
+                    for (int q = 0; q < kTrdWarps; ++q) t += vav[q];
+                    sc[2] = 0.5 * tau * tau * t;
+                }
+            }
+            __syncthreads();
+            // ---- C: w = p - K v ; A22 -= v w^T + w v^T (owned columns); the owner of
+            //      column k+1 then publishes reflector k+1 from the updated column
+            const double K = sc[2];
+            double wr[S];
+#pragma unroll
+            for (int s = 0; s < S; ++s) wr[s] = fma(-K, v[s], p[lane + 32 * s]);
+            for (int j = j0; j < n; j += kTrdWarps) {
+                const double vj = vk[j];
+                const double wj = fma(-K, vj, p[j]);
+                const int cj = pk(j, j, n) - j;
+                const int s0 = j >> 5;
+#pragma unroll
+                for (int s = 0; s < S; ++s) {
+                    if (s >= s0) {
+                        const int i = lane + 32 * s;
+                        const double nv = fma(-v[s], wj, fma(-wr[s], vj, AP[cj + i]));
+                        if (i >= j && i < n) AP[cj + i] = nv;
+                    }
+                }
+                if (j == k + 1 && next) {
+                    __syncwarp();
+                    publish_reflector<S>(AP, n, k + 1, vbuf + ((k + 1) & 1) * NR, sc + ((k + 1) & 1), d, e,
+                                         tau_out, scal_out);
+                }
+            }
+        } else if (next && w == ((k + 1) & (kTrdWarps - 1))) {  // H_k = I: column k+1 unchanged
+            publish_reflector<S>(AP, n, k + 1, vbuf + ((k + 1) & 1) * NR, sc + ((k + 1) & 1), d, e, tau_out,
+                                 scal_out);
+        }
+        __syncthreads();
+    }
+    if (tid == 0) {
+        if (n >= 2) {
+            d[n - 2] = AP[pk(n - 2, n - 2, n)];
+            e[n - 2] = AP[pk(n - 1, n - 2, n)];
+            tau_out[n - 2] = 0.0;
+            scal_out[n - 2] = 0.0;
+        }
+        d[n - 1] = AP[pk(n - 1, n - 1, n)];
+        tau_out[n - 1] = 0.0;
+        scal_out[n - 1] = 0.0;
+    }
+    for (int q = tid; q < np; q += kTrdThreads) hh[q] = AP[q];
+}
+
+// ||T||_1 (= ||T||_inf) and the Gershgorin interval, warp-cooperative.
+struct TNorm {
+    double lo, hi, norm;
+};
+__device__ TNorm tnorm_warp(const double* d, const double* e, int n) {
+    const int lane = threadIdx.x & 31;
+    double lo = DBL_MAX, hi = -DBL_MAX, nm = 0.0;
+    for (int i = lane; i < n; i += 32) {
+        const double r = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < n ? fabs(e[i]) : 0.0);
+        lo = fmin(lo, d[i] - r);
+        hi = fmax(hi, d[i] + r);
+        nm = fmax(nm, fabs(d[i]) + r);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        nm = fmax(nm, __shfl_xor_sync(0xffffffffu, nm, o));
+    }
+    return {lo, hi, nm};
+}
+
+// Number of eigenvalues of T below x (Sturm sequence of the LDL^T pivots).
+__device__ __forceinline__ int sturm_count(const double* __restrict__ d, const double* __restrict__ e2, int n,
+                                           double x, double pivmin) {
+    double q = d[0] - x;
+    if (fabs(q) < pivmin) q = -pivmin;
+    int c = q < 0.0;
+    for (int i = 1; i < n; ++i) {
+        // e2 / q by rcp.approx + two Newton steps (~1 ulp; the sign of q is what counts)
+        double r;
+        asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
+        r = r * fma(-q, r, 2.0);
+        r = r * fma(-q, r, 2.0);
+        q = fma(-e2[i - 1], r, d[i] - x);
+        if (fabs(q) < pivmin) q = -pivmin;
+        c += q < 0.0;
+    }
+    return c;
+}
+
+// values[j] = the j-th largest eigenvalue of T, j < nwant.  One warp per j.
+__global__ void __launch_bounds__(256) bisect_kernel(const double* __restrict__ d, const double* __restrict__ e,
+                                                     int n, int nwant, double* __restrict__ values) {
+    extern __shared__ double e2s[];
+    for (int i = threadIdx.x; i + 1 < n; i += blockDim.x) e2s[i] = e[i] * e[i];
+    __syncthreads();
+    const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (j >= nwant) return;
+    const TNorm tn = tnorm_warp(d, e, n);
+    double emax2 = 0.0;
+    for (int i = 0; i + 1 < n; ++i) emax2 = fmax(emax2, e2s[i]);
+    const double pivmin = DBL_MIN * fmax(1.0, emax2);
+    const double eps = DBL_EPSILON;
+    const double slack = 2.0 * eps * tn.norm * n + 2.0 * pivmin;
+    double lo = tn.lo - slack, hi = tn.hi + slack;
+    const int t = n - 1 - j;  // ascending index
+    const double atol = 2.0 * eps * tn.norm;
+    for (int it = 0; it < 64; ++it) {
+        const double wdt = hi - lo;
+        if (!(wdt > fmax(atol, 2.0 * eps * fmax(fabs(lo), fabs(hi))))) break;
+        const double x = lo + wdt * double(lane + 1) / 33.0;
+        const bool above = sturm_count(d, e2s, n, x, pivmin) >= t + 1;
+        const unsigned b = __ballot_sync(0xffffffffu, above);
+        const double xl = __shfl_sync(0xffffffffu, x, b ? __ffs(b) - 1 : 31);
+        const double xp = __shfl_sync(0xffffffffu, x, b ? max(__ffs(b) - 2, 0) : 31);
+        if (b) {
+            const int f = __ffs(b) - 1;
+            hi = xl;
+            if (f > 0) lo = xp;
+        } else {
+            lo = xl;
+        }
+    }
+    if (lane == 0) values[j] = tn.norm > 0.0 ? 0.5 * (lo + hi) : 0.0;  // T = 0: exactly zero
+}
+
+__device__ __forceinline__ double hash_unit(uint64_t x) {  // splitmix64 -> (-1, 1)
+    x += 0x9e3779b97f4a7c15ULL;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+    x ^= x >> 31;
+    return double(int64_t(x >> 11) - (int64_t(1) << 52)) * (1.0 / 4503599627370496.0);
+}
+
+// Inverse iteration for the wanted eigenvalues (descending, lam[0..nwant)).
+// X: n x nwant (ld n) eigenvectors of T.  wk: 5 n doubles per member.
+__global__ void __launch_bounds__(256) invit_kernel(const double* __restrict__ d, const double* __restrict__ e,
+                                                    int n, const double* __restrict__ lam, int nwant,
+                                                    double* __restrict__ X, double* __restrict__ wk) {
+    const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (j >= nwant) return;
+    const TNorm tn = tnorm_warp(d, e, n);
+    const double ortol = 1e-3 * tn.norm;
+    if (j > 0 && lam[j - 1] - lam[j] <= ortol) return;  // not a cluster leader
+    int end = j + 1;
+    while (end < nwant && lam[end - 1] - lam[end] <= ortol) ++end;
+    const double pertol = 10.0 * DBL_EPSILON * fmax(tn.norm, DBL_MIN);
+    const double tiny = tn.norm > 0.0 ? DBL_EPSILON * tn.norm : 1.0;  // pivot floor
+    for (int cb = j; cb < end; cb += 32) {
+        const int mm = cb + lane;
+        const bool mine = mm < end;
+        double* x = X + size_t(n) * (mine ? mm : j);
+        double* dl = wk + size_t(5) * n * (mine ? mm : j);
+        double* dd = dl + n;   // 1 / U(i, i)
+        double* du = dd + n;
+        double* du2 = du + n;
+        double* pv = du2 + n;  // 1.0 where rows i, i + 1 were interchanged
+        if (mine) {
+            // shift, kept >= pertol below the previous member (dstein)
+            double sh = lam[j];
+            for (int q = j + 1; q <= mm; ++q) sh = fmin(lam[q], sh - pertol);
+            // dgttrf on T - sh I
+            double di = d[0] - sh, ui = n > 1 ? e[0] : 0.0;
+            for (int i = 0; i + 1 < n; ++i) {
+                const double li = e[i], dn = d[i + 1] - sh, un = i + 2 < n ? e[i + 1] : 0.0;
+                if (fabs(di) >= fabs(li)) {
+                    if (fabs(di) < tiny) di = copysign(tiny, di);
+                    const double f = li / di;
+                    dl[i] = f;
+                    dd[i] = 1.0 / di;
+                    du[i] = ui;
+                    du2[i] = 0.0;
+                    pv[i] = 0.0;
+                    di = fma(-f, ui, dn);
+                    ui = un;
+                } else {
+                    const double f = di / li;
+                    dl[i] = f;
+                    dd[i] = 1.0 / li;
+                    du[i] = dn;
+                    du2[i] = un;
+                    pv[i] = 1.0;
+                    di = fma(-f, dn, ui);
+                    ui = -f * un;
+                }
+            }
+            if (fabs(di) < tiny) di = copysign(tiny, di);
+            dd[n - 1] = 1.0 / di;
+            for (int i = 0; i < n; ++i) x[i] = hash_unit(uint64_t(mm) * 1000003ULL + i);
+        }
+        for (int it = 0; it < 3; ++it) {
+            if (mine) {
+                // dgttrs: L (with interchanges; the running entry stays in a register) then U
+                double cr = x[0];
+                for (int i = 0; i + 1 < n; ++i) {
+                    const double nx = x[i + 1];
+                    if (pv[i] != 0.0) {
+                        x[i] = nx;
+                        cr = fma(-dl[i], nx, cr);
+                    } else {
+                        x[i] = cr;
+                        cr = fma(-dl[i], cr, nx);
+                    }
+                }
+                x[n - 1] = cr;
+                double x2 = 0.0, x1 = x[n - 1] * dd[n - 1];
+                x[n - 1] = x1;
+                for (int i = n - 2; i >= 0; --i) {
+                    const double xi = (x[i] - du[i] * x1 - du2[i] * x2) * dd[i];
+                    x[i] = xi;
+                    x2 = x1;
+                    x1 = xi;
+                }
+            }
+            __syncwarp();
+            // Gram-Schmidt of this chunk's members, in order, against every
+            // earlier member of the cluster (orthonormal already), then normalise
+            const int cend = min(end, cb + 32);
+            for (int q = cb; q < cend; ++q) {
+                double* xq = X + size_t(n) * q;
+                double mx = 0.0;
+                for (int i = lane; i < n; i += 32) mx = fmax(mx, fabs(xq[i]));
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                const double sc = mx > 0.0 ? 1.0 / mx : 1.0;  // pre-scale: the solve grows x by ~1/eps
+                for (int i = lane; i < n; i += 32) xq[i] *= sc;
+                __syncwarp();
+                for (int u = j; u < q; ++u) {
+                    const double* xu = X + size_t(n) * u;
+                    double dt = 0.0;
+                    for (int i = lane; i < n; i += 32) dt = fma(xu[i], xq[i], dt);
+                    dt = warp_sum(dt);
+                    for (int i = lane; i < n; i += 32) xq[i] = fma(-dt, xu[i], xq[i]);
+                    __syncwarp();
+                }
+                double nr = 0.0;
+                for (int i = lane; i < n; i += 32) nr = fma(xq[i], xq[i], nr);
+                nr = warp_sum(nr);
+                const double inv = nr > 0.0 ? 1.0 / sqrt(nr) : 0.0;
+                for (int i = lane; i < n; i += 32) xq[i] *= inv;
+                __syncwarp();
+            }
+        }
+    }
+}
+
+// vout(:, c) = H_0 ... H_{n-3} X(:, c); one warp per column, reflectors in smem.
+template <int S>
+__global__ void __launch_bounds__(1024) backtr_kernel(const double* __restrict__ hh, const double* __restrict__ tau,
+                                                      const double* __restrict__ scal, int n,
+                                                      const double* __restrict__ X, int nwant,
+                                                      double* __restrict__ vout, int ldv) {
+    extern __shared__ double sm[];
+    constexpr int NR = 32 * S;
+    const int np = n * (n + 1) / 2;
+    double* H = sm;            // np + NR zero pad
+    double* ts = H + np + NR;  // tau, scal
+    for (int q = threadIdx.x; q < np; q += blockDim.x) H[q] = hh[q];
+    for (int q = threadIdx.x; q < NR; q += blockDim.x) H[np + q] = 0.0;
+    for (int q = threadIdx.x; q < n; q += blockDim.x) {
+        ts[q] = tau[q];
+        ts[n + q] = scal[q];
+    }
+    __syncthreads();
+    const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (c >= nwant) return;
+    double x[S];
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        const int i = lane + 32 * s;
+        x[s] = i < n ? X[size_t(n) * c + i] : 0.0;
+    }
+    for (int k = n - 3; k >= 0; --k) {
+        const double tk = ts[k];
+        if (tk == 0.0) continue;
+        const double sk = ts[n + k];
+        const int ck = pk(k, k, n) - k;
+        const int s0 = (k + 1) >> 5;
+        double v[S], dt0 = 0.0, dt1 = 0.0;
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            v[s] = 0.0;
+            if (s >= s0) {  // warp-uniform
+                const int i = lane + 32 * s;
+                const double h = H[ck + i] * sk;
+                v[s] = (i == k + 1) ? 1.0 : (i > k + 1 && i < n) ? h : 0.0;  // pad rows stay 0
+                if (s & 1) dt1 = fma(v[s], x[s], dt1);
+                else dt0 = fma(v[s], x[s], dt0);
+            }
+        }
+        const double dt = tk * warp_sum(dt0 + dt1);
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+            if (s >= s0) x[s] = fma(-dt, v[s], x[s]);
+    }
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        const int i = lane + 32 * s;
+        if (i < n) vout[size_t(ldv) * c + i] = x[s];
+    }
+}
+
+size_t trd_smem(int n) {
+    const int nr = 32 * ((n + 31) / 32);
+    return (size_t(n) * (n + 1) / 2 + 4 * size_t(nr) + size_t(kTrdWarps) * (n + 1) + n + 4) * sizeof(double);
+}
+size_t backtr_smem(int n) {
+    const int nr = 32 * ((n + 31) / 32);
+    return (size_t(n) * (n + 1) / 2 + nr + 2 * size_t(n)) * sizeof(double);
+}
+
+template <int S>
+void launch_trd_backtr(atk_ctx* ctx, bool trd, const double* a, int n, int lda, double* hh, double* d, double* e,
+                       double* tau, double* scal, const double* X, int nwant, double* vout, int ldv) {
+    static bool attr = false;
+    if (!attr) {
+        ATK_CUDA(cudaFuncSetAttribute(trd_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(trd_smem(std::min(32 * S, kTridiagMax)))));
+        ATK_CUDA(cudaFuncSetAttribute(backtr_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(backtr_smem(std::min(32 * S, kTridiagMax)))));
+        attr = true;
+    }
+    if (trd) {
+        trd_kernel<S><<<1, kTrdThreads, trd_smem(n), ctx->stream>>>(a, n, lda, hh, d, e, tau, scal);
+    } else {
+        const int bw = std::min(32, nwant);
+        backtr_kernel<S><<<unsigned((nwant + bw - 1) / bw), 32 * bw, backtr_smem(n), ctx->stream>>>(
+            hh, tau, scal, n, X, nwant, vout, ldv);
+    }
+    ATK_LAUNCHED(ctx);
+}
+
+void trd_backtr(atk_ctx* ctx, bool trd, const double* a, int n, int lda, double* hh, double* d, double* e,
+                double* tau, double* scal, const double* X, int nwant, double* vout, int ldv) {
+    static_assert(kTridiagMax <= 224, "row slots");
+    switch ((n + 31) / 32) {
+        case 1: launch_trd_backtr<1>(ctx, trd, a, n, lda, hh, d, e, tau, scal, X, nwant, vout, ldv); break;
+        case 2: launch_trd_backtr<2>(ctx, trd, a, n, lda, hh, d, e, tau, scal, X, nwant, vout, ldv); break;
+        case 3: launch_trd_backtr<3>(ctx, trd, a, n, lda, hh, d, e, tau, scal, X, nwant, vout, ldv); break;
+        case 4: launch_trd_backtr<4>(ctx, trd, a, n, lda, hh, d, e, tau, scal, X, nwant, vout, ldv); break;
+        case 5: launch_trd_backtr<5>(ctx, trd, a, n, lda, hh, d, e, tau, scal, X, nwant, vout, ldv); break;
+        case 6: launch_trd_backtr<6>(ctx, trd, a, n, lda, hh, d, e, tau, scal, X, nwant, vout, ldv); break;
+        default: launch_trd_backtr<7>(ctx, trd, a, n, lda, hh, d, e, tau, scal, X, nwant, vout, ldv); break;
+    }
+}
+
+}  // namespace
+
+void tridiag_eig(atk_ctx* ctx, const double* a, int n, int lda, int nwant, double* values, double* vectors,
+                 int ldv, int nvals) {
+    if (n < 1 || n > kTridiagMax) fail(ATK_UNSUPPORTED, "tridiag_eig: n out of range");
+    if (nvals < nwant) nvals = nwant;
+    if (nwant < 0 || nvals > n) fail(ATK_RANK_TOO_LARGE, "tridiag_eig: nwant out of range");
+    cudaStream_t st = ctx->stream;
+    const size_t np = size_t(n) * (n + 1) / 2;
+    DevBuf<double> ws(ctx, np + 4 * size_t(n) + size_t(n) * nwant + 5 * size_t(n) * nwant);
+    double* hh = ws.get();
+    double* d = hh + np;
+    double* e = d + n;
+    double* tau = e + n;
+    double* scal = tau + n;
+    double* X = scal + n;
+    double* wk = X + size_t(n) * nwant;
+    trd_backtr(ctx, true, a, n, lda, hh, d, e, tau, scal, nullptr, 0, nullptr, 0);
+    const int wpb = 8;
+    bisect_kernel<<<unsigned((nvals + wpb - 1) / wpb), 32 * wpb, size_t(n) * sizeof(double), st>>>(d, e, n, nvals,
+                                                                                                  values);
+    ATK_LAUNCHED(ctx);
+    if (nwant == 0) return;
+    invit_kernel<<<unsigned((nwant + wpb - 1) / wpb), 32 * wpb, 0, st>>>(d, e, n, values, nwant, X, wk);
+    ATK_LAUNCHED(ctx);
+    trd_backtr(ctx, false, nullptr, n, 0, hh, d, e, tau, scal, X, nwant, vectors, ldv);
+}
+
+}  // namespace atk

@@ -1,6 +1,8 @@
 """Device symmetric eigensolver (linalg::sym_eig_top_r, linalg.hpp:101-123).
 
-Both Jacobi variants of jacobi.cu are checked against LAPACK (numpy eigh):
+The default dense solver (tridiag.cu: Householder + bisection + inverse
+iteration, n <= 200) is covered by tests/test_gpu_tridiag.py and by the
+"auto" parametrisation here.  Both Jacobi variants of jacobi.cu are checked against LAPACK (numpy eigh):
 * the general one (indefinite input: the API default);
 * the Cholesky-preconditioned, vector-free PSD one ("eig_assume_psd"). This
   includes rank-deficient Grams, where the shift keeps the factorisation
@@ -36,14 +38,19 @@ def _check(s, r, res, vec_tol=1e-9):
             assert principal_angle(res.vectors[:, j:j + 1], q[:, j:j + 1]) <= vec_tol
 
 
-@pytest.fixture(params=[False, True], ids=["general", "psd"])
+@pytest.fixture(params=[(False, 0), (True, 0), (False, -1)], ids=["jacobi-general", "jacobi-psd", "auto"])
 def ectx(request):
+    """Jacobi (eig_method 0, both variants) and the default dispatch (the
+    tridiagonal solver for n <= 200, ChFSI above with tridiagonal Rayleigh-Ritz)."""
     from paper_2010_10131_b200 import atucker
 
+    psd, method = request.param
     ctx = atucker.Context.default(0)
-    ctx.set_option("eig_assume_psd", 1.0 if request.param else 0.0)
+    ctx.set_option("eig_assume_psd", 1.0 if psd else 0.0)
+    ctx.set_option("eig_method", method)
     yield ctx
     ctx.set_option("eig_assume_psd", 0.0)
+    ctx.set_option("eig_method", -1)
 
 
 @pytest.mark.parametrize("n", [2, 5, 17, 48, 96, 112, 128, 152])
