@@ -262,6 +262,31 @@ long long atk_gemm_flops(void);
 double atk_cost_eig(double i, double r, double j);
 double atk_cost_als(double i, double r, double j, int num_iters);
 
+/* B200 roofline cost model for the selector hook.  The
+ * reference's model (selector.hpp:41-58) counts flops only, calibrated on a
+ * CPU, and routes C2/C5 to ALS; on B200 the Gram is tensor-core bound and ALS
+ * makes ~2 HBM passes over Y per iteration, so each stage is timed as
+ * max(flops / peak, bytes / HBM bandwidth) plus measured fixed costs:
+ *   EIG = max(I^2 J / P, s I J / BW) + eig(I) + max(2 I R J / P, s (I+R) J / BW)
+ *   ALS = (iters (2 I + 5 R) + 2 R) s J / BW + iters * als_iter_overhead
+ * (s = element bytes, P = tf32 or fp64 tensor rate).  Times in seconds. */
+typedef struct atk_roofline_params {
+    double hbm_gbs;              /* measured copy bandwidth (MEASURED_PEAKS.json hbm_gbs) */
+    double tf32_tflops;          /* 1/2 of the measured sustained bf16 rate */
+    double fp64_tflops;          /* effective DMMA fp64 contraction rate */
+    double eig_small_ms;         /* dense tridiagonal eig, I <= 200 */
+    double eig_large_ms;         /* ChFSI eig, I > 200 (gapped Gram spectra) */
+    double als_iter_overhead_ms; /* R x R solves + host syncs per ALS iteration */
+    int dtype;                   /* atk_dtype of the tensor */
+    int num_iters;               /* AlsOptions::num_iters */
+} atk_roofline_params;
+void atk_roofline_params_default(atk_roofline_params* p, int dtype, int num_iters);
+double atk_roofline_time_eig(const atk_roofline_params* p, double i, double r, double j);
+double atk_roofline_time_als(const atk_roofline_params* p, double i, double r, double j);
+/* An atk_selector_fn: `user` is a const atk_roofline_params*; EIG iff its
+ * modelled time is <= ALS's (ties to EIG, as heuristic_choice). */
+int atk_roofline_selector(void* user, int mode, uint64_t i, uint64_t r, uint64_t j);
+
 #ifdef __cplusplus
 }
 #endif

@@ -117,6 +117,17 @@ public:
                        ? SolverKind::Eig : SolverKind::Als;
         });
     }
+    // B200 roofline model (atk_roofline_selector): stage time = max(flops / peak,
+    // bytes / HBM bandwidth) + measured fixed costs; SURVEY §8(f) row 2.
+    static Strategy roofline(atk_dtype dtype = ATK_F32, int num_iters = 5) {
+        atk_roofline_params p;
+        atk_roofline_params_default(&p, int(dtype), num_iters);
+        return Strategy([p](std::size_t mode, std::size_t i, std::size_t r, std::size_t j) {
+            auto q = p;
+            return atk_roofline_selector(&q, int(mode), i, r, j) == ATK_SOLVER_EIG ? SolverKind::Eig
+                                                                                    : SolverKind::Als;
+        });
+    }
     static Strategy manual(std::vector<SolverKind> c) {
         for (auto k : c) if (k == SolverKind::Svd) throw Error("manual strategies choose between eig and als");
         return Strategy([c](std::size_t mode, std::size_t, std::size_t, std::size_t) { return c.at(mode); }, c.size());

@@ -32,6 +32,12 @@ class HostCollectives(C.Structure):
                 ("user", C.c_void_p)]
 
 
+class RooflineParams(C.Structure):
+    _fields_ = [("hbm_gbs", C.c_double), ("tf32_tflops", C.c_double), ("fp64_tflops", C.c_double),
+                ("eig_small_ms", C.c_double), ("eig_large_ms", C.c_double),
+                ("als_iter_overhead_ms", C.c_double), ("dtype", C.c_int), ("num_iters", C.c_int)]
+
+
 class AlsOpts(C.Structure):
     _fields_ = [("num_iters", C.c_int), ("rel_tol", C.c_double), ("seed", C.c_uint64)]
 
@@ -103,6 +109,10 @@ _SIGS = {
     "atk_alloc_tracking_stats": (C.c_int, [C.POINTER(AllocStats)]),
     "atk_cost_eig": (C.c_double, [C.c_double, C.c_double, C.c_double]),
     "atk_cost_als": (C.c_double, [C.c_double, C.c_double, C.c_double, C.c_int]),
+    "atk_roofline_params_default": (None, [C.POINTER(RooflineParams), C.c_int, C.c_int]),
+    "atk_roofline_time_eig": (C.c_double, [C.POINTER(RooflineParams), C.c_double, C.c_double, C.c_double]),
+    "atk_roofline_time_als": (C.c_double, [C.POINTER(RooflineParams), C.c_double, C.c_double, C.c_double]),
+    "atk_roofline_selector": (C.c_int, [C.c_void_p, C.c_int, C.c_uint64, C.c_uint64, C.c_uint64]),
 }
 
 _lib = None

@@ -1,5 +1,6 @@
 // api.cu — the C ABI (include/atk.h).  Every entry converts library errors
 // into an atk_status + thread-local message; no exception crosses the ABI.
+#include <algorithm>
 #include <atomic>
 #include <chrono>
 #include <cmath>
@@ -603,6 +604,48 @@ long long atk_gemm_calls(void) { return g_gemm_calls.load(); }
 long long atk_gemm_flops(void) { return g_gemm_flops.load(); }
 double atk_cost_eig(double i, double r, double j) { return cost_eig(i, r, j); }
 double atk_cost_als(double i, double r, double j, int num_iters) { return cost_als(i, r, j, num_iters); }
+
+// ---------------------------------------------------------------- roofline selector
+void atk_roofline_params_default(atk_roofline_params* p, int dtype, int num_iters) {
+    if (!p) return;
+    p->hbm_gbs = 6535.1;        // MEASURED_PEAKS.json (B200 copy bandwidth)
+    p->tf32_tflops = 690.2;     // 1/2 x measured sustained bf16 1380.4 TF/s
+    p->fp64_tflops = 10.0;      // measured: C3 mode-1 DMMA Gram
+    p->eig_small_ms = 1.0;      // measured: C1 n = 200 (tridiag.cu)
+    p->eig_large_ms = 1.5;      // measured: ChFSI 1.35-1.42 ms on gapped Grams (n = 2048); flat spectra cost more
+    p->als_iter_overhead_ms = 0.7;  // measured: C2 ALS mode 10.3 ms vs 6.8 ms of modelled HBM time
+    p->dtype = dtype;
+    p->num_iters = num_iters > 0 ? num_iters : 5;
+}
+
+static double rf_rate(const atk_roofline_params* p) {
+    return (p->dtype == ATK_F32 ? p->tf32_tflops : p->fp64_tflops) * 1e12;
+}
+
+double atk_roofline_time_eig(const atk_roofline_params* p, double i, double r, double j) {
+    if (!p) return 0.0;
+    const double s = p->dtype == ATK_F32 ? 4.0 : 8.0, bw = p->hbm_gbs * 1e9, P = rf_rate(p);
+    const double gram = std::max(i * i * j / P, s * i * j / bw);
+    const double ttm = std::max(2.0 * i * r * j / P, s * (i + r) * j / bw);
+    const double eig = 1e-3 * (i <= kTridiagMax ? p->eig_small_ms : p->eig_large_ms);
+    return gram + eig + ttm;
+}
+
+double atk_roofline_time_als(const atk_roofline_params* p, double i, double r, double j) {
+    if (!p) return 0.0;
+    const double s = p->dtype == ATK_F32 ? 4.0 : 8.0, bw = p->hbm_gbs * 1e9;
+    const double it = p->num_iters;
+    return (it * (2.0 * i + 5.0 * r) + 2.0 * r) * s * j / bw + it * p->als_iter_overhead_ms * 1e-3;
+}
+
+int atk_roofline_selector(void* user, int, uint64_t i, uint64_t r, uint64_t j) {
+    const auto* p = static_cast<const atk_roofline_params*>(user);
+    if (!p) return -1;
+    return atk_roofline_time_eig(p, double(i), double(r), double(j)) <=
+                   atk_roofline_time_als(p, double(i), double(r), double(j))
+               ? ATK_SOLVER_EIG
+               : ATK_SOLVER_ALS;
+}
 
 void atk_alloc_tracking_enable(uint64_t watch_elems) {
     std::lock_guard<std::mutex> lk(g_track_mu);

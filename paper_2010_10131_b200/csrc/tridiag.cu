@@ -33,8 +33,6 @@
 namespace atk {
 namespace {
 
-constexpr int kTrdThreads = 1024;
-constexpr int kTrdWarps = kTrdThreads / 32;
 constexpr int kRowSlots = (kTridiagMax + 31) / 32;  // rows per lane
 
 __device__ __forceinline__ int pk(int i, int j, int n) {  // A(i, j), i >= j, packed lower
@@ -88,29 +86,30 @@ __device__ __forceinline__ void publish_reflector(const double* AP, int n, int c
 // the unscaled Householder vector k); d, e: T; tau, scal: reflector k is
 // H_k = I - tau_k v v^T with v_{k+1} = 1, v_i = hh(i, k) * scal_k (i > k + 1).
 // S = ceil(n / 32) row slots per lane (a template: no dead slots for small n).
-template <int S>
-__global__ void __launch_bounds__(kTrdThreads, 1)
+template <int S, int NW>
+__global__ void __launch_bounds__(NW * 32, 1)
     trd_kernel(const double* __restrict__ a, int n, int lda, double* __restrict__ hh, double* __restrict__ d,
                double* __restrict__ e, double* __restrict__ tau_out, double* __restrict__ scal_out) {
     extern __shared__ double sm[];
     constexpr int NR = 32 * S;             // padded rows
     const int np = n * (n + 1) / 2;
     double* AP = sm;                       // np + NR zero pad (reads past the end stay finite)
-    double* part = AP + np + NR;           // kTrdWarps x n row partials of the matvec
-    double* dots = part + kTrdWarps * n;   // n: column dots of the matvec
+    double* part = AP + np + NR;           // NW x n row partials of the matvec
+    double* dots = part + NW * n;          // n: column dots of the matvec
     double* p = dots + n;                  // NR
     double* vbuf = p + NR;                 // 2 x NR (reflector k in vbuf[k & 1])
-    double* vav = vbuf + 2 * NR;           // kTrdWarps partials of v^T A v
-    double* sc = vav + kTrdWarps;          // tau[2], K
+    double* vav = vbuf + 2 * NR;           // NW partials of v^T A v
+    double* sc = vav + NW;                 // tau[2], K
+    constexpr int NT = NW * 32, TPR = NT / 256;  // B2: threads per row (rows <= 256)
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     for (int j = 0; j < n; ++j)
-        for (int i = j + tid; i < n; i += kTrdThreads)
+        for (int i = j + tid; i < n; i += NT)
             AP[pk(i, j, n)] = 0.5 * (a[i + size_t(lda) * j] + a[j + size_t(lda) * i]);
-    for (int q = tid; q < NR; q += kTrdThreads) {
+    for (int q = tid; q < NR; q += NT) {
         AP[np + q] = 0.0;
         p[q] = 0.0;
     }
-    for (int q = tid; q < kTrdWarps * n; q += kTrdThreads) part[q] = 0.0;
+    for (int q = tid; q < NW * n; q += NT) part[q] = 0.0;
     __syncthreads();
     if (n > 2 && w == 0) publish_reflector<S>(AP, n, 0, vbuf, sc, d, e, tau_out, scal_out);
     __syncthreads();
@@ -118,7 +117,7 @@ __global__ void __launch_bounds__(kTrdThreads, 1)
     for (int k = 0; k + 2 < n; ++k) {
         const double tau = sc[k & 1];
         const double* vk = vbuf + (k & 1) * NR;
-        const int j0 = k + 1 + ((w - (k + 1)) % kTrdWarps + kTrdWarps) % kTrdWarps;
+        const int j0 = k + 1 + ((w - (k + 1)) % NW + NW) % NW;
         const bool next = k + 3 < n;  // reflector k+1 exists
         if (tau != 0.0) {  // uniform
             double v[S], acc[S];
@@ -129,19 +128,22 @@ __global__ void __launch_bounds__(kTrdThreads, 1)
             }
             // ---- B: symmetric matvec A22 v (warp w: columns j = w mod 32), v^T A v partial
             double vav_l = 0.0;
-            for (int j = j0; j < n; j += kTrdWarps) {
+            for (int j = j0; j < n; j += NW) {
                 const double vj = vk[j];
                 const int cj = pk(j, j, n) - j;
                 const int s0 = j >> 5;
                 double dt = 0.0;
 #pragma unroll
                 for (int s = 0; s < S; ++s) {
-                    if (s >= s0) {  // warp-uniform
-                        const int i = lane + 32 * s;
-                        double aij = AP[cj + i];
-                        if (s == s0) aij = (i >= j) ? aij : 0.0;
-                        dt = fma(aij, v[s], dt);
+                    if (s < s0) continue;  // warp-uniform
+                    const int i = lane + 32 * s;
+                    const double aij = AP[cj + i];
+                    if (s == s0) {  // the diagonal slot: rows i >= j only
+                        dt = fma(i >= j ? aij : 0.0, v[s], dt);
                         acc[s] = fma(i > j ? aij : 0.0, vj, acc[s]);
+                    } else {
+                        dt = fma(aij, v[s], dt);
+                        acc[s] = fma(aij, vj, acc[s]);
                     }
                 }
                 dt = warp_sum(dt);
@@ -159,20 +161,20 @@ __global__ void __launch_bounds__(kTrdThreads, 1)
             vav_l = warp_sum(vav_l);
             if (lane == 0) vav[w] = vav_l;
             __syncthreads();
-            // ---- B2: p = tau (dots + sum_w part[w]) in a fixed order, 4 threads per row;
+            // ---- B2: p = tau (dots + sum_w part[w]) in a fixed order, TPR threads per row;
             //      K = (tau / 2) p^T v = (tau^2 / 2) v^T A v
             {
-                const int row = k + 1 + (tid >> 2), q0 = tid & 3;
+                const int row = k + 1 + tid / TPR, q0 = tid % TPR;
                 double s0 = 0.0;
                 if (row < n)
 #pragma unroll
-                    for (int q = q0; q < kTrdWarps; q += 4) s0 += part[q * n + row];
-                s0 += __shfl_xor_sync(0xffffffffu, s0, 1);
-                s0 += __shfl_xor_sync(0xffffffffu, s0, 2);
+                    for (int q = q0; q < NW; q += TPR) s0 += part[q * n + row];
+#pragma unroll
+                for (int o = 1; o < TPR; o <<= 1) s0 += __shfl_xor_sync(0xffffffffu, s0, o);
                 if (row < n && q0 == 0) p[row] = tau * (dots[row] + s0);
-                if (tid == kTrdThreads - 1) {
+                if (tid == NT - 1) {
                     double t = 0.0;
-                    for (int q = 0; q < kTrdWarps; ++q) t += vav[q];
+                    for (int q = 0; q < NW; ++q) t += vav[q];
                     sc[2] = 0.5 * tau * tau * t;
                 }
             }
@@ -183,17 +185,20 @@ __global__ void __launch_bounds__(kTrdThreads, 1)
             double wr[S];
 #pragma unroll
             for (int s = 0; s < S; ++s) wr[s] = fma(-K, v[s], p[lane + 32 * s]);
-            for (int j = j0; j < n; j += kTrdWarps) {
+            for (int j = j0; j < n; j += NW) {
                 const double vj = vk[j];
                 const double wj = fma(-K, vj, p[j]);
                 const int cj = pk(j, j, n) - j;
                 const int s0 = j >> 5;
 #pragma unroll
                 for (int s = 0; s < S; ++s) {
-                    if (s >= s0) {
-                        const int i = lane + 32 * s;
-                        const double nv = fma(-v[s], wj, fma(-wr[s], vj, AP[cj + i]));
+                    if (s < s0) continue;  // warp-uniform
+                    const int i = lane + 32 * s;
+                    const double nv = fma(-v[s], wj, fma(-wr[s], vj, AP[cj + i]));
+                    if (s == s0) {
                         if (i >= j && i < n) AP[cj + i] = nv;
+                    } else if (s + 1 < S || i < n) {  // only the last slot can run past n
+                        AP[cj + i] = nv;
                     }
                 }
                 if (j == k + 1 && next) {
@@ -202,7 +207,7 @@ __global__ void __launch_bounds__(kTrdThreads, 1)
                                          tau_out, scal_out);
                 }
             }
-        } else if (next && w == ((k + 1) & (kTrdWarps - 1))) {  // H_k = I: column k+1 unchanged
+        } else if (next && w == ((k + 1) & (NW - 1))) {  // H_k = I: column k+1 unchanged
             publish_reflector<S>(AP, n, k + 1, vbuf + ((k + 1) & 1) * NR, sc + ((k + 1) & 1), d, e, tau_out,
                                  scal_out);
         }
@@ -219,7 +224,7 @@ __global__ void __launch_bounds__(kTrdThreads, 1)
         tau_out[n - 1] = 0.0;
         scal_out[n - 1] = 0.0;
     }
-    for (int q = tid; q < np; q += kTrdThreads) hh[q] = AP[q];
+    for (int q = tid; q < np; q += NT) hh[q] = AP[q];
 }
 
 // ||T||_1 (= ||T||_inf) and the Gershgorin interval, warp-cooperative.
@@ -478,9 +483,9 @@ __global__ void __launch_bounds__(1024) backtr_kernel(const double* __restrict__
     }
 }
 
-size_t trd_smem(int n) {
+size_t trd_smem(int n, int nw) {
     const int nr = 32 * ((n + 31) / 32);
-    return (size_t(n) * (n + 1) / 2 + 4 * size_t(nr) + size_t(kTrdWarps) * (n + 1) + n + 4) * sizeof(double);
+    return (size_t(n) * (n + 1) / 2 + 4 * size_t(nr) + size_t(nw) * (n + 1) + n + 4) * sizeof(double);
 }
 size_t backtr_smem(int n) {
     const int nr = 32 * ((n + 31) / 32);
@@ -490,16 +495,18 @@ size_t backtr_smem(int n) {
 template <int S>
 void launch_trd_backtr(atk_ctx* ctx, bool trd, const double* a, int n, int lda, double* hh, double* d, double* e,
                        double* tau, double* scal, const double* X, int nwant, double* vout, int ldv) {
+    // 64 registers per thread at 1024 threads spill the 4+ slot variants: they run 16 warps
+    constexpr int NW = S >= 4 ? 16 : 32;
     static bool attr = false;
     if (!attr) {
-        ATK_CUDA(cudaFuncSetAttribute(trd_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      int(trd_smem(std::min(32 * S, kTridiagMax)))));
+        ATK_CUDA(cudaFuncSetAttribute(trd_kernel<S, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(trd_smem(std::min(32 * S, kTridiagMax), NW))));
         ATK_CUDA(cudaFuncSetAttribute(backtr_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       int(backtr_smem(std::min(32 * S, kTridiagMax)))));
         attr = true;
     }
     if (trd) {
-        trd_kernel<S><<<1, kTrdThreads, trd_smem(n), ctx->stream>>>(a, n, lda, hh, d, e, tau, scal);
+        trd_kernel<S, NW><<<1, NW * 32, trd_smem(n, NW), ctx->stream>>>(a, n, lda, hh, d, e, tau, scal);
     } else {
         const int bw = std::min(32, nwant);
         backtr_kernel<S><<<unsigned((nwant + bw - 1) / bw), 32 * bw, backtr_smem(n), ctx->stream>>>(

@@ -121,11 +121,14 @@ class Strategy:
         FixedAls = "als"
         FixedSvd = "svd"
         Manual = "manual"
+        Roofline = "roofline"
 
-    def __init__(self, kind: "Strategy.Kind", choices=None, model: DecisionTreeModel | None = None):
+    def __init__(self, kind: "Strategy.Kind", choices=None, model: DecisionTreeModel | None = None,
+                 roofline=None):
         self.kind = kind
         self.choices = list(choices or [])
         self.model = model
+        self.roofline_params = roofline
 
     @staticmethod
     def adaptive(model: DecisionTreeModel) -> "Strategy":
@@ -134,6 +137,33 @@ class Strategy:
     @staticmethod
     def cost_model() -> "Strategy":
         return Strategy(Strategy.Kind.CostModel)
+
+    @staticmethod
+    def roofline(dtype: str = "f32", num_iters: int = 5, **overrides) -> "Strategy":
+        """B200 roofline cost model (atk_roofline_selector):
+        each stage costs max(flops / peak, bytes / HBM bandwidth) plus measured
+        fixed costs; EIG iff its modelled time <= ALS's.  `overrides` set fields
+        of atk_roofline_params (hbm_gbs, tf32_tflops, fp64_tflops, eig_small_ms,
+        eig_large_ms, als_iter_overhead_ms)."""
+        from . import _lib
+
+        p = _lib.RooflineParams()
+        _lib.load().atk_roofline_params_default(p, 0 if dtype in ("f32", "float32") else 1, int(num_iters))
+        for k, v in overrides.items():
+            if not hasattr(p, k):
+                raise Error(f"unknown roofline parameter '{k}'")
+            setattr(p, k, v)
+        return Strategy(Strategy.Kind.Roofline, roofline=p)
+
+    def roofline_times(self, i: int, r: int, j: int) -> tuple:
+        """(EIG seconds, ALS seconds) under the roofline model."""
+        import ctypes as C
+
+        from . import _lib
+
+        lib, p = _lib.load(), C.byref(self.roofline_params)
+        return (lib.atk_roofline_time_eig(p, float(i), float(r), float(j)),
+                lib.atk_roofline_time_als(p, float(i), float(r), float(j)))
 
     @staticmethod
     def fixed_eig() -> "Strategy":
@@ -161,7 +191,7 @@ class Strategy:
         if spec.startswith("manual:"):
             return Strategy.manual(spec[len("manual:"):].split(","))
         table = {"costmodel": Strategy.cost_model, "eig": Strategy.fixed_eig,
-                 "als": Strategy.fixed_als, "svd": Strategy.fixed_svd}
+                 "als": Strategy.fixed_als, "svd": Strategy.fixed_svd, "roofline": Strategy.roofline}
         if spec not in table:
             raise Error(f"unknown strategy '{spec}'")
         return table[spec]()
@@ -173,6 +203,13 @@ class Strategy:
             return predict(self.model, extract_features(float(i), float(r), float(j)))
         if k is Strategy.Kind.CostModel:
             return heuristic_choice(float(i), float(r), float(j), params)
+        if k is Strategy.Kind.Roofline:
+            import ctypes as C
+
+            from . import _lib
+
+            return SolverKind(_lib.load().atk_roofline_selector(C.cast(C.pointer(self.roofline_params), C.c_void_p),
+                                                                 int(mode), int(i), int(r), int(j)))
         if k is Strategy.Kind.FixedEig:
             return SolverKind.Eig
         if k is Strategy.Kind.FixedAls:

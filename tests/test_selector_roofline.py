@@ -1,0 +1,60 @@
+"""The B200 roofline selector hook (atk_roofline_selector).
+
+The reference's flop-only cost model (selector.hpp:41-58, heuristic_choice)
+routes the big fp32 configs to ALS; on B200 the Gram runs on tensor cores and
+ALS is HBM-bound, so the roofline model must keep EIG there.  CPU-only: the
+model is host code in libatk_cuda.so and needs no GPU."""
+import pytest
+
+from paper_2010_10131_b200.selector import SolverKind, Strategy, heuristic_choice
+
+
+def _modes(dims, ranks):
+    dims = list(dims)
+    for n, r in enumerate(ranks):
+        j = 1
+        for m, d in enumerate(dims):
+            if m != n:
+                j *= d
+        yield n, dims[n], r, j
+        dims[n] = r
+
+
+def test_c5_and_c2_mode1_choose_eig_where_the_flop_model_says_als():
+    s = Strategy.roofline("f32")
+    picks = [s.decide(n, i, r, j) for n, i, r, j in _modes((2048,) * 3, (64,) * 3)]
+    assert picks == [SolverKind.Eig] * 3
+    assert [heuristic_choice(i, r, j) for _, i, r, j in _modes((2048,) * 3, (64,) * 3)] == [SolverKind.Als] * 3
+    n, i, r, j = next(_modes((1024,) * 3, (32,) * 3))
+    assert s.decide(n, i, r, j) == SolverKind.Eig
+
+
+def test_stage_times_are_rooflines():
+    s = Strategy.roofline("f32")
+    p = s.roofline_params
+    i, r, j = 1024, 32, 1 << 20
+    te, ta = s.roofline_times(i, r, j)
+    bw, P = p.hbm_gbs * 1e9, p.tf32_tflops * 1e12
+    want_e = max(i * i * j / P, 4 * i * j / bw) + p.eig_large_ms * 1e-3 + max(2 * i * r * j / P, 4 * (i + r) * j / bw)
+    want_a = (5 * (2 * i + 5 * r) + 2 * r) * 4 * j / bw + 5 * p.als_iter_overhead_ms * 1e-3
+    assert te == pytest.approx(want_e, rel=1e-12)
+    assert ta == pytest.approx(want_a, rel=1e-12)
+
+
+def test_fp64_uses_the_fp64_rate_and_overrides_apply():
+    f64 = Strategy.roofline("f64")
+    f32 = Strategy.roofline("f32")
+    assert f64.roofline_times(128, 16, 1 << 21)[0] > f32.roofline_times(128, 16, 1 << 21)[0]
+    slow = Strategy.roofline("f32", als_iter_overhead_ms=0.0, eig_large_ms=1e4)
+    n, i, r, j = next(_modes((1024,) * 3, (32,) * 3))
+    assert slow.decide(n, i, r, j) == SolverKind.Als  # a 10 s eig makes ALS win
+    with pytest.raises(Exception):
+        Strategy.roofline("f32", bogus=1.0)
+
+
+def test_parse_and_cpp_header_expose_it():
+    from pathlib import Path
+
+    assert Strategy.parse("roofline").kind is Strategy.Kind.Roofline
+    hdr = (Path(__file__).resolve().parent.parent / "include" / "atucker_b200.hpp").read_text()
+    assert "static Strategy roofline(" in hdr
