@@ -27,6 +27,8 @@
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 #include "atk_internal.cuh"
 
@@ -89,8 +91,17 @@ __device__ __forceinline__ void publish_reflector(const double* AP, int n, int c
 template <int S, int NW>
 __global__ void __launch_bounds__(NW * 32, 1)
     trd_kernel(const double* __restrict__ a, int n, int lda, double* __restrict__ hh, double* __restrict__ d,
-               double* __restrict__ e, double* __restrict__ tau_out, double* __restrict__ scal_out) {
+               double* __restrict__ e, double* __restrict__ tau_out, double* __restrict__ scal_out,
+               long long* __restrict__ prof) {
     extern __shared__ double sm[];
+    long long t_mark = clock64(), t_acc[6] = {0, 0, 0, 0, 0, 0};  // ATK_TRD_PROFILE: cycles per phase
+    auto lap = [&](int ph) {
+        if (prof) {
+            const long long t = clock64();
+            t_acc[ph] += t - t_mark;
+            t_mark = t;
+        }
+    };
     constexpr int NR = 32 * S;             // padded rows
     const int np = n * (n + 1) / 2;
     double* AP = sm;                       // np + NR zero pad (reads past the end stay finite)
@@ -111,8 +122,10 @@ __global__ void __launch_bounds__(NW * 32, 1)
     }
     for (int q = tid; q < NW * n; q += NT) part[q] = 0.0;
     __syncthreads();
+    lap(0);
     if (n > 2 && w == 0) publish_reflector<S>(AP, n, 0, vbuf, sc, d, e, tau_out, scal_out);
     __syncthreads();
+    lap(0);
 
     for (int k = 0; k + 2 < n; ++k) {
         const double tau = sc[k & 1];
@@ -126,31 +139,47 @@ __global__ void __launch_bounds__(NW * 32, 1)
                 v[s] = vk[lane + 32 * s];
                 acc[s] = 0.0;
             }
-            // ---- B: symmetric matvec A22 v (warp w: columns j = w mod 32), v^T A v partial
+            // ---- B: symmetric matvec A22 v (warp w: columns j = w mod NW), v^T A v partial.
+            //      Four columns per pass with their warp reductions interleaved (the
+            //      per-column shuffle chains are the latency that bounds this phase).
             double vav_l = 0.0;
-            for (int j = j0; j < n; j += NW) {
-                const double vj = vk[j];
-                const int cj = pk(j, j, n) - j;
-                const int s0 = j >> 5;
-                double dt = 0.0;
+            for (int jb = j0; jb < n; jb += 4 * NW) {
+                double dt[4];
 #pragma unroll
-                for (int s = 0; s < S; ++s) {
-                    if (s < s0) continue;  // warp-uniform
-                    const int i = lane + 32 * s;
-                    const double aij = AP[cj + i];
-                    if (s == s0) {  // the diagonal slot: rows i >= j only
-                        dt = fma(i >= j ? aij : 0.0, v[s], dt);
-                        acc[s] = fma(i > j ? aij : 0.0, vj, acc[s]);
-                    } else {
-                        dt = fma(aij, v[s], dt);
-                        acc[s] = fma(aij, vj, acc[s]);
+                for (int c = 0; c < 4; ++c) {
+                    const int j = jb + c * NW;
+                    dt[c] = 0.0;
+                    if (j >= n) continue;  // warp-uniform
+                    const double vj = vk[j];
+                    const int cj = pk(j, j, n) - j;
+                    const int s0 = j >> 5;
+#pragma unroll
+                    for (int s = 0; s < S; ++s) {
+                        if (s < s0) continue;  // warp-uniform
+                        const int i = lane + 32 * s;
+                        const double aij = AP[cj + i];
+                        if (s == s0) {  // the diagonal slot: rows i >= j only
+                            dt[c] = fma(i >= j ? aij : 0.0, v[s], dt[c]);
+                            acc[s] = fma(i > j ? aij : 0.0, vj, acc[s]);
+                        } else {
+                            dt[c] = fma(aij, v[s], dt[c]);
+                            acc[s] = fma(aij, vj, acc[s]);
+                        }
                     }
                 }
-                dt = warp_sum(dt);
-                if (lane == 0) {
-                    dots[j] = dt;
-                    vav_l = fma(vj, dt, vav_l);
-                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) dt[c] += __shfl_xor_sync(0xffffffffu, dt[c], o);
+                if (lane == 0)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        const int j = jb + c * NW;
+                        if (j < n) {
+                            dots[j] = dt[c];
+                            vav_l = fma(vk[j], dt[c], vav_l);
+                        }
+                    }
             }
 #pragma unroll
             for (int s = 0; s < S; ++s) {
@@ -160,7 +189,9 @@ __global__ void __launch_bounds__(NW * 32, 1)
             }
             vav_l = warp_sum(vav_l);
             if (lane == 0) vav[w] = vav_l;
+            lap(1);
             __syncthreads();
+            lap(2);
             // ---- B2: p = tau (dots + sum_w part[w]) in a fixed order, TPR threads per row;
             //      K = (tau / 2) p^T v = (tau^2 / 2) v^T A v
             {
@@ -179,39 +210,58 @@ __global__ void __launch_bounds__(NW * 32, 1)
                 }
             }
             __syncthreads();
+            lap(3);
             // ---- C: w = p - K v ; A22 -= v w^T + w v^T (owned columns); the owner of
             //      column k+1 then publishes reflector k+1 from the updated column
             const double K = sc[2];
             double wr[S];
 #pragma unroll
             for (int s = 0; s < S; ++s) wr[s] = fma(-K, v[s], p[lane + 32 * s]);
-            for (int j = j0; j < n; j += NW) {
-                const double vj = vk[j];
-                const double wj = fma(-K, vj, p[j]);
-                const int cj = pk(j, j, n) - j;
-                const int s0 = j >> 5;
+            // two columns per pass: all loads issued before the stores (ILP)
+            for (int jb = j0; jb < n; jb += 2 * NW) {
+                double nv[2][S];
 #pragma unroll
-                for (int s = 0; s < S; ++s) {
-                    if (s < s0) continue;  // warp-uniform
-                    const int i = lane + 32 * s;
-                    const double nv = fma(-v[s], wj, fma(-wr[s], vj, AP[cj + i]));
-                    if (s == s0) {
-                        if (i >= j && i < n) AP[cj + i] = nv;
-                    } else if (s + 1 < S || i < n) {  // only the last slot can run past n
-                        AP[cj + i] = nv;
-                    }
+                for (int c = 0; c < 2; ++c) {
+                    const int j = jb + c * NW;
+                    if (j >= n) continue;  // warp-uniform
+                    const double vj = vk[j];
+                    const double wj = fma(-K, vj, p[j]);
+                    const int cj = pk(j, j, n) - j;
+                    const int s0 = j >> 5;
+#pragma unroll
+                    for (int s = 0; s < S; ++s)
+                        if (s >= s0) nv[c][s] = fma(-v[s], wj, fma(-wr[s], vj, AP[cj + lane + 32 * s]));
                 }
-                if (j == k + 1 && next) {
-                    __syncwarp();
-                    publish_reflector<S>(AP, n, k + 1, vbuf + ((k + 1) & 1) * NR, sc + ((k + 1) & 1), d, e,
-                                         tau_out, scal_out);
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    const int j = jb + c * NW;
+                    if (j >= n) continue;
+                    const int cj = pk(j, j, n) - j;
+                    const int s0 = j >> 5;
+#pragma unroll
+                    for (int s = 0; s < S; ++s) {
+                        if (s < s0) continue;  // warp-uniform
+                        const int i = lane + 32 * s;
+                        if (s == s0) {
+                            if (i >= j && i < n) AP[cj + i] = nv[c][s];
+                        } else if (s + 1 < S || i < n) {  // only the last slot can run past n
+                            AP[cj + i] = nv[c][s];
+                        }
+                    }
+                    if (j == k + 1 && next) {
+                        __syncwarp();
+                        publish_reflector<S>(AP, n, k + 1, vbuf + ((k + 1) & 1) * NR, sc + ((k + 1) & 1), d, e,
+                                             tau_out, scal_out);
+                    }
                 }
             }
         } else if (next && w == ((k + 1) & (NW - 1))) {  // H_k = I: column k+1 unchanged
             publish_reflector<S>(AP, n, k + 1, vbuf + ((k + 1) & 1) * NR, sc + ((k + 1) & 1), d, e, tau_out,
                                  scal_out);
         }
+        lap(4);
         __syncthreads();
+        lap(5);
     }
     if (tid == 0) {
         if (n >= 2) {
@@ -225,6 +275,8 @@ __global__ void __launch_bounds__(NW * 32, 1)
         scal_out[n - 1] = 0.0;
     }
     for (int q = tid; q < np; q += NT) hh[q] = AP[q];
+    if (prof && (lane == 0))
+        for (int q = 0; q < 6; ++q) atomicAdd(reinterpret_cast<unsigned long long*>(prof + q), (unsigned long long)t_acc[q]);
 }
 
 // ||T||_1 (= ||T||_inf) and the Gershgorin interval, warp-cooperative.
@@ -495,8 +547,8 @@ size_t backtr_smem(int n) {
 template <int S>
 void launch_trd_backtr(atk_ctx* ctx, bool trd, const double* a, int n, int lda, double* hh, double* d, double* e,
                        double* tau, double* scal, const double* X, int nwant, double* vout, int ldv) {
-    // 64 registers per thread at 1024 threads spill the 4+ slot variants: they run 16 warps
-    constexpr int NW = S >= 4 ? 16 : 32;
+    // 64 registers per thread at 1024 threads spill the 3+ slot variants: they run 16 warps
+    constexpr int NW = S >= 3 ? 16 : 32;
     static bool attr = false;
     if (!attr) {
         ATK_CUDA(cudaFuncSetAttribute(trd_kernel<S, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -506,7 +558,19 @@ void launch_trd_backtr(atk_ctx* ctx, bool trd, const double* a, int n, int lda, 
         attr = true;
     }
     if (trd) {
-        trd_kernel<S, NW><<<1, NW * 32, trd_smem(n, NW), ctx->stream>>>(a, n, lda, hh, d, e, tau, scal);
+        static long long* prof = nullptr;
+        static const bool want = std::getenv("ATK_TRD_PROFILE") != nullptr;
+        if (want && !prof) ATK_CUDA(cudaMalloc(&prof, 6 * sizeof(long long)));
+        if (prof) ATK_CUDA(cudaMemsetAsync(prof, 0, 6 * sizeof(long long), ctx->stream));
+        trd_kernel<S, NW><<<1, NW * 32, trd_smem(n, NW), ctx->stream>>>(a, n, lda, hh, d, e, tau, scal, prof);
+        if (prof) {
+            long long h[6];
+            ATK_CUDA(cudaMemcpyAsync(h, prof, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+            ATK_CUDA(cudaStreamSynchronize(ctx->stream));
+            std::fprintf(stderr, "[trd n=%d NW=%d] cycles/warp: load %.0f B %.0f barB %.0f B2 %.0f C %.0f barC %.0f\n", n,
+                         NW, h[0] / double(NW), h[1] / double(NW), h[2] / double(NW), h[3] / double(NW),
+                         h[4] / double(NW), h[5] / double(NW));
+        }
     } else {
         const int bw = std::min(32, nwant);
         backtr_kernel<S><<<unsigned((nwant + bw - 1) / bw), 32 * bw, backtr_smem(n), ctx->stream>>>(
