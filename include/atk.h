@@ -49,6 +49,10 @@ typedef enum atk_status {
     ATK_RANK_DEFICIENT = 8,      /* atucker::RankDeficient         */
     ATK_NOT_SPD = 9,             /* atucker::NotSPD                */
     ATK_ZERO_NORM_INPUT = 10,    /* atucker::ZeroNormInput         */
+    ATK_EMPTY_DATASET = 11,      /* atucker::EmptyDataset (selector trainer; not raised here) */
+    ATK_FEATURE_VERSION = 12,    /* atucker::FeatureVersionMismatch */
+    ATK_SCHEMA_MISMATCH = 13,    /* atucker::SchemaMismatch        */
+    ATK_IO_FAILURE = 14,         /* atucker::IoFailure (.dten I/O) */
     ATK_CUDA_ERROR = 20,
     ATK_NCCL_ERROR = 21,
     ATK_OOM = 22,
@@ -251,6 +255,19 @@ atk_status atk_reconstruct(atk_ctx* ctx, const atk_tensor* core, const double* f
 /* relative_error (sthosvd.hpp:212-223). */
 atk_status atk_relative_error(atk_ctx* ctx, const atk_tensor* x, const atk_tensor* core,
                               const double* factors, double* out);
+
+/* ------------------------------------------------------------ .dten I/O
+ * The reference's tensor file (tensor_io.hpp:15-99: "DTEN", u32 version 1,
+ * u32 order, order x u64 dims, f64 LE column-major payload) streamed straight
+ * to / from device memory through double-buffered pinned chunks; fp32 tensors
+ * are narrowed / widened on the device.  Errors: ATK_IO_FAILURE with
+ * read_dten's messages (bad magic, version, empty header, zero dimension,
+ * > 2^40 elements, truncated payload).  SURVEY §8(f) row 3. */
+atk_status atk_dten_info(const char* path, int* order, uint64_t* dims /* ATK_MAX_ORDER */);
+/* read_dten (tensor_io.hpp:62-91) into a new device tensor of `dtype`. */
+atk_status atk_tensor_read_dten(atk_ctx* ctx, const char* path, atk_dtype dtype, atk_tensor** out);
+/* write_dten (tensor_io.hpp:39-52) of a device tensor (payload always f64). */
+atk_status atk_tensor_write_dten(atk_ctx* ctx, const atk_tensor* t, const char* path);
 
 /* ------------------------------------------------------------ instrumentation.hpp */
 /* Logical GEMM counters (instrumentation.hpp:13-34): one record per logical

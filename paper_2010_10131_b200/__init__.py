@@ -20,7 +20,7 @@ __all__ = [
 ]
 
 
-_SUBMODULES = {"atucker", "build", "dist", "errors", "selector"}
+_SUBMODULES = {"atucker", "build", "dist", "errors", "selector", "tensor_io"}
 
 
 def __getattr__(name):

@@ -247,6 +247,31 @@ atk_status atk_comm_init_host(atk_ctx* ctx, const atk_host_collectives* coll, in
     });
 }
 
+atk_status atk_dten_info(const char* path, int* order, uint64_t* dims) {
+    return guard([&] {
+        const DtenHeader h = dten_header(path);
+        if (order) *order = h.order;
+        if (dims)
+            for (int m = 0; m < ATK_MAX_ORDER; ++m) dims[m] = m < h.order ? h.dims[m] : 0;
+    });
+}
+
+atk_status atk_tensor_read_dten(atk_ctx* ctx, const char* path, atk_dtype dtype, atk_tensor** out) {
+    return guard([&] {
+        bind(ctx);
+        if (!out) fail(ATK_INVALID_ARGUMENT, "null output");
+        if (dtype != ATK_F32 && dtype != ATK_F64) fail(ATK_INVALID_ARGUMENT, "bad dtype");
+        *out = dten_read(ctx, path, dtype);
+    });
+}
+
+atk_status atk_tensor_write_dten(atk_ctx* ctx, const atk_tensor* t, const char* path) {
+    return guard([&] {
+        bind(ctx);
+        dten_write(ctx, t, path);
+    });
+}
+
 atk_status atk_comm_destroy(atk_ctx* ctx) {
     return guard([&] {
         bind(ctx);

@@ -92,6 +92,17 @@ atk_tensor* reconstruct(atk_ctx* ctx, const atk_tensor* core, const double* fact
 double relative_error(atk_ctx* ctx, const atk_tensor* x, const atk_tensor* core,
                       const double* factors);
 
+// dten_io.cu — .dten files (tensor_io.hpp) streamed to / from the device.
+struct DtenHeader {
+    int order = 0;
+    uint64_t dims[ATK_MAX_ORDER] = {};
+    uint64_t numel = 0;
+};
+// Validates the header; with `keep` the open FILE* (positioned at the payload) is returned.
+DtenHeader dten_header(const char* path, FILE** keep = nullptr);
+atk_tensor* dten_read(atk_ctx* ctx, const char* path, atk_dtype dt);
+void dten_write(atk_ctx* ctx, const atk_tensor* t, const char* path);
+
 // dist.cu — NCCL over NVLink (one process per GPU).
 void comm_init(atk_ctx* ctx, const void* unique_id, int rank, int world);
 void comm_destroy(atk_ctx* ctx);

@@ -47,6 +47,14 @@ class ZeroNormInput(Error):
     pass
 
 
+class EmptyDataset(Error):
+    pass
+
+
+class IoFailure(Error):
+    """atucker::IoFailure — .dten / .tucker I/O."""
+
+
 class FeatureVersionMismatch(Error):
     pass
 
@@ -86,6 +94,10 @@ STATUS = {
     8: RankDeficient,
     9: NotSPD,
     10: ZeroNormInput,
+    11: EmptyDataset,
+    12: FeatureVersionMismatch,
+    13: SchemaMismatch,
+    14: IoFailure,
     20: CudaError,
     21: NcclError,
     22: OutOfMemory,
