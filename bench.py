@@ -67,6 +67,9 @@ def flops_of(dims, ranks, kinds, num_iters=5):
     return out
 
 
+FP64_TC_TFLOPS = 40.0  # B200 spec fp64 tensor (DMMA) rate; MEASURED_PEAKS.json has no fp64 figure
+
+
 def peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -346,6 +349,25 @@ def main():
                 "peak_note": f"tf32 = 1/2 of the {pk['src']} sustained bf16 {pk['bf16_sus']} TF/s",
                 "algorithmic_flops_per_launch": gram_flops}
 
+    # SURVEY 8(d) pipeline fraction: sum over stages of max(F / P, B / BW) against
+    # the measured step (eig excluded from the bound, included in the step)
+    P = (tf32_peak if cfg["dtype"] == "f32" else FP64_TC_TFLOPS) * 1e12
+    BW = pk["hbm"] * 1e9
+    es = 4 if cfg["dtype"] == "f32" else 8
+    t_bound = 0.0
+    work = list(gdims)
+    for n, (r, k) in enumerate(zip(cfg["ranks"], kinds)):
+        i = work[n]
+        j = int(np.prod(work)) // i
+        if k == 1:
+            t_bound += (5 * (2 * i + 5 * r) + 2 * r) * es * j / BW
+        else:
+            t_bound += max(i * i * j / P, es * i * j / BW) + max(2 * i * r * j / P, es * (i + r) * j / BW)
+        work[n] = r
+    pipeline = {"t_bound_ms": t_bound * 1e3, "frac": t_bound * 1e3 / ms,
+                "note": "sum of max(flops/peak, bytes/HBM) over Gram/TTM (ALS: HBM bytes); eig not in the bound"
+                        + ("" if cfg["dtype"] == "f32" else f"; fp64 peak {FP64_TC_TFLOPS} TF/s (B200 spec DMMA)")}
+
     # e2e through the host-buffer C ABI (pinned host input, core back)
     e2e = None
     if world == 1 and args.e2e_steps > 0:
@@ -381,7 +403,7 @@ def main():
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                 "dtype": "tf32" if cfg["dtype"] == "f32" else "f64", "data": "synthetic",
                 "config": workload_config(cfg, args.config, world, total_flops),
-                "stages": stages, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "stages": stages, "pipeline": pipeline, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(launches), "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     if world > 1:

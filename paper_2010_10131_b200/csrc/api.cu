@@ -4,6 +4,7 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -28,6 +29,9 @@ void* dev_alloc(atk_ctx* ctx, size_t bytes) {
     if (e != cudaSuccess) {
         cudaGetLastError();
         // drain the pool's cached blocks and retry once
+        if (std::getenv("ATK_TRACE"))
+            std::fprintf(stderr, "[atk alloc] %zu bytes failed (%s): trimming the pool\n", bytes,
+                         cudaGetErrorString(e));
         cudaStreamSynchronize(ctx->stream);
         cudaMemPool_t pool;
         if (cudaDeviceGetDefaultMemPool(&pool, ctx->device) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
@@ -218,6 +222,7 @@ atk_status atk_ctx_set_option(atk_ctx* ctx, const char* key, double value) {
         if (k == "simt") ctx->force_simt = value != 0.0;
         else if (k == "eig_method") ctx->eig_method = int(value);
         else if (k == "chfsi_tol") ctx->chfsi_tol = value;
+        else if (k == "cheb_fused") ctx->cheb_fused = int(value);
         else if (k == "eig_assume_psd") ctx->eig_assume_psd = value != 0.0;
         else if (k == "tma_tf32") ctx->tma_tf32 = value != 0.0;
         else if (k == "gram_chunk_kb") ctx->gram_chunk_kb = int(value);

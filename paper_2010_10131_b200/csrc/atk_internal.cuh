@@ -56,6 +56,7 @@ struct atk_ctx {
     int force_simt = 0;        // option "simt": portable CUDA-core contractions
     int eig_method = -1;       // option "eig_method": -1 auto, 0 dense Jacobi, 1 ChFSI, 2 tridiagonal
     double chfsi_tol = 1e-12;  // option "chfsi_tol": relative Ritz residual target
+    int cheb_fused = 1;        // option "cheb_fused": whole Chebyshev filter in one cooperative launch
     bool eig_assume_psd = false;  // option "eig_assume_psd": atk_sym_eig_top_r input is a Gram
     int tma_tf32 = 1;          // option "tma_tf32": TMA converts fp32 -> tf32 with round-to-nearest
                                // (the MMA itself truncates: measured 6e-4 bias vs 1e-6, test_gpu_tc.py)
@@ -173,6 +174,12 @@ void ttm(atk_ctx* ctx, const void* x, atk_dtype dt, Split s, const double* u_dev
 
 // dense.cu — small fp64 device linear algebra.
 // C(m x n) = alpha op(A) op(B) + beta C, column-major with leading dims.
+// The degree-`deg` Chebyshev recurrence of ChFSI in one cooperative launch:
+// Y1 = a1 S V + b1 V, Y_{j+1} = a S Y_j + b Y_j + c Y_{j-1}; y = {V, 3 scratch
+// n x k blocks}.  Returns the index into y of Y_deg, or -1 if the grid cannot
+// be co-resident (the caller then runs the per-step launches).
+int cheb_filter(atk_ctx* ctx, const double* S, int n, int k, int deg, double* const y[4], double a1, double b1,
+                double a, double b, double c);
 void dgemm(atk_ctx* ctx, bool ta, bool tb, int m, int n, int k, double alpha, const double* a,
            int lda, const double* b, int ldb, double beta, double* c, int ldc);
 // Dense symmetric eigensolver for n <= kJacobiMax (one CTA, smem Jacobi):

@@ -30,18 +30,12 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 
 // K slices stream through a STAGES-deep cp.async ring (global latency hidden
 // behind the DMMA work of the slices already resident; one barrier per slice).
-__global__ void __launch_bounds__(NT) dgemm_tile(bool ta, bool tb, int m, int n, int k, int kchunk,
-                                                 const double* __restrict__ a, int lda,
-                                                 const double* __restrict__ b, int ldb,
-                                                 double* __restrict__ out, size_t out_split_stride,
-                                                 int ldo, double alpha, double beta, bool direct) {
-    extern __shared__ __align__(16) double dsm[];
-    const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
-    const int kb = blockIdx.z * kchunk, ke = min(k, kb + kchunk);
+// acc = op(A)[m0:m0+BM, kb:ke] x op(B)[kb:ke, n0:n0+BN]
+__device__ __forceinline__ void gemm_block(bool ta, bool tb, int m, int n, int m0, int n0, int kb, int ke,
+                                           const double* __restrict__ a, int lda, const double* __restrict__ b,
+                                           int ldb, double* dsm, dmma::Acc<FM, FN>& acc) {
     const int tid = threadIdx.x;
-    dmma::Acc<FM, FN> acc;
     dmma::zero(acc);
-
     auto issue = [&](int stage, int k0) {
         double* As = dsm + stage * STAGE_DOUBLES;
         double* Bs = As + BK * LDA;
@@ -62,7 +56,6 @@ __global__ void __launch_bounds__(NT) dgemm_tile(bool ta, bool tb, int m, int n,
             cp_async8(Bs + kk * LDB + nn, ok ? (tb ? b + gn + size_t(ldb) * gk : b + gk + size_t(ldb) * gn) : b, ok);
         }
     };
-
     const int nt = (ke > kb) ? (ke - kb + BK - 1) / BK : 0;
 #pragma unroll
     for (int s = 0; s < STAGES - 1; ++s) {
@@ -78,6 +71,20 @@ __global__ void __launch_bounds__(NT) dgemm_tile(bool ta, bool tb, int m, int n,
         const double* As = dsm + (t % STAGES) * STAGE_DOUBLES;
         dmma::tile_step<LDA, LDB, WM, FM, FN>(acc, As, As + BK * LDA, BK);
     }
+    cp_async_wait<0>();
+    __syncthreads();  // the ring may be refilled by the next call
+}
+
+__global__ void __launch_bounds__(NT) dgemm_tile(bool ta, bool tb, int m, int n, int k, int kchunk,
+                                                 const double* __restrict__ a, int lda,
+                                                 const double* __restrict__ b, int ldb,
+                                                 double* __restrict__ out, size_t out_split_stride,
+                                                 int ldo, double alpha, double beta, bool direct) {
+    extern __shared__ __align__(16) double dsm[];
+    const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+    const int kb = blockIdx.z * kchunk, ke = min(k, kb + kchunk);
+    dmma::Acc<FM, FN> acc;
+    gemm_block(ta, tb, m, n, m0, n0, kb, ke, a, lda, b, ldb, dsm, acc);
     double* o = out + size_t(blockIdx.z) * out_split_stride;
 #pragma unroll
     for (int i = 0; i < FM; ++i)
@@ -93,6 +100,91 @@ __global__ void __launch_bounds__(NT) dgemm_tile(bool ta, bool tb, int m, int n,
                     else *cp = v;
                 }
             }
+}
+
+// ------------------------------------------------------------------ Chebyshev filter
+// The whole degree-d three-term recurrence of ChFSI in ONE cooperative launch
+// (eig.cu): per step every CTA computes a split-K partial of S Y_j on DMMA,
+// a grid barrier, then all CTAs combine Y_{j+1} = a (sum of partials) +
+// b Y_j + c Y_{j-1} in a fixed order (deterministic), a second barrier.  S
+// (n x n fp64) and the n x k blocks stay L2-resident across steps; the
+// per-step cost is the DMMA work spread over ~all SMs plus two grid barriers,
+// instead of three launches (combine, GEMM, split-K reduce) per step.
+struct ChebArgs {
+    const double* S;
+    int n, k, deg;
+    double* y[4];        // y[0] = V (read-only start), y[1..3] rotating buffers
+    double* part;        // splits x n x k
+    unsigned* bar;       // [0] count, [1] generation
+    int gm, gn, splits, kchunk;
+    double a1, b1;       // step 1: Y1 = a1 S V + b1 V
+    double a, b, c;      // step j: Y_{j+1} = a S Y_j + b Y_j + c Y_{j-1}
+};
+
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned* gen = bar + 1;
+        const unsigned g = *gen;
+        __threadfence();
+        if (atomicAdd(bar, 1u) == nblocks - 1) {
+            bar[0] = 0;
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            while (*gen == g) __nanosleep(40);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(NT) cheb_filter_kernel(const ChebArgs p) {
+    extern __shared__ __align__(16) double dsm[];
+    const int ntile = p.gm * p.gn;
+    const int tile = blockIdx.x % ntile, split = blockIdx.x / ntile;
+    const bool worker = blockIdx.x < unsigned(ntile * p.splits);
+    const int m0 = (tile % p.gm) * BM, n0 = (tile / p.gm) * BN;
+    const int kb = split * p.kchunk, ke = min(p.n, kb + p.kchunk);
+    const size_t nk = size_t(p.n) * p.k;
+    int iprev = 0, icur = 0, inext = 1;  // step 1 reads V (y[0])
+    for (int step = 0; step < p.deg; ++step) {
+        const double* ycur = p.y[icur];
+        if (worker) {
+            dmma::Acc<FM, FN> acc;
+            gemm_block(false, false, p.n, p.k, m0, n0, kb, ke, p.S, p.n, ycur, p.n, dsm, acc);
+            double* o = p.part + size_t(split) * nk;
+#pragma unroll
+            for (int i = 0; i < FM; ++i)
+#pragma unroll
+                for (int j = 0; j < FN; ++j)
+#pragma unroll
+                    for (int t = 0; t < 2; ++t) {
+                        const int gm = m0 + dmma::row_of<WM, FM>(i), gn = n0 + dmma::col_of<WM, FN>(j, t);
+                        if (gm < p.n && gn < p.k) o[gm + size_t(p.n) * gn] = acc.v[i][j][t];
+                    }
+        }
+        grid_barrier(p.bar, gridDim.x);
+        const double a = step == 0 ? p.a1 : p.a, b = step == 0 ? p.b1 : p.b, c = step == 0 ? 0.0 : p.c;
+        const double* yprev = p.y[iprev];
+        double* ynext = p.y[inext];
+        for (size_t e = size_t(blockIdx.x) * NT + threadIdx.x; e < nk; e += size_t(gridDim.x) * NT) {
+            double s = 0.0;
+            for (int z = 0; z < p.splits; ++z) s += p.part[size_t(z) * nk + e];
+            double v = fma(a, s, b * ycur[e]);
+            if (c != 0.0) v = fma(c, yprev[e], v);
+            ynext[e] = v;
+        }
+        grid_barrier(p.bar, gridDim.x);
+        // rotation as in eig.cu's host loop: yprev <- ycur, ycur <- ynext, ynext <- a free
+        // buffer (never V = y[0], which the recurrence only reads)
+        if (step == 0) {
+            iprev = 0; icur = 1; inext = 2;
+        } else {
+            const int spare = (iprev == 0) ? 3 : iprev;
+            iprev = icur; icur = inext; inext = spare;
+        }
+    }
 }
 
 __global__ void dgemm_splitk_reduce(const double* __restrict__ part, int splits, int m, int n,
@@ -146,6 +238,47 @@ void dgemm(atk_ctx* ctx, bool ta, bool tb, int m, int n, int k, double alpha, co
     dgemm_splitk_reduce<<<unsigned(std::min<size_t>((mn + 255) / 256, size_t(ctx->num_sms) * 8)), 256, 0,
                           ctx->stream>>>(part.get(), splits, m, n, alpha, beta, c, ldc);
     ATK_LAUNCHED(ctx);
+}
+
+int cheb_filter(atk_ctx* ctx, const double* S, int n, int k, int deg, double* const y[4], double a1, double b1,
+                double a, double b, double c) {
+    static bool attr = false;
+    static int max_blocks = 0;
+    if (!attr) {
+        ATK_CUDA(cudaFuncSetAttribute(cheb_filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(SMEM_BYTES)));
+        int per_sm = 0;
+        ATK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cheb_filter_kernel, NT, SMEM_BYTES));
+        max_blocks = per_sm * ctx->num_sms;
+        attr = true;
+    }
+    const int gm = (n + BM - 1) / BM, gn = (k + BN - 1) / BN, tiles = gm * gn;
+    // one CTA per SM: split K so tiles x splits fills the SMs (K chunks of >= 64)
+    int splits = std::max(1, std::min(ctx->num_sms / tiles, n / 64));
+    int kchunk = (n + splits - 1) / splits;
+    kchunk = (kchunk + BK - 1) / BK * BK;
+    splits = (n + kchunk - 1) / kchunk;
+    const int grid = std::max(tiles * splits, std::min(ctx->num_sms, max_blocks));
+    if (tiles * splits > max_blocks) return -1;  // caller falls back to per-step launches
+    DevBuf<double> part(ctx, size_t(splits) * n * k);
+    DevBuf<unsigned> bar(ctx, 2);
+    ATK_CUDA(cudaMemsetAsync(bar.get(), 0, 2 * sizeof(unsigned), ctx->stream));
+    ChebArgs p{S, n, k, deg, {y[0], y[1], y[2], y[3]}, part.get(), bar.get(), gm, gn, splits, kchunk, a1, b1, a, b, c};
+    void* args[] = {&p};
+    ATK_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(cheb_filter_kernel), dim3(unsigned(grid)), dim3(NT),
+                                         args, SMEM_BYTES, ctx->stream));
+    ATK_LAUNCHED(ctx);
+    // final Y_deg sits in the buffer the rotation left as "current"
+    int iprev = 0, icur = 0, inext = 1;
+    for (int step = 0; step < deg; ++step) {
+        if (step == 0) {
+            iprev = 0; icur = 1; inext = 2;
+        } else {
+            const int spare = (iprev == 0) ? 3 : iprev;
+            iprev = icur; icur = inext; inext = spare;
+        }
+    }
+    return icur;
 }
 
 }  // namespace atk

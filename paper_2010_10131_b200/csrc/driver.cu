@@ -109,17 +109,25 @@ ModeOut eig_mode(atk_ctx* ctx, const atk_tensor* y, int mode, uint64_t r, int so
 // linalg.hpp:169-177, NotSPD on a non-positive pivot).  n <= 112: one-CTA
 // Cholesky fused with X = L^{-T}, then A^{-1} = X X^T (two launches instead of
 // a column-serial triangular solve).
-static void spd_inverse(atk_ctx* ctx, const double* a, int n, double* inv) {
-    DevBuf<int> info(ctx, 1);
+// With `info_slot` (n <= 112) the pivot status is left on the device for the
+// caller to check later (als_iterate checks all of its solves once, after the
+// loop: no host round trip per iteration); otherwise it is checked here.
+static void spd_inverse(atk_ctx* ctx, const double* a, int n, double* inv, int* info_slot = nullptr) {
+    DevBuf<int> info(ctx, info_slot ? 0 : 1);
     int h = 0;
     if (n <= kJacobiMax) {
         DevBuf<double> x(ctx, size_t(n) * n);
-        cholesky_inv_t(ctx, a, n, x.get(), info.get());
+        cholesky_inv_t(ctx, a, n, x.get(), info_slot ? info_slot : info.get());
         dgemm(ctx, false, true, n, n, n, 1.0, x.get(), n, x.get(), n, 0.0, inv, n);
+        if (info_slot) return;
         ATK_CUDA(cudaMemcpyAsync(&h, info.get(), sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
         ATK_CUDA(cudaStreamSynchronize(ctx->stream));
         if (h != 0) fail(ATK_NOT_SPD, "Cholesky factorization hit a non-positive pivot");
         return;
+    }
+    if (info_slot) {  // the large path reports through its own sync below
+        ATK_CUDA(cudaMemsetAsync(info_slot, 0, sizeof(int), ctx->stream));
+        info = DevBuf<int>(ctx, 1);
     }
     DevBuf<double> l(ctx, size_t(n) * n);
     ATK_CUDA(cudaMemcpyAsync(l.get(), a, size_t(n) * n * sizeof(double), cudaMemcpyDeviceToDevice,
@@ -150,35 +158,65 @@ AlsOut als_iterate(atk_ctx* ctx, const atk_tensor* y, int mode, const double* l0
     AlsOut out;
     DevBuf<double> L(ctx, I * r), Lt(ctx, I * r), GL(ctx, r * r), GLi(ctx, r * r), YR(ctx, I * r),
         GR(ctx, r * r), GRi(ctx, r * r), nxt(ctx, I * r);
+    DevBuf<int> infos(ctx, 2 * size_t(opts.num_iters));  // NotSPD status of every solve
+    ATK_CUDA(cudaMemsetAsync(infos.get(), 0, 2 * size_t(opts.num_iters) * sizeof(int), ctx->stream));
+    auto check_spd = [&](int upto) {  // linalg.hpp:169-177 NotSPD, in iteration order
+        std::vector<int> h(2 * size_t(upto));
+        ATK_CUDA(cudaMemcpyAsync(h.data(), infos.get(), h.size() * sizeof(int), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+        ATK_CUDA(cudaStreamSynchronize(ctx->stream));
+        for (int v : h)
+            if (v != 0) fail(ATK_NOT_SPD, "Cholesky factorization hit a non-positive pivot");
+    };
     ATK_CUDA(cudaMemcpyAsync(L.get(), l0_host, I * r * sizeof(double), cudaMemcpyHostToDevice,
                              ctx->stream));
+    static const bool trace = std::getenv("ATK_TRACE") != nullptr;
+    auto t_last = std::chrono::steady_clock::now();
+    auto mark = [&](const char* what, int it) {
+        if (!trace) return;
+        cudaStreamSynchronize(ctx->stream);
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[atk als I=%llu r=%llu J=%llu it=%d] %-8s %8.3f ms\n", (unsigned long long)I,
+                     (unsigned long long)r, (unsigned long long)J, it, what,
+                     std::chrono::duration<double, std::milli>(now - t_last).count());
+        t_last = now;
+    };
+    mark("start", -1);
     for (int k = 0; k < opts.num_iters; ++k) {
         transpose(ctx, L.get(), int(I), int(r), Lt.get());
         atk_tensor* w = contract_ttm(ctx, y, Lt.get(), r, mode);  // W = Y x_n L^T
+        mark("ttm_w", k);
         record_gemm(2LL * (long long)(r * J) * (long long)I);
         dgemm(ctx, true, false, int(r), int(r), int(I), 1.0, L.get(), int(I), L.get(), int(I), 0.0,
               GL.get(), int(r));
         record_gemm(2LL * (long long)(r * r) * (long long)I);
-        spd_inverse(ctx, GL.get(), int(r), GLi.get());
+        spd_inverse(ctx, GL.get(), int(r), GLi.get(), infos.get() + 2 * k);
+        mark("gl_inv", k);
         if (out.rfac) atk_tensor_free(out.rfac);
+        mark("free", k);
         out.rfac = contract_ttm(ctx, w, GLi.get(), r, mode);  // rfac = W x_n (L^T L)^{-1}
         record_gemm(2LL * (long long)(r * J) * (long long)r);
         atk_tensor_free(w);
+        mark("rfac", k);
         contract_ttt(ctx, y, out.rfac, mode, YR.get(), false);  // YR = Y_(n) rfac_(n)^T
         record_gemm(2LL * (long long)(I * r) * (long long)J);
+        mark("ttt_yr", k);
         contract_ttt(ctx, out.rfac, out.rfac, mode, GR.get(), true);  // symmetric: the Gram kernels
         record_gemm(2LL * (long long)(r * r) * (long long)J);
+        mark("gram_gr", k);
         // Sharded (SURVEY §8(e) "ALS modes"): YR and GR are sums over J, so the
         // local partials are combined with one grouped allreduce per iteration;
         // L, its Gram and every R x R solve are then replicated bit-identically.
         if (ctx->comm) allreduce_sum2(ctx, YR.get(), I * r, GR.get(), r * r, &out.comm_ms);
-        spd_inverse(ctx, GR.get(), int(r), GRi.get());
+        spd_inverse(ctx, GR.get(), int(r), GRi.get(), infos.get() + 2 * k + 1);
         dgemm(ctx, false, false, int(I), int(r), int(r), 1.0, YR.get(), int(I), GRi.get(), int(r),
               0.0, nxt.get(), int(I));
         record_gemm(2LL * (long long)(I * r) * (long long)r);
+        mark("solves", k);
         out.iterations_run = k + 1;
         double change = 0.0;
         if (opts.rel_tol > 0.0) {
+            check_spd(k + 1);
             const double diff = diff_norm2_sq(ctx, nxt.get(), L.get(), ATK_F64, I * r);
             const double base = norm2_sq(ctx, L.get(), ATK_F64, I * r);
             change = base > 0.0 ? std::sqrt(diff / base) : 0.0;
@@ -186,6 +224,7 @@ AlsOut als_iterate(atk_ctx* ctx, const atk_tensor* y, int mode, const double* l0
         std::swap(L, nxt);
         if (opts.rel_tol > 0.0 && change <= opts.rel_tol) break;
     }
+    check_spd(out.iterations_run);
     out.l.resize(I * r);
     ATK_CUDA(cudaMemcpyAsync(out.l.data(), L.get(), I * r * sizeof(double), cudaMemcpyDeviceToHost,
                              ctx->stream));

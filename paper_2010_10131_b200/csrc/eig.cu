@@ -650,20 +650,30 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
         const double ac = std::acosh(std::max(1.0 + 1e-12, (hth[r - 1] - c) / e));
         const int degree = std::max(1, std::min(64, int(23.0 / std::max(ac, 1e-3))));
         // Y1 = g (S V - c V) / e ; Y_{j+1} = g (2/e)(S Y_j - c Y_j) - g^2 Y_{j-1}
-        double* yprev = V.get();
-        double* ycur = Ya.get();
-        double* ynext = Yb.get();
-        cheb_combine<<<nblk(nk), 256, 0, st>>>(ycur, V.get(), nullptr, nk, -g * c / e, 0.0);
-        ATK_LAUNCHED(ctx);
-        dgemm(ctx, false, false, n, k, n, g / e, S.get(), n, V.get(), n, 1.0, ycur, n);
-        for (int j = 1; j < degree; ++j) {
-            cheb_combine<<<nblk(nk), 256, 0, st>>>(ynext, ycur, yprev, nk, -2.0 * g * c / e, -g * g);
+        double* ycur = nullptr;
+        double* const ys[4] = {V.get(), Ya.get(), Yb.get(), Yc.get()};
+        const int fused = ctx->cheb_fused
+                              ? cheb_filter(ctx, S.get(), n, k, degree, ys, g / e, -g * c / e, 2.0 * g / e,
+                                            -2.0 * g * c / e, -g * g)
+                              : -1;
+        if (fused >= 0) {
+            ycur = ys[fused];
+        } else {  // per-step launches (option cheb_fused = 0, or no co-resident grid)
+            double* yprev = V.get();
+            ycur = Ya.get();
+            double* ynext = Yb.get();
+            cheb_combine<<<nblk(nk), 256, 0, st>>>(ycur, V.get(), nullptr, nk, -g * c / e, 0.0);
             ATK_LAUNCHED(ctx);
-            dgemm(ctx, false, false, n, k, n, 2.0 * g / e, S.get(), n, ycur, n, 1.0, ynext, n);
-            double* spare = (yprev == V.get()) ? Yc.get() : yprev;
-            yprev = ycur;
-            ycur = ynext;
-            ynext = spare;
+            dgemm(ctx, false, false, n, k, n, g / e, S.get(), n, V.get(), n, 1.0, ycur, n);
+            for (int j = 1; j < degree; ++j) {
+                cheb_combine<<<nblk(nk), 256, 0, st>>>(ynext, ycur, yprev, nk, -2.0 * g * c / e, -g * g);
+                ATK_LAUNCHED(ctx);
+                dgemm(ctx, false, false, n, k, n, 2.0 * g / e, S.get(), n, ycur, n, 1.0, ynext, n);
+                double* spare = (yprev == V.get()) ? Yc.get() : yprev;
+                yprev = ycur;
+                ycur = ynext;
+                ynext = spare;
+            }
         }
         mark("filter", degree, worst / scale);
         orthonormalize(ctx, ycur, n, k, V.get(), ws);

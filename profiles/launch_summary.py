@@ -18,7 +18,7 @@ def summarise(path, skip=("fill_uniform", "axpy_kernel", "ttm_tile_kernel<float>
             continue
         name = d["Kernel Name"].split("(")[0].replace("void ", "").replace("(anonymous namespace)::", "")
         v = float(d["Metric Value"].replace(",", ""))
-        v *= {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(d["Metric Unit"], 1.0)
+        v *= {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(d["Metric Unit"], 1.0)
         a = agg.setdefault(name, [0, 0.0])
         a[0] += 1
         a[1] += v
