@@ -16,6 +16,8 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
+#include <cstring>
 #include <functional>
 #include <stdexcept>
 #include <string>
@@ -37,6 +39,10 @@ struct NoConvergence : Error { using Error::Error; };
 struct RankDeficient : Error { using Error::Error; };
 struct NotSPD : Error { using Error::Error; };
 struct ZeroNormInput : Error { using Error::Error; };
+struct EmptyDataset : Error { using Error::Error; };
+struct FeatureVersionMismatch : Error { using Error::Error; };
+struct SchemaMismatch : Error { using Error::Error; };
+struct IoFailure : Error { using Error::Error; };
 struct DeviceError : Error { using Error::Error; };  // CUDA / NCCL / OOM (no CPU fallback)
 
 inline void check(atk_status s) {
@@ -52,6 +58,10 @@ inline void check(atk_status s) {
         case ATK_RANK_DEFICIENT: throw RankDeficient(m);
         case ATK_NOT_SPD: throw NotSPD(m);
         case ATK_ZERO_NORM_INPUT: throw ZeroNormInput(m);
+        case ATK_EMPTY_DATASET: throw EmptyDataset(m);
+        case ATK_FEATURE_VERSION: throw FeatureVersionMismatch(m);
+        case ATK_SCHEMA_MISMATCH: throw SchemaMismatch(m);
+        case ATK_IO_FAILURE: throw IoFailure(m);
         case ATK_CUDA_ERROR: case ATK_NCCL_ERROR: case ATK_OOM: throw DeviceError(m);
         default: throw Error(m);
     }
@@ -359,6 +369,58 @@ inline DenseTensor reconstruct(const TuckerDecomposition& t) {
     std::vector<uint64_t> od(t.original_dims.begin(), t.original_dims.end());
     check(atk_reconstruct(Engine::instance().ctx(), c.t, flat.data(), od.data(), &y.t));
     return y.host();
+}
+
+// ---------------------------------------------------------------- tensor_io.hpp:15-99
+// Host containers: the reference's format, written and read on the host
+// (header-only, byte-identical to the reference's writer).  Large tensors:
+// read_dten_device streams the file straight into HBM through the engine
+// (atk_tensor_read_dten: double-buffered pinned chunks, fp32 narrowing on the
+// device) and hands back an engine handle for atk_sthosvd.
+inline void write_dten(const std::string& path, const std::vector<std::size_t>& dims, const double* data) {
+    FILE* f = std::fopen(path.c_str(), "wb");
+    if (!f) throw IoFailure("cannot open " + path + " for writing");
+    const std::uint32_t version = 1, order = static_cast<std::uint32_t>(dims.size());
+    std::vector<std::uint64_t> d64(dims.begin(), dims.end());
+    std::size_t n = 1;
+    for (auto d : dims) n *= d;
+    bool ok = std::fwrite("DTEN", 1, 4, f) == 4 && std::fwrite(&version, 4, 1, f) == 1 &&
+              std::fwrite(&order, 4, 1, f) == 1 && std::fwrite(d64.data(), 8, d64.size(), f) == d64.size() &&
+              std::fwrite(data, 8, n, f) == n;
+    ok = (std::fclose(f) == 0) && ok;
+    if (!ok) throw IoFailure("failed writing " + path);
+}
+inline void write_dten(const std::string& path, const DenseTensor& x) { write_dten(path, x.dims(), x.data()); }
+inline void write_dten(const std::string& path, const DenseMatrix& m) {
+    write_dten(path, {m.rows(), m.cols()}, m.data());
+}
+
+inline DenseTensor read_dten(const std::string& path) {
+    int order = 0;
+    std::uint64_t dims[ATK_MAX_ORDER] = {};
+    check(atk_dten_info(path.c_str(), &order, dims));  // the engine's header validation
+    std::vector<std::size_t> d(dims, dims + order);
+    DenseTensor t(d);
+    FILE* f = std::fopen(path.c_str(), "rb");
+    if (!f) throw IoFailure("cannot open " + path);
+    std::fseek(f, long(12 + 8 * order), SEEK_SET);
+    const std::size_t got = std::fread(t.data(), 8, t.size(), f);
+    std::fclose(f);
+    if (got != t.size())
+        throw IoFailure(path + ": truncated payload, expected " + std::to_string(t.size() * 8) +
+                        " bytes but read " + std::to_string(got * 8));
+    return t;
+}
+inline DenseMatrix read_dten_matrix(const std::string& path) {
+    DenseTensor t = read_dten(path);
+    if (t.order() != 2) throw IoFailure(path + ": expected an order-2 .dten");
+    return DenseMatrix(t.dim(0), t.dim(1), std::move(t.data_));
+}
+// Engine handle (caller frees with atk_tensor_free).
+inline atk_tensor* read_dten_device(const std::string& path, atk_dtype dtype = ATK_F32) {
+    atk_tensor* t = nullptr;
+    check(atk_tensor_read_dten(Engine::instance().ctx(), path.c_str(), dtype, &t));
+    return t;
 }
 
 }  // namespace atucker_b200

@@ -25,7 +25,7 @@ static DenseTensor random_signed(std::vector<std::size_t> dims, std::uint64_t se
         }                                                           \
     } while (0)
 
-int main() {
+int main(int argc, char** argv) {
     // full ranks give an exact decomposition (test_sthosvd.cpp:54-58)
     DenseTensor x = random_signed({8, 7, 6}, 5);
     SthosvdResult res = sthosvd(x, {8, 7, 6}, Strategy::fixed_eig());
@@ -73,5 +73,36 @@ int main() {
     }
     REQUIRE(thrown);
     std::printf("PASS error taxonomy\n");
+
+    // tensor_io.hpp: the reference-written golden round-trips byte-identically
+    // on the host; the engine streams it into HBM unchanged
+    if (argc > 1) {
+        const std::string golden = std::string(argv[1]) + "/ref_normal_4x3x5_seed7.dten";
+        DenseTensor g = read_dten(golden);
+        REQUIRE(g.dims() == std::vector<std::size_t>({4, 3, 5}));
+        const std::string out = std::string(argv[2]) + "/cpp_roundtrip.dten";
+        write_dten(out, g);
+        auto slurp = [](const std::string& p) {
+            std::vector<char> b;
+            FILE* f = std::fopen(p.c_str(), "rb");
+            for (int c; (c = std::fgetc(f)) != EOF;) b.push_back(char(c));
+            std::fclose(f);
+            return b;
+        };
+        REQUIRE(slurp(out) == slurp(golden));
+        atk_tensor* d = read_dten_device(golden, ATK_F64);
+        std::vector<double> back(g.size());
+        check(atk_tensor_to_host(Engine::instance().ctx(), d, back.data()));
+        atk_tensor_free(d);
+        for (std::size_t i = 0; i < back.size(); ++i) REQUIRE(back[i] == g.data()[i]);
+        thrown = false;
+        try {
+            read_dten(std::string(argv[2]) + "/missing.dten");
+        } catch (const IoFailure&) {
+            thrown = true;
+        }
+        REQUIRE(thrown);
+        std::printf("PASS dten io\n");
+    }
     return 0;
 }

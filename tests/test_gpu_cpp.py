@@ -22,7 +22,8 @@ def test_cpp_dropin_compiles(tmp_path):
 
 @pytest.mark.gpu
 def test_cpp_dropin_runs(tmp_path):
-    out = subprocess.run([str(_build(tmp_path))], capture_output=True, text=True, timeout=300)
+    out = subprocess.run([str(_build(tmp_path)), str(ROOT / "tests" / "golden"), str(tmp_path)],
+                         capture_output=True, text=True, timeout=300)
     print(out.stdout)
     assert out.returncode == 0, out.stdout + out.stderr
-    assert out.stdout.count("PASS") == 4
+    assert out.stdout.count("PASS") == 5
