@@ -271,6 +271,10 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         dist.init_process_group("gloo")
+    # ATK_BENCH_SHARE_GPU=1: every rank on cuda:0 with host-staged collectives
+    # (functional check of the N > 1 path on a one-GPU box; not a scaling number)
+    share = world > 1 and os.environ.get("ATK_BENCH_SHARE_GPU") == "1"
+    local = 0 if share else local
     torch.cuda.set_device(local)
     from paper_2010_10131_b200 import atucker
     from paper_2010_10131_b200.selector import Strategy
@@ -280,9 +284,9 @@ def main():
         k, v = kv.split("=", 1)
         ctx.set_option(k, float(v))
     if world > 1:
-        from paper_2010_10131_b200.dist import init_comm_from_torch
+        from paper_2010_10131_b200.dist import init_comm_from_torch, init_host_comm_from_torch
 
-        init_comm_from_torch(ctx)
+        (init_host_comm_from_torch if share else init_comm_from_torch)(ctx)
     strategy = Strategy.parse(cfg["strategy"])
     x = make_input(atucker, cfg, SEEDS[args.config], ctx, (rank, world))
     gdims = tuple(cfg["dims"])

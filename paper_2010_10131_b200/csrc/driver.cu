@@ -73,7 +73,7 @@ ModeOut eig_mode(atk_ctx* ctx, const atk_tensor* y, int mode, uint64_t r, int so
     if (!gram_pre) {
         tm.start();
         contract_ttt(ctx, y, y, mode, S.get(), true);
-        if (ctx->comm) allreduce_sum(ctx, S.get(), I * I, &out.times.comm_ms);
+        if (ctx->comm && !ctx->replicated) allreduce_sum(ctx, S.get(), I * I, &out.times.comm_ms);
         out.times.gram_ms = tm.stop_ms();
         Sg = S.get();
     } else {
@@ -207,7 +207,7 @@ AlsOut als_iterate(atk_ctx* ctx, const atk_tensor* y, int mode, const double* l0
         // Sharded (SURVEY §8(e) "ALS modes"): YR and GR are sums over J, so the
         // local partials are combined with one grouped allreduce per iteration;
         // L, its Gram and every R x R solve are then replicated bit-identically.
-        if (ctx->comm) allreduce_sum2(ctx, YR.get(), I * r, GR.get(), r * r, &out.comm_ms);
+        if (ctx->comm && !ctx->replicated) allreduce_sum2(ctx, YR.get(), I * r, GR.get(), r * r, &out.comm_ms);
         spd_inverse(ctx, GR.get(), int(r), GRi.get(), infos.get() + 2 * k + 1);
         dgemm(ctx, false, false, int(I), int(r), int(r), 1.0, YR.get(), int(I), GRi.get(), int(r),
               0.0, nxt.get(), int(I));
@@ -315,6 +315,9 @@ atk_tensor* sthosvd(atk_ctx* ctx, const atk_tensor* x, const uint64_t* ranks, at
     size_t foff = 0;
     try {
         for (int n = 0; n < order; ++n) {
+            // after the all-gather the last mode runs on the full (replicated)
+            // tensor: its Gram / YR / GR are complete on every rank, no allreduce
+            ctx->replicated = ctx->comm && n == order - 1;
             if (ctx->comm && n == order - 1) {
                 // the shard mode: gather the (small) shrunk tensor, finish replicated
                 atk_tensor* full = allgather_last_mode(ctx, work);
@@ -367,9 +370,11 @@ atk_tensor* sthosvd(atk_ctx* ctx, const atk_tensor* x, const uint64_t* ranks, at
             if (reports) reports[n] = rep;
         }
     } catch (...) {
+        ctx->replicated = false;
         if (owned) atk_tensor_free(owned);
         throw;
     }
+    ctx->replicated = false;
     return owned;
 }
 
