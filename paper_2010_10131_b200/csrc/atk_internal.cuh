@@ -228,7 +228,8 @@ struct EigInfo {
 };
 // `psd`: the caller guarantees S is positive semidefinite (a Gram), which
 // clamps the filter's lower spectrum bound at 0.  `tol` <= 0: ctx->chfsi_tol.
+// `exact_sym`: S is bitwise symmetric (the engine's mirrored Grams): no copy.
 EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* values_dev,
-                      double* vectors_dev, bool psd = false, double tol = 0.0);
+                      double* vectors_dev, bool psd = false, double tol = 0.0, bool exact_sym = false);
 
 }  // namespace atk

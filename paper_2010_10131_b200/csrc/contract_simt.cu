@@ -18,6 +18,29 @@
 namespace atk {
 namespace {
 
+// (p, o) of the linear index base + off, given (p0, o0) of base: one 32-bit
+// division at most (off < 2^31) instead of a 64-bit div/mod per element.
+__device__ __forceinline__ void split_po(uint64_t p0, uint64_t o0, uint32_t off, uint64_t P, uint64_t& p,
+                                         uint64_t& o) {
+    if (P == 1) {  // mode 0: k is the outer index itself
+        p = 0;
+        o = o0 + off;
+        return;
+    }
+    p = p0 + off;
+    o = o0;
+    if (p >= P) {
+        if (P <= 0xffffffffull && p <= 0xffffffffull) {
+            const uint32_t q = uint32_t(p) / uint32_t(P);
+            o += q;
+            p -= uint64_t(q) * P;
+        } else {
+            o += p / P;
+            p %= P;
+        }
+    }
+}
+
 // LD = 68 = 4 (mod 16): conflict-free DMMA fragment loads (dmma.cuh)
 constexpr int TM = 64, TN = 64, KT = 16, NT = 256, LD = TM + 4;
 constexpr int WM = 2, FM = 4, FN = 2;  // 8 warps: 2 x 4, each 32 x 16
@@ -39,6 +62,7 @@ __global__ void __launch_bounds__(NT) ttt_tile_kernel(const T* __restrict__ x, c
     double acc[4][4] = {};
     dmma::Acc<FM, FN> dacc;
     dmma::zero(dacc);
+    uint64_t tp0 = kb % P, to0 = kb / P;  // (p, o) of the tile's first k, advanced per tile
     for (uint64_t k0 = kb; k0 < ke; k0 += KT) {
         for (int e = tid; e < KT * TM; e += NT) {
             int kk, ii;
@@ -46,7 +70,8 @@ __global__ void __launch_bounds__(NT) ttt_tile_kernel(const T* __restrict__ x, c
             const uint64_t k = k0 + kk, i = i0 + ii;
             double v = 0.0;
             if (k < ke && i < I) {
-                const uint64_t p = k % P, o = k / P;
+                uint64_t p, o;
+                split_po(tp0, to0, uint32_t(kk), P, p, o);
                 v = double(x[p + P * i + P * I * o]);
             }
             As[kk][ii] = v;
@@ -57,11 +82,13 @@ __global__ void __launch_bounds__(NT) ttt_tile_kernel(const T* __restrict__ x, c
             const uint64_t k = k0 + kk, r = r0 + rr;
             double v = 0.0;
             if (k < ke && r < R) {
-                const uint64_t p = k % P, o = k / P;
+                uint64_t p, o;
+                split_po(tp0, to0, uint32_t(kk), P, p, o);
                 v = double(y[p + P * r + P * R * o]);
             }
             Bs[kk][rr] = v;
         }
+        split_po(tp0, to0, KT, P, tp0, to0);
         __syncthreads();
         if constexpr (std::is_same_v<T, double>) {
             dmma::tile_step<LD, LD, WM, FM, FN>(dacc, &As[0][0], &Bs[0][0], KT);
@@ -147,6 +174,7 @@ __global__ void __launch_bounds__(NT) ttm_tile_kernel(const T* __restrict__ x, c
     double acc[4][4] = {};
     dmma::Acc<FM, FN> dacc;
     dmma::zero(dacc);
+    const uint64_t mp0 = m0 % P, mo0 = m0 / P;  // (p, o) of the tile's first row
     for (uint64_t k0 = 0; k0 < I; k0 += KT) {
         for (int e = tid; e < KT * TM; e += NT) {
             int kk, mm;
@@ -154,7 +182,8 @@ __global__ void __launch_bounds__(NT) ttm_tile_kernel(const T* __restrict__ x, c
             const uint64_t i = k0 + kk, m = m0 + mm;
             double v = 0.0;
             if (i < I && m < M) {
-                const uint64_t p = m % P, o = m / P;
+                uint64_t p, o;
+                split_po(mp0, mo0, uint32_t(mm), P, p, o);
                 v = double(x[p + P * i + P * I * o]);
             }
             As[kk][mm] = v;
@@ -190,9 +219,11 @@ __global__ void __launch_bounds__(NT) ttm_tile_kernel(const T* __restrict__ x, c
             for (int j = 0; j < FN; ++j)
 #pragma unroll
                 for (int t = 0; t < 2; ++t) {
-                    const uint64_t m = m0 + dmma::row_of<WM, FM>(i), r = r0 + dmma::col_of<WM, FN>(j, t);
+                    const int mm = dmma::row_of<WM, FM>(i);
+                    const uint64_t m = m0 + mm, r = r0 + dmma::col_of<WM, FN>(j, t);
                     if (m < M && r < R) {
-                        const uint64_t p = m % P, o = m / P;
+                        uint64_t p, o;
+                        split_po(mp0, mo0, uint32_t(mm), P, p, o);
                         y[p + P * r + P * R * o] = dacc.v[i][j][t];
                     }
                 }
@@ -203,7 +234,8 @@ __global__ void __launch_bounds__(NT) ttm_tile_kernel(const T* __restrict__ x, c
             for (int v = 0; v < 4; ++v) {
                 const uint64_t m = m0 + ty + 16 * q, r = r0 + tx + 16 * v;
                 if (m < M && r < R) {
-                    const uint64_t p = m % P, o = m / P;
+                    uint64_t p, o;
+                    split_po(mp0, mo0, uint32_t(ty + 16 * q), P, p, o);
                     y[p + P * r + P * R * o] = T(acc[q][v]);
                 }
             }

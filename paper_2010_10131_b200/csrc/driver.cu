@@ -87,7 +87,10 @@ ModeOut eig_mode(atk_ctx* ctx, const atk_tensor* y, int mode, uint64_t r, int so
     // resolving its eigenpairs beyond a 1e-9 Ritz residual buys nothing (the
     // factor error is ~residual / gap, far below the tf32 Gram error); fp64 keeps 1e-12.
     out.eig = sym_eig_top_r(ctx, Sg, int(I), int(r), vals.get(), vecs.get(), true,
-                            y->dtype == ATK_F32 ? std::max(1e-9, ctx->chfsi_tol) : ctx->chfsi_tol);
+                            y->dtype == ATK_F32 ? std::max(1e-9, ctx->chfsi_tol) : ctx->chfsi_tol,
+                            // the engine's Grams are mirrored (bitwise symmetric); an allreduce
+                            // may sum (i, j) and (j, i) in different orders, so sharded modes symmetrise
+                            /*exact_sym=*/!ctx->comm || ctx->replicated);
     out.times.eig_ms = tm.stop_ms();
 
     tm.start();

@@ -523,7 +523,7 @@ void rayleigh_ritz(atk_ctx* ctx, const double* S, int n, int k, int r, const dou
 }  // namespace
 
 EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* values_dev, double* vectors_dev,
-                      bool psd, double tol) {
+                      bool psd, double tol, bool exact_sym) {
     EigInfo info;
     cudaStream_t st = ctx->stream;
     if (n <= kTridiagMax && (ctx->eig_method == -1 || ctx->eig_method == 2)) {
@@ -565,7 +565,9 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
     if (k < r) fail(ATK_UNSUPPORTED, "sym_eig_top_r: r > 112 with n > 112 is not supported");
     const size_t nn = size_t(n) * n, nk = size_t(n) * k, kk = size_t(k) * k;
     const size_t nr = size_t(n) * r;
-    DevBuf<double> S(ctx, nn), V(ctx, nk), W(ctx, nk), Ya(ctx, nk), Yb(ctx, nk), Yc(ctx, nk), T(ctx, kk), Z(ctx, kk),
+    // an exactly symmetric input (the engine's Grams are mirrored) is used in
+    // place; anything else is copied and symmetrised first (linalg.hpp:104)
+    DevBuf<double> Sbuf(ctx, exact_sym ? 0 : nn), V(ctx, nk), W(ctx, nk), Ya(ctx, nk), Yb(ctx, nk), Yc(ctx, nk), T(ctx, kk), Z(ctx, kk),
         theta(ctx, k), res(ctx, k), Vr(ctx, nr), Wr(ctx, nr);
     Ws ws{DevBuf<double>(ctx, kk), DevBuf<double>(ctx, kk), DevBuf<double>(ctx, k), DevBuf<double>(ctx, k),
           DevBuf<double>(ctx, kk), DevBuf<double>(ctx, nk), DevBuf<int>(ctx, 1), DevBuf<int>(ctx, 3)};
@@ -585,18 +587,21 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
         if (trace) cudaMemcpy(&h, d, sizeof(int), cudaMemcpyDeviceToHost);
         return h;
     };
-    ATK_CUDA(cudaMemcpyAsync(S.get(), s_dev, nn * sizeof(double), cudaMemcpyDeviceToDevice, st));
-    symmetrize(ctx, S.get(), n);
+    if (!exact_sym) {
+        ATK_CUDA(cudaMemcpyAsync(Sbuf.get(), s_dev, nn * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        symmetrize(ctx, Sbuf.get(), n);
+    }
+    const double* Sp = exact_sym ? s_dev : Sbuf.get();
     mark("prep");
     // start: two power steps on a random block (S^2 Omega: on gapped spectra this
     // alone resolves the wanted subspace), orthonormalise, Rayleigh-Ritz
     fill_normalish<<<nblk(nk), 256, 0, st>>>(Yb.get(), nk, 0xc0ffee11ULL);
     ATK_LAUNCHED(ctx);
-    dgemm(ctx, false, false, n, k, n, 1.0, S.get(), n, Yb.get(), n, 0.0, Ya.get(), n);
-    dgemm(ctx, false, false, n, k, n, 1.0, S.get(), n, Ya.get(), n, 0.0, Yb.get(), n);
+    dgemm(ctx, false, false, n, k, n, 1.0, Sp, n, Yb.get(), n, 0.0, Ya.get(), n);
+    dgemm(ctx, false, false, n, k, n, 1.0, Sp, n, Ya.get(), n, 0.0, Yb.get(), n);
     orthonormalize(ctx, Yb.get(), n, k, V.get(), ws);
     mark("qr0");
-    rayleigh_ritz(ctx, S.get(), n, k, r, V.get(), W.get(), T.get(), Z.get(), theta.get(), Vr.get(), Wr.get(),
+    rayleigh_ritz(ctx, Sp, n, k, r, V.get(), W.get(), T.get(), Z.get(), theta.get(), Vr.get(), Wr.get(),
                   sweeps.get(), psd);
     mark("rr0", trace_sweeps(sweeps.get()));
 
@@ -628,7 +633,7 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
             if (gapped) {
                 b = Bounds{0.0, hth[0]};
             } else {
-                b = lanczos_bounds(ctx, S.get(), n, psd);
+                b = lanczos_bounds(ctx, Sp, n, psd);
                 mark("lanczos", 0, b.lo);
             }
             have_bounds = true;
@@ -653,7 +658,7 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
         double* ycur = nullptr;
         double* const ys[4] = {V.get(), Ya.get(), Yb.get(), Yc.get()};
         const int fused = ctx->cheb_fused
-                              ? cheb_filter(ctx, S.get(), n, k, degree, ys, g / e, -g * c / e, 2.0 * g / e,
+                              ? cheb_filter(ctx, Sp, n, k, degree, ys, g / e, -g * c / e, 2.0 * g / e,
                                             -2.0 * g * c / e, -g * g)
                               : -1;
         if (fused >= 0) {
@@ -664,11 +669,11 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
             double* ynext = Yb.get();
             cheb_combine<<<nblk(nk), 256, 0, st>>>(ycur, V.get(), nullptr, nk, -g * c / e, 0.0);
             ATK_LAUNCHED(ctx);
-            dgemm(ctx, false, false, n, k, n, g / e, S.get(), n, V.get(), n, 1.0, ycur, n);
+            dgemm(ctx, false, false, n, k, n, g / e, Sp, n, V.get(), n, 1.0, ycur, n);
             for (int j = 1; j < degree; ++j) {
                 cheb_combine<<<nblk(nk), 256, 0, st>>>(ynext, ycur, yprev, nk, -2.0 * g * c / e, -g * g);
                 ATK_LAUNCHED(ctx);
-                dgemm(ctx, false, false, n, k, n, 2.0 * g / e, S.get(), n, ycur, n, 1.0, ynext, n);
+                dgemm(ctx, false, false, n, k, n, 2.0 * g / e, Sp, n, ycur, n, 1.0, ynext, n);
                 double* spare = (yprev == V.get()) ? Yc.get() : yprev;
                 yprev = ycur;
                 ycur = ynext;
@@ -678,7 +683,7 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
         mark("filter", degree, worst / scale);
         orthonormalize(ctx, ycur, n, k, V.get(), ws);
         mark("qr");
-        rayleigh_ritz(ctx, S.get(), n, k, r, V.get(), W.get(), T.get(), Z.get(), theta.get(), Vr.get(), Wr.get(),
+        rayleigh_ritz(ctx, Sp, n, k, r, V.get(), W.get(), T.get(), Z.get(), theta.get(), Vr.get(), Wr.get(),
                       sweeps.get(), psd);
         mark("rr", trace_sweeps(sweeps.get()));
     }
