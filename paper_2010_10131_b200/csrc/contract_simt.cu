@@ -242,6 +242,59 @@ __global__ void __launch_bounds__(NT) ttm_tile_kernel(const T* __restrict__ x, c
     }
 }
 
+// fp64 TTM with the DMMA tile narrowed to R: TN_ = 16 / 32 columns (8 warps
+// stacked along M), so R = 16 (C3) no longer pays for 64 DMMA columns.
+template <int TN_, int WM_, int FM_, int FN_>
+__global__ void __launch_bounds__(NT) ttm_f64_kernel(const double* __restrict__ x, const double* __restrict__ u,
+                                                     uint64_t P, uint64_t I, uint64_t O, uint64_t R,
+                                                     double* __restrict__ y) {
+    constexpr int LDB_ = TN_ + 4;  // = 4 (mod 16)
+    __shared__ double As[KT][LD];
+    __shared__ double Bs[KT][LDB_];
+    const uint64_t M = P * O;
+    const uint64_t m0 = uint64_t(blockIdx.x) * TM, r0 = uint64_t(blockIdx.y) * TN_;
+    const int tid = threadIdx.x;
+    dmma::Acc<FM_, FN_> dacc;
+    dmma::zero(dacc);
+    const uint64_t mp0 = m0 % P, mo0 = m0 / P;
+    for (uint64_t k0 = 0; k0 < I; k0 += KT) {
+        for (int e = tid; e < KT * TM; e += NT) {
+            int kk, mm;
+            if (P == 1) { kk = e % KT; mm = e / KT; } else { mm = e % TM; kk = e / TM; }
+            const uint64_t i = k0 + kk, m = m0 + mm;
+            double v = 0.0;
+            if (i < I && m < M) {
+                uint64_t p, o;
+                split_po(mp0, mo0, uint32_t(mm), P, p, o);
+                v = x[p + P * i + P * I * o];
+            }
+            As[kk][mm] = v;
+        }
+        for (int e = tid; e < KT * TN_; e += NT) {
+            const int rr = e % TN_, kk = e / TN_;
+            const uint64_t i = k0 + kk, r = r0 + rr;
+            Bs[kk][rr] = (i < I && r < R) ? u[r + R * i] : 0.0;
+        }
+        __syncthreads();
+        dmma::tile_step<LD, LDB_, WM_, FM_, FN_>(dacc, &As[0][0], &Bs[0][0], KT);
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < FM_; ++i)
+#pragma unroll
+        for (int j = 0; j < FN_; ++j)
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+                const int mm = dmma::row_of<WM_, FM_>(i);
+                const uint64_t m = m0 + mm, r = r0 + dmma::col_of<WM_, FN_>(j, t);
+                if (m < M && r < R) {
+                    uint64_t p, o;
+                    split_po(mp0, mo0, uint32_t(mm), P, p, o);
+                    y[p + P * r + P * R * o] = dacc.v[i][j][t];
+                }
+            }
+}
+
 }  // namespace
 
 void ttt_simt(atk_ctx* ctx, const void* x, const void* y, atk_dtype dt, Split s, uint64_t R, double* z_dev, bool sym) {
@@ -285,7 +338,18 @@ void ttm_simt(atk_ctx* ctx, const void* x, atk_dtype dt, Split s, const double* 
     if (dt == ATK_F32)
         ttm_tile_kernel<float><<<grid, NT, 0, ctx->stream>>>((const float*)x, u_dev, s.P, s.I, s.O, R, (float*)y);
     else
-        ttm_tile_kernel<double><<<grid, NT, 0, ctx->stream>>>((const double*)x, u_dev, s.P, s.I, s.O, R, (double*)y);
+        if (R <= 16) {  // 8 warps x (8 rows x 16 cols): no DMMA columns wasted on R
+            const dim3 g{grid.x, unsigned((R + 15) / 16)};
+            ttm_f64_kernel<16, 8, 1, 2><<<g, NT, 0, ctx->stream>>>((const double*)x, u_dev, s.P, s.I, s.O, R,
+                                                                   (double*)y);
+        } else if (R <= 32) {
+            const dim3 g{grid.x, unsigned((R + 31) / 32)};
+            ttm_f64_kernel<32, 4, 2, 2><<<g, NT, 0, ctx->stream>>>((const double*)x, u_dev, s.P, s.I, s.O, R,
+                                                                   (double*)y);
+        } else {
+            ttm_tile_kernel<double><<<grid, NT, 0, ctx->stream>>>((const double*)x, u_dev, s.P, s.I, s.O, R,
+                                                                  (double*)y);
+        }
     ATK_LAUNCHED(ctx);
 }
 
