@@ -23,6 +23,21 @@ void contract_ttt(atk_ctx* ctx, const atk_tensor* x, const atk_tensor* y, int mo
         tc_ttt(ctx, x, y, mode, z_dev, sym);
         return;
     }
+    // fp64, first or last mode: the unfolding is a plain column-major matrix
+    // (kernels.hpp:49-58), so the pipelined DMMA GEMM (cp.async ring, split-K
+    // with a fixed-order reduction) applies directly; Grams are symmetrised
+    // exactly afterwards (kernels.hpp:127-138)
+    if (!ctx->force_simt && x->dtype == ATK_F64 && y->dtype == ATK_F64 && (s.P == 1 || s.O == 1) &&
+        s.I <= 0x7fffffffULL && R <= 0x7fffffffULL && s.P * s.O <= 0x7fffffffULL) {
+        const auto* xd = static_cast<const double*>(x->data);
+        const auto* yd = static_cast<const double*>(y->data);
+        if (s.P == 1)  // Z = X(I x J) Y(R x J)^T
+            dgemm(ctx, false, true, int(s.I), int(R), int(s.O), 1.0, xd, int(s.I), yd, int(R), 0.0, z_dev, int(s.I));
+        else  // Z = X(P x I)^T Y(P x R)
+            dgemm(ctx, true, false, int(s.I), int(R), int(s.P), 1.0, xd, int(s.P), yd, int(s.P), 0.0, z_dev, int(s.I));
+        if (sym) symmetrize(ctx, z_dev, int(s.I));
+        return;
+    }
     ttt_simt(ctx, x->data, y->data, x->dtype, s, R, z_dev, sym);
 }
 
