@@ -97,8 +97,13 @@ def test_dense_indefinite(ectx):
 
 
 @pytest.mark.parametrize("kind", ["gapped", "flat"])
-def test_chfsi(ectx, kind):
+@pytest.mark.parametrize("fused", [1, 0], ids=["cheb-fused", "cheb-steps"])
+def test_chfsi(ectx, kind, fused):
+    """ChFSI with the Chebyshev filter as one cooperative launch per pass
+    (default) and as per-step launches; both must give the same quality."""
     from paper_2010_10131_b200 import atucker
+
+    ectx.set_option("cheb_fused", fused)
 
     n, r = 640, 32
     rng = np.random.default_rng(5)
@@ -110,4 +115,5 @@ def test_chfsi(ectx, kind):
     s = (q * lam) @ q.T
     s = (s + s.T) / 2
     res = atucker.sym_eig_top_r(s, r, ctx=ectx)
+    ectx.set_option("cheb_fused", 1)
     _check(s, r, res, vec_tol=1e-8 if kind == "gapped" else 1e-5)

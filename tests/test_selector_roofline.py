@@ -58,3 +58,25 @@ def test_parse_and_cpp_header_expose_it():
     assert Strategy.parse("roofline").kind is Strategy.Kind.Roofline
     hdr = (Path(__file__).resolve().parent.parent / "include" / "atucker_b200.hpp").read_text()
     assert "static Strategy roofline(" in hdr
+
+
+@pytest.mark.gpu
+def test_roofline_hook_drives_sthosvd():
+    """The hook plugs into sthosvd like any Strategy (called per mode with the
+    shrunk J, sthosvd.hpp:149-166) and its picks show up in the reports."""
+    import numpy as np
+
+    from paper_2010_10131_b200 import atucker
+
+    ctx = atucker.Context.default(0)
+    x = atucker.DeviceTensor.uniform([96, 64, 40], 21, np.float32, ctx=ctx)
+    s = Strategy.roofline("f32")
+    res = atucker.sthosvd(x, [12, 8, 6], s, ctx=ctx)
+    ref = atucker.sthosvd(x, [12, 8, 6], Strategy.fixed_eig(), ctx=ctx)
+    dims = [96, 64, 40]
+    for n, rep in enumerate(res.reports):
+        j = int(np.prod(dims)) // dims[n]
+        assert rep.solver_used == s.decide(n, dims[n], [12, 8, 6][n], j)
+        dims[n] = [12, 8, 6][n]
+    if all(r.solver_used == SolverKind.Eig for r in res.reports):
+        np.testing.assert_array_equal(res.decomposition.core.to_numpy(), ref.decomposition.core.to_numpy())
