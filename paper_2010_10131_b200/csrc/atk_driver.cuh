@@ -57,6 +57,10 @@ struct AlsOut {
 };
 void contract_ttt(atk_ctx* ctx, const atk_tensor* x, const atk_tensor* y, int mode, double* z_dev,
                   bool sym);
+// als_tc.cu — one ALS iteration's contractions in one pass over Y (mode 0, fp32, R <= 32)
+bool als_fused_supported(atk_ctx* ctx, const atk_tensor* y, int mode, uint64_t R);
+void als_fused_pass(atk_ctx* ctx, const atk_tensor* y, const double* m_dev, uint64_t R, double* yr_dev,
+                    double* gr_dev, atk_tensor* rfac_out);
 atk_tensor* contract_ttm(atk_ctx* ctx, const atk_tensor* x, const double* u_dev, uint64_t R,
                          int mode);
 uint64_t j_of(const atk_tensor* t, int mode);

@@ -200,6 +200,50 @@ AlsOut als_iterate(atk_ctx* ctx, const atk_tensor* y, int mode, const double* l0
         t_last = now;
     };
     mark("start", -1);
+    if (als_fused_supported(ctx, y, mode, r)) {
+        // One pass over Y per iteration (als_tc.cu): rfac = M Y_(0) with
+        // M = (L^T L)^{-1} L^T, and YR / GR, from the same streamed tiles.  The
+        // update order, seeding, NotSPD checks and early stop are those below.
+        uint64_t rdims[ATK_MAX_ORDER];
+        for (int m = 0; m < y->order; ++m) rdims[m] = y->dims[m];
+        rdims[mode] = r;
+        DevBuf<double> M(ctx, I * r);
+        out.rfac = new_tensor(ctx, y->dtype, y->order, rdims);
+        for (int k = 0; k < opts.num_iters; ++k) {
+            dgemm(ctx, true, false, int(r), int(r), int(I), 1.0, L.get(), int(I), L.get(), int(I), 0.0, GL.get(),
+                  int(r));
+            record_gemm(2LL * (long long)(r * r) * (long long)I);
+            spd_inverse(ctx, GL.get(), int(r), GLi.get(), infos.get() + 2 * k);
+            dgemm(ctx, false, true, int(r), int(I), int(r), 1.0, GLi.get(), int(r), L.get(), int(I), 0.0, M.get(),
+                  int(r));
+            // rfac is only consumed after the last iteration (shrunk = rfac x_n R): with a
+            // fixed count only that pass writes it; with an early stop every pass does
+            const bool keep = opts.rel_tol > 0.0 || k + 1 == opts.num_iters;
+            als_fused_pass(ctx, y, M.get(), r, YR.get(), GR.get(), keep ? out.rfac : nullptr);
+            // the reference's logical contractions: W = ttm, rfac = ttm, YR = ttt, GR = ttt
+            record_gemm(2LL * (long long)(r * J) * (long long)I);
+            record_gemm(2LL * (long long)(r * J) * (long long)r);
+            record_gemm(2LL * (long long)(I * r) * (long long)J);
+            record_gemm(2LL * (long long)(r * r) * (long long)J);
+            mark("fused", k);
+            if (ctx->comm && !ctx->replicated)
+                allreduce_sum2(ctx, YR.get(), I * r, GR.get(), r * r, &out.comm_ms);
+            spd_inverse(ctx, GR.get(), int(r), GRi.get(), infos.get() + 2 * k + 1);
+            dgemm(ctx, false, false, int(I), int(r), int(r), 1.0, YR.get(), int(I), GRi.get(), int(r), 0.0,
+                  nxt.get(), int(I));
+            record_gemm(2LL * (long long)(I * r) * (long long)r);
+            out.iterations_run = k + 1;
+            double change = 0.0;
+            if (opts.rel_tol > 0.0) {
+                check_spd(k + 1);
+                const double diff = diff_norm2_sq(ctx, nxt.get(), L.get(), ATK_F64, I * r);
+                const double base = norm2_sq(ctx, L.get(), ATK_F64, I * r);
+                change = base > 0.0 ? std::sqrt(diff / base) : 0.0;
+            }
+            std::swap(L, nxt);
+            if (opts.rel_tol > 0.0 && change <= opts.rel_tol) break;
+        }
+    } else
     for (int k = 0; k < opts.num_iters; ++k) {
         transpose(ctx, L.get(), int(I), int(r), Lt.get());
         atk_tensor* w = contract_ttm(ctx, y, Lt.get(), r, mode);  // W = Y x_n L^T
