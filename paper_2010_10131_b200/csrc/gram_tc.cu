@@ -35,6 +35,8 @@ struct GramParams {
     int chunk_kb;       // K-blocks accumulated in TMEM before an fp64 drain
     int kmajor;         // 0: MN-major mode-0 map, 1: permuted 3-D K-major map
     int nkb_p;          // K-major: K-blocks per o (= ceil(P / 32))
+    int panel;          // 1: P in {4, 8, 16}: unswizzled K-major 16-byte panels (4-D map {4, I, P/4, O})
+    int opb;            // panel mode: o values per K-block (32 / P)
     double* acc;        // [unit][BN][BM] fp64 partial tiles
     uint32_t* progress; // [gridDim.x] K-blocks issued per CTA (drift limiter), or null
     int slack_kb;       // allowed lead over the slowest CTA, in K-blocks
@@ -114,10 +116,19 @@ __global__ void __launch_bounds__(THREADS, 1)
                         for (int q = q0; q < q1; ++q)
                             tc::tma_load_2d(b + (q - q0) * 4096, &tma_a, &full[stage], un.y * BN + q * 32, k0);
                     } else {
-                        const int p0 = (kb % p.nkb_p) * BK, o0 = kb / p.nkb_p;
-                        tc::tma_load_3d(a, &tma_a, &full[stage], p0, o0, tm * BM);
-                        if (half) tc::tma_load_3d(b, &tma_a, &full[stage], p0, o0, un.y * BN + (half == 1 ? BN / 2 : 0));
-                        else tc::tma_load_3d(b, &tma_b, &full[stage], p0, o0, un.y * BN);
+                        if (p.panel) {  // K-block = 32/P whole o slabs: panels [o][p_hi][row][4 p]
+                            const int o0 = kb * p.opb;
+                            tc::tma_load_4d(a, &tma_a, &full[stage], 0, tm * BM, 0, o0);
+                            if (half)
+                                tc::tma_load_4d(b, &tma_a, &full[stage], 0, un.y * BN + (half == 1 ? BN / 2 : 0), 0, o0);
+                            else
+                                tc::tma_load_4d(b, &tma_b, &full[stage], 0, un.y * BN, 0, o0);
+                        } else {
+                            const int p0 = (kb % p.nkb_p) * BK, o0 = kb / p.nkb_p;
+                            tc::tma_load_3d(a, &tma_a, &full[stage], p0, o0, tm * BM);
+                            if (half) tc::tma_load_3d(b, &tma_a, &full[stage], p0, o0, un.y * BN + (half == 1 ? BN / 2 : 0));
+                            else tc::tma_load_3d(b, &tma_b, &full[stage], p0, o0, un.y * BN);
+                        }
                     }
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
@@ -136,6 +147,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
                 const int4 un = p.units[u];
                 const uint32_t idesc = (un.x >> 16) ? idesc_half : idesc_full;
+                const uint32_t bpanel = (un.x >> 16) ? BM * 16 : BN * 16;  // panel mode: B rows x 16 B
                 for (int c0 = un.z; c0 < un.w; c0 += p.chunk_kb) {
                     const int c1 = min(un.w, c0 + p.chunk_kb);
                     tc::mbar_wait(&tempty[abuf], aphase ^ 1);
@@ -154,6 +166,11 @@ __global__ void __launch_bounds__(THREADS, 1)
                                 // 32-element MN blocks one TMA box apart (LBO 4 KB)
                                 ad = tc::smem_desc(a_base + k * 1024, 4096, 512, 1);
                                 bd = tc::smem_desc(b_base + k * 1024, 4096, 512, 1);
+                            } else if (p.panel) {
+                                // no swizzle, K-major: 8-row x 16-B core matrices, K-adjacent
+                                // ones a panel apart (LBO), M/N-adjacent ones 128 B apart (SBO)
+                                ad = tc::smem_desc(a_base + k * 2 * (BM * 16), BM * 16, 128, 0);
+                                bd = tc::smem_desc(b_base + k * 2 * bpanel, bpanel, 128, 0);
                             } else {
                                 ad = tc::smem_desc_sw128(a_base + k * 32, 16, 1024);
                                 bd = tc::smem_desc_sw128(b_base + k * 32, 16, 1024);
@@ -261,7 +278,8 @@ static bool gram_tc_layout_ok(const atk_tensor* x, int mode) {
     // half-width 128 x 128 tile (the SIMT path ran C4 mode 1 at 4.4 ms vs 0.16 HBM)
     if (s.I < 8) return false;
     if (s.P == 1) return s.I % 4 == 0 && s.O < (1ull << 31) / BK;
-    return s.P >= 32 && s.P % 4 == 0 && s.P * s.I < (1ull << 40) && s.O < (1ull << 31);
+    const bool panel = s.P == 4 || s.P == 8 || s.P == 16;  // unswizzled 16-B panels, 32/P o per K-block
+    return (s.P >= 32 || panel) && s.P % 4 == 0 && s.P * s.I < (1ull << 40) && s.O < (1ull << 31);
 }
 
 bool tc_gram_supported(atk_ctx* ctx, const atk_tensor* x, int mode) {
@@ -276,7 +294,7 @@ void tc_gram(atk_ctx* ctx, const atk_tensor* x, int mode, double* s_dev) {
     CUtensorMap ta{}, tb{};
     const CUtensorMapDataType dt = ctx->tma_tf32 ? CU_TENSOR_MAP_DATA_TYPE_TFLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
     uint64_t nkb;
-    int nkb_p = 1;
+    int nkb_p = 1, panel = 0, opb = 1;
     if (!kmajor) {
         const uint64_t K = s.O;
         const uint64_t dims[2] = {s.I, K};
@@ -287,6 +305,19 @@ void tc_gram(atk_ctx* ctx, const atk_tensor* x, int mode, double* s_dev) {
             fail(ATK_CUDA_ERROR, "gram: tensor map (mode 0) encoding failed");
         tb = ta;
         nkb = (K + BK - 1) / BK;
+    } else if (s.P < 32) {
+        // 4-D map {4 p_lo, I, P/4 p_hi, O}: box {4, rows, P/4, 32/P} lands as 8 panels of
+        // rows x 16 B, i.e. unswizzled K-major core matrices (8 rows x 16 B) for tcgen05
+        panel = 1;
+        opb = int(BK / s.P);
+        const uint64_t dims[4] = {4, s.I, s.P / 4, s.O};
+        const uint64_t str[3] = {s.P * 4, 16, s.P * s.I * 4};
+        const uint32_t boxa[4] = {4, BM, uint32_t(s.P / 4), uint32_t(opb)};
+        const uint32_t boxb[4] = {4, BN, uint32_t(s.P / 4), uint32_t(opb)};
+        if (encode_tensor_map(&ta, dt, 4, x->data, dims, str, boxa, CU_TENSOR_MAP_SWIZZLE_NONE) != CUDA_SUCCESS ||
+            encode_tensor_map(&tb, dt, 4, x->data, dims, str, boxb, CU_TENSOR_MAP_SWIZZLE_NONE) != CUDA_SUCCESS)
+            fail(ATK_CUDA_ERROR, "gram: tensor map (panel) encoding failed");
+        nkb = (s.O + opb - 1) / opb;
     } else {
         nkb_p = int((s.P + BK - 1) / BK);
         const uint64_t dims[3] = {s.P, s.O, s.I};
@@ -339,7 +370,7 @@ void tc_gram(atk_ctx* ctx, const atk_tensor* x, int mode, double* s_dev) {
     // lockstep window well inside the 126 MB L2.
     const double kb_bytes = double(I) * BK * 4.0 * splits;
     const int slack = int(std::max(8.0, std::min(256.0, 32e6 / kb_bytes)));
-    GramParams prm{du.get(), int(units.size()), chunk_kb, kmajor ? 1 : 0, nkb_p, acc.get(),
+    GramParams prm{du.get(), int(units.size()), chunk_kb, kmajor ? 1 : 0, nkb_p, panel, opb, acc.get(),
                    ctx->gram_lockstep ? progress.get() : nullptr, slack};
     static bool attr = false;
     if (!attr) {

@@ -31,6 +31,7 @@ def gram_np(x, n):
     ((256, 1000), 0), ((300, 64, 7), 0), ((1024, 2048), 0), ((128, 4096), 0),   # MN-major (mode 0)
     ((32, 256, 40), 1), ((64, 512, 9), 1), ((4096, 300), 1), ((96, 200, 5), 1),  # K-major (P >= 32)
     ((48, 9000), 0), ((32, 20000), 0), ((8, 4000), 0), ((48, 48, 300), 1),       # small I: half-width tile
+    ((8, 48, 301), 1), ((16, 40, 77), 1), ((4, 64, 50, 3), 1), ((8, 300, 61), 1),  # P in {4, 8, 16}: 16-B panels
 ])
 @pytest.mark.parametrize("tma_tf32", [0, 1])
 def test_tc_gram_vs_oracle(dims, mode, tma_tf32, capsys):
