@@ -289,6 +289,8 @@ double atk_cost_als(double i, double r, double j, int num_iters);
  * max(flops / peak, bytes / HBM bandwidth) plus measured fixed costs:
  *   EIG = max(I^2 J / P, s I J / BW) + eig(I) + max(2 I R J / P, s (I+R) J / BW)
  *   ALS = (iters (2 I + 5 R) + 2 R) s J / BW + iters * als_iter_overhead
+ *   (mode 0, fp32, R <= 32, I % 128 == 0, I <= 1024 runs the one-pass iteration:
+ *    iters * (als_fused_factor * s I J / BW + als_fused_overhead))
  * (s = element bytes, P = tf32 or fp64 tensor rate).  Times in seconds. */
 typedef struct atk_roofline_params {
     double hbm_gbs;              /* measured copy bandwidth (MEASURED_PEAKS.json hbm_gbs) */
@@ -299,10 +301,14 @@ typedef struct atk_roofline_params {
     double als_iter_overhead_ms; /* R x R solves + host syncs per ALS iteration */
     int dtype;                   /* atk_dtype of the tensor */
     int num_iters;               /* AlsOptions::num_iters */
+    double als_fused_factor;     /* one-pass ALS (mode 0, fp32, R <= 32): measured time / (s I J / BW) */
+    double als_fused_overhead_ms; /* its per-iteration fixed cost */
 } atk_roofline_params;
 void atk_roofline_params_default(atk_roofline_params* p, int dtype, int num_iters);
 double atk_roofline_time_eig(const atk_roofline_params* p, double i, double r, double j);
 double atk_roofline_time_als(const atk_roofline_params* p, double i, double r, double j);
+/* The same for a given mode (the one-pass ALS applies to mode 0 only). */
+double atk_roofline_time_als_mode(const atk_roofline_params* p, int mode, double i, double r, double j);
 /* An atk_selector_fn: `user` is a const atk_roofline_params*; EIG iff its
  * modelled time is <= ALS's (ties to EIG, as heuristic_choice). */
 int atk_roofline_selector(void* user, int mode, uint64_t i, uint64_t r, uint64_t j);

@@ -35,7 +35,8 @@ class HostCollectives(C.Structure):
 class RooflineParams(C.Structure):
     _fields_ = [("hbm_gbs", C.c_double), ("tf32_tflops", C.c_double), ("fp64_tflops", C.c_double),
                 ("eig_small_ms", C.c_double), ("eig_large_ms", C.c_double),
-                ("als_iter_overhead_ms", C.c_double), ("dtype", C.c_int), ("num_iters", C.c_int)]
+                ("als_iter_overhead_ms", C.c_double), ("dtype", C.c_int), ("num_iters", C.c_int),
+                ("als_fused_factor", C.c_double), ("als_fused_overhead_ms", C.c_double)]
 
 
 class AlsOpts(C.Structure):
@@ -115,6 +116,8 @@ _SIGS = {
     "atk_roofline_params_default": (None, [C.POINTER(RooflineParams), C.c_int, C.c_int]),
     "atk_roofline_time_eig": (C.c_double, [C.POINTER(RooflineParams), C.c_double, C.c_double, C.c_double]),
     "atk_roofline_time_als": (C.c_double, [C.POINTER(RooflineParams), C.c_double, C.c_double, C.c_double]),
+    "atk_roofline_time_als_mode": (C.c_double, [C.POINTER(RooflineParams), C.c_int, C.c_double, C.c_double,
+                                                C.c_double]),
     "atk_roofline_selector": (C.c_int, [C.c_void_p, C.c_int, C.c_uint64, C.c_uint64, C.c_uint64]),
 }
 

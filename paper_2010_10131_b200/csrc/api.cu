@@ -647,6 +647,8 @@ void atk_roofline_params_default(atk_roofline_params* p, int dtype, int num_iter
     p->als_iter_overhead_ms = 0.7;  // measured: C2 ALS mode 10.3 ms vs 6.8 ms of modelled HBM time
     p->dtype = dtype;
     p->num_iters = num_iters > 0 ? num_iters : 5;
+    p->als_fused_factor = 1.75;     // measured: C2 mode 0, 1.16 ms per pass vs 0.66 ms of HBM time
+    p->als_fused_overhead_ms = 0.1;
 }
 
 static double rf_rate(const atk_roofline_params* p) {
@@ -669,11 +671,20 @@ double atk_roofline_time_als(const atk_roofline_params* p, double i, double r, d
     return (it * (2.0 * i + 5.0 * r) + 2.0 * r) * s * j / bw + it * p->als_iter_overhead_ms * 1e-3;
 }
 
-int atk_roofline_selector(void* user, int, uint64_t i, uint64_t r, uint64_t j) {
+double atk_roofline_time_als_mode(const atk_roofline_params* p, int mode, double i, double r, double j) {
+    if (!p) return 0.0;
+    const bool fused = mode == 0 && p->dtype == ATK_F32 && r <= 32 && std::fmod(i, 128.0) == 0.0 && i >= 128 &&
+                       i <= 1024 && p->als_fused_factor > 0.0;
+    if (!fused) return atk_roofline_time_als(p, i, r, j);
+    const double bw = p->hbm_gbs * 1e9;
+    return p->num_iters * (p->als_fused_factor * 4.0 * i * j / bw + p->als_fused_overhead_ms * 1e-3);
+}
+
+int atk_roofline_selector(void* user, int mode, uint64_t i, uint64_t r, uint64_t j) {
     const auto* p = static_cast<const atk_roofline_params*>(user);
     if (!p) return -1;
     return atk_roofline_time_eig(p, double(i), double(r), double(j)) <=
-                   atk_roofline_time_als(p, double(i), double(r), double(j))
+                   atk_roofline_time_als_mode(p, mode, double(i), double(r), double(j))
                ? ATK_SOLVER_EIG
                : ATK_SOLVER_ALS;
 }

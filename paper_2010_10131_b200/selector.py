@@ -155,15 +155,17 @@ class Strategy:
             setattr(p, k, v)
         return Strategy(Strategy.Kind.Roofline, roofline=p)
 
-    def roofline_times(self, i: int, r: int, j: int) -> tuple:
-        """(EIG seconds, ALS seconds) under the roofline model."""
+    def roofline_times(self, i: int, r: int, j: int, mode: int | None = None) -> tuple:
+        """(EIG seconds, ALS seconds) under the roofline model (with `mode`, the
+        one-pass ALS of mode 0 is priced as such)."""
         import ctypes as C
 
         from . import _lib
 
         lib, p = _lib.load(), C.byref(self.roofline_params)
-        return (lib.atk_roofline_time_eig(p, float(i), float(r), float(j)),
-                lib.atk_roofline_time_als(p, float(i), float(r), float(j)))
+        als = (lib.atk_roofline_time_als(p, float(i), float(r), float(j)) if mode is None else
+               lib.atk_roofline_time_als_mode(p, int(mode), float(i), float(r), float(j)))
+        return lib.atk_roofline_time_eig(p, float(i), float(r), float(j)), als
 
     @staticmethod
     def fixed_eig() -> "Strategy":

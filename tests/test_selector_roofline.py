@@ -80,3 +80,18 @@ def test_roofline_hook_drives_sthosvd():
         dims[n] = [12, 8, 6][n]
     if all(r.solver_used == SolverKind.Eig for r in res.reports):
         np.testing.assert_array_equal(res.decomposition.core.to_numpy(), ref.decomposition.core.to_numpy())
+
+
+def test_one_pass_als_is_priced_on_mode_0():
+    s = Strategy.roofline("f32")
+    p = s.roofline_params
+    i, r, j = 1024, 32, 1 << 20
+    _, two_pass = s.roofline_times(i, r, j)
+    _, fused = s.roofline_times(i, r, j, mode=0)
+    _, other = s.roofline_times(i, r, j, mode=1)
+    assert other == pytest.approx(two_pass, rel=1e-12)
+    want = 5 * (p.als_fused_factor * 4 * i * j / (p.hbm_gbs * 1e9) + p.als_fused_overhead_ms * 1e-3)
+    assert fused == pytest.approx(want, rel=1e-12) and fused < two_pass
+    # not eligible: R > 32 or I not a multiple of 128
+    assert s.roofline_times(1000, r, j, mode=0)[1] == pytest.approx(s.roofline_times(1000, r, j)[1], rel=1e-12)
+    assert s.roofline_times(i, 48, j, mode=0)[1] == pytest.approx(s.roofline_times(i, 48, j)[1], rel=1e-12)
