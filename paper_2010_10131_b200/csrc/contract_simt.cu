@@ -295,6 +295,40 @@ __global__ void __launch_bounds__(NT) ttm_f64_kernel(const double* __restrict__ 
             }
 }
 
+// Small-R TTM, one output row m = (p, o) per thread: y(p, :, o) = U x(p, :, o).
+// The I-vector of a row is read once (threads with consecutive p share 32-B
+// sectors), U (R x I, fp64) sits in shared memory, the R accumulators in
+// registers (fp64).  For the HBM-bound shapes the tile kernels waste on
+// (R <= 32, e.g. C4 mode 1: P = 8, I = 48, R = 8).
+template <class T, int RMAX>
+__global__ void __launch_bounds__(256) ttm_rows_kernel(const T* __restrict__ x, const double* __restrict__ u,
+                                                       uint64_t P, uint64_t I, uint64_t O, int R, T* __restrict__ y) {
+    extern __shared__ double us[];  // [i][r], R x I
+    for (int e = threadIdx.x; e < int(I) * R; e += blockDim.x) {
+        const int r = e % R, i = e / R;
+        us[e] = u[r + size_t(R) * i];
+    }
+    __syncthreads();
+    const uint64_t m = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (m >= P * O) return;
+    const uint64_t pp = m % P, o = m / P;  // one division per thread (row), not per element
+    const T* xr = x + pp + P * I * o;
+    double acc[RMAX];
+#pragma unroll
+    for (int r = 0; r < RMAX; ++r) acc[r] = 0.0;
+    for (uint64_t i = 0; i < I; ++i) {
+        const double v = double(xr[P * i]);
+        const double* ui = us + i * R;
+#pragma unroll
+        for (int r = 0; r < RMAX; ++r)
+            if (r < R) acc[r] = fma(ui[r], v, acc[r]);
+    }
+    T* yr = y + pp + P * uint64_t(R) * o;
+#pragma unroll
+    for (int r = 0; r < RMAX; ++r)
+        if (r < R) yr[P * uint64_t(r)] = T(acc[r]);
+}
+
 }  // namespace
 
 void ttt_simt(atk_ctx* ctx, const void* x, const void* y, atk_dtype dt, Split s, uint64_t R, double* z_dev, bool sym) {
@@ -334,6 +368,21 @@ void ttt_simt(atk_ctx* ctx, const void* x, const void* y, atk_dtype dt, Split s,
 
 void ttm_simt(atk_ctx* ctx, const void* x, atk_dtype dt, Split s, const double* u_dev, uint64_t R, void* y) {
     const uint64_t M = s.P * s.O;
+    if (R <= 32 && s.I * R <= 6144 && s.P > 1 && M >= uint64_t(ctx->num_sms) * 256) {
+        const unsigned blocks = unsigned((M + 255) / 256);
+        const size_t smem = size_t(s.I) * R * sizeof(double);
+        if (dt == ATK_F32) {
+            if (R <= 8) ttm_rows_kernel<float, 8><<<blocks, 256, smem, ctx->stream>>>((const float*)x, u_dev, s.P, s.I, s.O, int(R), (float*)y);
+            else if (R <= 16) ttm_rows_kernel<float, 16><<<blocks, 256, smem, ctx->stream>>>((const float*)x, u_dev, s.P, s.I, s.O, int(R), (float*)y);
+            else ttm_rows_kernel<float, 32><<<blocks, 256, smem, ctx->stream>>>((const float*)x, u_dev, s.P, s.I, s.O, int(R), (float*)y);
+        } else {
+            if (R <= 8) ttm_rows_kernel<double, 8><<<blocks, 256, smem, ctx->stream>>>((const double*)x, u_dev, s.P, s.I, s.O, int(R), (double*)y);
+            else if (R <= 16) ttm_rows_kernel<double, 16><<<blocks, 256, smem, ctx->stream>>>((const double*)x, u_dev, s.P, s.I, s.O, int(R), (double*)y);
+            else ttm_rows_kernel<double, 32><<<blocks, 256, smem, ctx->stream>>>((const double*)x, u_dev, s.P, s.I, s.O, int(R), (double*)y);
+        }
+        ATK_LAUNCHED(ctx);
+        return;
+    }
     dim3 grid{unsigned((M + TM - 1) / TM), unsigned((R + TN - 1) / TN)};
     if (dt == ATK_F32)
         ttm_tile_kernel<float><<<grid, NT, 0, ctx->stream>>>((const float*)x, u_dev, s.P, s.I, s.O, R, (float*)y);
