@@ -535,6 +535,223 @@ __global__ void __launch_bounds__(1024) backtr_kernel(const double* __restrict__
     }
 }
 
+// ---------------------------------------------------------------------------
+// Tile variant (n <= 192): the lower triangle as 32 x 32 tiles (diagonal tiles
+// hold the full symmetric block), leading dimension 33 so both the row walk
+// (lane = row) and the column walk (lane = column) are near conflict-free.
+// Warps own tiles.  Per Householder step: warp 0 forms the reflector; the
+// matvec of tile (I, J) yields a row part B v_J (lane = row) and, off the
+// diagonal, a column part B^T v_I (lane = column) -- no shuffles; a fixed-order
+// sum of those parts gives p; every warp forms K = (tau/2) p.v redundantly and
+// applies the rank-2 update to its tiles.  Four barriers per step, ~10x fewer
+// instructions than the column-slot kernel.  Output: the same hh / d / e / tau
+// / scal as trd_kernel (hh written packed at the end for backtr_kernel).
+constexpr int kTileLd = 33, kTileDbl = 32 * kTileLd;
+
+__device__ __forceinline__ int tile_index(int I, int J) { return I * (I + 1) / 2 + J; }
+
+constexpr int kTileThreads = 256;  // 8 warps: 255 registers/thread (at 512 the CTA-id read was rematerialised per step)
+
+template <int NT>
+__global__ void __launch_bounds__(kTileThreads, 1)
+    trd_tile_kernel(const double* __restrict__ a, int n, int lda, double* __restrict__ hh, double* __restrict__ d,
+                    double* __restrict__ e, double* __restrict__ tau_out, double* __restrict__ scal_out,
+                    long long* __restrict__ prof) {
+    constexpr int NTILES = NT * (NT + 1) / 2, NR = 32 * NT, NWARP = kTileThreads / 32;
+    long long t_mark = clock64(), t_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // ATK_TRD_PROFILE
+    auto lap = [&](int ph) {
+        if (prof) {
+            const long long t = clock64();
+            t_acc[ph] += t - t_mark;
+            t_mark = t;
+        }
+    };
+    extern __shared__ double sm[];
+    double* T = sm;                       // NTILES x (32 x 33)
+    double* crow = T + NTILES * kTileDbl; // NTILES x 32: row parts
+    double* ccol = crow + NTILES * 32;    // NTILES x 32: column parts
+    double* v = ccol + NTILES * 32;       // NR
+    double* pb = v + NR;                  // NR
+    // tau lives in the dynamic buffer: a static __shared__ variable costs an
+    // SR_CgaCtaId read (S2UR, long latency) at every access in this kernel
+    double& sh_tau = pb[NR];
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    auto at = [&](int i, int j) -> double& {  // i >= j or same diagonal tile
+        const int I = i >> 5, J = j >> 5;
+        return T[tile_index(I, J) * kTileDbl + (i & 31) + kTileLd * (j & 31)];
+    };
+    // load: symmetrised, zero padding
+    for (int q = tid; q < NTILES * kTileDbl; q += kTileThreads) T[q] = 0.0;
+    __syncthreads();
+    for (int q = tid; q < n * n; q += kTileThreads) {
+        const int i = q % n, j = q / n;
+        if ((i >> 5) >= (j >> 5)) at(i, j) = 0.5 * (a[i + size_t(lda) * j] + a[j + size_t(lda) * i]);
+    }
+    __syncthreads();
+
+    for (int k = 0; k + 2 < n; ++k) {
+        // ---- A: reflector from column k (warp 0)
+        if (w == 0) {
+            const double alpha = at(k + 1, k);
+            double xn = 0.0;
+            for (int i = k + 2 + lane; i < n; i += 32) {
+                const double x = at(i, k);
+                xn = fma(x, x, xn);
+            }
+            xn = warp_sum(xn);
+            double tau = 0.0, scal = 0.0, beta = alpha;
+            if (xn > 0.0) {
+                beta = -copysign(sqrt(fma(alpha, alpha, xn)), alpha);
+                scal = 1.0 / (alpha - beta);
+                tau = (beta - alpha) / beta;
+            }
+            for (int i = lane; i < NR; i += 32)
+                v[i] = (i == k + 1) ? 1.0 : (i > k + 1 && i < n) ? at(i, k) * scal : 0.0;
+            if (lane == 0) {
+                d[k] = at(k, k);
+                e[k] = beta;
+                tau_out[k] = tau;
+                scal_out[k] = scal;
+                sh_tau = tau;
+            }
+        }
+        lap(0);
+        __syncthreads();
+        lap(1);
+        const double tau = sh_tau;
+        if (tau == 0.0) continue;  // uniform: H_k = I
+        const int J0 = (k + 1) >> 5;
+        const int nact = (NT - J0) * (NT - J0 + 1) / 2;
+        // ---- B: per-tile matvec parts
+        for (int q = w; q < nact; q += NWARP) {
+            // q -> (I, J), J0 <= J <= I < NT, enumerated column by column
+            int J = J0, rem = q;
+            while (rem >= NT - J) { rem -= NT - J; ++J; }
+            const int I = J + rem;
+            const double* B = T + tile_index(I, J) * kTileDbl;
+            const double* vJ = v + J * 32;
+            const double* vI = v + I * 32;
+            // 8 independent accumulators per walk: the fp64 FMA chains, not the loads,
+            // bound this loop
+            double ra[8], ca[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) ra[u] = ca[u] = 0.0;
+            const bool off = I != J;
+#pragma unroll
+            for (int c = 0; c < 32; c += 8)
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    ra[u] = fma(B[lane + kTileLd * (c + u)], vJ[c + u], ra[u]);
+                    if (off) ca[u] = fma(B[c + u + kTileLd * lane], vI[c + u], ca[u]);
+                }
+            crow[tile_index(I, J) * 32 + lane] = ((ra[0] + ra[1]) + (ra[2] + ra[3])) + ((ra[4] + ra[5]) + (ra[6] + ra[7]));
+            if (off)
+                ccol[tile_index(I, J) * 32 + lane] =
+                    ((ca[0] + ca[1]) + (ca[2] + ca[3])) + ((ca[4] + ca[5]) + (ca[6] + ca[7]));
+        }
+        lap(2);
+        __syncthreads();
+        lap(3);
+        // ---- B2: p = tau (row parts of row block I + column parts of tiles below), fixed order
+        for (int i = tid; i < NR; i += kTileThreads) {
+            double s0 = 0.0;
+            if (i > k && i < n) {
+                const int I = i >> 5, r = i & 31;
+                for (int J = J0; J <= I; ++J) s0 += crow[tile_index(I, J) * 32 + r];
+                for (int I2 = I + 1; I2 < NT; ++I2) s0 += ccol[tile_index(I2, I) * 32 + r];
+                s0 *= tau;
+            }
+            pb[i] = s0;
+        }
+        lap(4);
+        __syncthreads();
+        lap(5);
+        // ---- C: K = (tau/2) p.v (every warp, identical arithmetic); A -= v w^T + w v^T
+        double pv = 0.0;
+#pragma unroll
+        for (int t = 0; t < NT; ++t) pv = fma(pb[lane + 32 * t], v[lane + 32 * t], pv);
+        const double K = 0.5 * tau * warp_sum(pv);
+        for (int q = w; q < nact; q += NWARP) {
+            int J = J0, rem = q;
+            while (rem >= NT - J) { rem -= NT - J; ++J; }
+            const int I = J + rem;
+            double* B = T + tile_index(I, J) * kTileDbl;
+            const double vr = v[I * 32 + lane];
+            const double wr = fma(-K, vr, pb[I * 32 + lane]);
+            const double* vJ = v + J * 32;
+            const double* pJ = pb + J * 32;
+            // batches of 8 columns: all loads issued before the stores (no aliasing stalls)
+#pragma unroll
+            for (int c = 0; c < 32; c += 8) {
+                double xs[8], vc[8], pc[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    xs[u] = B[lane + kTileLd * (c + u)];
+                    vc[u] = vJ[c + u];
+                    pc[u] = pJ[c + u];
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const double wc = fma(-K, vc[u], pc[u]);
+                    B[lane + kTileLd * (c + u)] = fma(-vr, wc, fma(-wr, vc[u], xs[u]));
+                }
+            }
+        }
+        lap(6);
+        __syncthreads();
+        lap(7);
+    }
+    if (tid == 0) {
+        if (n >= 2) {
+            d[n - 2] = at(n - 2, n - 2);
+            e[n - 2] = at(n - 1, n - 2);
+            tau_out[n - 2] = 0.0;
+            scal_out[n - 2] = 0.0;
+        }
+        d[n - 1] = at(n - 1, n - 1);
+        tau_out[n - 1] = 0.0;
+        scal_out[n - 1] = 0.0;
+    }
+    for (int j = 0; j < n; ++j)  // packed lower triangle for backtr_kernel
+        for (int i = j + tid; i < n; i += kTileThreads) hh[pk(i, j, n)] = at(i, j);
+    if (prof && lane == 0 && (w == 0 || w == 1))
+        for (int q = 0; q < 8; ++q)
+            atomicAdd(reinterpret_cast<unsigned long long*>(prof + 8 * w + q), (unsigned long long)t_acc[q]);
+}
+
+size_t trd_tile_smem(int nt) {
+    const int ntiles = nt * (nt + 1) / 2;
+    return (size_t(ntiles) * kTileDbl + size_t(ntiles) * 64 + 64 * size_t(nt) + 2) * sizeof(double);
+}
+
+template <int NT>
+void launch_trd_tile(atk_ctx* ctx, const double* a, int n, int lda, double* hh, double* d, double* e, double* tau,
+                     double* scal) {
+    static bool attr = false;
+    if (!attr) {
+        ATK_CUDA(cudaFuncSetAttribute(trd_tile_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(trd_tile_smem(NT))));
+        attr = true;
+    }
+    static long long* prof = nullptr;
+    static const bool want = std::getenv("ATK_TRD_PROFILE") != nullptr;
+    if (want && !prof) ATK_CUDA(cudaMalloc(&prof, 16 * sizeof(long long)));
+    if (prof) ATK_CUDA(cudaMemsetAsync(prof, 0, 16 * sizeof(long long), ctx->stream));
+    trd_tile_kernel<NT><<<1, kTileThreads, trd_tile_smem(NT), ctx->stream>>>(a, n, lda, hh, d, e, tau, scal, prof);
+    ATK_LAUNCHED(ctx);
+    if (prof) {
+        long long h[16];
+        ATK_CUDA(cudaMemcpyAsync(h, prof, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+        ATK_CUDA(cudaStreamSynchronize(ctx->stream));
+        for (int ww = 0; ww < 2; ++ww)
+            std::fprintf(stderr,
+                         "[trd_tile n=%d warp %d] cycles: A %lld barA %lld B %lld barB %lld B2 %lld barB2 %lld C %lld "
+                         "barC %lld\n",
+                         n, ww, h[8 * ww], h[8 * ww + 1], h[8 * ww + 2], h[8 * ww + 3], h[8 * ww + 4], h[8 * ww + 5],
+                         h[8 * ww + 6], h[8 * ww + 7]);
+    }
+}
+
 size_t trd_smem(int n, int nw) {
     const int nr = 32 * ((n + 31) / 32);
     return (size_t(n) * (n + 1) / 2 + 4 * size_t(nr) + size_t(nw) * (n + 1) + n + 4) * sizeof(double);
@@ -582,6 +799,16 @@ void launch_trd_backtr(atk_ctx* ctx, bool trd, const double* a, int n, int lda, 
 void trd_backtr(atk_ctx* ctx, bool trd, const double* a, int n, int lda, double* hh, double* d, double* e,
                 double* tau, double* scal, const double* X, int nwant, double* vout, int ldv) {
     static_assert(kTridiagMax <= 224, "row slots");
+    if (trd && ctx->trd_tiles && n <= 192) {  // tile variant (fits shared memory up to 6 x 6 tiles)
+        switch ((n + 31) / 32) {
+            case 1: launch_trd_tile<1>(ctx, a, n, lda, hh, d, e, tau, scal); return;
+            case 2: launch_trd_tile<2>(ctx, a, n, lda, hh, d, e, tau, scal); return;
+            case 3: launch_trd_tile<3>(ctx, a, n, lda, hh, d, e, tau, scal); return;
+            case 4: launch_trd_tile<4>(ctx, a, n, lda, hh, d, e, tau, scal); return;
+            case 5: launch_trd_tile<5>(ctx, a, n, lda, hh, d, e, tau, scal); return;
+            default: launch_trd_tile<6>(ctx, a, n, lda, hh, d, e, tau, scal); return;
+        }
+    }
     switch ((n + 31) / 32) {
         case 1: launch_trd_backtr<1>(ctx, trd, a, n, lda, hh, d, e, tau, scal, X, nwant, vout, ldv); break;
         case 2: launch_trd_backtr<2>(ctx, trd, a, n, lda, hh, d, e, tau, scal, X, nwant, vout, ldv); break;
