@@ -144,6 +144,8 @@ uint64_t atk_ctx_launch_count(const atk_ctx* ctx);
  *   "als_fused"     1 = an ALS iteration on mode 0 (fp32, R <= 32) reads Y once: rfac, YR and GR
  *                   from one tcgen05 pass (default), 0 = the two-pass TTM + TTT schedule
  *   "trd_tiles"     1 = tridiagonalise n <= 192 on 32 x 32 tiles (default), 0 = column-slot kernel
+ *   "chfsi_k"       ChFSI block size (0 = r + max(16, r/4); measured: larger blocks only slow C2's
+ *                   flat spectra down)
  *   "eig_assume_psd" 1 = atk_sym_eig_top_r inputs are Grams (Cholesky-preconditioned Jacobi)
  *   "tma_tf32"      1 = round-to-nearest tf32 operand loads (default), 0 = hardware truncation
  *   "gram_2cta"     1 = CTA-pair (cta_group::2) Gram where supported (default)

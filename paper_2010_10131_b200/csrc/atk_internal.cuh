@@ -59,6 +59,7 @@ struct atk_ctx {
     int cheb_fused = 1;        // option "cheb_fused": whole Chebyshev filter in one cooperative launch
     int als_fused = 1;         // option "als_fused": one pass over Y per ALS iteration (mode 0, fp32)
     int trd_tiles = 1;         // option "trd_tiles": 32 x 32-tile tridiagonalisation for n <= 192
+    int chfsi_k = 0;           // option "chfsi_k": ChFSI block size override (0 = r + max(16, r/4))
     bool replicated = false;   // sthosvd's last mode under a comm: the work tensor is whole on every rank
     bool eig_assume_psd = false;  // option "eig_assume_psd": atk_sym_eig_top_r input is a Gram
     int tma_tf32 = 1;          // option "tma_tf32": TMA converts fp32 -> tf32 with round-to-nearest

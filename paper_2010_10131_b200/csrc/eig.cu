@@ -561,8 +561,10 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
     // block size: r + max(16, r / 4) (the Rayleigh-Ritz Jacobi costs ~k^2; the
     // S^2 Omega start makes a thin guard band enough on gapped spectra)
     int k = std::min(n, r + std::max(16, r / 4));
+    if (ctx->chfsi_k > 0) k = std::min(n, std::max(r, ctx->chfsi_k));  // option "chfsi_k"
+    // the block's CholeskyQR / SVQB kernels hold k x k in one CTA's shared memory
     k = std::min(k, kJacobiMax);
-    if (k < r) fail(ATK_UNSUPPORTED, "sym_eig_top_r: r > 112 with n > 112 is not supported");
+    if (k < r) fail(ATK_UNSUPPORTED, "sym_eig_top_r: r > 112 with n > 200 is not supported");
     const size_t nn = size_t(n) * n, nk = size_t(n) * k, kk = size_t(k) * k;
     const size_t nr = size_t(n) * r;
     // an exactly symmetric input (the engine's Grams are mirrored) is used in
