@@ -18,6 +18,14 @@ constexpr int LDA = BM + 4, LDB = BN + 4;   // = 4 (mod 16): conflict-free fragm
 constexpr int WM = 4, FM = 4, FN = 4;       // 8 warps: 4 x 2, each 32 x 32
 constexpr int STAGE_DOUBLES = BK * (LDA + LDB);
 constexpr size_t SMEM_BYTES = size_t(STAGES) * STAGE_DOUBLES * sizeof(double);
+// Column-tile variants: BN_ = 16 FN_ (2 warps along N), so an 80- or 96-column
+// right operand (the ChFSI blocks) is one tile instead of 64 + a mostly empty one.
+template <int FN_>
+struct Tile {
+    static constexpr int BN_ = 16 * FN_, LDB_ = BN_ + 4;  // = 4 (mod 16)
+    static constexpr int STAGE = BK * (LDA + LDB_);
+    static constexpr size_t SMEM = size_t(STAGES) * STAGE * sizeof(double);
+};
 
 // 8-byte global -> shared async copy; src_bytes = 0 zero-fills (out-of-range).
 __device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
@@ -31,13 +39,15 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // K slices stream through a STAGES-deep cp.async ring (global latency hidden
 // behind the DMMA work of the slices already resident; one barrier per slice).
 // acc = op(A)[m0:m0+BM, kb:ke] x op(B)[kb:ke, n0:n0+BN]
+template <int FN_ = FN>
 __device__ __forceinline__ void gemm_block(bool ta, bool tb, int m, int n, int m0, int n0, int kb, int ke,
                                            const double* __restrict__ a, int lda, const double* __restrict__ b,
-                                           int ldb, double* dsm, dmma::Acc<FM, FN>& acc) {
+                                           int ldb, double* dsm, dmma::Acc<FM, FN_>& acc) {
+    constexpr int BN_ = Tile<FN_>::BN_, LDB_ = Tile<FN_>::LDB_, STAGE_ = Tile<FN_>::STAGE;
     const int tid = threadIdx.x;
     dmma::zero(acc);
     auto issue = [&](int stage, int k0) {
-        double* As = dsm + stage * STAGE_DOUBLES;
+        double* As = dsm + stage * STAGE_;
         double* Bs = As + BK * LDA;
 #pragma unroll
         for (int e = tid; e < BK * BM; e += NT) {
@@ -48,12 +58,12 @@ __device__ __forceinline__ void gemm_block(bool ta, bool tb, int m, int n, int m
             cp_async8(As + kk * LDA + mm, ok ? (ta ? a + gk + size_t(lda) * gm : a + gm + size_t(lda) * gk) : a, ok);
         }
 #pragma unroll
-        for (int e = tid; e < BK * BN; e += NT) {
+        for (int e = tid; e < BK * BN_; e += NT) {
             int kk, nn;
-            if (tb) { nn = e % BN; kk = e / BN; } else { kk = e % BK; nn = e / BK; }
+            if (tb) { nn = e % BN_; kk = e / BN_; } else { kk = e % BK; nn = e / BK; }
             const int gn = n0 + nn, gk = k0 + kk;
             const bool ok = gn < n && gk < ke;
-            cp_async8(Bs + kk * LDB + nn, ok ? (tb ? b + gn + size_t(ldb) * gk : b + gk + size_t(ldb) * gn) : b, ok);
+            cp_async8(Bs + kk * LDB_ + nn, ok ? (tb ? b + gn + size_t(ldb) * gk : b + gk + size_t(ldb) * gn) : b, ok);
         }
     };
     const int nt = (ke > kb) ? (ke - kb + BK - 1) / BK : 0;
@@ -68,31 +78,32 @@ __device__ __forceinline__ void gemm_block(bool ta, bool tb, int m, int n, int m
         const int tn = t + STAGES - 1;
         if (tn < nt) issue(tn % STAGES, kb + tn * BK);
         cp_async_commit();
-        const double* As = dsm + (t % STAGES) * STAGE_DOUBLES;
-        dmma::tile_step<LDA, LDB, WM, FM, FN>(acc, As, As + BK * LDA, BK);
+        const double* As = dsm + (t % STAGES) * STAGE_;
+        dmma::tile_step<LDA, LDB_, WM, FM, FN_>(acc, As, As + BK * LDA, BK);
     }
     cp_async_wait<0>();
     __syncthreads();  // the ring may be refilled by the next call
 }
 
+template <int FN_>
 __global__ void __launch_bounds__(NT) dgemm_tile(bool ta, bool tb, int m, int n, int k, int kchunk,
                                                  const double* __restrict__ a, int lda,
                                                  const double* __restrict__ b, int ldb,
                                                  double* __restrict__ out, size_t out_split_stride,
                                                  int ldo, double alpha, double beta, bool direct) {
     extern __shared__ __align__(16) double dsm[];
-    const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+    const int m0 = blockIdx.x * BM, n0 = blockIdx.y * Tile<FN_>::BN_;
     const int kb = blockIdx.z * kchunk, ke = min(k, kb + kchunk);
-    dmma::Acc<FM, FN> acc;
-    gemm_block(ta, tb, m, n, m0, n0, kb, ke, a, lda, b, ldb, dsm, acc);
+    dmma::Acc<FM, FN_> acc;
+    gemm_block<FN_>(ta, tb, m, n, m0, n0, kb, ke, a, lda, b, ldb, dsm, acc);
     double* o = out + size_t(blockIdx.z) * out_split_stride;
 #pragma unroll
     for (int i = 0; i < FM; ++i)
 #pragma unroll
-        for (int j = 0; j < FN; ++j)
+        for (int j = 0; j < FN_; ++j)
 #pragma unroll
             for (int t = 0; t < 2; ++t) {
-                const int gm = m0 + dmma::row_of<WM, FM>(i), gn = n0 + dmma::col_of<WM, FN>(j, t);
+                const int gm = m0 + dmma::row_of<WM, FM>(i), gn = n0 + dmma::col_of<WM, FN_>(j, t);
                 if (gm < m && gn < n) {
                     double* cp = o + gm + size_t(ldo) * gn;
                     const double v = acc.v[i][j][t];
@@ -201,18 +212,22 @@ __global__ void dgemm_splitk_reduce(const double* __restrict__ part, int splits,
 
 }  // namespace
 
-void dgemm(atk_ctx* ctx, bool ta, bool tb, int m, int n, int k, double alpha, const double* a, int lda,
-           const double* b, int ldb, double beta, double* c, int ldc) {
-    if (m <= 0 || n <= 0) return;
+namespace {
+
+template <int FN_>
+void dgemm_launch(atk_ctx* ctx, bool ta, bool tb, int m, int n, int k, double alpha, const double* a, int lda,
+                  const double* b, int ldb, double beta, double* c, int ldc) {
+    constexpr int BN_ = Tile<FN_>::BN_;
+    constexpr size_t SMEM_ = Tile<FN_>::SMEM;
     static bool attr = false;
     if (!attr) {
-        ATK_CUDA(cudaFuncSetAttribute(dgemm_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES)));
+        ATK_CUDA(cudaFuncSetAttribute(dgemm_tile<FN_>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_)));
         attr = true;
     }
-    const int gm = (m + BM - 1) / BM, gn = (n + BN - 1) / BN;
+    const int gm = (m + BM - 1) / BM, gn = (n + BN_ - 1) / BN_;
     const int tiles = gm * gn;
     int splits = 1;
-    // up to 4 resident CTAs per SM (51 KB smem each); K chunks of >= 16 slices
+    // up to 4 resident CTAs per SM (51-59 KB smem each); K chunks of >= 16 slices
     if (tiles < 4 * ctx->num_sms && k >= 256)
         splits = std::min(std::max(1, (4 * ctx->num_sms + tiles - 1) / tiles), std::max(1, k / 128));
     int kchunk = (k + splits - 1) / splits;
@@ -224,20 +239,31 @@ void dgemm(atk_ctx* ctx, bool ta, bool tb, int m, int n, int k, double alpha, co
     }
     if (splits == 1) {
         dim3 grid{unsigned(gm), unsigned(gn), 1u};
-        dgemm_tile<<<grid, NT, SMEM_BYTES, ctx->stream>>>(ta, tb, m, n, std::max(k, 0), std::max(kchunk, BK), a, lda,
+        dgemm_tile<FN_><<<grid, NT, SMEM_, ctx->stream>>>(ta, tb, m, n, std::max(k, 0), std::max(kchunk, BK), a, lda,
                                                           b, ldb, c, 0, ldc, alpha, beta, true);
         ATK_LAUNCHED(ctx);
         return;
     }
     DevBuf<double> part(ctx, size_t(splits) * m * n);
     dim3 grid{unsigned(gm), unsigned(gn), unsigned(splits)};
-    dgemm_tile<<<grid, NT, SMEM_BYTES, ctx->stream>>>(ta, tb, m, n, k, kchunk, a, lda, b, ldb, part.get(),
+    dgemm_tile<FN_><<<grid, NT, SMEM_, ctx->stream>>>(ta, tb, m, n, k, kchunk, a, lda, b, ldb, part.get(),
                                                       size_t(m) * n, m, 1.0, 0.0, false);
     ATK_LAUNCHED(ctx);
     const size_t mn = size_t(m) * n;
     dgemm_splitk_reduce<<<unsigned(std::min<size_t>((mn + 255) / 256, size_t(ctx->num_sms) * 8)), 256, 0,
                           ctx->stream>>>(part.get(), splits, m, n, alpha, beta, c, ldc);
     ATK_LAUNCHED(ctx);
+}
+
+}  // namespace
+
+void dgemm(atk_ctx* ctx, bool ta, bool tb, int m, int n, int k, double alpha, const double* a, int lda,
+           const double* b, int ldb, double beta, double* c, int ldc) {
+    if (m <= 0 || n <= 0) return;
+    // one column tile for the ChFSI block widths (n = 65..96) instead of 64 + a mostly empty one
+    if (n > 64 && n <= 80) dgemm_launch<5>(ctx, ta, tb, m, n, k, alpha, a, lda, b, ldb, beta, c, ldc);
+    else if (n > 80 && n <= 96) dgemm_launch<6>(ctx, ta, tb, m, n, k, alpha, a, lda, b, ldb, beta, c, ldc);
+    else dgemm_launch<4>(ctx, ta, tb, m, n, k, alpha, a, lda, b, ldb, beta, c, ldc);
 }
 
 int cheb_filter(atk_ctx* ctx, const double* S, int n, int k, int deg, double* const y[4], double a1, double b1,
