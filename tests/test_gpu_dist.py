@@ -78,6 +78,7 @@ def _host_comm_worker(rank, world, port, dims, ranks, kinds, dtype, out):
     ([24, 20, 18, 16], [5, 4, 4, 3], [0, 1, 0, 1], np.float64, 1e-10),
     ([96, 64, 80], [12, 10, 8], [1, 1, 0], np.float32, 1e-4),
     ([256, 64, 96], [16, 12, 8], [0, 0, 0], np.float32, 1e-4),
+    ([256, 40, 60], [16, 8, 6], [1, 0, 1], np.float32, 1e-4),  # mode 0 on the one-pass ALS kernel
 ])
 def test_two_ranks_one_gpu_host_collectives(dims, ranks, kinds, dtype, tol):
     """N = 2 on the one GPU: both ranks share cuda:0 and exchange through the
