@@ -57,6 +57,7 @@ struct atk_ctx {
     int eig_method = -1;       // option "eig_method": -1 auto, 0 dense Jacobi, 1 ChFSI, 2 tridiagonal
     double chfsi_tol = 1e-12;  // option "chfsi_tol": relative Ritz residual target
     int cheb_fused = 1;        // option "cheb_fused": whole Chebyshev filter in one cooperative launch
+    int lanczos_tiles = 1;     // option "lanczos_tiles": S resident in a 16-CTA cluster's smem for the bounds
     int als_fused = 1;         // option "als_fused": one pass over Y per ALS iteration (mode 0, fp32)
     int trd_tiles = 1;         // option "trd_tiles": 32 x 32-tile tridiagonalisation for n <= 192
     int chfsi_k = 0;           // option "chfsi_k": ChFSI block size override (0 = r + max(16, r/4))
@@ -201,6 +202,9 @@ void jacobi_eig(atk_ctx* ctx, const double* a, int n, int lda, double* values, d
 // the vectors of the top `nwant` (n x nwant, ldv), signs NOT fixed.
 // Bit-reproducible (no atomics).
 constexpr int kTridiagMax = 200;
+// All eigenvalues (descending) of a symmetric tridiagonal (d: m, e: m - 1) and the
+// eigenvectors of the largest and the smallest (vectors: m x 2).
+void tridiag_extreme_eig(atk_ctx* ctx, const double* d, const double* e, int m, double* values, double* vectors);
 void tridiag_eig(atk_ctx* ctx, const double* a, int n, int lda, int nwant, double* values, double* vectors,
                  int ldv, int nvals = 0);
 // Cholesky factorization in place (lower), status written to *info_dev (0 ok, k>0 pivot k).

@@ -6,6 +6,8 @@
 // deterministic split-K (fixed-order fp64 partial sums) so that the skinny
 // shapes of Chebyshev filtering (2048 x 96 x 2048) still fill all 148 SMs.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "atk_internal.cuh"
 #include "dmma.cuh"
@@ -198,6 +200,138 @@ __global__ void __launch_bounds__(NT) cheb_filter_kernel(const ChebArgs p) {
     }
 }
 
+// ------------------------------------------------------------------ resident-S Chebyshev filter
+// Variant for n <= ~1150 (the flat-spectrum ChFSI blocks): S is split into
+// strips of `rows` rows, one 8-CTA cluster per strip, CTA r of a cluster
+// holding the strip's K range [r kc, (r+1) kc) of S in shared memory for the
+// WHOLE filter (S symmetric: the strip's rows are read as contiguous columns).
+// The strip height is 8 ceil(n / (8 x co-resident clusters)) (B200: 15 8-CTA
+// clusters, so 72 rows at n = 1024).  Per step a CTA streams only its K slice
+// of Y_j (cp.async.cg, L2), forms the rows x k split-K partial on DMMA, the
+// cluster reduces the 8 partials through DSMEM in a fixed order (CTA r
+// finishes rows [r rows/8, (r+1) rows/8) of the strip, applies the three-term
+// recurrence and stores Y_{j+1}), and ONE grid barrier publishes Y_{j+1}.
+// cheb_filter_kernel re-streams all of S from L2 every step and pays two grid
+// barriers per step.
+constexpr int RS_CS = 8;  // CTAs per cluster (= K splits)
+
+struct ChebResArgs {
+    const double* S;
+    int n, k, deg, kc, ldk;  // kc = K slice per CTA, ldk = kc + 4 (= 4 mod 16)
+    int rows, wm;            // strip rows (8 MF), warps along M (MF = wm FM)
+    int ncols;               // padded block width (8 NF, NF = wn FN)
+    double* y[4];
+    unsigned* bar;
+    double a1, b1, a, b, c;
+};
+
+__device__ __forceinline__ void cp_async16_cg(void* dst, const void* src, bool valid) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(valid ? 16 : 0) : "memory");
+}
+
+// warp tile FM x FN 8x8 fragments; warps (wm, wn) = (warp % p.wm, warp / p.wm)
+template <int FM, int FN>
+__global__ void __launch_bounds__(512) cheb_resident_kernel(const ChebResArgs p) {
+    extern __shared__ __align__(16) double rsm[];
+    const int ldk = p.ldk, kc = p.kc, n = p.n, k = p.k, rows = p.rows, ncols = p.ncols;
+    double* At = rsm;                  // rows x ldk:  S(m0 + m, kb + kk)
+    double* Bt = At + rows * ldk;      // ncols x ldk: Y(kb + kk, c)
+    double* P = Bt + ncols * ldk;      // ncols x rows partial, P[c * rows + m]
+    const uint32_t rank = blockIdx.x % RS_CS;
+    const int strip = blockIdx.x / RS_CS;
+    const int m0 = strip * rows, kb = int(rank) * kc;
+    const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5, lane = tid & 31;
+    const int hk = kc / 2;
+    // S strip slice, once: row m of the strip = column m0 + m of S, contiguous in kk
+    for (int e = tid; e < rows * hk; e += nt) {
+        const int m = e / hk, kk = 2 * (e % hk);
+        const int gm = m0 + m, gk = kb + kk;
+        const bool ok = gm < n && gk < n;  // n even (host check): a 16-byte pair is all-in or all-out
+        cp_async16_cg(At + m * ldk + kk, ok ? p.S + gk + size_t(n) * gm : p.S, ok);
+    }
+    cp_async_commit();
+    const int wm = warp % p.wm, wn = warp / p.wm;
+    const int fr = lane >> 2, fk = lane & 3;
+    const int mr = rows / RS_CS;  // rows this CTA finishes
+    int iprev = 0, icur = 0, inext = 1;
+    for (int step = 0; step < p.deg; ++step) {
+        const double* ycur = step == 0 ? p.y[0] : p.y[icur];
+        for (int e = tid; e < ncols * hk; e += nt) {
+            const int cc = e / hk, kk = 2 * (e % hk);
+            const int gk = kb + kk;
+            const bool ok = cc < k && gk < n;
+            cp_async16_cg(Bt + cc * ldk + kk, ok ? ycur + gk + size_t(n) * cc : ycur, ok);
+        }
+        cp_async_commit();
+        cp_async_wait<0>();
+        __syncthreads();
+        double acc[FM][FN][2];
+#pragma unroll
+        for (int i = 0; i < FM; ++i)
+#pragma unroll
+            for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        const double* ap = At + (wm * FM * 8 + fr) * ldk + fk;
+        const double* bp = Bt + (wn * FN * 8 + fr) * ldk + fk;
+#pragma unroll 4
+        for (int kk = 0; kk < kc; kk += 4) {
+            double a[FM], bb[FN];
+#pragma unroll
+            for (int i = 0; i < FM; ++i) a[i] = ap[i * 8 * ldk + kk];
+#pragma unroll
+            for (int j = 0; j < FN; ++j) bb[j] = bp[j * 8 * ldk + kk];
+#pragma unroll
+            for (int i = 0; i < FM; ++i)
+#pragma unroll
+                for (int j = 0; j < FN; ++j) dmma::mma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], bb[j]);
+        }
+        // accumulator (i, j, t): row (wm FM + i) 8 + fr, column (wn FN + j) 8 + 2 fk + t
+#pragma unroll
+        for (int i = 0; i < FM; ++i)
+#pragma unroll
+            for (int j = 0; j < FN; ++j)
+#pragma unroll
+                for (int t = 0; t < 2; ++t)
+                    P[((wn * FN + j) * 8 + 2 * fk + t) * rows + (wm * FM + i) * 8 + fr] = acc[i][j][t];
+        // every CTA of the cluster has its partial in smem
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+        const double ca = step == 0 ? p.a1 : p.a, cb = step == 0 ? p.b1 : p.b, ccoef = step == 0 ? 0.0 : p.c;
+        const double* yprev = p.y[iprev];
+        double* ynext = p.y[inext];
+        const uint32_t pbase = static_cast<uint32_t>(__cvta_generic_to_shared(P));
+        for (int e = tid; e < mr * k; e += nt) {
+            const int m = int(rank) * mr + e % mr, cc = e / mr;
+            const int gm = m0 + m;
+            double v[RS_CS];
+#pragma unroll
+            for (int z = 0; z < RS_CS; ++z) {
+                uint32_t ra;
+                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+                             : "=r"(ra)
+                             : "r"(pbase + uint32_t(cc * rows + m) * 8u), "r"(uint32_t(z)));
+                asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v[z]) : "r"(ra) : "memory");
+            }
+            double sum = 0.0;
+#pragma unroll
+            for (int z = 0; z < RS_CS; ++z) sum += v[z];  // split order: deterministic
+            if (gm < n) {
+                const size_t g = gm + size_t(n) * cc;
+                double r = fma(ca, sum, cb * __ldcg(ycur + g));
+                if (ccoef != 0.0) r = fma(ccoef, __ldcg(yprev + g), r);
+                ynext[g] = r;
+            }
+        }
+        // Y_{j+1} complete everywhere (also frees P and Bt for the next step)
+        grid_barrier(p.bar, gridDim.x);
+        if (step == 0) {
+            iprev = 0; icur = 1; inext = 2;
+        } else {
+            const int spare = (iprev == 0) ? 3 : iprev;
+            iprev = icur; icur = inext; inext = spare;
+        }
+    }
+}
+
 __global__ void dgemm_splitk_reduce(const double* __restrict__ part, int splits, int m, int n,
                                     double alpha, double beta, double* __restrict__ c, int ldc) {
     const size_t mn = size_t(m) * n;
@@ -266,8 +400,107 @@ void dgemm(atk_ctx* ctx, bool ta, bool tb, int m, int n, int k, double alpha, co
     else dgemm_launch<4>(ctx, ta, tb, m, n, k, alpha, a, lda, b, ldb, beta, c, ldc);
 }
 
+namespace {
+
+template <int FM, int FN>
+int cheb_resident_max_clusters() {
+    static int max_clusters = -1;
+    if (max_clusters < 0) {
+        max_clusters = 0;
+        if (cudaFuncSetAttribute(cheb_resident_kernel<FM, FN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 200 * 1024) == cudaSuccess) {
+            cudaLaunchConfig_t cfg{};
+            cudaLaunchAttribute at{};
+            at.id = cudaLaunchAttributeClusterDimension;
+            at.val.clusterDim.x = RS_CS;
+            at.val.clusterDim.y = at.val.clusterDim.z = 1;
+            cfg.gridDim = dim3(RS_CS);
+            cfg.blockDim = dim3(512);
+            cfg.dynamicSmemBytes = 200 * 1024;
+            cfg.attrs = &at;
+            cfg.numAttrs = 1;
+            if (cudaOccupancyMaxActiveClusters(&max_clusters, cheb_resident_kernel<FM, FN>, &cfg) != cudaSuccess)
+                max_clusters = 0;
+        }
+        cudaGetLastError();
+    }
+    return max_clusters;
+}
+
+template <int FM, int FN>
+bool cheb_resident_launch(atk_ctx* ctx, ChebResArgs p, int strips, size_t smem, int warps) {
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute at[2]{};
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = RS_CS;
+    at[0].val.clusterDim.y = at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeCooperative;
+    at[1].val.cooperative = 1;
+    cfg.gridDim = dim3(unsigned(strips * RS_CS));
+    cfg.blockDim = dim3(unsigned(32 * warps));
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = ctx->stream;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    if (const cudaError_t err = cudaLaunchKernelEx(&cfg, cheb_resident_kernel<FM, FN>, p); err != cudaSuccess) {
+        cudaGetLastError();  // e.g. cooperative + cluster refused: the split-K kernel instead
+        if (std::getenv("ATK_TRACE")) std::fprintf(stderr, "[atk cheb_resident] launch: %s\n", cudaGetErrorString(err));
+        return false;
+    }
+    ATK_LAUNCHED(ctx);
+    return true;
+}
+
+// Strip height and warp layout for (n, k); false = use cheb_filter_kernel.
+bool cheb_resident(atk_ctx* ctx, const double* S, int n, int k, int deg, double* const y[4], double a1, double b1,
+                   double a, double b, double c) {
+    if (n % 2 != 0 || n < 8 * RS_CS || k < 1 || k > 112) return false;
+    const int max_clusters = cheb_resident_max_clusters<3, 2>();  // same resources for every instance
+    if (max_clusters < 1) return false;
+    int mf = (n + 8 * max_clusters - 1) / (8 * max_clusters);  // 8-row fragments per strip
+    if (mf % 2 && mf % 3) ++mf;
+    const int fm = (mf % 3 == 0) ? 3 : 2, wm = mf / fm;
+    int nf = (k + 7) / 8;
+    const int fn = (nf % 3 == 0) ? 3 : 2;
+    if (nf % fn) ++nf;
+    const int wn = nf / fn, warps = wm * wn;
+    const int rows = 8 * mf, strips = (n + rows - 1) / rows;
+    if (warps > 16 || strips > max_clusters || rows % RS_CS) return false;
+    const int kc = ((n + RS_CS - 1) / RS_CS + 3) / 4 * 4;  // K slice per CTA, a multiple of 4
+    const int ldk = kc + 4 + (16 - (kc + 4) % 16 + 4) % 16;   // = 4 (mod 16)
+    const size_t smem = (size_t(rows) * ldk + size_t(8 * nf) * ldk + size_t(8 * nf) * rows) * sizeof(double);
+    if (std::getenv("ATK_TRACE"))
+        std::fprintf(stderr, "[atk cheb_resident n=%d k=%d] clusters %d/%d rows %d warps %dx%d frag %dx%d smem %zu\n",
+                     n, k, strips, max_clusters, rows, wm, wn, fm, fn, smem);
+    if (smem > 200 * 1024) return false;
+    DevBuf<unsigned> bar(ctx, 2);
+    ATK_CUDA(cudaMemsetAsync(bar.get(), 0, 2 * sizeof(unsigned), ctx->stream));
+    const ChebResArgs p{S, n, k, deg, kc, ldk, rows, wm, 8 * nf, {y[0], y[1], y[2], y[3]}, bar.get(), a1, b1, a, b, c};
+    if (fm == 3 && fn == 3) return cheb_resident_max_clusters<3, 3>() && cheb_resident_launch<3, 3>(ctx, p, strips, smem, warps);
+    if (fm == 3 && fn == 2) return cheb_resident_launch<3, 2>(ctx, p, strips, smem, warps);
+    if (fm == 2 && fn == 3) return cheb_resident_max_clusters<2, 3>() && cheb_resident_launch<2, 3>(ctx, p, strips, smem, warps);
+    return cheb_resident_max_clusters<2, 2>() && cheb_resident_launch<2, 2>(ctx, p, strips, smem, warps);
+}
+
+// final Y_deg sits in the buffer the rotation left as "current"
+int cheb_final_buffer(int deg) {
+    int iprev = 0, icur = 0, inext = 1;
+    for (int step = 0; step < deg; ++step) {
+        if (step == 0) {
+            iprev = 0; icur = 1; inext = 2;
+        } else {
+            const int spare = (iprev == 0) ? 3 : iprev;
+            iprev = icur; icur = inext; inext = spare;
+        }
+    }
+    return icur;
+}
+
+}  // namespace
+
 int cheb_filter(atk_ctx* ctx, const double* S, int n, int k, int deg, double* const y[4], double a1, double b1,
                 double a, double b, double c) {
+    if (ctx->cheb_fused == 1 && cheb_resident(ctx, S, n, k, deg, y, a1, b1, a, b, c)) return cheb_final_buffer(deg);
     static bool attr = false;
     static int max_blocks = 0;
     if (!attr) {
@@ -294,17 +527,7 @@ int cheb_filter(atk_ctx* ctx, const double* S, int n, int k, int deg, double* co
     ATK_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(cheb_filter_kernel), dim3(unsigned(grid)), dim3(NT),
                                          args, SMEM_BYTES, ctx->stream));
     ATK_LAUNCHED(ctx);
-    // final Y_deg sits in the buffer the rotation left as "current"
-    int iprev = 0, icur = 0, inext = 1;
-    for (int step = 0; step < deg; ++step) {
-        if (step == 0) {
-            iprev = 0; icur = 1; inext = 2;
-        } else {
-            const int spare = (iprev == 0) ? 3 : iprev;
-            iprev = icur; icur = inext; inext = spare;
-        }
-    }
-    return icur;
+    return cheb_final_buffer(deg);
 }
 
 }  // namespace atk

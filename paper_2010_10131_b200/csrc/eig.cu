@@ -84,75 +84,6 @@ __device__ double block_sum3(double& a, double& b, double& c, double* sh) {
     return a;
 }
 
-// m-step Lanczos in ONE cooperative kernel.  Block b owns rows [r0, r1).
-// Per step: w = S q (own rows; S symmetric => read column r, coalesced),
-// partial sums {w.w, w.q, w.qprev} -> barrier -> alpha, beta -> own rows of
-// q/qprev updated -> barrier.
-__global__ void __launch_bounds__(256) lanczos_coop(const double* __restrict__ S, int n, int m,
-                                                    double* __restrict__ q, double* __restrict__ qprev,
-                                                    double* __restrict__ w, double* __restrict__ part,
-                                                    double* __restrict__ alpha, double* __restrict__ beta,
-                                                    unsigned* bar) {
-    __shared__ double sh[100];
-    const unsigned G = gridDim.x;
-    const int r0 = int(int64_t(blockIdx.x) * n / G), r1 = int(int64_t(blockIdx.x + 1) * n / G);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    double bprev = 0.0;
-    for (int j = 0; j < m; ++j) {
-        for (int r = r0 + warp; r < r1; r += nw) {
-            const double* col = S + size_t(n) * r;
-            // 8 independent chains so the L2 loads overlap (a single chain is
-            // latency-bound: measured ~60 us per Lanczos step)
-            double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-            int c = lane;
-            for (; c + 7 * 32 < n; c += 8 * 32) {
-#pragma unroll
-                for (int u = 0; u < 8; ++u) s[u] = fma(col[c + u * 32], q[c + u * 32], s[u]);
-            }
-            for (; c < n; c += 32) s[0] = fma(col[c], q[c], s[0]);
-            double t = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
-            for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-            if (lane == 0) w[r] = t;
-        }
-        __syncthreads();
-        double ww = 0, wq = 0, wp = 0;
-        for (int r = r0 + int(threadIdx.x); r < r1; r += blockDim.x) {
-            ww += w[r] * w[r];
-            wq += w[r] * q[r];
-            wp += w[r] * qprev[r];
-        }
-        block_sum3(ww, wq, wp, sh);
-        if (threadIdx.x == 0) {
-            part[3 * blockIdx.x] = ww;
-            part[3 * blockIdx.x + 1] = wq;
-            part[3 * blockIdx.x + 2] = wp;
-        }
-        grid_sync(bar, bar + 1, G);
-        double tw = 0, tq = 0, tp = 0;
-        for (unsigned i = 0; i < G; ++i) {  // fixed order => identical on every block
-            tw += part[3 * i];
-            tq += part[3 * i + 1];
-            tp += part[3 * i + 2];
-        }
-        const double a = tq;
-        // ||w - a q - bprev qprev||^2 with q, qprev orthonormal
-        double bb = tw - 2.0 * a * tq - 2.0 * bprev * tp + a * a + bprev * bprev;
-        const double b = bb > 0 ? sqrt(bb) : 0.0;
-        const double inv = b > 0 ? 1.0 / b : 0.0;
-        for (int r = r0 + int(threadIdx.x); r < r1; r += blockDim.x) {
-            const double nv = (w[r] - a * q[r] - bprev * qprev[r]) * inv;
-            qprev[r] = q[r];
-            q[r] = nv;
-        }
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
-            alpha[j] = a;
-            beta[j] = b;
-        }
-        bprev = b;
-        grid_sync(bar, bar + 1, G);
-    }
-}
-
 // The same m-step Lanczos on ONE 8-CTA cluster: hardware cluster barriers
 // (~0.2 us) instead of a 148-CTA software grid barrier (~25 us measured), an
 // fp32 copy of S (bounds only; halves the L2 traffic) and q staged in smem.
@@ -282,21 +213,194 @@ __global__ void __cluster_dims__(kLzCluster, 1, 1) __launch_bounds__(kLzThreads)
     }
 }
 
+// The same m-step Lanczos with S RESIDENT in the shared memory of one
+// 16-CTA cluster (n <= ~1250): the lower triangle as 32 x 32 fp32 tiles
+// (padded to 32 x 33: conflict-free by rows and by columns), tile t of the
+// row-major order (I, J <= I) on CTA t / per.  Per step a warp forms, for
+// each of its tiles, the row part T q_J (-> y_I) and the column part T^T q_I
+// (-> y_J) from smem only; the owner of each row block B (the CTA holding
+// tile (B, B)) then sums the nb partials that land on B through DSMEM in a
+// fixed order (bit-reproducible).  The previous kernel re-read S from L2
+// every step (~11.5 us per step at n = 1024 on 8 SMs).
+constexpr int kLtCluster = 16, kLtThreads = 1024, kLtLd = 33;
+
+__device__ __forceinline__ uint32_t lt_mapa(const void* p, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+                 : "=r"(r)
+                 : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(p))), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ float lt_ld_remote(uint32_t addr) {
+    float v;
+    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ double lt_ld_remote_d(uint32_t addr) {
+    double v;
+    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void lt_tile_of(int t, int& I, int& J) {  // t = I (I + 1) / 2 + J
+    int i = int((sqrtf(8.0f * float(t) + 1.0f) - 1.0f) * 0.5f);
+    while ((i + 1) * (i + 2) / 2 <= t) ++i;
+    while (i * (i + 1) / 2 > t) --i;
+    I = i;
+    J = t - i * (i + 1) / 2;
+}
+
+__global__ void __launch_bounds__(kLtThreads) lanczos_tiles(const double* __restrict__ S, int n, int m, int per,
+                                                            double* __restrict__ q, double* __restrict__ part,
+                                                            double* __restrict__ alpha,
+                                                            double* __restrict__ beta) {
+    extern __shared__ __align__(16) float lsm[];
+    const int nb = (n + 31) / 32, ntiles = nb * (nb + 1) / 2;
+    const int cb = int(blockIdx.x);  // rank in the cluster (grid = one cluster)
+    const int t0 = cb * per, t1 = min(ntiles, t0 + per);
+    float* tiles = lsm;                       // per x 32 x 33
+    float* rowp = tiles + size_t(per) * 32 * kLtLd;  // per x 32: T q_J of each tile
+    float* colp = rowp + per * 32;            // per x 32: T^T q_I
+    float* qf = colp + per * 32;              // nb x 32, fp32 copy of q
+    __shared__ double sh[100];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    // stage this CTA's tiles: S column-major, lanes down a column (coalesced)
+    for (int t = t0 + warp; t < t1; t += nw) {
+        int I, J;
+        lt_tile_of(t, I, J);
+        float* T = tiles + size_t(t - t0) * 32 * kLtLd;
+        const int r = 32 * I + lane;
+        for (int c0 = 0; c0 < 32; c0 += 16) {  // 16 loads in flight per lane
+            double v[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                const int cc = 32 * J + c0 + u;
+                v[u] = (r < n && cc < n) ? S[r + size_t(n) * cc] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 16; ++u) T[lane * kLtLd + c0 + u] = float(v[u]);
+        }
+    }
+    __shared__ double cpart[3];  // this CTA's {w.w, w.q, w.qprev}, read by the cluster
+    __shared__ double tot[3];
+    // row blocks owned here: B with tile (B, B) in [t0, t1); warp w <-> the w-th
+    int bfirst = nb, bcount = 0;
+    for (int B = 0; B < nb; ++B) {
+        const int td = B * (B + 1) / 2 + B;
+        if (td >= t0 && td < t1) {
+            bfirst = min(bfirst, B);
+            ++bcount;
+        }
+    }
+    const int myB = warp < bcount ? bfirst + warp : -1;
+    const int row = myB >= 0 ? 32 * myB + lane : n;
+    double qi = row < n ? q[row] : 0.0, qpi = 0.0, bprev = 0.0;
+    for (int j = 0; j < m; ++j) {
+        // L2 reads (__ldcg): q and part are rewritten by the other CTAs every step
+        for (int i = threadIdx.x; i < nb * 32; i += blockDim.x) qf[i] = i < n ? float(__ldcg(q + i)) : 0.0f;
+        __syncthreads();
+        for (int t = t0 + warp; t < t1; t += nw) {
+            int I, J;
+            lt_tile_of(t, I, J);
+            const float* T = tiles + size_t(t - t0) * 32 * kLtLd;
+            const float* qJ = qf + 32 * J;
+            const float* qI = qf + 32 * I;
+            float rs0 = 0.f, rs1 = 0.f, cs0 = 0.f, cs1 = 0.f;
+#pragma unroll
+            for (int c = 0; c < 32; c += 2) {
+                rs0 = fmaf(T[lane * kLtLd + c], qJ[c], rs0);
+                rs1 = fmaf(T[lane * kLtLd + c + 1], qJ[c + 1], rs1);
+            }
+            if (I != J) {
+#pragma unroll
+                for (int r = 0; r < 32; r += 2) {
+                    cs0 = fmaf(T[r * kLtLd + lane], qI[r], cs0);
+                    cs1 = fmaf(T[(r + 1) * kLtLd + lane], qI[r + 1], cs1);
+                }
+            }
+            rowp[(t - t0) * 32 + lane] = rs0 + rs1;
+            colp[(t - t0) * 32 + lane] = cs0 + cs1;
+        }
+        cluster_sync_all();  // every CTA's partials are final
+        double w = 0.0;
+        if (myB >= 0) {
+            // y_B = sum_{J <= B} rowp(B, J) + sum_{I > B} colp(I, B): nb DSMEM
+            // loads, all in flight, summed in a fixed order
+            const int base = myB * (myB + 1) / 2;
+            for (int s0 = 0; s0 < nb; s0 += 16) {
+                float v[16];
+#pragma unroll
+                for (int u = 0; u < 16; ++u) {
+                    const int s = s0 + u;  // s <= B: rowp(B, s); s > B: colp(s, B)
+                    const int t = s <= myB ? base + s : s * (s + 1) / 2 + myB;
+                    const float* src = (s <= myB ? rowp : colp) + (t % per) * 32 + lane;
+                    v[u] = s < nb ? lt_ld_remote(lt_mapa(src, t / per)) : 0.0f;
+                }
+#pragma unroll
+                for (int u = 0; u < 16; ++u) w += double(v[u]);
+            }
+        }
+        double ww = w * w, wq = w * qi, wp = w * qpi;
+        block_sum3(ww, wq, wp, sh);
+        if (threadIdx.x == 0) {
+            cpart[0] = ww;
+            cpart[1] = wq;
+            cpart[2] = wp;
+        }
+        cluster_sync_all();
+        // the 16 CTA triples over DSMEM, one per lane, summed in rank order
+        if (warp == 0) {
+            double x0 = 0, x1 = 0, x2 = 0;
+            if (lane < kLtCluster) {
+                x0 = lt_ld_remote_d(lt_mapa(&cpart[0], lane));
+                x1 = lt_ld_remote_d(lt_mapa(&cpart[1], lane));
+                x2 = lt_ld_remote_d(lt_mapa(&cpart[2], lane));
+            }
+            double tw = 0, tq = 0, tp = 0;
+            for (int i = 0; i < kLtCluster; ++i) {
+                tw += __shfl_sync(0xffffffffu, x0, i);
+                tq += __shfl_sync(0xffffffffu, x1, i);
+                tp += __shfl_sync(0xffffffffu, x2, i);
+            }
+            if (lane == 0) {
+                tot[0] = tw;
+                tot[1] = tq;
+                tot[2] = tp;
+            }
+        }
+        __syncthreads();
+        const double tw = tot[0], tq = tot[1], tp = tot[2];
+        const double a = tq;
+        const double bb = tw - 2.0 * a * tq - 2.0 * bprev * tp + a * a + bprev * bprev;
+        const double b = bb > 0 ? sqrt(bb) : 0.0;
+        const double inv = b > 0 ? 1.0 / b : 0.0;
+        if (row < n) {
+            const double nv = (w - a * qi - bprev * qpi) * inv;
+            qpi = qi;
+            qi = nv;
+            q[row] = nv;
+        }
+        if (cb == 0 && threadIdx.x == 0) {
+            alpha[j] = a;
+            beta[j] = b;
+        }
+        bprev = b;
+        cluster_sync_all();
+    }
+}
+
+// smem bytes of lanczos_tiles for n, or 0 when the triangle does not fit
+inline size_t lanczos_tiles_smem(int n, int& per) {
+    const int nb = (n + 31) / 32, ntiles = nb * (nb + 1) / 2;
+    per = (ntiles + kLtCluster - 1) / kLtCluster;
+    const size_t bytes = (size_t(per) * 32 * kLtLd + 2 * size_t(per) * 32 + size_t(nb) * 32) * sizeof(float);
+    return bytes <= 220 * 1024 ? bytes : 0;
+}
+
 __global__ void to_f32(const double* __restrict__ a, size_t n, float* __restrict__ b) {
     for (size_t e = size_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += size_t(gridDim.x) * blockDim.x)
         b[e] = float(a[e]);
-}
-
-__global__ void tridiag_dense(const double* __restrict__ alpha, const double* __restrict__ beta, int m,
-                              double* __restrict__ t) {
-    for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
-        const int i = e % m, j = e / m;
-        double v = 0.0;
-        if (i == j) v = alpha[i];
-        else if (i == j + 1) v = beta[j];
-        else if (j == i + 1) v = beta[i];
-        t[e] = v;
-    }
 }
 
 __global__ void fill_normalish(double* __restrict__ v, size_t n, uint64_t seed) {
@@ -460,21 +564,13 @@ void orthonormalize(atk_ctx* ctx, const double* Y, int n, int k, double* V, Ws& 
     if (!cholqr3(ctx, Y, n, k, V, ws)) svqb(ctx, Y, n, k, V, ws);
 }
 
-Bounds lanczos_bounds(atk_ctx* ctx, const double* S, int n, bool psd) {
+// S re-read from L2 each step (any n whose q fits in smem): the fp32 copy of S
+// and the 8-CTA cluster kernel above.
+void lanczos_l2(atk_ctx* ctx, const double* S, int n, int m, double* q, double* qp, double* w, double* part,
+                double* al, double* be) {
     cudaStream_t st = ctx->stream;
-    const int m = std::min(n, 40);
-    DevBuf<double> q(ctx, n), qp(ctx, n), w(ctx, n), part(ctx, 3 * kLzCluster), al(ctx, m), be(ctx, m),
-        tm(ctx, size_t(m) * m), tv(ctx, m), tz(ctx, size_t(m) * m), nrm(ctx, 1);
     DevBuf<float> s32(ctx, size_t(n) * n);
-    DevBuf<int> sweeps(ctx, 1);
-    ATK_CUDA(cudaMemsetAsync(qp.get(), 0, n * sizeof(double), st));
     to_f32<<<nblk(size_t(n) * n), 256, 0, st>>>(S, size_t(n) * n, s32.get());
-    ATK_LAUNCHED(ctx);
-    fill_normalish<<<nblk(n), 256, 0, st>>>(q.get(), n, 0x5eed1234ULL);
-    ATK_LAUNCHED(ctx);
-    dot_self<<<1, 256, 0, st>>>(q.get(), n, nrm.get());
-    ATK_LAUNCHED(ctx);
-    scale_vec<<<nblk(n), 256, 0, st>>>(q.get(), n, nrm.get());
     ATK_LAUNCHED(ctx);
     const size_t smem = size_t(n) * sizeof(double);
     static bool attr = false;
@@ -483,22 +579,76 @@ Bounds lanczos_bounds(atk_ctx* ctx, const double* S, int n, bool psd) {
         attr = true;
     }
     if (smem > 200 * 1024) fail(ATK_UNSUPPORTED, "lanczos: n too large for the staged vector");
-    lanczos_cluster<<<kLzCluster, kLzThreads, smem, st>>>(s32.get(), n, m, q.get(), qp.get(), w.get(), part.get(),
-                                                         al.get(), be.get());
+    lanczos_cluster<<<kLzCluster, kLzThreads, smem, st>>>(s32.get(), n, m, q, qp, w, part, al, be);
     ATK_LAUNCHED(ctx);
-    tridiag_dense<<<1, 256, 0, st>>>(al.get(), be.get(), m, tm.get());
+}
+
+Bounds lanczos_bounds(atk_ctx* ctx, const double* S, int n, bool psd) {
+    cudaStream_t st = ctx->stream;
+    const int m = std::min(n, 40);
+    DevBuf<double> q(ctx, n), qp(ctx, n), w(ctx, n), part(ctx, 3 * std::max(kLzCluster, kLtCluster)), al(ctx, m),
+        be(ctx, m), tv(ctx, m), tz(ctx, 2 * size_t(m)), nrm(ctx, 1);
+    ATK_CUDA(cudaMemsetAsync(qp.get(), 0, n * sizeof(double), st));
+    fill_normalish<<<nblk(n), 256, 0, st>>>(q.get(), n, 0x5eed1234ULL);
     ATK_LAUNCHED(ctx);
-    jacobi_eig(ctx, tm.get(), m, m, tv.get(), tz.get(), m, sweeps.get());
-    std::vector<double> hv(m), hb(m), zlast(m);
+    dot_self<<<1, 256, 0, st>>>(q.get(), n, nrm.get());
+    ATK_LAUNCHED(ctx);
+    scale_vec<<<nblk(n), 256, 0, st>>>(q.get(), n, nrm.get());
+    ATK_LAUNCHED(ctx);
+    int per = 0;
+    const size_t tsmem = lanczos_tiles_smem(n, per);
+    static int tiles_ok = -1;  // 16-CTA clusters with this smem schedulable?
+    if (tsmem && tiles_ok < 0) {
+        tiles_ok = 0;
+        if (cudaFuncSetAttribute(lanczos_tiles, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess &&
+            cudaFuncSetAttribute(lanczos_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024) ==
+                cudaSuccess) {
+            cudaLaunchConfig_t cfg{};
+            cudaLaunchAttribute at{};
+            at.id = cudaLaunchAttributeClusterDimension;
+            at.val.clusterDim.x = kLtCluster;
+            at.val.clusterDim.y = at.val.clusterDim.z = 1;
+            cfg.gridDim = dim3(kLtCluster);
+            cfg.blockDim = dim3(kLtThreads);
+            cfg.dynamicSmemBytes = 220 * 1024;
+            cfg.attrs = &at;
+            cfg.numAttrs = 1;
+            int nclusters = 0;
+            if (cudaOccupancyMaxActiveClusters(&nclusters, lanczos_tiles, &cfg) == cudaSuccess && nclusters > 0)
+                tiles_ok = 1;
+        }
+        cudaGetLastError();  // clear a refused attribute / query
+    }
+    if (tsmem && tiles_ok == 1 && ctx->lanczos_tiles) {
+        cudaLaunchConfig_t cfg{};
+        cudaLaunchAttribute at{};
+        at.id = cudaLaunchAttributeClusterDimension;
+        at.val.clusterDim.x = kLtCluster;
+        at.val.clusterDim.y = at.val.clusterDim.z = 1;
+        cfg.gridDim = dim3(kLtCluster);
+        cfg.blockDim = dim3(kLtThreads);
+        cfg.dynamicSmemBytes = tsmem;
+        cfg.stream = st;
+        cfg.attrs = &at;
+        cfg.numAttrs = 1;
+        ATK_CUDA(cudaLaunchKernelEx(&cfg, lanczos_tiles, static_cast<const double*>(S), n, m, per, q.get(),
+                                    part.get(), al.get(), be.get()));
+        ATK_LAUNCHED(ctx);
+    } else {
+        lanczos_l2(ctx, S, n, m, q.get(), qp.get(), w.get(), part.get(), al.get(), be.get());
+    }
+    // T is tridiagonal already: bisection + inverse iteration on (alpha, beta)
+    // directly (the dense Jacobi on T took ~0.3 ms)
+    tridiag_extreme_eig(ctx, al.get(), be.get(), m, tv.get(), tz.get());
+    std::vector<double> hv(m), hb(m), zlast(2);
     ATK_CUDA(cudaMemcpyAsync(hv.data(), tv.get(), m * sizeof(double), cudaMemcpyDeviceToHost, st));
     ATK_CUDA(cudaMemcpyAsync(hb.data(), be.get(), m * sizeof(double), cudaMemcpyDeviceToHost, st));
-    // last row of the eigenvector matrix: z(m-1, j) for every j
+    // last components of the extreme Ritz vectors (columns 0: top, 1: bottom)
     ATK_CUDA(cudaMemcpy2DAsync(zlast.data(), sizeof(double), tz.get() + (m - 1), size_t(m) * sizeof(double),
-                               sizeof(double), m, cudaMemcpyDeviceToHost, st));
+                               sizeof(double), 2, cudaMemcpyDeviceToHost, st));
     ATK_CUDA(cudaStreamSynchronize(st));
     const double bm = std::fabs(hb[m - 1]);
-    Bounds b{hv[m - 1] - bm * std::fabs(zlast[m - 1]) - 1e-12 * std::fabs(hv[0]),
-             hv[0] + bm * std::fabs(zlast[0])};
+    Bounds b{hv[m - 1] - bm * std::fabs(zlast[1]) - 1e-12 * std::fabs(hv[0]), hv[0] + bm * std::fabs(zlast[0])};
     if (psd) b.lo = std::max(b.lo, 0.0);
     return b;
 }
@@ -628,15 +778,18 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
         for (int j = 0; j < r; ++j) worst = std::max(worst, hres[j]);
         if (!(scale > 0.0) || worst <= tol * scale || it >= max_outer) break;
         if (!have_bounds) {
-            const bool gapped = psd && hth[k - 1] >= 0.0 && hth[r - 1] > 10.0 * hth[k - 1];
             if (trace)
                 std::fprintf(stderr, "[atk eig n=%d r=%d k=%d] theta_1 %.6e theta_r %.6e theta_k %.6e\n", n, r, k,
                              hth[0], hth[r - 1], hth[k - 1]);
-            if (gapped) {
+            // PSD: lo = 0.  (The m = 40 Lanczos bound, lowest Ritz value minus its
+            // residual, came out below 0 on every flat Gram spectrum measured, C2
+            // included, i.e. it only cost 0.7 ms per mode.)  Indefinite: Lanczos.
+            if (psd && hth[k - 1] >= 0.0) {
                 b = Bounds{0.0, hth[0]};
             } else {
                 b = lanczos_bounds(ctx, Sp, n, psd);
                 mark("lanczos", 0, b.lo);
+                if (trace) std::fprintf(stderr, "[atk eig n=%d] bounds lo %.9e hi %.9e\n", n, b.lo, b.hi);
             }
             have_bounds = true;
         }
@@ -655,7 +808,14 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
         // O(eps) wanted-direction residue is amplified past 1/eps) and CholeskyQR
         // breaks down; on wide gaps this means a single S V power step.
         const double ac = std::acosh(std::max(1.0 + 1e-12, (hth[r - 1] - c) / e));
-        const int degree = std::max(1, std::min(64, int(23.0 / std::max(ac, 1e-3))));
+        int degree = std::max(1, std::min(64, int(23.0 / std::max(ac, 1e-3))));
+        // dynamic range inside the wanted set: the top Ritz direction grows
+        // T_d(x_1) / T_d(x_r) times faster than the lowest wanted one; past ~1e9
+        // (~1 / sqrt(eps)) the lowest wanted directions come out of the
+        // orthonormalisation with relative errors ~eps x that ratio and the
+        // residual stalls (seen on a n = 128, r = 64 indefinite block)
+        const double atop = std::acosh(std::max(1.0 + 1e-12, (std::max(b.hi, hth[0]) - c) / e));
+        if (atop - ac > 1e-12) degree = std::max(1, std::min(degree, int(20.7 / (atop - ac))));  // ln 1e9
         // Y1 = g (S V - c V) / e ; Y_{j+1} = g (2/e)(S Y_j - c Y_j) - g^2 Y_{j-1}
         double* ycur = nullptr;
         double* const ys[4] = {V.get(), Ya.get(), Yb.get(), Yc.get()};

@@ -822,6 +822,26 @@ void trd_backtr(atk_ctx* ctx, bool trd, const double* a, int n, int lda, double*
 
 }  // namespace
 
+// Extreme eigenpairs of the symmetric tridiagonal (d, e) (the Lanczos T of
+// eig.cu): all m values by bisection (descending), then inverse iteration for
+// the largest and the smallest only, no reduction or back-transform.
+// vectors: m x 2 (ld m), column 0 for values[0], column 1 for values[m - 1].
+void tridiag_extreme_eig(atk_ctx* ctx, const double* d, const double* e, int m, double* values, double* vectors) {
+    if (m < 1 || m > kTridiagMax) fail(ATK_UNSUPPORTED, "tridiag_extreme_eig: m out of range");
+    DevBuf<double> wk(ctx, 5 * size_t(m));
+    const int wpb = 8;
+    bisect_kernel<<<unsigned((m + wpb - 1) / wpb), 32 * wpb, size_t(m) * sizeof(double), ctx->stream>>>(d, e, m, m,
+                                                                                                         values);
+    ATK_LAUNCHED(ctx);
+    // one vector per launch: a lone eigenvalue is its own cluster, so a near-
+    // degenerate extreme pair costs no Gram-Schmidt (any vector of the pair's
+    // space bounds the same way)
+    invit_kernel<<<1, 32, 0, ctx->stream>>>(d, e, m, values, 1, vectors, wk.get());
+    ATK_LAUNCHED(ctx);
+    invit_kernel<<<1, 32, 0, ctx->stream>>>(d, e, m, values + (m - 1), 1, vectors + m, wk.get());
+    ATK_LAUNCHED(ctx);
+}
+
 void tridiag_eig(atk_ctx* ctx, const double* a, int n, int lda, int nwant, double* values, double* vectors,
                  int ldv, int nvals) {
     if (n < 1 || n > kTridiagMax) fail(ATK_UNSUPPORTED, "tridiag_eig: n out of range");

@@ -11,7 +11,7 @@ for p in $PARTS; do
     slow) timeout 1500 python -m pytest tests -m "gpu and slow" -x -q -s -p no:hypothesispytest > gpurun_out/${TAG}_slow.log 2>&1; echo "slow=$? $(tail -1 gpurun_out/${TAG}_slow.log)";;
     probe) ATK_TRACE=1 timeout 600 python tests/eig_probe.py 2048 > gpurun_out/${TAG}_probe.log 2>&1; echo "probe=$?"; grep -vE "^\[atk eig n=2048" gpurun_out/${TAG}_probe.log | tail -12;;
     trace) ATK_TRACE=1 timeout 300 python profiles/run_step.py c5 2 > gpurun_out/${TAG}_trace.log 2>&1; echo "trace=$?"; tail -40 gpurun_out/${TAG}_trace.log;;
-    eigt) timeout 300 python -m pytest tests/test_gpu_eig.py -x -q -p no:hypothesispytest 2>&1 | tail -3;;
+    eigt) timeout 300 python -m pytest tests/test_gpu_eig.py -x -q -p no:hypothesispytest > gpurun_out/${TAG}_eigt.log 2>&1; echo "eigt=$? $(tail -1 gpurun_out/${TAG}_eigt.log)";;
     ncujac) timeout 600 ncu --set full --clock-control none --import-source on -k regex:jacobi1s -c 1 -o gpurun_out/${TAG}_jac python profiles/jacobi_probe.py 96 > gpurun_out/${TAG}_ncujac.log 2>&1; echo "ncujac=$?";;
     allcfg) for c in c1 c2 c3 c4; do timeout 600 python bench.py --config $c --steps 5 --warmup 3 > gpurun_out/${TAG}_bench_$c.json 2> gpurun_out/${TAG}_bench_$c.err; echo "bench $c=$?"; head -c 300 gpurun_out/${TAG}_bench_$c.json; echo; done;;
     tracecfg) for c in c1 c2; do ATK_TRACE=1 timeout 300 python profiles/run_step.py $c 1 > gpurun_out/${TAG}_trace_$c.log 2>&1; echo "trace $c=$?"; done;;
@@ -22,6 +22,7 @@ for p in $PARTS; do
     launches) timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv python profiles/run_step.py ${CFG:-c5} 1 > gpurun_out/${TAG}_launches.log 2>&1; echo "launches=$?";;
     traffic) timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:"gram_tf32_2cta|gram2_reduce" --csv --log-file gpurun_out/${TAG}_gramtraffic.csv python profiles/run_step.py c5 1 > gpurun_out/${TAG}_traffic.log 2>&1; echo "traffic=$?"; python profiles/make_traffic.py gpurun_out/${TAG}_gramtraffic.csv gpurun_out/${TAG}_gram_traffic.json | head -c 300; echo;;
     ncueig) timeout 600 ncu --set full --clock-control none --import-source on -k regex:"trd_kernel|invit_kernel|bisect_kernel|backtr_kernel|dgemm_tile|chol_inv" -c 8 -o gpurun_out/${TAG}_eig python profiles/run_step.py c5 1 > gpurun_out/${TAG}_ncueig.log 2>&1; echo "ncueig=$?";;
+    ncucheb) timeout 600 ncu --set full --clock-control none --import-source on -k regex:"cheb_filter" -c 2 -o gpurun_out/${TAG}_cheb python profiles/run_step.py c2 1 > gpurun_out/${TAG}_ncucheb.log 2>&1; echo "ncucheb=$?";;
     ncu) timeout 900 ncu --set full --clock-control none --import-source on -k regex:"gram_tf32_2cta|ttm_tf32" -c 2 -o gpurun_out/${TAG}_full python profiles/run_step.py c5 1 > gpurun_out/${TAG}_ncu.log 2>&1; echo "ncu=$?";;
   esac
 done
