@@ -441,7 +441,11 @@ bool cheb_resident_launch(atk_ctx* ctx, ChebResArgs p, int strips, size_t smem, 
     cfg.dynamicSmemBytes = smem;
     cfg.stream = ctx->stream;
     cfg.attrs = at;
-    cfg.numAttrs = 2;
+    // ncu cannot replay a cooperative cluster launch (LaunchFailed): under the
+    // profiler, ATK_PROFILE_NONCOOP=1 drops the cooperative attribute (the
+    // grid is still sized to co-resident clusters, and ncu serialises kernels)
+    static const bool noncoop = std::getenv("ATK_PROFILE_NONCOOP") != nullptr;
+    cfg.numAttrs = noncoop ? 1 : 2;
     if (const cudaError_t err = cudaLaunchKernelEx(&cfg, cheb_resident_kernel<FM, FN>, p); err != cudaSuccess) {
         cudaGetLastError();  // e.g. cooperative + cluster refused: the split-K kernel instead
         if (std::getenv("ATK_TRACE")) std::fprintf(stderr, "[atk cheb_resident] launch: %s\n", cudaGetErrorString(err));

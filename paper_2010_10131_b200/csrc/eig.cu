@@ -654,20 +654,27 @@ Bounds lanczos_bounds(atk_ctx* ctx, const double* S, int n, bool psd) {
 }
 
 // Rayleigh-Ritz on the orthonormal block V (n x k): W = S V, T = V^T W,
-// theta = all k Ritz values (descending), Z = the top r Ritz vectors of T;
-// Vr = V Z, Wr = W Z (n x r).  V itself stays unrotated: the next Chebyshev
-// filter only needs a basis of span(V), so the k - r guard-band vectors are
-// never formed (their values still set the filter's cut).
-void rayleigh_ritz(atk_ctx* ctx, const double* S, int n, int k, int r, const double* V, double* W, double* T,
-                   double* Z, double* theta, double* Vr, double* Wr, int* sweeps, bool psd) {
+// theta = all k Ritz values (descending), Z = the top nv Ritz vectors of T
+// (nv = r, or k when converged pairs are being locked);
+// Vk = V Z (n x nv), Wr = W Z (n x r, for the residuals).
+void rayleigh_ritz(atk_ctx* ctx, const double* S, int n, int k, int r, int nv, const double* V, double* W,
+                   double* T, double* Z, double* theta, double* Vk, double* Wr, int* sweeps, bool psd) {
     dgemm(ctx, false, false, n, k, n, 1.0, S, n, V, n, 0.0, W, n);
     dgemm(ctx, true, false, k, k, n, 1.0, V, n, W, n, 0.0, T, k);
     if (ctx->eig_method == 0)
         jacobi_eig(ctx, T, k, k, theta, Z, k, sweeps, psd);  // V^T S V is PSD when S is; all k vectors
     else
-        tridiag_eig(ctx, T, k, k, r, theta, Z, k, k);
-    dgemm(ctx, false, false, n, r, k, 1.0, V, n, Z, k, 0.0, Vr, n);
+        tridiag_eig(ctx, T, k, k, nv, theta, Z, k, k);
+    dgemm(ctx, false, false, n, nv, k, 1.0, V, n, Z, k, 0.0, Vk, n);
     dgemm(ctx, false, false, n, r, k, 1.0, W, n, Z, k, 0.0, Wr, n);
+}
+
+// M(:, j) = (theta_j - sigma) L(:, j), j < nc: the deflation term of S - L diag(theta - sigma) L^T
+__global__ void scale_cols_shift(const double* __restrict__ l, const double* __restrict__ theta, double sigma,
+                                 int n, int nc, double* __restrict__ m) {
+    const size_t tot = size_t(n) * nc;
+    for (size_t e = size_t(blockIdx.x) * blockDim.x + threadIdx.x; e < tot; e += size_t(gridDim.x) * blockDim.x)
+        m[e] = (theta[e / n] - sigma) * l[e];
 }
 
 }  // namespace
@@ -720,7 +727,8 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
     // an exactly symmetric input (the engine's Grams are mirrored) is used in
     // place; anything else is copied and symmetrised first (linalg.hpp:104)
     DevBuf<double> Sbuf(ctx, exact_sym ? 0 : nn), V(ctx, nk), W(ctx, nk), Ya(ctx, nk), Yb(ctx, nk), Yc(ctx, nk), T(ctx, kk), Z(ctx, kk),
-        theta(ctx, k), res(ctx, k), Vr(ctx, nr), Wr(ctx, nr);
+        theta(ctx, k), res(ctx, k), Vr(ctx, nk), Wr(ctx, nr);
+    DevBuf<double> Sd(ctx, 0), Dm(ctx, 0);  // deflated copy of S, deflation term (allocated on first lock)
     Ws ws{DevBuf<double>(ctx, kk), DevBuf<double>(ctx, kk), DevBuf<double>(ctx, k), DevBuf<double>(ctx, k),
           DevBuf<double>(ctx, kk), DevBuf<double>(ctx, nk), DevBuf<int>(ctx, 1), DevBuf<int>(ctx, 3)};
     DevBuf<int> sweeps(ctx, 1);
@@ -753,7 +761,9 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
     dgemm(ctx, false, false, n, k, n, 1.0, Sp, n, Ya.get(), n, 0.0, Yb.get(), n);
     orthonormalize(ctx, Yb.get(), n, k, V.get(), ws);
     mark("qr0");
-    rayleigh_ritz(ctx, Sp, n, k, r, V.get(), W.get(), T.get(), Z.get(), theta.get(), Vr.get(), Wr.get(),
+    // all k Ritz vectors when locking is on: the active (unlocked) block is Vk(:, nc:k)
+    const int nv = ctx->chfsi_lock ? k : r;
+    rayleigh_ritz(ctx, Sp, n, k, r, nv, V.get(), W.get(), T.get(), Z.get(), theta.get(), Vr.get(), Wr.get(),
                   sweeps.get(), psd);
     mark("rr0", trace_sweeps(sweeps.get()));
 
@@ -793,12 +803,22 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
             }
             have_bounds = true;
         }
+        // locking: the leading nc Ritz pairs that already meet tol are kept as
+        // they are, and the filter runs on the k - nc others with S deflated,
+        // S' = S - L diag(theta_L - c) L^T, which moves the locked eigenvalues
+        // to the centre of the damped interval.  Without it a dominant top
+        // eigenvalue (a non-centred Gram's mean direction, 1e3 x the rest)
+        // forces the dynamic-range cap below down to degree 2.
+        int nc = 0;
+        if (ctx->chfsi_lock)
+            while (nc < r - 1 && hres[nc] <= tol * scale) ++nc;
         // Chebyshev filter on the unwanted interval [lo, cut]
         const double cut = hth[k - 1];
         const double lo = std::min(b.lo, cut - 1e-12 * scale);
         double e = 0.5 * (cut - lo), c = 0.5 * (cut + lo);
         if (!(e > 0.0)) e = 1e-12 * scale;
-        const double smax = std::max(1.0, (std::max(b.hi, hth[0]) - c) / e);
+        const double top = nc > 0 ? hth[nc] : std::max(b.hi, hth[0]);  // top of the filtered spectrum
+        const double smax = std::max(1.0, (top - c) / e);
         const double g = 1.0 / (2.0 * smax + 1.0);  // per-step rescale, keeps the recurrence linear
         // degree: damp [lo, cut] relative to the wanted end by at most ~1e10 per
         // pass (T_d(x) ~ e^{d acosh x} / 2), 1..64: on flat spectra a pass costs
@@ -814,38 +834,67 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
         // (~1 / sqrt(eps)) the lowest wanted directions come out of the
         // orthonormalisation with relative errors ~eps x that ratio and the
         // residual stalls (seen on a n = 128, r = 64 indefinite block)
-        const double atop = std::acosh(std::max(1.0 + 1e-12, (std::max(b.hi, hth[0]) - c) / e));
+        const double atop = std::acosh(std::max(1.0 + 1e-12, (top - c) / e));
         if (atop - ac > 1e-12) degree = std::max(1, std::min(degree, int(20.7 / (atop - ac))));  // ln 1e9
         // Y1 = g (S V - c V) / e ; Y_{j+1} = g (2/e)(S Y_j - c Y_j) - g^2 Y_{j-1}
+        const double* Sf = Sp;      // the filter's matrix
+        double* X = V.get();        // the filtered block (n x ka)
+        int ka = k;
+        if (nc > 0) {
+            if (!Sd.get()) {
+                Sd = DevBuf<double>(ctx, nn);
+                Dm = DevBuf<double>(ctx, nr);
+            }
+            ATK_CUDA(cudaMemcpyAsync(Sd.get(), Sp, nn * sizeof(double), cudaMemcpyDeviceToDevice, st));
+            scale_cols_shift<<<nblk(size_t(n) * nc), 256, 0, st>>>(Vr.get(), theta.get(), c, n, nc, Dm.get());
+            ATK_LAUNCHED(ctx);
+            dgemm(ctx, false, true, n, n, nc, -1.0, Dm.get(), n, Vr.get(), n, 1.0, Sd.get(), n);
+            Sf = Sd.get();
+            X = Vr.get() + size_t(n) * nc;  // Ritz vectors nc..k-1
+            ka = k - nc;
+        }
+        const size_t nka = size_t(n) * ka;
         double* ycur = nullptr;
-        double* const ys[4] = {V.get(), Ya.get(), Yb.get(), Yc.get()};
+        double* const ys[4] = {X, Ya.get(), Yb.get(), Yc.get()};
         const int fused = ctx->cheb_fused
-                              ? cheb_filter(ctx, Sp, n, k, degree, ys, g / e, -g * c / e, 2.0 * g / e,
+                              ? cheb_filter(ctx, Sf, n, ka, degree, ys, g / e, -g * c / e, 2.0 * g / e,
                                             -2.0 * g * c / e, -g * g)
                               : -1;
         if (fused >= 0) {
             ycur = ys[fused];
         } else {  // per-step launches (option cheb_fused = 0, or no co-resident grid)
-            double* yprev = V.get();
+            double* yprev = X;
             ycur = Ya.get();
             double* ynext = Yb.get();
-            cheb_combine<<<nblk(nk), 256, 0, st>>>(ycur, V.get(), nullptr, nk, -g * c / e, 0.0);
+            cheb_combine<<<nblk(nka), 256, 0, st>>>(ycur, X, nullptr, nka, -g * c / e, 0.0);
             ATK_LAUNCHED(ctx);
-            dgemm(ctx, false, false, n, k, n, g / e, Sp, n, V.get(), n, 1.0, ycur, n);
+            dgemm(ctx, false, false, n, ka, n, g / e, Sf, n, X, n, 1.0, ycur, n);
             for (int j = 1; j < degree; ++j) {
-                cheb_combine<<<nblk(nk), 256, 0, st>>>(ynext, ycur, yprev, nk, -2.0 * g * c / e, -g * g);
+                cheb_combine<<<nblk(nka), 256, 0, st>>>(ynext, ycur, yprev, nka, -2.0 * g * c / e, -g * g);
                 ATK_LAUNCHED(ctx);
-                dgemm(ctx, false, false, n, k, n, 2.0 * g / e, Sp, n, ycur, n, 1.0, ynext, n);
-                double* spare = (yprev == V.get()) ? Yc.get() : yprev;
+                dgemm(ctx, false, false, n, ka, n, 2.0 * g / e, Sf, n, ycur, n, 1.0, ynext, n);
+                double* spare = (yprev == X) ? Yc.get() : yprev;
                 yprev = ycur;
                 ycur = ynext;
                 ynext = spare;
             }
         }
         mark("filter", degree, worst / scale);
-        orthonormalize(ctx, ycur, n, k, V.get(), ws);
-        mark("qr");
-        rayleigh_ritz(ctx, Sp, n, k, r, V.get(), W.get(), T.get(), Z.get(), theta.get(), Vr.get(), Wr.get(),
+        if (nc > 0) {
+            // V = [L, orth((I - L L^T) Y)]: project the locked directions out twice
+            double* P = ws.M.get();  // nc x ka <= k x k
+            for (int pass = 0; pass < 2; ++pass) {
+                dgemm(ctx, true, false, nc, ka, n, 1.0, Vr.get(), n, ycur, n, 0.0, P, nc);
+                dgemm(ctx, false, false, n, ka, nc, -1.0, Vr.get(), n, P, nc, 1.0, ycur, n);
+            }
+            orthonormalize(ctx, ycur, n, ka, V.get() + size_t(n) * nc, ws);
+            ATK_CUDA(cudaMemcpyAsync(V.get(), Vr.get(), size_t(n) * nc * sizeof(double), cudaMemcpyDeviceToDevice,
+                                     st));
+        } else {
+            orthonormalize(ctx, ycur, n, k, V.get(), ws);
+        }
+        mark("qr", nc);
+        rayleigh_ritz(ctx, Sp, n, k, r, nv, V.get(), W.get(), T.get(), Z.get(), theta.get(), Vr.get(), Wr.get(),
                       sweeps.get(), psd);
         mark("rr", trace_sweeps(sweeps.get()));
     }

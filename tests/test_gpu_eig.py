@@ -117,3 +117,47 @@ def test_chfsi(ectx, kind, fused):
     res = atucker.sym_eig_top_r(s, r, ctx=ectx)
     ectx.set_option("cheb_fused", 1)
     _check(s, r, res, vec_tol=1e-8 if kind == "gapped" else 1e-5)
+
+
+@pytest.mark.parametrize("fused", [1, 2, 0], ids=["cheb-resident", "cheb-splitk", "cheb-steps"])
+def test_chfsi_dominant_top(fused):
+    """Gram of non-centred data: the mean direction's eigenvalue is ~1e3 x the
+    rest.  Converged top pairs are locked and the filter runs on a deflated S
+    (eig.cu); without locking the wanted-set dynamic-range cap would hold the
+    filter at degree ~2 for ~100 passes.  Also compares the three Chebyshev
+    filter implementations (resident-S clusters, split-K cooperative, per-step)."""
+    from paper_2010_10131_b200 import atucker
+
+    ctx = atucker.Context.default(0)
+    ctx.set_option("eig_assume_psd", 1.0)
+    ctx.set_option("cheb_fused", fused)
+    try:
+        n, r = 512, 24
+        rng = np.random.default_rng(9)
+        a = rng.random((n, 3 * n))
+        s = a @ a.T
+        _check(s, r, atucker.sym_eig_top_r(s, r, ctx=ctx), vec_tol=1e-6)
+    finally:
+        ctx.set_option("cheb_fused", 1)
+        ctx.set_option("eig_assume_psd", 0.0)
+
+
+@pytest.mark.parametrize("tiles", [1, 0], ids=["lanczos-tiles", "lanczos-l2"])
+def test_chfsi_indefinite_lanczos(tiles):
+    """Indefinite input above the tridiagonal limit: the filter's lower bound
+    comes from the Lanczos run, with S resident in a 16-CTA cluster or
+    re-read from L2; both must converge to LAPACK's values."""
+    from paper_2010_10131_b200 import atucker
+
+    ctx = atucker.Context.default(0)
+    ctx.set_option("lanczos_tiles", tiles)
+    try:
+        n, r = 400, 20
+        rng = np.random.default_rng(11)
+        q = np.linalg.qr(rng.standard_normal((n, n)))[0]
+        lam = np.concatenate([np.linspace(10.0, 6.0, r), rng.uniform(-4.0, 5.0, n - r)])
+        s = (q * lam) @ q.T
+        s = (s + s.T) / 2
+        _check(s, r, atucker.sym_eig_top_r(s, r, ctx=ctx), vec_tol=1e-6)
+    finally:
+        ctx.set_option("lanczos_tiles", 1)
