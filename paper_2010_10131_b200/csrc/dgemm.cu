@@ -152,6 +152,29 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks) {
     __syncthreads();
 }
 
+// Grid barrier with release/acquire atomics instead of full fences: the
+// arrival is atom.add.acq_rel (publishes this CTA's writes, ordered before it
+// by bar.sync; the last arriver also acquires everyone else's), waiters poll
+// the generation word with ld.acquire and no back-off.
+__device__ __forceinline__ void grid_barrier_ra(unsigned* bar, unsigned nblocks) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned g, old;
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(bar + 1) : "memory");
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(bar) : "memory");
+        if (old == nblocks - 1) {
+            asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(bar) : "memory");
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar + 1) : "memory");
+        } else {
+            unsigned cur;
+            do {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(bar + 1) : "memory");
+            } while (cur == g);
+        }
+    }
+    __syncthreads();
+}
+
 __global__ void __launch_bounds__(NT) cheb_filter_kernel(const ChebArgs p) {
     extern __shared__ __align__(16) double dsm[];
     const int ntile = p.gm * p.gn;
@@ -213,7 +236,8 @@ __global__ void __launch_bounds__(NT) cheb_filter_kernel(const ChebArgs p) {
 // recurrence and stores Y_{j+1}), and ONE grid barrier publishes Y_{j+1}.
 // cheb_filter_kernel re-streams all of S from L2 every step and pays two grid
 // barriers per step.
-constexpr int RS_CS = 8;  // CTAs per cluster (= K splits)
+constexpr int RS_CS = 8;   // CTAs per cluster (= K splits)
+constexpr int RS_EPT = 4;  // output elements per thread in the cluster reduction
 
 struct ChebResArgs {
     const double* S;
@@ -293,36 +317,57 @@ __global__ void __launch_bounds__(512) cheb_resident_kernel(const ChebResArgs p)
 #pragma unroll
                 for (int t = 0; t < 2; ++t)
                     P[((wn * FN + j) * 8 + 2 * fk + t) * rows + (wm * FM + i) * 8 + fr] = acc[i][j][t];
-        // every CTA of the cluster has its partial in smem
-        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
         const double ca = step == 0 ? p.a1 : p.a, cb = step == 0 ? p.b1 : p.b, ccoef = step == 0 ? 0.0 : p.c;
         const double* yprev = p.y[iprev];
         double* ynext = p.y[inext];
         const uint32_t pbase = static_cast<uint32_t>(__cvta_generic_to_shared(P));
-        for (int e = tid; e < mr * k; e += nt) {
-            const int m = int(rank) * mr + e % mr, cc = e / mr;
-            const int gm = m0 + m;
-            double v[RS_CS];
+        // this thread's (up to RS_EPT) output elements; their Y_j / Y_{j-1}
+        // terms are loaded before the cluster barrier so the L2 latency hides
+        // behind it
+        double base[RS_EPT];
+        int off[RS_EPT];  // P offset (cc * rows + m), or -1
 #pragma unroll
-            for (int z = 0; z < RS_CS; ++z) {
-                uint32_t ra;
-                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
-                             : "=r"(ra)
-                             : "r"(pbase + uint32_t(cc * rows + m) * 8u), "r"(uint32_t(z)));
-                asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v[z]) : "r"(ra) : "memory");
-            }
-            double sum = 0.0;
-#pragma unroll
-            for (int z = 0; z < RS_CS; ++z) sum += v[z];  // split order: deterministic
-            if (gm < n) {
-                const size_t g = gm + size_t(n) * cc;
-                double r = fma(ca, sum, cb * __ldcg(ycur + g));
-                if (ccoef != 0.0) r = fma(ccoef, __ldcg(yprev + g), r);
-                ynext[g] = r;
+        for (int u = 0; u < RS_EPT; ++u) {
+            const int e = tid + u * nt;
+            off[u] = -1;
+            base[u] = 0.0;
+            if (e < mr * k) {
+                const int m = int(rank) * mr + e % mr, cc = e / mr;
+                if (m0 + m < n) {
+                    const size_t g = (m0 + m) + size_t(n) * cc;
+                    off[u] = cc * rows + m;
+                    base[u] = cb * __ldcg(ycur + g);
+                    if (ccoef != 0.0) base[u] = fma(ccoef, __ldcg(yprev + g), base[u]);
+                }
             }
         }
+        // every CTA of the cluster has its partial in smem
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+        double v[RS_EPT][RS_CS];
+#pragma unroll
+        for (int u = 0; u < RS_EPT; ++u)
+#pragma unroll
+            for (int z = 0; z < RS_CS; ++z) {
+                v[u][z] = 0.0;
+                if (off[u] >= 0) {
+                    uint32_t ra;
+                    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+                                 : "=r"(ra)
+                                 : "r"(pbase + uint32_t(off[u]) * 8u), "r"(uint32_t(z)));
+                    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v[u][z]) : "r"(ra) : "memory");
+                }
+            }
+#pragma unroll
+        for (int u = 0; u < RS_EPT; ++u) {
+            if (off[u] < 0) continue;
+            double sum = 0.0;
+#pragma unroll
+            for (int z = 0; z < RS_CS; ++z) sum += v[u][z];  // split order: deterministic
+            const int m = off[u] % rows, cc = off[u] / rows;
+            ynext[(m0 + m) + size_t(n) * cc] = fma(ca, sum, base[u]);
+        }
         // Y_{j+1} complete everywhere (also frees P and Bt for the next step)
-        grid_barrier(p.bar, gridDim.x);
+        grid_barrier_ra(p.bar, gridDim.x);
         if (step == 0) {
             iprev = 0; icur = 1; inext = 2;
         } else {
@@ -470,6 +515,7 @@ bool cheb_resident(atk_ctx* ctx, const double* S, int n, int k, int deg, double*
     const int wn = nf / fn, warps = wm * wn;
     const int rows = 8 * mf, strips = (n + rows - 1) / rows;
     if (warps > 16 || strips > max_clusters || rows % RS_CS) return false;
+    if ((rows / RS_CS) * k > RS_EPT * 32 * warps) return false;  // reduction: <= RS_EPT elements per thread
     const int kc = ((n + RS_CS - 1) / RS_CS + 3) / 4 * 4;  // K slice per CTA, a multiple of 4
     const int ldk = kc + 4 + (16 - (kc + 4) % 16 + 4) % 16;   // = 4 (mod 16)
     const size_t smem = (size_t(rows) * ldk + size_t(8 * nf) * ldk + size_t(8 * nf) * rows) * sizeof(double);

@@ -724,6 +724,125 @@ size_t trd_tile_smem(int nt) {
     return (size_t(ntiles) * kTileDbl + size_t(ntiles) * 64 + 64 * size_t(nt) + 2) * sizeof(double);
 }
 
+// n <= 32 NW: the same reduction (dsytd2 conventions, same outputs as
+// trd_kernel / trd_tile_kernel) by NW warps, lane-owned rows of the FULL
+// symmetric matrix in shared memory (column-major, odd ld: conflict-free).
+// Warp w owns rows 32 w + lane in the matvec and the rank-2 update, so the
+// only cross-warp traffic is two scalar sums per step.  For the Rayleigh-Ritz
+// blocks of ChFSI (k = 48) and the small modes (n = 48) the tile kernel's
+// 256-thread barriers were the whole cost (~107 us at n = 48).
+template <int NW>
+__global__ void __launch_bounds__(NW * 32, 1)
+    trd_small_kernel(const double* __restrict__ a, int n, int lda, double* __restrict__ hh, double* __restrict__ d,
+                     double* __restrict__ e, double* __restrict__ tau_out, double* __restrict__ scal_out) {
+    constexpr int NR = 32 * NW, LD = NR + 1;
+    extern __shared__ double sm[];
+    double* A = sm;              // NR x LD
+    double* vs = A + NR * LD;    // NR: reflector
+    double* ws = vs + NR;        // NR: w = p - K v
+    double* red = ws + NR;       // 2 x NW cross-warp partials
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int i = w * 32 + lane;  // the row this thread owns
+    for (int j = 0; j < n; ++j)
+        A[i + LD * j] = i < n ? 0.5 * (a[i + size_t(lda) * j] + a[j + size_t(lda) * i]) : 0.0;
+    vs[i] = 0.0;
+    ws[i] = 0.0;
+    __syncthreads();
+    auto sum_all = [&](double x, int slot) {  // fixed order across warps
+        x = warp_sum(x);
+        if (NW == 1) return x;
+        if (lane == 0) red[slot * NW + w] = x;
+        __syncthreads();
+        double t = 0.0;
+#pragma unroll
+        for (int q = 0; q < NW; ++q) t += red[slot * NW + q];
+        return t;
+    };
+    for (int k = 0; k + 2 < n; ++k) {
+        // reflector k from column k, rows k+1..n-1 (dlarfg)
+        const double x = (i >= k + 2 && i < n) ? A[i + LD * k] : 0.0;
+        const double xn = sum_all(x * x, 0);
+        const double alpha = A[(k + 1) + LD * k];
+        double tau = 0.0, scal = 0.0, beta = alpha;
+        if (xn > 0.0) {
+            beta = -copysign(sqrt(fma(alpha, alpha, xn)), alpha);
+            scal = 1.0 / (alpha - beta);
+            tau = (beta - alpha) / beta;
+        }
+        const double vi = (i == k + 1) ? 1.0 : x * scal;
+        vs[i] = vi;
+        if (threadIdx.x == 0) {
+            d[k] = A[k + LD * k];
+            e[k] = beta;
+            tau_out[k] = tau;
+            scal_out[k] = scal;
+        }
+        __syncthreads();
+        if (tau == 0.0) continue;  // uniform: H_k = I
+        // p = tau A22 v (row i), four independent chains
+        double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
+        int j = k + 1;
+#pragma unroll 2
+        for (; j + 3 < n; j += 4) {
+            p0 = fma(A[i + LD * j], vs[j], p0);
+            p1 = fma(A[i + LD * (j + 1)], vs[j + 1], p1);
+            p2 = fma(A[i + LD * (j + 2)], vs[j + 2], p2);
+            p3 = fma(A[i + LD * (j + 3)], vs[j + 3], p3);
+        }
+        for (; j < n; ++j) p0 = fma(A[i + LD * j], vs[j], p0);
+        const double pi = (i > k && i < n) ? tau * ((p0 + p1) + (p2 + p3)) : 0.0;
+        const double K = 0.5 * tau * sum_all(pi * vi, 1);
+        const double wi = fma(-K, vi, pi);
+        ws[i] = wi;
+        __syncthreads();
+        if (i > k && i < n) {
+            // four columns per pass, loads first (a rolled loop is one shared-
+            // memory round trip per element)
+            for (j = k + 1; j + 3 < n; j += 4) {
+                double av[4], wv[4], vv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    av[u] = A[i + LD * (j + u)];
+                    wv[u] = ws[j + u];
+                    vv[u] = vs[j + u];
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) A[i + LD * (j + u)] = fma(-vi, wv[u], fma(-wi, vv[u], av[u]));
+            }
+            for (; j < n; ++j) A[i + LD * j] = fma(-vi, ws[j], fma(-wi, vs[j], A[i + LD * j]));
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        if (n >= 2) {
+            d[n - 2] = A[(n - 2) + LD * (n - 2)];
+            e[n - 2] = A[(n - 1) + LD * (n - 2)];
+            tau_out[n - 2] = 0.0;
+            scal_out[n - 2] = 0.0;
+        }
+        d[n - 1] = A[(n - 1) + LD * (n - 1)];
+        tau_out[n - 1] = 0.0;
+        scal_out[n - 1] = 0.0;
+    }
+    // packed lower triangle (column k below the diagonal: the raw reflector k)
+    for (int jj = 0; jj < n; ++jj)
+        if (i >= jj && i < n) hh[pk(i, jj, n)] = A[i + LD * jj];
+}
+
+template <int NW>
+void launch_trd_small(atk_ctx* ctx, const double* a, int n, int lda, double* hh, double* d, double* e, double* tau,
+                      double* scal) {
+    constexpr int NR = 32 * NW;
+    const size_t smem = (size_t(NR) * (NR + 1) + 2 * NR + 2 * NW) * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+        ATK_CUDA(cudaFuncSetAttribute(trd_small_kernel<NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        attr = true;
+    }
+    trd_small_kernel<NW><<<1, NW * 32, smem, ctx->stream>>>(a, n, lda, hh, d, e, tau, scal);
+    ATK_LAUNCHED(ctx);
+}
+
 template <int NT>
 void launch_trd_tile(atk_ctx* ctx, const double* a, int n, int lda, double* hh, double* d, double* e, double* tau,
                      double* scal) {
@@ -799,6 +918,11 @@ void launch_trd_backtr(atk_ctx* ctx, bool trd, const double* a, int n, int lda, 
 void trd_backtr(atk_ctx* ctx, bool trd, const double* a, int n, int lda, double* hh, double* d, double* e,
                 double* tau, double* scal, const double* X, int nwant, double* vout, int ldv) {
     static_assert(kTridiagMax <= 224, "row slots");
+    if (trd && ctx->trd_tiles == 1 && n <= 64) {  // one or two warps, no 256-thread barriers
+        if (n <= 32) launch_trd_small<1>(ctx, a, n, lda, hh, d, e, tau, scal);
+        else launch_trd_small<2>(ctx, a, n, lda, hh, d, e, tau, scal);
+        return;
+    }
     if (trd && ctx->trd_tiles && n <= 192) {  // tile variant (fits shared memory up to 6 x 6 tiles)
         switch ((n + 31) / 32) {
             case 1: launch_trd_tile<1>(ctx, a, n, lda, hh, d, e, tau, scal); return;

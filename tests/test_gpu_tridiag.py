@@ -143,3 +143,26 @@ def test_bit_reproducible(tctx):
     r2 = atucker.sym_eig_top_r(s, 20, ctx=tctx)
     np.testing.assert_array_equal(r1.values, r2.values)
     np.testing.assert_array_equal(r1.vectors, r2.vectors)
+
+
+@pytest.mark.parametrize("variant", [1, 2, 0], ids=["warps", "tiles", "slots"])
+@pytest.mark.parametrize("n", [5, 32, 33, 48, 64])
+def test_reduction_kernels(variant, n):
+    """The three Householder reductions (option trd_tiles): 1 = one or two
+    warps for n <= 64 (the default), 2 = the 32 x 32 tile kernel, 0 = the
+    column-slot kernel.  Same outputs, same bars."""
+    from paper_2010_10131_b200 import atucker
+
+    ctx = atucker.Context(0)
+    ctx.set_option("eig_method", 2)
+    ctx.set_option("trd_tiles", variant)
+    try:
+        rng = np.random.default_rng(7 * n + variant)
+        a = rng.standard_normal((n, 3 * n))
+        s = a @ a.T
+        _check(s, max(1, n // 2), atucker.sym_eig_top_r(s, max(1, n // 2), ctx=ctx))
+        b = rng.standard_normal((n, n))
+        _check((b + b.T) / 2, n, atucker.sym_eig_top_r((b + b.T) / 2, n, ctx=ctx))
+    finally:
+        ctx.set_option("trd_tiles", 1)
+        ctx.set_option("eig_method", -1)
