@@ -1,23 +1,25 @@
 // eig.cu — linalg::sym_eig_top_r (linalg.hpp:101-123) on the device, fp64.
 //
 // The reference computes ALL eigenpairs with Eigen's SelfAdjointEigenSolver
-// and keeps the top r.  On the device:
-//   n <= kJacobiMax : dense one-CTA one-sided Jacobi (jacobi.cu), keep top r.
-//   n  > kJacobiMax : Chebyshev-filtered subspace iteration (ChFSI) on a block
-//                     of k = min(n, max(r+16, 3r/2)) vectors:
-//                       bounds  : one cooperative-kernel Lanczos run (m = 40
-//                                 steps, 2 grid barriers per step) + its
-//                                 tridiagonal solved by the Jacobi kernel;
-//                       filter  : T_d on [lo, cut] (scaled recurrence, fp64
-//                                 split-K DGEMMs);
-//                       orthonormalisation : shifted CholeskyQR3 (GEMMs + one-CTA
-//                                 Cholesky); on the rank loss a strong filter
-//                                 produces it falls back to SVQB twice (Gram ->
-//                                 Jacobi -> Y D Z Theta^-1/2, clamped spectrum);
-//                       Rayleigh-Ritz : Jacobi on V^T S V;
-//                     until every wanted Ritz pair has relative residual
-//                     ||S v - theta v|| <= tol * max|theta| (tol 1e-12 for fp64
-//                     data, 1e-9 for tf32-computed Grams).
+// and keeps the top r.  On the device (eig_method -1):
+//   n <= 200 : the tridiagonal solver (tridiag.cu); one-sided Jacobi
+//              (jacobi.cu) as eig_method 0 for n <= 112;
+//   n  > 200 : Chebyshev-filtered subspace iteration (ChFSI) on a block of
+//              k = r + max(16, r/4) vectors:
+//                bounds  : lo = 0 for PSD input; otherwise one m = 40 Lanczos
+//                          run on a cluster (S resident in 16 CTAs' shared
+//                          memory when it fits) + bisection / inverse
+//                          iteration on its tridiagonal;
+//                filter  : T_d on [lo, cut] (scaled recurrence, fp64 DMMA,
+//                          one cooperative launch per pass, dgemm.cu), on
+//                          the unconverged Ritz vectors with S deflated by
+//                          the locked (converged) pairs;
+//                orthonormalisation : shifted CholeskyQR3 (GEMMs + one-CTA
+//                          Cholesky); SVQB if a pivot still fails;
+//                Rayleigh-Ritz : tridiagonal solver on V^T S V;
+//              until every wanted Ritz pair has relative residual
+//              ||S v - theta v|| <= tol * max|theta| (tol 1e-12 for fp64
+//              data, 1e-9 for tf32-computed Grams).
 // Both paths finish with descending order + fix_signs (linalg.hpp:34-50) so
 // factors compare entry-wise with the reference on gapped spectra.
 #include <algorithm>
