@@ -141,6 +141,8 @@ uint64_t atk_ctx_launch_count(const atk_ctx* ctx);
  *                  also the Rayleigh-Ritz solver), 1 ChFSI, 2 tridiagonal (n <= 200)
  *   "chfsi_tol"     relative Ritz-residual target of ChFSI (default 1e-12; fp32 Grams use >= 1e-9)
  *   "cheb_fused"    1 = each Chebyshev filter pass is one cooperative launch (default), 0 = per-step launches
+ *   "als_head"      -1 = one-pass ALS: phase 1 and phase 2 of a tile in turn (default); k >= 0 interleaves
+ *                   tile t+1's phase 1 with t's phase 2, k K-blocks first (measured slower)
  *   "chfsi_lock"    1 = ChFSI locks converged Ritz pairs and filters the rest with a deflated S (default)
  *   "lanczos_tiles" 1 = the ChFSI bounds Lanczos keeps S in a 16-CTA cluster's shared memory (n <= ~1250;
  *                   default), 0 = re-read S from L2 every step

@@ -42,6 +42,7 @@ struct AlsParams {
     uint64_t J;           // columns of Y_(0)
     int tiles;            // ceil(J / 128)
     int stages;
+    int head;             // phase-1 K-blocks of tile t+1 issued before phase 2 of t (< 0: no overlap)
     float* rfac;          // R x J output (the iteration whose rfac is kept) or null
     double* acc_yr;       // [cta][I][NB]
 };
@@ -53,6 +54,36 @@ __device__ __forceinline__ float tf32_rn(float x) {
     uint32_t r;
     asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
     return __uint_as_float(r);
+}
+
+// The stage order both the TMA warp and the MMA thread follow.  Default
+// (head < 0): P1(t), P2(t) strictly in turn.  head >= 0 (option als_head)
+// interleaves tile t's phase 2 (the L2 re-read) with tile t+1's phase 1 (the
+// HBM stream), `head` phase-1 K-blocks of t+1 first, so the MMA pipe has work
+// while rfac_t is converted; measured slower on C2 (1.63 vs 1.31 ms per
+// iteration on one box), so it stays off.
+template <class F1, class F2>
+__device__ __forceinline__ void als_schedule(int t0, int t1, int nkb1, int n2, int head, F1&& p1, F2&& p2) {
+    if (t0 >= t1) return;
+    if (head < 0) {  // P1(t), P2(t) strictly in turn
+        for (int t = t0; t < t1; ++t) {
+            for (int kb = 0; kb < nkb1; ++kb) p1(t, kb);
+            for (int q = 0; q < n2; ++q) p2(t, q);
+        }
+        return;
+    }
+    for (int kb = 0; kb < nkb1; ++kb) p1(t0, kb);
+    for (int t = t0; t < t1; ++t) {
+        const bool nxt = t + 1 < t1;
+        const int h = nxt ? min(head, nkb1) : 0, rem = nxt ? nkb1 - h : 0;
+        int done = 0;
+        for (; done < h; ++done) p1(t + 1, done);
+        for (int q = 0; q < n2; ++q) {
+            p2(t, q);
+            const int target = h + int(int64_t(q + 1) * rem / n2);
+            for (; done < target; ++done) p1(t + 1, done);
+        }
+    }
 }
 
 __global__ void __launch_bounds__(THREADS, 1)
@@ -112,39 +143,28 @@ __global__ void __launch_bounds__(THREADS, 1)
             auto next = [&]() {
                 if (++stage == S) { stage = 0; phase ^= 1; }
             };
-            auto load_p1 = [&](int t) {
-                for (int kb = 0; kb < nkb1; ++kb) {
-                    tc::mbar_wait(&empty[stage], phase ^ 1);
-                    tc::mbar_arrive_expect_tx(&full[stage], P1_A + P1_B);
-                    uint8_t* a = smem + size_t(stage) * STAGE;
-                    tc::tma_load_2d_hint(a, &tma_yk, &full[stage], kb * BK, t * JT, keep);  // re-read in phase 2
-                    tc::tma_load_2d(a + P1_A, &tma_f, &full[stage], kb * BK, 0);
-                    next();
-                }
+            auto load_p1 = [&](int t, int kb) {
+                tc::mbar_wait(&empty[stage], phase ^ 1);
+                tc::mbar_arrive_expect_tx(&full[stage], P1_A + P1_B);
+                uint8_t* a = smem + size_t(stage) * STAGE;
+                tc::tma_load_2d_hint(a, &tma_yk, &full[stage], kb * BK, t * JT, keep);  // re-read in phase 2
+                tc::tma_load_2d(a + P1_A, &tma_f, &full[stage], kb * BK, 0);
+                next();
             };
-            auto load_p2 = [&](int t) {
+            auto load_p2 = [&](int t, int q) {
                 // i-tiles newest-first: phase 1 streamed i upwards, so the last rows are the
                 // likeliest to still be in L2
-                for (int it = p.ntiles_i - 1; it >= 0; --it)
-                    for (int c = 0; c < JT / BK; ++c) {
-                        tc::mbar_wait(&empty[stage], phase ^ 1);
-                        tc::mbar_arrive_expect_tx(&full[stage], 16384);
-                        uint8_t* a = smem + size_t(stage) * STAGE;
+                const int it = p.ntiles_i - 1 - q / (JT / BK), c = q % (JT / BK);
+                tc::mbar_wait(&empty[stage], phase ^ 1);
+                tc::mbar_arrive_expect_tx(&full[stage], 16384);
+                uint8_t* a = smem + size_t(stage) * STAGE;
 #pragma unroll
-                        for (int q = 0; q < 4; ++q)
-                            tc::tma_load_2d_hint(a + q * 4096, &tma_ym, &full[stage], it * 128 + q * 32,
-                                                 t * JT + c * BK, drop);  // last use of the tile
-                        next();
-                    }
+                for (int qq = 0; qq < 4; ++qq)
+                    tc::tma_load_2d_hint(a + qq * 4096, &tma_ym, &full[stage], it * 128 + qq * 32, t * JT + c * BK,
+                                         drop);  // last use of the tile
+                next();
             };
-            // same order as the MMA warp: P1(t), P2(t) -- the phase-2 re-read of a
-            // tile follows its phase-1 read directly, while it is still in L2
-            // (issuing P1(t+1) first doubled the HBM traffic: 148 CTAs x 2 x 512 KB
-            // of live tiles overflow the L2; measured 8.5 GB read per pass)
-            for (int t = t0; t < t1; ++t) {
-                load_p1(t);
-                load_p2(t);
-            }
+            als_schedule(t0, t1, nkb1, p.ntiles_i * (JT / BK), p.head, load_p1, load_p2);
         }
         __syncwarp();
     } else if (warp == 1) {
@@ -158,53 +178,55 @@ __global__ void __launch_bounds__(THREADS, 1)
             auto next = [&]() {
                 if (++stage == S) { stage = 0; phase ^= 1; }
             };
-            auto issue_p1 = [&](int t, int buf) {
-                // the TMEM buffer must have been read by the conversion of tile t - 2
-                if (t - t0 >= 2) {
-                    tc::mbar_wait(&rf_empty[buf], rfe_phase[buf]);
-                    rfe_phase[buf] ^= 1;
-                }
-                tc::tc_fence_after();
+            auto issue_p1 = [&](int t, int kb) {
+                const int buf = (t - t0) & 1;
                 const uint32_t d = tmem + uint32_t(buf * NB);
-                for (int kb = 0; kb < nkb1; ++kb) {
-                    tc::mbar_wait(&full[stage], phase);
-                    tc::tc_fence_after();
-                    const uint32_t a_base = tc::smem_u32(smem + size_t(stage) * STAGE);
-                    const uint32_t b_base = a_base + P1_A;
-#pragma unroll
-                    for (int k = 0; k < BK / 8; ++k)
-                        tc::mma_tf32(d, tc::smem_desc(a_base + k * 32, 16, 1024, 2),
-                                     tc::smem_desc(b_base + k * 32, 16, 1024, 2), id_p1, (kb > 0 || k > 0) ? 1u : 0u);
-                    tc::mma_commit(&empty[stage]);
-                    next();
-                }
-                tc::mma_commit(&rf_full[buf]);
-            };
-            auto issue_p23 = [&]() {
-                tc::mbar_wait(rb_full, rbe_phase);  // the tile's rfac operand is in smem
-                rbe_phase ^= 1;
-                tc::tc_fence_after();
-                const uint32_t rb_base = tc::smem_u32(rb);
-                for (int it = p.ntiles_i - 1; it >= 0; --it)
-                    for (int c = 0; c < JT / BK; ++c) {
-                        tc::mbar_wait(&full[stage], phase);
-                        tc::tc_fence_after();
-                        const uint32_t a_base = tc::smem_u32(smem + size_t(stage) * STAGE);
-#pragma unroll
-                        for (int k = 0; k < BK / 8; ++k)
-                            tc::mma_tf32(tmem + col_yr + uint32_t(it * NB), tc::smem_desc(a_base + k * 1024, 4096, 512, 1),
-                                         tc::smem_desc(rb_base + c * RB_CHUNK + k * 32, 16, 1024, 2), id_p2,
-                                         (yr_started || c > 0 || k > 0) ? 1u : 0u);
-                        tc::mma_commit(&empty[stage]);
-                        next();
+                if (kb == 0) {
+                    // the TMEM buffer must have been read by the conversion of tile t - 2
+                    if (t - t0 >= 2) {
+                        tc::mbar_wait(&rf_empty[buf], rfe_phase[buf]);
+                        rfe_phase[buf] ^= 1;
                     }
-                yr_started = true;
-                tc::mma_commit(rb_empty);
+                    tc::tc_fence_after();
+                }
+                tc::mbar_wait(&full[stage], phase);
+                tc::tc_fence_after();
+                const uint32_t a_base = tc::smem_u32(smem + size_t(stage) * STAGE);
+                const uint32_t b_base = a_base + P1_A;
+#pragma unroll
+                for (int k = 0; k < BK / 8; ++k)
+                    tc::mma_tf32(d, tc::smem_desc(a_base + k * 32, 16, 1024, 2),
+                                 tc::smem_desc(b_base + k * 32, 16, 1024, 2), id_p1, (kb > 0 || k > 0) ? 1u : 0u);
+                tc::mma_commit(&empty[stage]);
+                next();
+                if (kb == nkb1 - 1) tc::mma_commit(&rf_full[buf]);
             };
-            for (int t = t0; t < t1; ++t) {
-                issue_p1(t, (t - t0) & 1);
-                issue_p23();
-            }
+            const int n2 = p.ntiles_i * (JT / BK);
+            auto issue_p2 = [&](int t, int q) {
+                (void)t;
+                if (q == 0) {
+                    tc::mbar_wait(rb_full, rbe_phase);  // the tile's rfac operand is in smem
+                    rbe_phase ^= 1;
+                    tc::tc_fence_after();
+                }
+                const int it = p.ntiles_i - 1 - q / (JT / BK), c = q % (JT / BK);
+                const uint32_t rb_base = tc::smem_u32(rb);
+                tc::mbar_wait(&full[stage], phase);
+                tc::tc_fence_after();
+                const uint32_t a_base = tc::smem_u32(smem + size_t(stage) * STAGE);
+#pragma unroll
+                for (int k = 0; k < BK / 8; ++k)
+                    tc::mma_tf32(tmem + col_yr + uint32_t(it * NB), tc::smem_desc(a_base + k * 1024, 4096, 512, 1),
+                                 tc::smem_desc(rb_base + c * RB_CHUNK + k * 32, 16, 1024, 2), id_p2,
+                                 (yr_started || c > 0 || k > 0) ? 1u : 0u);
+                tc::mma_commit(&empty[stage]);
+                next();
+                if (q == n2 - 1) {
+                    yr_started = true;
+                    tc::mma_commit(rb_empty);
+                }
+            };
+            als_schedule(t0, t1, nkb1, n2, p.head, issue_p1, issue_p2);
         }
         __syncwarp();
     } else {
@@ -338,6 +360,7 @@ void als_fused_pass(atk_ctx* ctx, const atk_tensor* y, const double* m_dev, uint
     p.J = J;
     p.tiles = int((J + JT - 1) / JT);
     p.stages = 10;
+    p.head = ctx->als_head;
     const int grid = std::min(ctx->num_sms, p.tiles);
     DevBuf<double> ayr(ctx, size_t(grid) * I * NB);
     p.rfac = rfac_out ? static_cast<float*>(rfac_out->data) : nullptr;

@@ -57,6 +57,8 @@ struct atk_ctx {
     int eig_method = -1;       // option "eig_method": -1 auto, 0 dense Jacobi, 1 ChFSI, 2 tridiagonal
     double chfsi_tol = 1e-12;  // option "chfsi_tol": relative Ritz residual target
     int cheb_fused = 1;        // option "cheb_fused": whole Chebyshev filter in one cooperative launch
+    int als_head = -1;         // option "als_head": one-pass ALS, >= 0 interleaves tile t+1's phase 1 with t's phase 2
+                               // (that many K-blocks first); measured slower (C2: 1.63 vs 1.31 ms per iteration)
     int chfsi_lock = 1;        // option "chfsi_lock": lock converged Ritz pairs, filter a deflated S
     int lanczos_tiles = 1;     // option "lanczos_tiles": S resident in a 16-CTA cluster's smem for the bounds
     int als_fused = 1;         // option "als_fused": one pass over Y per ALS iteration (mode 0, fp32)
