@@ -763,8 +763,11 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
     dgemm(ctx, false, false, n, k, n, 1.0, Sp, n, Ya.get(), n, 0.0, Yb.get(), n);
     orthonormalize(ctx, Yb.get(), n, k, V.get(), ws);
     mark("qr0");
-    // all k Ritz vectors when locking is on: the active (unlocked) block is Vk(:, nc:k)
-    const int nv = ctx->chfsi_lock ? k : r;
+    // Ritz vectors formed: the top r; all k once locking has started (the
+    // active block is then Vk(:, nc:k)).  Forming all k from the start cost
+    // C5 0.85 ms per step: its 16 guard-band Ritz values are noise, one tight
+    // cluster for inverse iteration, and C5 never filters.
+    int nv = r;
     rayleigh_ritz(ctx, Sp, n, k, r, nv, V.get(), W.get(), T.get(), Z.get(), theta.get(), Vr.get(), Wr.get(),
                   sweeps.get(), psd);
     mark("rr0", trace_sweeps(sweeps.get()));
@@ -812,8 +815,13 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
         // eigenvalue (a non-centred Gram's mean direction, 1e3 x the rest)
         // forces the dynamic-range cap below down to degree 2.
         int nc = 0;
-        if (ctx->chfsi_lock)
+        if (ctx->chfsi_lock) {
             while (nc < r - 1 && hres[nc] <= tol * scale) ++nc;
+            if (nc > 0 && nv < k) {  // no guard-band vectors yet: lock from the next pass on
+                nc = 0;
+                nv = k;
+            }
+        }
         // Chebyshev filter on the unwanted interval [lo, cut]
         const double cut = hth[k - 1];
         const double lo = std::min(b.lo, cut - 1e-12 * scale);

@@ -393,7 +393,9 @@ void cholesky_inv_t(atk_ctx* ctx, const double* g, int k, double* x, int* info_d
                                       int(size_t(2) * (kJacobiMax + 1) * kJacobiMax * sizeof(double))));
         attr = true;
     }
-    const int threads = std::min(1024, std::max(64, 32 * k));  // one warp per column (measured: 128 threads 4x slower)
+    int threads = std::min(1024, std::max(64, 32 * k));  // one warp per column (measured: 128 threads 4x slower)
+    static const int th_env = std::getenv("ATK_CHOL_THREADS") ? std::atoi(std::getenv("ATK_CHOL_THREADS")) : 0;
+    if (th_env >= 32 && th_env <= 1024) threads = th_env / 32 * 32;  // probe knob
     chol_inv_kernel<<<1, threads, smem, ctx->stream>>>(g, k, x, info_dev);
     ATK_LAUNCHED(ctx);
 }
