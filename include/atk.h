@@ -148,7 +148,7 @@ uint64_t atk_ctx_launch_count(const atk_ctx* ctx);
  *                   default), 0 = re-read S from L2 every step
  *   "als_fused"     1 = an ALS iteration on mode 0 (fp32, R <= 32) reads Y once: rfac, YR and GR
  *                   from one tcgen05 pass (default), 0 = the two-pass TTM + TTT schedule
- *   "trd_tiles"     1 = tridiagonalise n <= 64 with one or two warps and n <= 192 on 32 x 32 tiles (default),
+ *   "trd_tiles"     1 = tridiagonalise n <= 128 with one to four warps and n <= 192 on 32 x 32 tiles (default),
  *                   2 = tiles for every n <= 192, 0 = column-slot kernel
  *   "chfsi_k"       ChFSI block size (0 = r + max(16, r/4); measured: larger blocks only slow C2's
  *                   flat spectra down)

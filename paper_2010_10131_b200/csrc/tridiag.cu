@@ -724,7 +724,7 @@ size_t trd_tile_smem(int nt) {
     return (size_t(ntiles) * kTileDbl + size_t(ntiles) * 64 + 64 * size_t(nt) + 2) * sizeof(double);
 }
 
-// n <= 32 NW: the same reduction (dsytd2 conventions, same outputs as
+// n <= 32 NW (NW <= 4): the same reduction (dsytd2 conventions, same outputs as
 // trd_kernel / trd_tile_kernel) by NW warps, lane-owned rows of the FULL
 // symmetric matrix in shared memory (column-major, odd ld: conflict-free).
 // Warp w owns rows 32 w + lane in the matvec and the rank-2 update, so the
@@ -918,9 +918,15 @@ void launch_trd_backtr(atk_ctx* ctx, bool trd, const double* a, int n, int lda, 
 void trd_backtr(atk_ctx* ctx, bool trd, const double* a, int n, int lda, double* hh, double* d, double* e,
                 double* tau, double* scal, const double* X, int nwant, double* vout, int ldv) {
     static_assert(kTridiagMax <= 224, "row slots");
-    if (trd && ctx->trd_tiles == 1 && n <= 64) {  // one or two warps, no 256-thread barriers
-        if (n <= 32) launch_trd_small<1>(ctx, a, n, lda, hh, d, e, tau, scal);
-        else launch_trd_small<2>(ctx, a, n, lda, hh, d, e, tau, scal);
+    // n <= 128: one to four warps, no 256-thread barriers (n = 48 / 80-96 / 128:
+    // 69 / 168 / 320 us against the tile kernel's 108 / 229 / 411 us)
+    if (trd && ctx->trd_tiles == 1 && n <= 128) {
+        switch ((n + 31) / 32) {
+            case 1: launch_trd_small<1>(ctx, a, n, lda, hh, d, e, tau, scal); break;
+            case 2: launch_trd_small<2>(ctx, a, n, lda, hh, d, e, tau, scal); break;
+            case 3: launch_trd_small<3>(ctx, a, n, lda, hh, d, e, tau, scal); break;
+            default: launch_trd_small<4>(ctx, a, n, lda, hh, d, e, tau, scal); break;
+        }
         return;
     }
     if (trd && ctx->trd_tiles && n <= 192) {  // tile variant (fits shared memory up to 6 x 6 tiles)

@@ -146,10 +146,10 @@ def test_bit_reproducible(tctx):
 
 
 @pytest.mark.parametrize("variant", [1, 2, 0], ids=["warps", "tiles", "slots"])
-@pytest.mark.parametrize("n", [5, 32, 33, 48, 64])
+@pytest.mark.parametrize("n", [5, 32, 33, 48, 64, 80, 97, 128])
 def test_reduction_kernels(variant, n):
-    """The three Householder reductions (option trd_tiles): 1 = one or two
-    warps for n <= 64 (the default), 2 = the 32 x 32 tile kernel, 0 = the
+    """The three Householder reductions (option trd_tiles): 1 = one to four
+    warps for n <= 128 (the default), 2 = the 32 x 32 tile kernel, 0 = the
     column-slot kernel.  Same outputs, same bars."""
     from paper_2010_10131_b200 import atucker
 
