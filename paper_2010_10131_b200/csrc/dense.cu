@@ -328,14 +328,18 @@ __global__ void __launch_bounds__(1024) householder_qr_kernel(double* __restrict
 
 // ------------------------------------------------------------------ misc
 // fix_signs: one warp per column; largest |v| with the first index on ties.
-__global__ void fix_signs_kernel(double* __restrict__ v, int n, int r, int ldv) {
-    const int col = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-    const int lane = threadIdx.x & 31;
-    if (col >= r) return;
+// One CTA per column (a warp per column was a 64-deep chain of L2 round trips
+// at n = 2048): largest |v_i|, ties to the lowest i, then flip if negative.
+__global__ void __launch_bounds__(256) fix_signs_kernel(double* __restrict__ v, int n, int r, int ldv) {
+    __shared__ double sb[8];
+    __shared__ int si[8];
+    __shared__ int flip_sh;
+    const int col = blockIdx.x;
+    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
     double* c = v + size_t(ldv) * col;
     double best = -1.0;
     int bi = 0;
-    for (int i = lane; i < n; i += 32) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
         const double a = fabs(c[i]);
         if (a > best) { best = a; bi = i; }
     }
@@ -344,9 +348,21 @@ __global__ void fix_signs_kernel(double* __restrict__ v, int n, int r, int ldv) 
         const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
         if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
     }
-    const bool flip = c[bi] < 0.0;
-    if (flip)
-        for (int i = lane; i < n; i += 32) c[i] = -c[i];
+    if (lane == 0) {
+        sb[wp] = best;
+        si[wp] = bi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double b = sb[0];
+        int ib = si[0];
+        for (int q = 1; q < int(blockDim.x >> 5); ++q)
+            if (sb[q] > b || (sb[q] == b && si[q] < ib)) { b = sb[q]; ib = si[q]; }
+        flip_sh = c[ib] < 0.0;
+    }
+    __syncthreads();
+    if (flip_sh)
+        for (int i = threadIdx.x; i < n; i += blockDim.x) c[i] = -c[i];
 }
 
 __global__ void symmetrize_kernel(double* a, int n) {
@@ -414,7 +430,8 @@ void householder_qr(atk_ctx* ctx, const double* a, int m, int n, double* q, doub
 }
 
 void fix_signs(atk_ctx* ctx, double* v, int n, int r, int ldv) {
-    fix_signs_kernel<<<blocks_for(r, 8), 256, 0, ctx->stream>>>(v, n, r, ldv);
+    if (r <= 0 || n <= 0) return;
+    fix_signs_kernel<<<unsigned(r), 256, 0, ctx->stream>>>(v, n, r, ldv);
     ATK_LAUNCHED(ctx);
 }
 

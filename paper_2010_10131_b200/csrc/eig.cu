@@ -441,20 +441,29 @@ __global__ void cheb_combine(double* __restrict__ ynew, const double* __restrict
         ynew[e] = g1 * y[e] + (yprev ? g2 * yprev[e] : 0.0);
 }
 
-// res[j] = || W(:, j) - theta_j V(:, j) ||, j < r   (one warp per column)
-__global__ void ritz_residual(const double* __restrict__ w, const double* __restrict__ v,
-                              const double* __restrict__ theta, int n, int r, double* __restrict__ res) {
-    const int col = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-    const int lane = threadIdx.x & 31;
-    if (col >= r) return;
+// res[j] = || W(:, j) - theta_j V(:, j) ||, j < r   (one CTA per column, a
+// fixed-order block sum; one warp per column was a 64-deep chain of L2
+// round trips at n = 2048)
+__global__ void __launch_bounds__(256) ritz_residual(const double* __restrict__ w, const double* __restrict__ v,
+                                                     const double* __restrict__ theta, int n, int r,
+                                                     double* __restrict__ res) {
+    __shared__ double sh[8];
+    const int col = blockIdx.x;
+    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
     const double th = theta[col];
     double s = 0.0;
-    for (int i = lane; i < n; i += 32) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
         const double d = w[i + size_t(n) * col] - th * v[i + size_t(n) * col];
-        s += d * d;
+        s = fma(d, d, s);
     }
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) res[col] = sqrt(s);
+    if (lane == 0) sh[wp] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int q = 0; q < int(blockDim.x >> 5); ++q) t += sh[q];
+        res[col] = sqrt(t);
+    }
 }
 
 // SVQB step 1: d_i = 1/sqrt(G_ii); G <- D G D.
@@ -783,7 +792,7 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
     int it = 0;
     double worst = 0.0;
     for (;; ++it) {
-        ritz_residual<<<(r + 7) / 8, 256, 0, st>>>(Wr.get(), Vr.get(), theta.get(), n, r, res.get());
+        ritz_residual<<<r, 256, 0, st>>>(Wr.get(), Vr.get(), theta.get(), n, r, res.get());
         ATK_LAUNCHED(ctx);
         ATK_CUDA(cudaMemcpyAsync(hth.data(), theta.get(), k * sizeof(double), cudaMemcpyDeviceToHost, st));
         ATK_CUDA(cudaMemcpyAsync(hres.data(), res.get(), r * sizeof(double), cudaMemcpyDeviceToHost, st));
