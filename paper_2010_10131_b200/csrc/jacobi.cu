@@ -359,14 +359,22 @@ __global__ void __launch_bounds__(1024) chol_inv_kernel(const double* __restrict
             break;
         }
         const double inv = 1.0 / d;
-        // warps over columns, lanes over rows i > c; A(i, c) = A[c + ld i] (symmetry)
-        for (int j = tid >> 5; j < k; j += nt >> 5) {
+        // warps over columns, lanes over rows i > c; A(i, c) = A[c + ld i] (symmetry).
+        // At most 4 columns per warp (k <= 112 <= 4 x 32 warps... or 4 x nw):
+        // unrolled, so the per-column set-up is not a loop-carried chain.
+        const int nw = nt >> 5, w0 = tid >> 5, lane = tid & 31;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int j = w0 + q * nw;
+            if (j >= k) break;
             if (j <= c) {
                 const double wcj = W[c + ld * j] * inv;
-                for (int i = c + 1 + (tid & 31); i < k; i += 32) W[i + ld * j] = fma(-A[c + ld * i], wcj, W[i + ld * j]);
+                double* wc = W + ld * j;
+                for (int i = c + 1 + lane; i < k; i += 32) wc[i] = fma(-A[c + ld * i], wcj, wc[i]);
             } else {
                 const double acj = A[c + ld * j] * inv;
-                for (int i = c + 1 + (tid & 31); i <= j; i += 32) A[i + ld * j] = fma(-A[c + ld * i], acj, A[i + ld * j]);
+                double* ac = A + ld * j;
+                for (int i = c + 1 + lane; i <= j; i += 32) ac[i] = fma(-A[c + ld * i], acj, ac[i]);
             }
         }
         __syncthreads();
@@ -396,6 +404,7 @@ void cholesky_inv_t(atk_ctx* ctx, const double* g, int k, double* x, int* info_d
     int threads = std::min(1024, std::max(64, 32 * k));  // one warp per column (measured: 128 threads 4x slower)
     static const int th_env = std::getenv("ATK_CHOL_THREADS") ? std::atoi(std::getenv("ATK_CHOL_THREADS")) : 0;
     if (th_env >= 32 && th_env <= 1024) threads = th_env / 32 * 32;  // probe knob
+    threads = std::max(threads, 32 * ((k + 3) / 4));                  // <= 4 columns per warp (kernel unroll)
     chol_inv_kernel<<<1, threads, smem, ctx->stream>>>(g, k, x, info_dev);
     ATK_LAUNCHED(ctx);
 }
