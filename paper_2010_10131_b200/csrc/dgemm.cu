@@ -377,6 +377,26 @@ __global__ void __launch_bounds__(512) cheb_resident_kernel(const ChebResArgs p)
     }
 }
 
+// Small outputs: G lanes per element (G | 32), lane t sums splits t, t+G, ...
+// in order, then a fixed xor tree over the G lanes (deterministic).  The
+// one-thread-per-element loop is a chain of `splits` L2 round trips.
+__global__ void dgemm_splitk_reduce_g(const double* __restrict__ part, int splits, int m, int n, int G,
+                                      double alpha, double beta, double* __restrict__ c, int ldc) {
+    const size_t mn = size_t(m) * n;
+    const size_t gid = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const size_t e = gid / G;
+    const int t = int(gid % G);
+    double s = 0.0;
+    if (e < mn)
+        for (int z = t; z < splits; z += G) s += part[size_t(z) * mn + e];
+    for (int o = G >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (e < mn && t == 0) {
+        const int i = int(e % m), j = int(e / m);
+        double* cp = c + i + size_t(ldc) * j;
+        *cp = alpha * s + (beta == 0.0 ? 0.0 : beta * *cp);
+    }
+}
+
 __global__ void dgemm_splitk_reduce(const double* __restrict__ part, int splits, int m, int n,
                                     double alpha, double beta, double* __restrict__ c, int ldc) {
     const size_t mn = size_t(m) * n;
@@ -406,9 +426,13 @@ void dgemm_launch(atk_ctx* ctx, bool ta, bool tb, int m, int n, int k, double al
     const int gm = (m + BM - 1) / BM, gn = (n + BN_ - 1) / BN_;
     const int tiles = gm * gn;
     int splits = 1;
-    // up to 4 resident CTAs per SM (51-59 KB smem each); K chunks of >= 16 slices
-    if (tiles < 4 * ctx->num_sms && k >= 256)
-        splits = std::min(std::max(1, (4 * ctx->num_sms + tiles - 1) / tiles), std::max(1, k / 128));
+    // up to 4 resident CTAs per SM (51-59 KB smem each)
+    // K chunks of >= 32 (4 slices): the skinny ChFSI GEMMs (k x k over n, n x k x k) were
+    // latency-bound on 8-16 CTAs with 128-deep chunks (C2: 1.60 -> 1.00 ms of dgemm per step,
+    // with the lane-parallel split-K reduction below); ATK_DGEMM_MIN_CHUNK is a probe knob
+    static const int min_chunk = std::getenv("ATK_DGEMM_MIN_CHUNK") ? std::atoi(std::getenv("ATK_DGEMM_MIN_CHUNK")) : 32;
+    if (tiles < 4 * ctx->num_sms && k >= 2 * min_chunk)
+        splits = std::min(std::max(1, (4 * ctx->num_sms + tiles - 1) / tiles), std::max(1, k / min_chunk));
     int kchunk = (k + splits - 1) / splits;
     kchunk = (kchunk + BK - 1) / BK * BK;
     splits = std::max(1, (k + kchunk - 1) / std::max(1, kchunk));
@@ -429,8 +453,17 @@ void dgemm_launch(atk_ctx* ctx, bool ta, bool tb, int m, int n, int k, double al
                                                       size_t(m) * n, m, 1.0, 0.0, false);
     ATK_LAUNCHED(ctx);
     const size_t mn = size_t(m) * n;
-    dgemm_splitk_reduce<<<unsigned(std::min<size_t>((mn + 255) / 256, size_t(ctx->num_sms) * 8)), 256, 0,
-                          ctx->stream>>>(part.get(), splits, m, n, alpha, beta, c, ldc);
+    // lanes per element: enough threads to cover ~8 waves' worth, at most 32
+    int G = 1;
+    while (G < 32 && G < splits && mn * size_t(G) < size_t(ctx->num_sms) * 2048) G <<= 1;
+    if (G > 1) {
+        const size_t threads = mn * size_t(G);
+        dgemm_splitk_reduce_g<<<unsigned((threads + 255) / 256), 256, 0, ctx->stream>>>(part.get(), splits, m, n, G,
+                                                                                      alpha, beta, c, ldc);
+    } else {
+        dgemm_splitk_reduce<<<unsigned(std::min<size_t>((mn + 255) / 256, size_t(ctx->num_sms) * 8)), 256, 0,
+                              ctx->stream>>>(part.get(), splits, m, n, alpha, beta, c, ldc);
+    }
     ATK_LAUNCHED(ctx);
 }
 
