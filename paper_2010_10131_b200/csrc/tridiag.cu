@@ -384,42 +384,49 @@ __global__ void __launch_bounds__(256) invit_kernel(const double* __restrict__ d
         const int mm = cb + lane;
         const bool mine = mm < end;
         double* x = X + size_t(n) * (mine ? mm : j);
-        double* dl = wk + size_t(5) * n * (mine ? mm : j);
-        double* dd = dl + n;   // 1 / U(i, i)
-        double* du = dd + n;
-        double* du2 = du + n;
-        double* pv = du2 + n;  // 1.0 where rows i, i + 1 were interchanged
+        // the chunk's factors interleaved by member (lane): array a, row i at
+        // base[(a n + i) cs + lane], so a warp's accesses are contiguous
+        const int cs = min(32, end - cb);
+        double* base = wk + size_t(5) * n * cb + (mine ? lane : 0);
+        const size_t st = size_t(cs);
+        double* dl = base;                  // L multipliers
+        double* dd = base + size_t(n) * st;  // 1 / U(i, i)
+        double* du = dd + size_t(n) * st;
+        double* du2 = du + size_t(n) * st;
+        double* pv = du2 + size_t(n) * st;  // 1.0 where rows i, i + 1 were interchanged
         if (mine) {
             // shift, kept >= pertol below the previous member (dstein)
             double sh = lam[j];
             for (int q = j + 1; q <= mm; ++q) sh = fmin(lam[q], sh - pertol);
-            // dgttrf on T - sh I
+            // dgttrf on T - sh I (one division per row: f = l * (1 / pivot))
             double di = d[0] - sh, ui = n > 1 ? e[0] : 0.0;
             for (int i = 0; i + 1 < n; ++i) {
                 const double li = e[i], dn = d[i + 1] - sh, un = i + 2 < n ? e[i + 1] : 0.0;
                 if (fabs(di) >= fabs(li)) {
                     if (fabs(di) < tiny) di = copysign(tiny, di);
-                    const double f = li / di;
-                    dl[i] = f;
-                    dd[i] = 1.0 / di;
-                    du[i] = ui;
-                    du2[i] = 0.0;
-                    pv[i] = 0.0;
+                    const double r = 1.0 / di;
+                    const double f = li * r;
+                    dl[i * st] = f;
+                    dd[i * st] = r;
+                    du[i * st] = ui;
+                    du2[i * st] = 0.0;
+                    pv[i * st] = 0.0;
                     di = fma(-f, ui, dn);
                     ui = un;
                 } else {
-                    const double f = di / li;
-                    dl[i] = f;
-                    dd[i] = 1.0 / li;
-                    du[i] = dn;
-                    du2[i] = un;
-                    pv[i] = 1.0;
+                    const double r = 1.0 / li;
+                    const double f = di * r;
+                    dl[i * st] = f;
+                    dd[i * st] = r;
+                    du[i * st] = dn;
+                    du2[i * st] = un;
+                    pv[i * st] = 1.0;
                     di = fma(-f, dn, ui);
                     ui = -f * un;
                 }
             }
             if (fabs(di) < tiny) di = copysign(tiny, di);
-            dd[n - 1] = 1.0 / di;
+            dd[(n - 1) * st] = 1.0 / di;
             for (int i = 0; i < n; ++i) x[i] = hash_unit(uint64_t(mm) * 1000003ULL + i);
         }
         for (int it = 0; it < 3; ++it) {
@@ -428,19 +435,19 @@ __global__ void __launch_bounds__(256) invit_kernel(const double* __restrict__ d
                 double cr = x[0];
                 for (int i = 0; i + 1 < n; ++i) {
                     const double nx = x[i + 1];
-                    if (pv[i] != 0.0) {
+                    if (pv[i * st] != 0.0) {
                         x[i] = nx;
-                        cr = fma(-dl[i], nx, cr);
+                        cr = fma(-dl[i * st], nx, cr);
                     } else {
                         x[i] = cr;
-                        cr = fma(-dl[i], cr, nx);
+                        cr = fma(-dl[i * st], cr, nx);
                     }
                 }
                 x[n - 1] = cr;
-                double x2 = 0.0, x1 = x[n - 1] * dd[n - 1];
+                double x2 = 0.0, x1 = x[n - 1] * dd[(n - 1) * st];
                 x[n - 1] = x1;
                 for (int i = n - 2; i >= 0; --i) {
-                    const double xi = (x[i] - du[i] * x1 - du2[i] * x2) * dd[i];
+                    const double xi = (x[i] - du[i * st] * x1 - du2[i * st] * x2) * dd[i * st];
                     x[i] = xi;
                     x2 = x1;
                     x1 = xi;
