@@ -27,6 +27,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 #include <vector>
 
 #include "atk_internal.cuh"
@@ -745,8 +746,24 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
     DevBuf<int> sweeps(ctx, 1);
     static const bool trace = std::getenv("ATK_TRACE") != nullptr;
     auto t_last = std::chrono::steady_clock::now();
+    // ATK_TRACE=events: CUDA events instead of synchronising at every mark
+    // (the launch / host-sync gaps stay in), printed when the solve ends
+    static const bool trace_ev = trace && std::string(std::getenv("ATK_TRACE")) == "events";
+    struct Ev {
+        cudaEvent_t e;
+        const char* what;
+        std::chrono::steady_clock::time_point host;
+    };
+    std::vector<Ev> evs;
     auto mark = [&](const char* what, int a = -1, double v = 0.0) {
         if (!trace) return;
+        if (trace_ev) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            cudaEventRecord(e, st);
+            evs.push_back({e, what, std::chrono::steady_clock::now()});
+            return;
+        }
         cudaStreamSynchronize(st);
         const auto now = std::chrono::steady_clock::now();
         std::fprintf(stderr, "[atk eig n=%d r=%d k=%d] %-10s %8.3f ms  %d %.3e\n", n, r, k, what,
@@ -755,9 +772,10 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
     };
     auto trace_sweeps = [&](const int* d) {  // Jacobi sweeps of the last RR (trace only)
         int h = -1;
-        if (trace) cudaMemcpy(&h, d, sizeof(int), cudaMemcpyDeviceToHost);
+        if (trace && !trace_ev) cudaMemcpy(&h, d, sizeof(int), cudaMemcpyDeviceToHost);
         return h;
     };
+    mark("begin");
     if (!exact_sym) {
         ATK_CUDA(cudaMemcpyAsync(Sbuf.get(), s_dev, nn * sizeof(double), cudaMemcpyDeviceToDevice, st));
         symmetrize(ctx, Sbuf.get(), n);
@@ -918,6 +936,17 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
         mark("rr", trace_sweeps(sweeps.get()));
     }
     mark("done", it, worst / scale);
+    if (trace_ev && !evs.empty()) {
+        cudaEventSynchronize(evs.back().e);
+        for (size_t q = 1; q < evs.size(); ++q) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, evs[q - 1].e, evs[q].e);
+            std::fprintf(stderr, "[atk eig n=%d r=%d k=%d] gpu %-10s %8.3f ms  (host enqueue %.3f ms)\n", n, r, k,
+                         evs[q].what, ms,
+                         std::chrono::duration<double, std::milli>(evs[q].host - evs[q - 1].host).count());
+        }
+        for (auto& x : evs) cudaEventDestroy(x.e);
+    }
     ATK_CUDA(cudaMemcpyAsync(values_dev, theta.get(), r * sizeof(double), cudaMemcpyDeviceToDevice, st));
     ATK_CUDA(cudaMemcpyAsync(vectors_dev, Vr.get(), nr * sizeof(double), cudaMemcpyDeviceToDevice, st));
     fix_signs(ctx, vectors_dev, n, r, n);
