@@ -738,27 +738,34 @@ size_t trd_tile_smem(int nt) {
 // only cross-warp traffic is two scalar sums per step.  For the Rayleigh-Ritz
 // blocks of ChFSI (k = 48) and the small modes (n = 48) the tile kernel's
 // 256-thread barriers were the whole cost (~107 us at n = 48).
-template <int NW>
-__global__ void __launch_bounds__(NW * 32, 1)
+template <int NW, int CS>
+__global__ void __launch_bounds__(NW * CS * 32, 1)
     trd_small_kernel(const double* __restrict__ a, int n, int lda, double* __restrict__ hh, double* __restrict__ d,
                      double* __restrict__ e, double* __restrict__ tau_out, double* __restrict__ scal_out) {
+    // CS warps per 32-row block: warp (w, s) owns rows 32 w + lane and the s-th
+    // contiguous part of the trailing columns in the matvec and the update
     constexpr int NR = 32 * NW, LD = NR + 1;
     extern __shared__ double sm[];
     double* A = sm;              // NR x LD
     double* vs = A + NR * LD;    // NR: reflector
     double* ws = vs + NR;        // NR: w = p - K v
-    double* red = ws + NR;       // 2 x NW cross-warp partials
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    double* pp = ws + NR;        // CS x NR: matvec partials
+    double* red = pp + CS * NR;  // 2 x NW cross-warp partials
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int w = wid % NW, sp = wid / NW;
     const int i = w * 32 + lane;  // the row this thread owns
-    for (int j = 0; j < n; ++j)
-        A[i + LD * j] = i < n ? 0.5 * (a[i + size_t(lda) * j] + a[j + size_t(lda) * i]) : 0.0;
-    vs[i] = 0.0;
-    ws[i] = 0.0;
+    if (sp == 0)
+        for (int j = 0; j < n; ++j)
+            A[i + LD * j] = i < n ? 0.5 * (a[i + size_t(lda) * j] + a[j + size_t(lda) * i]) : 0.0;
+    if (sp == 0) {
+        vs[i] = 0.0;
+        ws[i] = 0.0;
+    }
     __syncthreads();
-    auto sum_all = [&](double x, int slot) {  // fixed order across warps
+    auto sum_all = [&](double x, int slot) {  // split-0 warps' sums, fixed order across warps
         x = warp_sum(x);
-        if (NW == 1) return x;
-        if (lane == 0) red[slot * NW + w] = x;
+        if (NW == 1 && CS == 1) return x;
+        if (sp == 0 && lane == 0) red[slot * NW + w] = x;
         __syncthreads();
         double t = 0.0;
 #pragma unroll
@@ -777,7 +784,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
             tau = (beta - alpha) / beta;
         }
         const double vi = (i == k + 1) ? 1.0 : x * scal;
-        vs[i] = vi;
+        if (sp == 0) vs[i] = vi;
         if (threadIdx.x == 0) {
             d[k] = A[k + LD * k];
             e[k] = beta;
@@ -786,26 +793,38 @@ __global__ void __launch_bounds__(NW * 32, 1)
         }
         __syncthreads();
         if (tau == 0.0) continue;  // uniform: H_k = I
-        // p = tau A22 v (row i), four independent chains
+        const int len = n - k - 1;
+        const int ja = k + 1 + (sp * len) / CS, jb = k + 1 + ((sp + 1) * len) / CS;
+        // this split's part of p = tau A22 v (row i), four independent chains
         double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
-        int j = k + 1;
+        int j = ja;
 #pragma unroll 2
-        for (; j + 3 < n; j += 4) {
+        for (; j + 3 < jb; j += 4) {
             p0 = fma(A[i + LD * j], vs[j], p0);
             p1 = fma(A[i + LD * (j + 1)], vs[j + 1], p1);
             p2 = fma(A[i + LD * (j + 2)], vs[j + 2], p2);
             p3 = fma(A[i + LD * (j + 3)], vs[j + 3], p3);
         }
-        for (; j < n; ++j) p0 = fma(A[i + LD * j], vs[j], p0);
-        const double pi = (i > k && i < n) ? tau * ((p0 + p1) + (p2 + p3)) : 0.0;
+        for (; j < jb; ++j) p0 = fma(A[i + LD * j], vs[j], p0);
+        double pi;
+        if (CS == 1) {
+            pi = (i > k && i < n) ? tau * ((p0 + p1) + (p2 + p3)) : 0.0;
+        } else {
+            pp[sp * NR + i] = (p0 + p1) + (p2 + p3);
+            __syncthreads();
+            double t = 0.0;
+#pragma unroll
+            for (int q = 0; q < CS; ++q) t += pp[q * NR + i];
+            pi = (i > k && i < n) ? tau * t : 0.0;
+        }
         const double K = 0.5 * tau * sum_all(pi * vi, 1);
         const double wi = fma(-K, vi, pi);
-        ws[i] = wi;
+        if (sp == 0) ws[i] = wi;
         __syncthreads();
         if (i > k && i < n) {
             // four columns per pass, loads first (a rolled loop is one shared-
             // memory round trip per element)
-            for (j = k + 1; j + 3 < n; j += 4) {
+            for (j = ja; j + 3 < jb; j += 4) {
                 double av[4], wv[4], vv[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
@@ -816,7 +835,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
 #pragma unroll
                 for (int u = 0; u < 4; ++u) A[i + LD * (j + u)] = fma(-vi, wv[u], fma(-wi, vv[u], av[u]));
             }
-            for (; j < n; ++j) A[i + LD * j] = fma(-vi, ws[j], fma(-wi, vs[j], A[i + LD * j]));
+            for (; j < jb; ++j) A[i + LD * j] = fma(-vi, ws[j], fma(-wi, vs[j], A[i + LD * j]));
         }
         __syncthreads();
     }
@@ -832,22 +851,33 @@ __global__ void __launch_bounds__(NW * 32, 1)
         scal_out[n - 1] = 0.0;
     }
     // packed lower triangle (column k below the diagonal: the raw reflector k)
-    for (int jj = 0; jj < n; ++jj)
-        if (i >= jj && i < n) hh[pk(i, jj, n)] = A[i + LD * jj];
+    if (sp == 0)
+        for (int jj = 0; jj < n; ++jj)
+            if (i >= jj && i < n) hh[pk(i, jj, n)] = A[i + LD * jj];
 }
 
-template <int NW>
+template <int NW, int CS>
 void launch_trd_small(atk_ctx* ctx, const double* a, int n, int lda, double* hh, double* d, double* e, double* tau,
                       double* scal) {
     constexpr int NR = 32 * NW;
-    const size_t smem = (size_t(NR) * (NR + 1) + 2 * NR + 2 * NW) * sizeof(double);
+    const size_t smem = (size_t(NR) * (NR + 1) + 2 * NR + size_t(CS) * NR + 2 * NW) * sizeof(double);
     static bool attr = false;
     if (!attr) {
-        ATK_CUDA(cudaFuncSetAttribute(trd_small_kernel<NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        ATK_CUDA(cudaFuncSetAttribute(trd_small_kernel<NW, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(smem)));
         attr = true;
     }
-    trd_small_kernel<NW><<<1, NW * 32, smem, ctx->stream>>>(a, n, lda, hh, d, e, tau, scal);
+    trd_small_kernel<NW, CS><<<1, NW * CS * 32, smem, ctx->stream>>>(a, n, lda, hh, d, e, tau, scal);
     ATK_LAUNCHED(ctx);
+}
+
+template <int NW>
+void launch_trd_small_cs(atk_ctx* ctx, const double* a, int n, int lda, double* hh, double* d, double* e,
+                         double* tau, double* scal) {
+    static const int cs = std::getenv("ATK_TRD_CS") ? std::atoi(std::getenv("ATK_TRD_CS")) : 2;  // probe knob
+    if (cs == 1) launch_trd_small<NW, 1>(ctx, a, n, lda, hh, d, e, tau, scal);
+    else if (cs == 4) launch_trd_small<NW, 4>(ctx, a, n, lda, hh, d, e, tau, scal);
+    else launch_trd_small<NW, 2>(ctx, a, n, lda, hh, d, e, tau, scal);
 }
 
 template <int NT>
@@ -929,10 +959,10 @@ void trd_backtr(atk_ctx* ctx, bool trd, const double* a, int n, int lda, double*
     // 69 / 168 / 320 us against the tile kernel's 108 / 229 / 411 us)
     if (trd && ctx->trd_tiles == 1 && n <= 128) {
         switch ((n + 31) / 32) {
-            case 1: launch_trd_small<1>(ctx, a, n, lda, hh, d, e, tau, scal); break;
-            case 2: launch_trd_small<2>(ctx, a, n, lda, hh, d, e, tau, scal); break;
-            case 3: launch_trd_small<3>(ctx, a, n, lda, hh, d, e, tau, scal); break;
-            default: launch_trd_small<4>(ctx, a, n, lda, hh, d, e, tau, scal); break;
+            case 1: launch_trd_small_cs<1>(ctx, a, n, lda, hh, d, e, tau, scal); break;
+            case 2: launch_trd_small_cs<2>(ctx, a, n, lda, hh, d, e, tau, scal); break;
+            case 3: launch_trd_small_cs<3>(ctx, a, n, lda, hh, d, e, tau, scal); break;
+            default: launch_trd_small_cs<4>(ctx, a, n, lda, hh, d, e, tau, scal); break;
         }
         return;
     }
