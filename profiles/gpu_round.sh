@@ -22,7 +22,7 @@ for p in $PARTS; do
     launches) ATK_PROFILE_NONCOOP=1 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv python profiles/run_step.py ${CFG:-c5} 1 > gpurun_out/${TAG}_launches.log 2>&1; echo "launches=$?";;
     traffic) timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:"gram_tf32_2cta|gram2_reduce" --csv --log-file gpurun_out/${TAG}_gramtraffic.csv python profiles/run_step.py c5 1 > gpurun_out/${TAG}_traffic.log 2>&1; echo "traffic=$?"; python profiles/make_traffic.py gpurun_out/${TAG}_gramtraffic.csv gpurun_out/${TAG}_gram_traffic.json | head -c 300; echo;;
     ncueig) timeout 600 ncu --set full --clock-control none --import-source on -k regex:"trd_|invit_kernel|bisect_kernel|backtr_kernel|dgemm_tile|chol_inv" -c 8 -o gpurun_out/${TAG}_eig python profiles/run_step.py c5 1 > gpurun_out/${TAG}_ncueig.log 2>&1; echo "ncueig=$?";;
-    ncucheb) timeout 600 ncu --set full --clock-control none --import-source on -k regex:"cheb_filter" -c 2 -o gpurun_out/${TAG}_cheb python profiles/run_step.py c2 1 > gpurun_out/${TAG}_ncucheb.log 2>&1; echo "ncucheb=$?";;
+    ncucheb) ATK_PROFILE_NONCOOP=1 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"cheb_" -c 2 -o gpurun_out/${TAG}_cheb python profiles/run_step.py c2 1 > gpurun_out/${TAG}_ncucheb.log 2>&1; echo "ncucheb=$?";;
     ncu) timeout 900 ncu --set full --clock-control none --import-source on -k regex:"gram_tf32_2cta|ttm_tf32" -c 2 -o gpurun_out/${TAG}_full python profiles/run_step.py c5 1 > gpurun_out/${TAG}_ncu.log 2>&1; echo "ncu=$?";;
   esac
 done
