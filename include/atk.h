@@ -144,6 +144,8 @@ uint64_t atk_ctx_launch_count(const atk_ctx* ctx);
  *   "als_head"      -1 = one-pass ALS: phase 1 and phase 2 of a tile in turn (default); k >= 0 interleaves
  *                   tile t+1's phase 1 with t's phase 2, k K-blocks first (measured slower)
  *   "chfsi_lock"    1 = ChFSI locks converged Ritz pairs and filters the rest with a deflated S (default)
+ *   "cheb_dataflow" 0 = resident Chebyshev steps end in a grid barrier (default); 1 = per-CTA ready flags
+ *                   (each CTA waits only for the producers of its K slice; measured slower)
  *   "lanczos_tiles" 1 = the ChFSI bounds Lanczos keeps S in a 16-CTA cluster's shared memory (n <= ~1250;
  *                   default), 0 = re-read S from L2 every step
  *   "als_fused"     1 = an ALS iteration on mode 0 (fp32, R <= 32) reads Y once: rfac, YR and GR

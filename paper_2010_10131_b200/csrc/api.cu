@@ -224,6 +224,7 @@ atk_status atk_ctx_set_option(atk_ctx* ctx, const char* key, double value) {
         else if (k == "chfsi_tol") ctx->chfsi_tol = value;
         else if (k == "cheb_fused") ctx->cheb_fused = int(value);
         else if (k == "lanczos_tiles") ctx->lanczos_tiles = int(value);
+        else if (k == "cheb_dataflow") ctx->cheb_dataflow = int(value);
         else if (k == "chfsi_lock") ctx->chfsi_lock = int(value);
         else if (k == "als_head") ctx->als_head = int(value);
         else if (k == "als_fused") ctx->als_fused = int(value);

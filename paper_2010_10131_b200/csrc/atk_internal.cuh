@@ -60,6 +60,8 @@ struct atk_ctx {
     int als_head = -1;         // option "als_head": one-pass ALS, >= 0 interleaves tile t+1's phase 1 with t's phase 2
                                // (that many K-blocks first); measured slower (C2: 1.63 vs 1.31 ms per iteration)
     int chfsi_lock = 1;        // option "chfsi_lock": lock converged Ritz pairs, filter a deflated S
+    int cheb_dataflow = 0;     // option "cheb_dataflow": resident Chebyshev steps synchronised by per-CTA ready
+                               // flags instead of a grid barrier (measured slower: 14.0 vs 12.5 us per step)
     int lanczos_tiles = 1;     // option "lanczos_tiles": S resident in a 16-CTA cluster's smem for the bounds
     int als_fused = 1;         // option "als_fused": one pass over Y per ALS iteration (mode 0, fp32)
     int trd_tiles = 1;         // option "trd_tiles": 32 x 32-tile tridiagonalisation for n <= 192

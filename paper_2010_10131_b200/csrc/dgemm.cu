@@ -246,6 +246,7 @@ struct ChebResArgs {
     int ncols;               // padded block width (8 NF, NF = wn FN)
     double* y[4];
     unsigned* bar;
+    unsigned* ready;         // per-CTA count of Y steps written (dataflow mode), or null: grid barrier
     double a1, b1, a, b, c;
 };
 
@@ -261,7 +262,7 @@ __global__ void __launch_bounds__(512) cheb_resident_kernel(const ChebResArgs p)
     const int ldk = p.ldk, kc = p.kc, n = p.n, k = p.k, rows = p.rows, ncols = p.ncols;
     double* At = rsm;                  // rows x ldk:  S(m0 + m, kb + kk)
     double* Bt = At + rows * ldk;      // ncols x ldk: Y(kb + kk, c)
-    double* P = Bt + ncols * ldk;      // ncols x rows partial, P[c * rows + m]
+    double* Pbuf = Bt + ncols * ldk;   // [2] ncols x rows partials, P[c * rows + m] (by step parity)
     const uint32_t rank = blockIdx.x % RS_CS;
     const int strip = blockIdx.x / RS_CS;
     const int m0 = strip * rows, kb = int(rank) * kc;
@@ -279,8 +280,28 @@ __global__ void __launch_bounds__(512) cheb_resident_kernel(const ChebResArgs p)
     const int fr = lane >> 2, fk = lane & 3;
     const int mr = rows / RS_CS;  // rows this CTA finishes
     int iprev = 0, icur = 0, inext = 1;
+    // dataflow mode: the CTAs that write rows [kb, kb + kc) of Y (a contiguous
+    // id range: row g is finished by CTA (g / rows) * 8 + (g % rows) / mr)
+    const int kend = min(n, kb + kc);
+    const int prod0 = kb < n ? (kb / rows) * RS_CS + (kb % rows) / mr : 0;
+    const int prod1 = kb < n ? ((kend - 1) / rows) * RS_CS + ((kend - 1) % rows) / mr : -1;
     for (int step = 0; step < p.deg; ++step) {
         const double* ycur = step == 0 ? p.y[0] : p.y[icur];
+        double* P = Pbuf + size_t(step & 1) * ncols * rows;
+        if (p.ready && step > 0) {
+            // wait for the producers of this CTA's K slice of Y_step (release/acquire
+            // counters); the cluster barrier below then orders this step after every
+            // CTA's step - 1 (the union of the cluster's slices is all of Y), which
+            // is what the buffer rotation and the partial double-buffer rely on
+            if (warp == 0)
+                for (int q = prod0 + lane; q <= prod1; q += 32) {
+                    unsigned v;
+                    do {
+                        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.ready + q) : "memory");
+                    } while (v < unsigned(step));
+                }
+            __syncthreads();
+        }
         for (int e = tid; e < ncols * hk; e += nt) {
             const int cc = e / hk, kk = 2 * (e % hk);
             const int gk = kb + kk;
@@ -366,8 +387,16 @@ __global__ void __launch_bounds__(512) cheb_resident_kernel(const ChebResArgs p)
             const int m = off[u] % rows, cc = off[u] / rows;
             ynext[(m0 + m) + size_t(n) * cc] = fma(ca, sum, base[u]);
         }
-        // Y_{j+1} complete everywhere (also frees P and Bt for the next step)
-        grid_barrier_ra(p.bar, gridDim.x);
+        if (p.ready) {
+            // publish: this CTA's rows of Y_{step+1} are written
+            __syncthreads();
+            if (tid == 0)
+                asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.ready + blockIdx.x), "r"(unsigned(step + 1))
+                             : "memory");
+        } else {
+            // Y_{j+1} complete everywhere (also frees P and Bt for the next step)
+            grid_barrier_ra(p.bar, gridDim.x);
+        }
         if (step == 0) {
             iprev = 0; icur = 1; inext = 2;
         } else {
@@ -375,6 +404,9 @@ __global__ void __launch_bounds__(512) cheb_resident_kernel(const ChebResArgs p)
             iprev = icur; icur = inext; inext = spare;
         }
     }
+    // no CTA may exit while a cluster peer can still read its partials through
+    // DSMEM (dataflow mode has no closing grid barrier)
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 // Small outputs: G lanes per element (G | 32), lane t sums splits t, t+G, ...
@@ -551,14 +583,17 @@ bool cheb_resident(atk_ctx* ctx, const double* S, int n, int k, int deg, double*
     if ((rows / RS_CS) * k > RS_EPT * 32 * warps) return false;  // reduction: <= RS_EPT elements per thread
     const int kc = ((n + RS_CS - 1) / RS_CS + 3) / 4 * 4;  // K slice per CTA, a multiple of 4
     const int ldk = kc + 4 + (16 - (kc + 4) % 16 + 4) % 16;   // = 4 (mod 16)
-    const size_t smem = (size_t(rows) * ldk + size_t(8 * nf) * ldk + size_t(8 * nf) * rows) * sizeof(double);
+    const size_t smem = (size_t(rows) * ldk + size_t(8 * nf) * ldk + size_t(2) * (8 * nf) * rows) * sizeof(double);
     if (std::getenv("ATK_TRACE"))
         std::fprintf(stderr, "[atk cheb_resident n=%d k=%d] clusters %d/%d rows %d warps %dx%d frag %dx%d smem %zu\n",
                      n, k, strips, max_clusters, rows, wm, wn, fm, fn, smem);
     if (smem > 200 * 1024) return false;
-    DevBuf<unsigned> bar(ctx, 2);
-    ATK_CUDA(cudaMemsetAsync(bar.get(), 0, 2 * sizeof(unsigned), ctx->stream));
-    const ChebResArgs p{S, n, k, deg, kc, ldk, rows, wm, 8 * nf, {y[0], y[1], y[2], y[3]}, bar.get(), a1, b1, a, b, c};
+    const int ncta = strips * RS_CS;
+    DevBuf<unsigned> bar(ctx, 2 + size_t(ncta));
+    ATK_CUDA(cudaMemsetAsync(bar.get(), 0, (2 + size_t(ncta)) * sizeof(unsigned), ctx->stream));
+    const ChebResArgs p{S,  n,  k,        deg,   kc,    ldk,  rows,
+                        wm, 8 * nf,       {y[0], y[1], y[2], y[3]},   bar.get(),
+                        ctx->cheb_dataflow ? bar.get() + 2 : nullptr, a1,   b1,   a, b, c};
     if (fm == 3 && fn == 3) return cheb_resident_max_clusters<3, 3>() && cheb_resident_launch<3, 3>(ctx, p, strips, smem, warps);
     if (fm == 3 && fn == 2) return cheb_resident_launch<3, 2>(ctx, p, strips, smem, warps);
     if (fm == 2 && fn == 3) return cheb_resident_max_clusters<2, 3>() && cheb_resident_launch<2, 3>(ctx, p, strips, smem, warps);
