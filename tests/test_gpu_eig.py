@@ -161,3 +161,24 @@ def test_chfsi_indefinite_lanczos(tiles):
         _check(s, r, atucker.sym_eig_top_r(s, r, ctx=ctx), vec_tol=1e-6)
     finally:
         ctx.set_option("lanczos_tiles", 1)
+
+
+def test_chfsi_cheb_dataflow():
+    """The resident Chebyshev filter with per-CTA ready flags instead of the grid
+    barrier (option cheb_dataflow) on a flat spectrum: same bars as the default."""
+    from paper_2010_10131_b200 import atucker
+
+    ctx = atucker.Context.default(0)
+    ctx.set_option("eig_assume_psd", 1.0)
+    ctx.set_option("cheb_dataflow", 1)
+    try:
+        n, r = 640, 32
+        rng = np.random.default_rng(5)
+        q = np.linalg.qr(rng.standard_normal((n, n)))[0]
+        lam = np.sort(1.0 + 0.3 * rng.random(n))[::-1]
+        s = (q * lam) @ q.T
+        s = (s + s.T) / 2
+        _check(s, r, atucker.sym_eig_top_r(s, r, ctx=ctx), vec_tol=1e-5)
+    finally:
+        ctx.set_option("cheb_dataflow", 0)
+        ctx.set_option("eig_assume_psd", 0.0)
