@@ -255,8 +255,7 @@ __device__ __forceinline__ void lt_tile_of(int t, int& I, int& J) {  // t = I (I
 }
 
 __global__ void __launch_bounds__(kLtThreads) lanczos_tiles(const double* __restrict__ S, int n, int m, int per,
-                                                            double* __restrict__ q, double* __restrict__ part,
-                                                            double* __restrict__ alpha,
+                                                            double* __restrict__ q, double* __restrict__ alpha,
                                                             double* __restrict__ beta) {
     extern __shared__ __align__(16) float lsm[];
     const int nb = (n + 31) / 32, ntiles = nb * (nb + 1) / 2;
@@ -598,7 +597,7 @@ void lanczos_l2(atk_ctx* ctx, const double* S, int n, int m, double* q, double* 
 Bounds lanczos_bounds(atk_ctx* ctx, const double* S, int n, bool psd) {
     cudaStream_t st = ctx->stream;
     const int m = std::min(n, 40);
-    DevBuf<double> q(ctx, n), qp(ctx, n), w(ctx, n), part(ctx, 3 * std::max(kLzCluster, kLtCluster)), al(ctx, m),
+    DevBuf<double> q(ctx, n), qp(ctx, n), w(ctx, n), part(ctx, 3 * kLzCluster), al(ctx, m),
         be(ctx, m), tv(ctx, m), tz(ctx, 2 * size_t(m)), nrm(ctx, 1);
     ATK_CUDA(cudaMemsetAsync(qp.get(), 0, n * sizeof(double), st));
     fill_normalish<<<nblk(n), 256, 0, st>>>(q.get(), n, 0x5eed1234ULL);
@@ -643,8 +642,8 @@ Bounds lanczos_bounds(atk_ctx* ctx, const double* S, int n, bool psd) {
         cfg.stream = st;
         cfg.attrs = &at;
         cfg.numAttrs = 1;
-        ATK_CUDA(cudaLaunchKernelEx(&cfg, lanczos_tiles, static_cast<const double*>(S), n, m, per, q.get(),
-                                    part.get(), al.get(), be.get()));
+        ATK_CUDA(cudaLaunchKernelEx(&cfg, lanczos_tiles, static_cast<const double*>(S), n, m, per, q.get(), al.get(),
+                                    be.get()));
         ATK_LAUNCHED(ctx);
     } else {
         lanczos_l2(ctx, S, n, m, q.get(), qp.get(), w.get(), part.get(), al.get(), be.get());
