@@ -216,7 +216,9 @@ void tridiag_eig(atk_ctx* ctx, const double* a, int n, int lda, int nwant, doubl
 void cholesky(atk_ctx* ctx, double* a, int n, int* info_dev);
 // Shared-memory Cholesky of G (k x k, k <= kJacobiMax) fused with X = L^{-T};
 // *info_dev = 0 or 1 + failing pivot.
-void cholesky_inv_t(atk_ctx* ctx, const double* g, int k, double* x, int* info_dev);
+// identity_tol > 0: if max |G - I| <= identity_tol, X = I exactly (the last
+// CholeskyQR pass on an already orthonormal block)
+void cholesky_inv_t(atk_ctx* ctx, const double* g, int k, double* x, int* info_dev, double identity_tol = 0.0);
 // Q (m x n, n <= kJacobiMax) = orthonormal basis of span(A) by shifted
 // CholeskyQR3; false if a Cholesky pivot failed (caller falls back).
 bool orthonormal_basis_cholqr(atk_ctx* ctx, const double* a, int m, int n, double* q);

@@ -557,8 +557,19 @@ bool cholqr3(atk_ctx* ctx, const double* Y, int n, int k, double* V, Ws& ws) {
         if (pass == 0) {
             add_shift<<<1, 128, 0, ctx->stream>>>(ws.G.get(), k, n);
             ATK_LAUNCHED(ctx);
+        } else if (std::getenv("ATK_TRACE_QR")) {  // orthogonality defect entering this pass
+            std::vector<double> g(size_t(k) * k);
+            ATK_CUDA(cudaStreamSynchronize(ctx->stream));
+            ATK_CUDA(cudaMemcpy(g.data(), ws.G.get(), g.size() * sizeof(double), cudaMemcpyDeviceToHost));
+            double mx = 0.0;
+            for (int c = 0; c < k; ++c)
+                for (int r = 0; r < k; ++r) mx = std::max(mx, std::fabs(g[r + size_t(k) * c] - (r == c ? 1.0 : 0.0)));
+            std::fprintf(stderr, "[atk cholqr n=%d k=%d] pass %d: max|G - I| = %.3e\n", n, k, pass, mx);
         }
-        cholesky_inv_t(ctx, ws.G.get(), k, ws.M.get(), ws.info.get() + pass);
+        // the third pass is the identity when the second already left the block
+        // orthonormal to ~1e-16 (C2's filtered blocks, measured); then X = I and
+        // the apply below is an exact copy
+        cholesky_inv_t(ctx, ws.G.get(), k, ws.M.get(), ws.info.get() + pass, pass == 2 ? 1e-14 : 0.0);
         dgemm(ctx, false, false, n, k, k, 1.0, src, n, ws.M.get(), k, 0.0, dst, n);
         src = dst;
     }

@@ -339,12 +339,28 @@ namespace {
 // One CTA, k <= 112.  info = 0 on success, else 1 + the failing pivot
 // (linalg.hpp:169-177 NotSPD).
 __global__ void __launch_bounds__(1024) chol_inv_kernel(const double* __restrict__ g, int k,
-                                                        double* __restrict__ x, int* __restrict__ info) {
+                                                        double* __restrict__ x, int* __restrict__ info,
+                                                        double identity_tol) {
     extern __shared__ double sm[];
     const int ld = k + 1;
     double* A = sm;                  // k x k, upper triangle live
     double* W = A + size_t(ld) * k;  // k x k, becomes L^{-1} (unscaled rows)
     const int tid = threadIdx.x, nt = blockDim.x;
+    if (identity_tol > 0.0) {  // uniform
+        double dev = 0.0;
+        for (int e = tid; e < k * k; e += nt) dev = fmax(dev, fabs(g[e] - ((e % k) == (e / k) ? 1.0 : 0.0)));
+        for (int o = 16; o > 0; o >>= 1) dev = fmax(dev, __shfl_xor_sync(0xffffffffu, dev, o));
+        if ((tid & 31) == 0) sm[tid >> 5] = dev;
+        __syncthreads();
+        dev = 0.0;
+        for (int q = 0; q < (nt >> 5); ++q) dev = fmax(dev, sm[q]);
+        __syncthreads();
+        if (dev <= identity_tol) {
+            for (int e = tid; e < k * k; e += nt) x[e] = ((e % k) == (e / k)) ? 1.0 : 0.0;
+            if (tid == 0) *info = 0;
+            return;
+        }
+    }
     for (int e = tid; e < k * k; e += nt) {
         const int i = e % k, j = e / k;
         A[i + ld * j] = g[e];
@@ -392,7 +408,7 @@ __global__ void __launch_bounds__(1024) chol_inv_kernel(const double* __restrict
 
 }  // namespace
 
-void cholesky_inv_t(atk_ctx* ctx, const double* g, int k, double* x, int* info_dev) {
+void cholesky_inv_t(atk_ctx* ctx, const double* g, int k, double* x, int* info_dev, double identity_tol) {
     if (k > kJacobiMax) fail(ATK_UNSUPPORTED, "cholesky_inv_t: k too large");
     const size_t smem = size_t(2) * (k + 1) * k * sizeof(double);
     static bool attr = false;
@@ -405,7 +421,7 @@ void cholesky_inv_t(atk_ctx* ctx, const double* g, int k, double* x, int* info_d
     static const int th_env = std::getenv("ATK_CHOL_THREADS") ? std::atoi(std::getenv("ATK_CHOL_THREADS")) : 0;
     if (th_env >= 32 && th_env <= 1024) threads = th_env / 32 * 32;  // probe knob
     threads = std::max(threads, 32 * ((k + 3) / 4));                  // <= 4 columns per warp (kernel unroll)
-    chol_inv_kernel<<<1, threads, smem, ctx->stream>>>(g, k, x, info_dev);
+    chol_inv_kernel<<<1, threads, smem, ctx->stream>>>(g, k, x, info_dev, identity_tol);
     ATK_LAUNCHED(ctx);
 }
 
