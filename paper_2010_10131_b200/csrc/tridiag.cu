@@ -513,7 +513,43 @@ __global__ void __launch_bounds__(1024) backtr_kernel(const double* __restrict__
         const int i = lane + 32 * s;
         x[s] = i < n ? X[size_t(n) * c + i] : 0.0;
     }
-    for (int k = n - 3; k >= 0; --k) {
+    // reflectors in pairs (H_{k-1} H_k x): the three dots a.x, b.x, b.a are reduced
+    // together, so each pair costs one warp-reduction latency instead of two
+    int k = n - 3;
+    for (; k >= 1; k -= 2) {
+        const double ta = ts[k], tb = ts[k - 1];
+        if (ta == 0.0 && tb == 0.0) continue;
+        const double sa = ts[n + k], sb = ts[n + k - 1];
+        const int ca = pk(k, k, n) - k, cb = pk(k - 1, k - 1, n) - (k - 1);
+        const int s0 = k >> 5;
+        double va[S], vb[S], da = 0.0, db = 0.0, dab = 0.0;
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            va[s] = 0.0;
+            vb[s] = 0.0;
+            if (s >= s0) {  // warp-uniform
+                const int i = lane + 32 * s;
+                const double ha = H[ca + i] * sa, hb = H[cb + i] * sb;
+                va[s] = (i == k + 1) ? 1.0 : (i > k + 1 && i < n) ? ha : 0.0;  // pad rows stay 0
+                vb[s] = (i == k) ? 1.0 : (i > k && i < n) ? hb : 0.0;
+                da = fma(va[s], x[s], da);
+                db = fma(vb[s], x[s], db);
+                dab = fma(vb[s], va[s], dab);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            da += __shfl_xor_sync(0xffffffffu, da, o);
+            db += __shfl_xor_sync(0xffffffffu, db, o);
+            dab += __shfl_xor_sync(0xffffffffu, dab, o);
+        }
+        const double c1 = ta * da;                  // H_k:     x -= c1 a
+        const double c2 = tb * fma(-c1, dab, db);   // H_{k-1}: x -= c2 b, with b.(x - c1 a)
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+            if (s >= s0) x[s] = fma(-c2, vb[s], fma(-c1, va[s], x[s]));
+    }
+    for (; k >= 0; --k) {  // the odd one left (k = 0)
         const double tk = ts[k];
         if (tk == 0.0) continue;
         const double sk = ts[n + k];
