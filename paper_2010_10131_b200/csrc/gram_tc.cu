@@ -247,6 +247,30 @@ __global__ void gram_reduce(const double* __restrict__ acc, const int* __restric
     }
 }
 
+// Small Grams (I <= 256, many split partials: C4's 48 x 5.3M): 32 lanes per
+// element, lane t sums splits t, t+32, ... in order, then a fixed xor tree.  The
+// one-thread-per-element loop was a chain of ~150 L2 round trips (34 us at I = 48).
+__global__ void gram_reduce_lanes(const double* __restrict__ acc, const int* __restrict__ tile_unit, int splits,
+                                  int ntn, int I, double* __restrict__ s) {
+    const size_t gid = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const size_t e = gid >> 5;
+    const int t = int(gid & 31);
+    const size_t n = size_t(I) * I;
+    const int i = e < n ? int(e % I) : 0, j = e < n ? int(e / I) : 0;
+    const bool live = e < n && i <= j;
+    double v = 0.0;
+    if (live) {
+        const int u0 = tile_unit[(i / BM) * ntn + (j / BN)];
+        const size_t off = size_t(j % BN) * BM + (i % BM);
+        for (int k = t; k < splits; k += 32) v += acc[size_t(u0 + k) * BM * BN + off];
+    }
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (live && t == 0) {
+        s[size_t(i) + size_t(I) * j] = v;
+        s[size_t(j) + size_t(I) * i] = v;
+    }
+}
+
 }  // namespace
 
 CUresult encode_tensor_map(CUtensorMap* map, CUtensorMapDataType dt, uint32_t rank, void* base,
@@ -380,8 +404,12 @@ void tc_gram(atk_ctx* ctx, const atk_tensor* x, int mode, double* s_dev) {
     gram_tf32_kernel<<<grid, THREADS, SMEM_BYTES, ctx->stream>>>(ta, tb, prm);
     ATK_LAUNCHED(ctx);
     const size_t n = size_t(I) * I;
-    gram_reduce<<<unsigned(std::min<size_t>((n + 255) / 256, size_t(ctx->num_sms) * 8)), 256, 0, ctx->stream>>>(
-        acc.get(), dtu.get(), splits, ntn, I, s_dev);
+    if (I <= 256 && splits >= 8)
+        gram_reduce_lanes<<<unsigned((n * 32 + 255) / 256), 256, 0, ctx->stream>>>(acc.get(), dtu.get(), splits, ntn,
+                                                                                  I, s_dev);
+    else
+        gram_reduce<<<unsigned(std::min<size_t>((n + 255) / 256, size_t(ctx->num_sms) * 8)), 256, 0, ctx->stream>>>(
+            acc.get(), dtu.get(), splits, ntn, I, s_dev);
     ATK_LAUNCHED(ctx);
 }
 
