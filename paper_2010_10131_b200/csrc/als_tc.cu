@@ -297,15 +297,28 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
 }
 
-// YR (I x R) = fixed-order sum of the per-CTA partials
-__global__ void als_reduce(const double* __restrict__ acc_yr, int ncta, int I, int R, double* __restrict__ yr) {
-    const size_t n1 = size_t(I) * R;
-    for (size_t e = size_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n1; e += size_t(gridDim.x) * blockDim.x) {
-        const int i = int(e % I), r = int(e / I);
-        double v = 0.0;
-        for (int c = 0; c < ncta; ++c) v += acc_yr[(size_t(c) * I + i) * NB + r];
-        yr[e] = v;
+// YR (I x R) = sum of the per-CTA partials [cta][I][NB]: one 128-thread block
+// per row i, lane = r (a warp reads one contiguous 256-byte row per CTA), warp g
+// sums CTAs g, g+4, ... in order (8 loads in flight), then the 4 warp partials in
+// order (deterministic).  Element-per-thread loops were 148-deep chains of
+// uncoalesced L2 reads (30 us per call at C2's I = 1024).
+__global__ void __launch_bounds__(128) als_reduce_rows(const double* __restrict__ acc_yr, int ncta, int I, int R,
+                                                       double* __restrict__ yr) {
+    __shared__ double part[4][NB];
+    const int i = blockIdx.x, lane = threadIdx.x & 31, g = threadIdx.x >> 5;
+    double v = 0.0;
+    int c = g;
+    for (; c + 28 < ncta; c += 32) {
+        double t[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) t[u] = acc_yr[(size_t(c + 4 * u) * I + i) * NB + lane];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v += t[u];
     }
+    for (; c < ncta; c += 4) v += acc_yr[(size_t(c) * I + i) * NB + lane];
+    part[g][lane] = v;
+    __syncthreads();
+    if (g == 0 && lane < R) yr[i + size_t(I) * lane] = ((part[0][lane] + part[1][lane]) + part[2][lane]) + part[3][lane];
 }
 
 // F[i + I r] = M(r, i) (fp32), rows r >= R zero: the K-major B operand of phase 1
@@ -373,9 +386,7 @@ void als_fused_pass(atk_ctx* ctx, const atk_tensor* y, const double* m_dev, uint
     }
     als_pass_kernel<<<grid, THREADS, smem, ctx->stream>>>(tyk, tym, tf, p);
     ATK_LAUNCHED(ctx);
-    const size_t n = size_t(I) * R;
-    als_reduce<<<unsigned(std::min<size_t>((n + 255) / 256, size_t(ctx->num_sms) * 4)), 256, 0, ctx->stream>>>(
-        ayr.get(), grid, I, int(R), yr_dev);
+    als_reduce_rows<<<unsigned(I), 128, 0, ctx->stream>>>(ayr.get(), grid, I, int(R), yr_dev);
     ATK_LAUNCHED(ctx);
     // GR = rfac rfac^T = M (Y_(0) rfac^T) = M YR, exactly symmetrised
     dgemm(ctx, false, false, int(R), int(R), I, 1.0, m_dev, int(R), yr_dev, I, 0.0, gr_dev, int(R));
