@@ -54,7 +54,10 @@ struct atk_ctx {
     cudaStream_t own_stream = nullptr;
     uint64_t launches = 0;
     int force_simt = 0;        // option "simt": portable CUDA-core contractions
-    int eig_method = -1;       // option "eig_method": -1 auto, 0 dense Jacobi, 1 ChFSI, 2 tridiagonal
+    int eig_method = -1;       // option "eig_method": -1 auto, 0 dense Jacobi, 1 ChFSI, 2 tridiagonal,
+                               // 3 tridiagonal at every n (the grid-wide reduction above 200)
+    int eig_dense_passes = 3;  // option "eig_dense_passes": ChFSI filter passes before the exact dense
+                               // solver takes over (n > 200; -1 never)
     double chfsi_tol = 1e-12;  // option "chfsi_tol": relative Ritz residual target
     int cheb_fused = 1;        // option "cheb_fused": whole Chebyshev filter in one cooperative launch
     int als_head = -1;         // option "als_head": one-pass ALS, >= 0 interleaves tile t+1's phase 1 with t's phase 2
@@ -212,6 +215,17 @@ constexpr int kTridiagMax = 200;
 void tridiag_extreme_eig(atk_ctx* ctx, const double* d, const double* e, int m, double* values, double* vectors);
 void tridiag_eig(atk_ctx* ctx, const double* a, int n, int lda, int nwant, double* values, double* vectors,
                  int ldv, int nvals = 0);
+// Bisection (top nvals, descending) + inverse iteration (top nwant vectors of T,
+// X: n x nwant, wk: 5 n nwant doubles) on the tridiagonal (d, e).
+void tridiag_tail(atk_ctx* ctx, const double* d, const double* e, int n, int nvals, int nwant, double* values,
+                  double* X, double* wk);
+// trd_big.cu — the same solver for kTridiagMax < n <= kBigEigMax with the
+// reduction spread over every SM (one persistent cooperative CTA per SM):
+// bounded time on any spectrum; vectors n x nwant (ldv), signs NOT fixed.
+constexpr int kBigEigMax = 4096;
+void dense_eig_big(atk_ctx* ctx, const double* a, int n, int lda, int nwant, double* values, double* vectors,
+                   int ldv, bool exact_sym);
+size_t smem_cap_bytes();  // opt-in shared memory per block
 // Cholesky factorization in place (lower), status written to *info_dev (0 ok, k>0 pivot k).
 void cholesky(atk_ctx* ctx, double* a, int n, int* info_dev);
 // Shared-memory Cholesky of G (k x k, k <= kJacobiMax) fused with X = L^{-T};

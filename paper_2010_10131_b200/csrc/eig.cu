@@ -705,13 +705,26 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
                       bool psd, double tol, bool exact_sym) {
     EigInfo info;
     cudaStream_t st = ctx->stream;
-    if (n <= kTridiagMax && (ctx->eig_method == -1 || ctx->eig_method == 2)) {
+    if (n <= kTridiagMax && (ctx->eig_method == -1 || ctx->eig_method >= 2)) {
         tridiag_eig(ctx, s_dev, n, n, r, values_dev, vectors_dev, n);
         fix_signs(ctx, vectors_dev, n, r, n);
         if (std::getenv("ATK_TRACE")) std::fprintf(stderr, "[atk eig n=%d r=%d] tridiagonal\n", n, r);
         info.method = 2;
         return info;
     }
+    // exact dense path above 200 (trd_big.cu): on request, or when the ChFSI block
+    // cannot hold r + a guard band (r > kJacobiMax)
+    auto dense_big = [&](const char* why) {
+        dense_eig_big(ctx, s_dev, n, n, r, values_dev, vectors_dev, n, exact_sym);
+        fix_signs(ctx, vectors_dev, n, r, n);
+        if (std::getenv("ATK_TRACE")) std::fprintf(stderr, "[atk eig n=%d r=%d] dense tridiagonal (%s)\n", n, r, why);
+        info.method = 3;
+        return info;
+    };
+    if (n <= kBigEigMax && (ctx->eig_method == 3 || ctx->eig_method == 2)) return dense_big("requested");
+    if (n <= kBigEigMax && ctx->eig_method != 1 && std::min(n, r + std::max(16, r / 4)) > kJacobiMax &&
+        !(n <= kJacobiMax || (psd && n <= kJacobiPsdMax)))
+        return dense_big("r too large for the ChFSI block");
     const bool dense = (n <= kJacobiMax || (psd && n <= kJacobiPsdMax)) && ctx->eig_method != 1;
     if (dense) {
         DevBuf<double> vals(ctx, n), vecs(ctx, size_t(n) * n);
@@ -829,6 +842,12 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
         worst = 0.0;
         for (int j = 0; j < r; ++j) worst = std::max(worst, hres[j]);
         if (!(scale > 0.0) || worst <= tol * scale || it >= max_outer) break;
+        // pass budget spent (flat spectrum): the exact dense solver's cost is bounded
+        if (ctx->eig_dense_passes >= 0 && it >= ctx->eig_dense_passes && n <= kBigEigMax &&
+            ctx->eig_method == -1) {
+            mark("to-dense", it, worst / scale);
+            return dense_big("ChFSI pass budget");
+        }
         if (!have_bounds) {
             if (trace)
                 std::fprintf(stderr, "[atk eig n=%d r=%d k=%d] theta_1 %.6e theta_r %.6e theta_k %.6e\n", n, r, k,

@@ -1046,6 +1046,17 @@ void tridiag_extreme_eig(atk_ctx* ctx, const double* d, const double* e, int m, 
     ATK_LAUNCHED(ctx);
 }
 
+void tridiag_tail(atk_ctx* ctx, const double* d, const double* e, int n, int nvals, int nwant, double* values,
+                  double* X, double* wk) {
+    const int wpb = 8;
+    bisect_kernel<<<unsigned((nvals + wpb - 1) / wpb), 32 * wpb, size_t(n) * sizeof(double), ctx->stream>>>(
+        d, e, n, nvals, values);
+    ATK_LAUNCHED(ctx);
+    if (nwant == 0) return;
+    invit_kernel<<<unsigned((nwant + wpb - 1) / wpb), 32 * wpb, 0, ctx->stream>>>(d, e, n, values, nwant, X, wk);
+    ATK_LAUNCHED(ctx);
+}
+
 void tridiag_eig(atk_ctx* ctx, const double* a, int n, int lda, int nwant, double* values, double* vectors,
                  int ldv, int nvals) {
     if (n < 1 || n > kTridiagMax) fail(ATK_UNSUPPORTED, "tridiag_eig: n out of range");
