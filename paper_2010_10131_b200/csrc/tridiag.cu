@@ -486,6 +486,155 @@ __global__ void __launch_bounds__(256) invit_kernel(const double* __restrict__ d
     }
 }
 
+// The same inverse iteration for large n (the dense path of trd_big.cu): ONE CTA
+// per cluster.  Members are solved in parallel (one thread each, factors
+// interleaved by member so a warp's loads are contiguous), then the whole CTA
+// orthonormalises them in order by classical Gram-Schmidt with
+// re-orthogonalisation (CGS2): member q against the cluster's earlier members,
+// the dot products spread over the warps.  In exact arithmetic this is the
+// sequential Gram-Schmidt of invit_kernel / dstein; at n = 2048 with a flat
+// spectrum (one 64-member cluster) it is ~10x faster than one warp per cluster.
+constexpr int kIvT = 512;
+__device__ __forceinline__ double block_reduce(double v, double* red, bool is_max) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double x = __shfl_xor_sync(0xffffffffu, v, o);
+        v = is_max ? fmax(v, x) : v + x;
+    }
+    __syncthreads();  // red may still be read by the previous call
+    if (lane == 0) red[w] = v;
+    __syncthreads();
+    double s = is_max ? 0.0 : 0.0;
+    for (int q = 0; q < kIvT / 32; ++q) s = is_max ? fmax(s, red[q]) : s + red[q];
+    return s;
+}
+
+__global__ void __launch_bounds__(kIvT) invit_cta_kernel(const double* __restrict__ d, const double* __restrict__ e,
+                                                        int n, const double* __restrict__ lam, int nwant,
+                                                        double* __restrict__ X, double* __restrict__ wk) {
+    extern __shared__ double dsh[];  // nwant: dot products of the current member
+    __shared__ double red[kIvT / 32];
+    __shared__ TNorm tnsh;
+    const int j = blockIdx.x, t = threadIdx.x, lane = t & 31, w = t >> 5;
+    if (t < 32) {
+        const TNorm tn = tnorm_warp(d, e, n);
+        if (t == 0) tnsh = tn;
+    }
+    __syncthreads();
+    const TNorm tn = tnsh;
+    const double ortol = 1e-3 * tn.norm;
+    if (j > 0 && lam[j - 1] - lam[j] <= ortol) return;  // not a cluster leader (CTA-uniform)
+    int end = j + 1;
+    while (end < nwant && lam[end - 1] - lam[end] <= ortol) ++end;
+    const double pertol = 10.0 * DBL_EPSILON * fmax(tn.norm, DBL_MIN);
+    const double tiny = tn.norm > 0.0 ? DBL_EPSILON * tn.norm : 1.0;
+    for (int cb = j; cb < end; cb += kIvT) {
+        const int cs = min(kIvT, end - cb);
+        const int mm = cb + t;
+        const bool mine = t < cs;
+        const size_t st = size_t(cs);
+        double* base = wk + size_t(5) * n * cb + (mine ? t : 0);
+        double* dl = base;
+        double* dd = base + size_t(n) * st;
+        double* du = dd + size_t(n) * st;
+        double* du2 = du + size_t(n) * st;
+        double* pv = du2 + size_t(n) * st;
+        double* x = X + size_t(n) * (mine ? mm : j);
+        if (mine) {
+            double sh = lam[j];
+            for (int q = j + 1; q <= mm; ++q) sh = fmin(lam[q], sh - pertol);
+            double di = d[0] - sh, ui = n > 1 ? e[0] : 0.0;
+            for (int i = 0; i + 1 < n; ++i) {
+                const double li = e[i], dn = d[i + 1] - sh, un = i + 2 < n ? e[i + 1] : 0.0;
+                if (fabs(di) >= fabs(li)) {
+                    if (fabs(di) < tiny) di = copysign(tiny, di);
+                    const double r = 1.0 / di;
+                    const double f = li * r;
+                    dl[i * st] = f;
+                    dd[i * st] = r;
+                    du[i * st] = ui;
+                    du2[i * st] = 0.0;
+                    pv[i * st] = 0.0;
+                    di = fma(-f, ui, dn);
+                    ui = un;
+                } else {
+                    const double r = 1.0 / li;
+                    const double f = di * r;
+                    dl[i * st] = f;
+                    dd[i * st] = r;
+                    du[i * st] = dn;
+                    du2[i * st] = un;
+                    pv[i * st] = 1.0;
+                    di = fma(-f, dn, ui);
+                    ui = -f * un;
+                }
+            }
+            if (fabs(di) < tiny) di = copysign(tiny, di);
+            dd[(n - 1) * st] = 1.0 / di;
+            for (int i = 0; i < n; ++i) x[i] = hash_unit(uint64_t(mm) * 1000003ULL + i);
+        }
+        for (int it = 0; it < 3; ++it) {
+            if (mine) {
+                double cr = x[0];
+                for (int i = 0; i + 1 < n; ++i) {
+                    const double nx = x[i + 1];
+                    if (pv[i * st] != 0.0) {
+                        x[i] = nx;
+                        cr = fma(-dl[i * st], nx, cr);
+                    } else {
+                        x[i] = cr;
+                        cr = fma(-dl[i * st], cr, nx);
+                    }
+                }
+                x[n - 1] = cr;
+                double x2 = 0.0, x1 = x[n - 1] * dd[(n - 1) * st];
+                x[n - 1] = x1;
+                for (int i = n - 2; i >= 0; --i) {
+                    const double xi = (x[i] - du[i * st] * x1 - du2[i * st] * x2) * dd[i * st];
+                    x[i] = xi;
+                    x2 = x1;
+                    x1 = xi;
+                }
+            }
+            __syncthreads();
+            // CGS2 of this chunk's members, in order, against every earlier cluster member
+            for (int q = cb; q < cb + cs; ++q) {
+                double* xq = X + size_t(n) * q;
+                double mx = 0.0;
+                for (int i = t; i < n; i += kIvT) mx = fmax(mx, fabs(xq[i]));
+                mx = block_reduce(mx, red, true);
+                const double sc = mx > 0.0 ? 1.0 / mx : 1.0;  // pre-scale: the solve grows x by ~1/eps
+                for (int i = t; i < n; i += kIvT) xq[i] *= sc;
+                const int np = q - j;
+                for (int pass = 0; pass < 2 && np > 0; ++pass) {
+                    __syncthreads();
+                    for (int u = w; u < np; u += kIvT / 32) {
+                        const double* xu = X + size_t(n) * (j + u);
+                        double dt = 0.0;
+                        for (int i = lane; i < n; i += 32) dt = fma(xu[i], xq[i], dt);
+#pragma unroll
+                        for (int o = 16; o > 0; o >>= 1) dt += __shfl_xor_sync(0xffffffffu, dt, o);
+                        if (lane == 0) dsh[u] = dt;
+                    }
+                    __syncthreads();
+                    for (int i = t; i < n; i += kIvT) {
+                        double a = 0.0;
+                        for (int u = 0; u < np; ++u) a = fma(dsh[u], X[size_t(n) * (j + u) + i], a);
+                        xq[i] -= a;
+                    }
+                }
+                double nr = 0.0;
+                for (int i = t; i < n; i += kIvT) nr = fma(xq[i], xq[i], nr);
+                nr = block_reduce(nr, red, false);
+                const double inv = nr > 0.0 ? 1.0 / sqrt(nr) : 0.0;
+                for (int i = t; i < n; i += kIvT) xq[i] *= inv;
+                __syncthreads();
+            }
+        }
+    }
+}
+
 // vout(:, c) = H_0 ... H_{n-3} X(:, c); one warp per column, reflectors in smem.
 template <int S>
 __global__ void __launch_bounds__(1024) backtr_kernel(const double* __restrict__ hh, const double* __restrict__ tau,
@@ -1049,12 +1198,29 @@ void tridiag_extreme_eig(atk_ctx* ctx, const double* d, const double* e, int m, 
 void tridiag_tail(atk_ctx* ctx, const double* d, const double* e, int n, int nvals, int nwant, double* values,
                   double* X, double* wk) {
     const int wpb = 8;
+    static const bool trace = std::getenv("ATK_TRACE") != nullptr;
+    cudaEvent_t ev[3] = {};
+    if (trace)
+        for (auto& x : ev) cudaEventCreate(&x);
+    if (trace) cudaEventRecord(ev[0], ctx->stream);
     bisect_kernel<<<unsigned((nvals + wpb - 1) / wpb), 32 * wpb, size_t(n) * sizeof(double), ctx->stream>>>(
         d, e, n, nvals, values);
     ATK_LAUNCHED(ctx);
-    if (nwant == 0) return;
-    invit_kernel<<<unsigned((nwant + wpb - 1) / wpb), 32 * wpb, 0, ctx->stream>>>(d, e, n, values, nwant, X, wk);
-    ATK_LAUNCHED(ctx);
+    if (trace) cudaEventRecord(ev[1], ctx->stream);
+    if (nwant > 0) {
+        invit_cta_kernel<<<unsigned(nwant), kIvT, size_t(nwant) * sizeof(double), ctx->stream>>>(d, e, n, values,
+                                                                                               nwant, X, wk);
+        ATK_LAUNCHED(ctx);
+    }
+    if (trace) {
+        cudaEventRecord(ev[2], ctx->stream);
+        cudaEventSynchronize(ev[2]);
+        float a = 0.f, b = 0.f;
+        cudaEventElapsedTime(&a, ev[0], ev[1]);
+        cudaEventElapsedTime(&b, ev[1], ev[2]);
+        std::fprintf(stderr, "[atk tridiag n=%d] bisect %.3f ms, inverse iteration %.3f ms\n", n, a, b);
+        for (auto& x : ev) cudaEventDestroy(x);
+    }
 }
 
 void tridiag_eig(atk_ctx* ctx, const double* a, int n, int lda, int nwant, double* values, double* vectors,

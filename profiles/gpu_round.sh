@@ -17,7 +17,7 @@ for p in $PARTS; do
     tracecfg) for c in c1 c2; do ATK_TRACE=1 timeout 300 python profiles/run_step.py $c 1 > gpurun_out/${TAG}_trace_$c.log 2>&1; echo "trace $c=$?"; done;;
     c5u) timeout 600 python bench.py --config c5u --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/${TAG}_bench_c5u.json 2> gpurun_out/${TAG}_bench_c5u.err; echo "c5u=$?";;
     peaks) timeout 300 python profiles/measure_peaks.py gpurun_out/${TAG}_peaks.json > gpurun_out/${TAG}_peaks.log 2>&1; echo "peaks=$?"; tail -c 600 gpurun_out/${TAG}_peaks.json; echo;;
-    bigeig) timeout 600 python profiles/eig_big_probe.py > gpurun_out/${TAG}_bigeig.log 2>&1; echo "bigeig=$?"; grep -E "dense eig|method=|Error|error" gpurun_out/${TAG}_bigeig.log | tail -30;;
+    bigeig) ATK_TRD_PROFILE=1 timeout 600 python profiles/eig_big_probe.py > gpurun_out/${TAG}_bigeig.log 2>&1; echo "bigeig=$?"; grep -E "dense eig|trd n|method=|Error|error" gpurun_out/${TAG}_bigeig.log | tail -30;;
     bigeigt) timeout 900 python -m pytest tests/test_gpu_eig_big.py -x -q -p no:hypothesispytest > gpurun_out/${TAG}_bigeigt.log 2>&1; echo "bigeigt=$? $(tail -1 gpurun_out/${TAG}_bigeigt.log)"; grep -E "Error|assert|FAIL" gpurun_out/${TAG}_bigeigt.log | head -20;;
     fast) timeout 900 python -m pytest tests -m "gpu and not slow" -x -q -p no:hypothesispytest > gpurun_out/${TAG}_tests.log 2>&1; echo "fast=$? $(tail -1 gpurun_out/${TAG}_tests.log)";;
     bench) timeout 600 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err; echo "bench=$?"; head -c 400 gpurun_out/${TAG}_bench.json; echo;;

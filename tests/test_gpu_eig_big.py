@@ -116,3 +116,25 @@ def test_large_rank_above_chfsi_block(dctx):
 
     s = _sym(400, 3, "indefinite")
     _check(s, 128, atucker.sym_eig_top_r(s, 128, ctx=dctx))
+
+
+@pytest.mark.parametrize("n", [700, 1024, 1300])
+def test_grid_only_reduction(dctx, n, monkeypatch):
+    """The grid phase alone (no 16-CTA cluster tail): same exactness."""
+    from paper_2010_10131_b200 import atucker
+
+    monkeypatch.setenv("ATK_TRD_NOCLUSTER", "1")
+    dctx.set_option("eig_method", 3)
+    s = _sym(n, 5, "indefinite")
+    _check(s, 24, atucker.sym_eig_top_r(s, 24, ctx=dctx))
+
+
+def test_warp_backtransform_matches(dctx, monkeypatch):
+    """The one-warp-per-vector back-transformation (kept for n where the blocked
+    WY kernel's shared-memory block does not fit) on the same input."""
+    from paper_2010_10131_b200 import atucker
+
+    dctx.set_option("eig_method", 3)
+    s = _sym(900, 13, "flat_gram")
+    monkeypatch.setenv("ATK_BACKTR_WARP", "1")
+    _check(s, 40, atucker.sym_eig_top_r(s, 40, ctx=dctx))
