@@ -137,8 +137,11 @@ atk_status atk_ctx_synchronize(atk_ctx* ctx);
 uint64_t atk_ctx_launch_count(const atk_ctx* ctx);
 /* Engine tuning knobs (unknown keys -> ATK_INVALID_ARGUMENT):
  *   "simt"          1 = CUDA-core contractions for every shape (default 0: tcgen05 / DMMA)
- *   "eig_method"   -1 auto (tridiagonal for n <= 200, else ChFSI), 0 dense Jacobi (n <= 112;
- *                  also the Rayleigh-Ritz solver), 1 ChFSI, 2 tridiagonal (n <= 200)
+ *   "eig_method"   -1 auto (tridiagonal for n <= 200, else ChFSI handing over to the dense solver
+ *                  after "eig_dense_passes" filter passes), 0 dense Jacobi (n <= 112; also the
+ *                  Rayleigh-Ritz solver), 1 ChFSI only, 2 / 3 exact dense tridiagonal (any n <= 4096)
+ *   "eig_dense_passes" ChFSI filter passes before the exact dense solver takes over (default 3;
+ *                  -1 = never)
  *   "chfsi_tol"     relative Ritz-residual target of ChFSI (default 1e-12; fp32 Grams use >= 1e-9)
  *   "cheb_fused"    1 = each Chebyshev filter pass is one cooperative launch (default), 0 = per-step launches
  *   "als_head"      -1 = one-pass ALS: phase 1 and phase 2 of a tile in turn (default); k >= 0 interleaves
