@@ -17,7 +17,11 @@ roofline : dominant kernel = the mode-1 Gram (gram_tf32_kernel + its split-K
         reduction), I^2 J flops per launch / its event-timed duration, against
         half the measured bf16 peak (tf32 rate).
 cpu_baseline : the CPU oracle (oracle/, reference port) on a bounded sample of
-        the same workload (first 32 slabs of the last mode), all host cores.
+        the same workload (the leading slabs of the last mode, ~15 s), all host
+        threads, with its per-stage split and the host's lscpu model / RAM.
+--impl reference : the oracle on the FULL workload, one timed run after W
+        warm-ups (harness.hpp:58-72), plus 1-thread and all-thread legs on a
+        bounded sample (see run_reference).
 Multi-GPU (torchrun): the input is sharded along the last mode, one NCCL
 allreduce of the Gram partials per mode inside the engine.
 """
@@ -161,26 +165,101 @@ def make_input(atucker, cfg, seed, ctx, shard=(0, 1)):
 
 
 # ---------------------------------------------------------------- reference arm / CPU baseline
-def cpu_sample(cfg, name, threads, budget_s=20.0):
-    """Oracle st-HOSVD on a bounded sample (leading slabs of the last mode)."""
+def host_info():
+    """lscpu model, host threads and RAM of the box the CPU legs run on."""
+    model = None
+    try:
+        for line in subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout.splitlines():
+            if line.startswith("Model name"):
+                model = line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    ram = avail = None
+    try:
+        mi = dict(ln.split(":", 1) for ln in Path("/proc/meminfo").read_text().splitlines() if ":" in ln)
+        ram = round(int(mi["MemTotal"].split()[0]) / 2 ** 20, 1)
+        avail = round(int(mi["MemAvailable"].split()[0]) / 2 ** 20, 1)
+    except Exception:
+        pass
+    return {"cpu_model": model, "host_threads": os.cpu_count(), "ram_gb": ram, "ram_avail_gb": avail}
+
+
+def _oracle():
     sys.path.insert(0, str(ROOT / "oracle"))
     import oracle as o
-    from paper_2010_10131_b200.selector import CostModelParams, Strategy
 
     o.load()
-    o.set_threads(threads)
-    dims, ranks = list(cfg["dims"]), list(cfg["ranks"])
-    slab = int(np.prod(dims[:-1]))
-    target_elems = 2 * 10 ** 8 if name in ("c5", "c2") else int(np.prod(dims))
-    nl = max(1, min(dims[-1], target_elems // slab))
+    return o
+
+
+def host_input(cfg, seed, nl=None, threads=None):
+    """The leading `nl` slabs (last mode) of the configured input, built on the
+    host with the same recipe as make_input: the counter-hash uniform stream
+    (bit-identical to the device generator), or the low-rank core expanded
+    through the same orthonormal factors plus the 1e-2 hash noise (computed in
+    fp64 and rounded once, so not bit-identical to the device's fp32
+    expansion; the CPU timing does not depend on it)."""
+    from concurrent.futures import ThreadPoolExecutor
+    import ctypes as C
+
+    o = _oracle()
+    dims = list(cfg["dims"])
+    nl = dims[-1] if nl is None else nl
+    threads = threads or os.cpu_count() or 1
+    dt = np.float32 if cfg["dtype"] == "f32" else np.float64
     sdims = dims[:-1] + [nl]
-    sranks = ranks[:-1] + [min(ranks[-1], nl)]
-    seed = SEEDS[name]
     if cfg["input"] == "reference":
-        x = o.random_tensor(dims, seed, "normal")[..., :nl]
-    else:
-        x = o.hash_uniform(seed, int(np.prod(sdims))).astype(np.float64).reshape(sdims, order="F")
-    x = np.asfortranarray(x)
+        return np.asfortranarray(o.random_tensor(dims, seed, "normal")[..., :nl].astype(dt))
+    slab = int(np.prod(dims[:-1]))
+    out = np.empty(slab * nl, dtype=dt)
+    lib = o.load()
+
+    def fill_noise(dst, sd, start, scale=1.0, add=False):
+        chunk = 1 << 24
+
+        def work(a):
+            b = min(a + chunk, dst.size)
+            buf = np.empty(b - a, np.float32)
+            lib.or_hash_uniform(C.c_uint64(sd), C.c_uint64(start + a), C.c_uint64(b - a),
+                                buf.ctypes.data_as(C.POINTER(C.c_float)))
+            if add:
+                dst[a:b] = (dst[a:b] + scale * buf.astype(np.float64)).astype(dst.dtype)
+            else:
+                dst[a:b] = buf
+        with ThreadPoolExecutor(threads) as ex:
+            list(ex.map(work, range(0, dst.size, chunk)))
+
+    if cfg["input"] == "uniform":
+        fill_noise(out, seed, 0)
+        return out.reshape(sdims, order="F")
+    assert len(dims) == 3, "host low-rank input is built for 3-way configs"
+    ranks = list(cfg["ranks"])
+    rng = np.random.default_rng(seed)
+    u = [np.linalg.qr(rng.standard_normal((d, r)))[0] for d, r in zip(dims, ranks)]
+    core = o.hash_uniform(seed, int(np.prod(ranks))).astype(np.float64).reshape(ranks, order="F")
+    scale = float(np.sqrt(np.prod(dims) / np.prod(ranks)))
+    kb = 32
+    for k0 in range(0, nl, kb):
+        k1 = min(nl, k0 + kb)
+        m = np.einsum("abc,kc->kab", core, u[2][k0:k1])          # (kb, R0, R1)
+        a = np.matmul(u[0][None], m)                              # (kb, I0, R1)
+        blk = scale * np.matmul(u[1][None], a.transpose(0, 2, 1))  # (kb, I1, I0): C order = F slab
+        seg = out[k0 * slab:k1 * slab]
+        seg[:] = blk.reshape(-1)
+        fill_noise(seg, seed + 1000, k0 * slab, 1e-2, add=True)
+    return out.reshape(sdims, order="F")
+
+
+def cpu_run(cfg, x, threads):
+    """One timed oracle st-HOSVD of host tensor x (fp64 OpenBLAS on `threads`
+    host threads; an fp32 EIG-first workload streams through the memory-lean
+    entry).  Returns seconds, credited flops and the per-stage split."""
+    from paper_2010_10131_b200.selector import CostModelParams, Strategy
+
+    o = _oracle()
+    o.set_threads(threads)
+    dims = list(x.shape)
+    ranks = [min(r, d) for r, d in zip(cfg["ranks"], dims)]
     s = Strategy.parse(cfg["strategy"])
     p = CostModelParams()
     kinds = []
@@ -190,15 +269,44 @@ def cpu_sample(cfg, name, threads, budget_s=20.0):
         kinds.append(k)
         return k
 
+    lean = x.dtype == np.float32 and int(s.decide(0, dims[0], ranks[0], int(np.prod(dims[1:])), p)) == 0
+    if not lean and x.dtype != np.float64:
+        x = np.asfortranarray(x, dtype=np.float64)
     o.reset_counters()
+    t_before = o.stage_times()
     t0 = time.perf_counter()
-    o.sthosvd(x, sranks, decide)
+    if lean:
+        kinds.append(0)
+        o.sthosvd_f32_eig0(x, ranks, decide, threads=threads)
+    else:
+        o.sthosvd(x, ranks, decide)
     dt = time.perf_counter() - t0
-    fl = sum(sum(f.values()) for f in flops_of(sdims, sranks, kinds))
-    return {"value": fl / dt / 1e9, "unit": "GFLOP/s", "cores": threads, "kind": "port",
-            "sample": f"st-HOSVD of the leading {nl} slabs: dims {sdims} ranks {sranks} "
-                      f"({cfg['strategy']}), fp64 OpenBLAS, {dt:.2f} s",
-            "seconds": dt, "stage_s": o.stage_times()}
+    t_after = o.stage_times()
+    fl = sum(sum(f.values()) for f in flops_of(dims, ranks, kinds))
+    stage = {k: round(t_after[k] - t_before[k], 3) for k in t_after}
+    return {"seconds": dt, "flops": fl, "value": fl / dt / 1e9, "dims": dims, "ranks": ranks, "stage_s": stage}
+
+
+def _sample_slabs(cfg, threads, budget_s):
+    """Leading slabs whose oracle st-HOSVD takes ~budget_s on `threads` threads
+    (at ~25 GFLOP/s per thread for the dominant mode-0 Gram)."""
+    dims = list(cfg["dims"])
+    i0, slab = dims[0], int(np.prod(dims[:-1]))
+    per_slab = i0 * slab + 2 * cfg["ranks"][0] * slab  # Gram + TTM flops of one slab
+    nl = int(budget_s * 25e9 * threads / per_slab)
+    return max(1, min(dims[-1], nl))
+
+
+def cpu_sample(cfg, name, threads, budget_s=15.0):
+    """Oracle st-HOSVD on a bounded sample (the leading slabs of the last mode)."""
+    nl = _sample_slabs(cfg, threads, budget_s)
+    x = host_input(cfg, SEEDS[name], nl, threads)
+    r = cpu_run(cfg, x, threads)
+    return {"value": r["value"], "unit": "GFLOP/s", "cores": threads, "kind": "port",
+            "sample": f"oracle st-HOSVD of the leading {nl} of {cfg['dims'][-1]} slabs: dims {r['dims']} "
+                      f"ranks {r['ranks']} ({cfg['strategy']}, input={cfg['input']}), fp64 OpenBLAS, "
+                      f"{r['seconds']:.2f} s, {r['flops']:.4g} credited flops",
+            "sampled": True, "sample_flops": r["flops"], "seconds": r["seconds"], "stage_s": r["stage_s"]}
 
 
 def planned_flops(cfg):
@@ -226,23 +334,64 @@ def workload_config(cfg, name, world, flops):
 
 
 def run_reference(args, cfg, name):
+    """The reference arm: the CPU restatement of the reference path (oracle/,
+    `kind` "port": Eigen is absent, so the reference itself cannot be built
+    here) on the box's host cores.  Following harness.hpp:58-72 / BASELINE.md
+    §4: W warm-up runs, then ONE timed run of the FULL workload on all host
+    threads (the line's value, ms_per_step and stage split; steps = 1), plus a
+    bounded-sample leg at 1 thread (the reference build is single-threaded,
+    proj/README.md:95-96) and at all threads, K steps each (median)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    info = host_info()
     threads = os.cpu_count() or 1
-    vals = []
-    for step in range(args.warmup + args.steps):
-        r = cpu_sample(cfg, name, threads)
-        if step >= args.warmup:
-            vals.append(r)
-    v = float(np.median([r["value"] for r in vals]))
-    ms = float(np.median([r["seconds"] for r in vals])) * 1e3
+    seed = SEEDS[name]
+    small = host_input(cfg, seed, _sample_slabs(cfg, threads, 1.0), threads)
+    for _ in range(args.warmup):
+        cpu_run(cfg, small, threads)
+    del small
+    # per-thread legs on one bounded sample
+    nl = _sample_slabs(cfg, 1, 12.0)
+    xs = host_input(cfg, seed, nl, threads)
+    legs = []
+    for th in (1, threads):
+        runs = [cpu_run(cfg, xs, th) for _ in range(max(1, args.steps if th > 1 else 1))]
+        med = sorted(runs, key=lambda r: r["seconds"])[len(runs) // 2]
+        legs.append({"cores": th, "runs": len(runs), "value": med["value"], "unit": "GFLOP/s",
+                     "seconds": round(med["seconds"], 3), "stage_s": med["stage_s"],
+                     "sample": f"leading {nl} of {cfg['dims'][-1]} slabs: dims {med['dims']} ranks {med['ranks']}, "
+                               f"{med['flops']:.4g} credited flops"})
+    del xs
+    # the full workload, once, if it fits host memory (input + the oracle's fp64 work)
+    es = 4 if cfg["dtype"] == "f32" else 8
+    need_gb = np.prod(cfg["dims"]) * (es + (0 if cfg["dtype"] == "f32" and cfg["strategy"] == "eig" else 8)) / 2 ** 30
+    full = None
+    if info["ram_avail_gb"] is None or need_gb * 1.1 + 4 < info["ram_avail_gb"]:
+        t0 = time.perf_counter()
+        x = host_input(cfg, seed, None, threads)
+        gen_s = time.perf_counter() - t0
+        full = cpu_run(cfg, x, threads)
+        del x
+    flops = planned_flops(cfg)
+    if full is not None:
+        v, ms, stage, sampled = full["value"], full["seconds"] * 1e3, full["stage_s"], False
+        sample = (f"FULL workload {'x'.join(map(str, cfg['dims']))} ranks {'x'.join(map(str, cfg['ranks']))}, "
+                  f"one timed run on {threads} host threads (fp64 OpenBLAS; input built in {gen_s:.1f} s, untimed)")
+    else:  # does not fit: the all-thread sample stands in, flagged as such
+        v, ms, stage, sampled = legs[1]["value"], legs[1]["seconds"] * 1e3, legs[1]["stage_s"], True
+        sample = f"SAMPLED ({need_gb:.0f} GB does not fit host RAM): {legs[1]['sample']}"
+    conf = workload_config(cfg, name, args.gpus, flops)
+    if sampled:
+        conf["sampled_flops_per_step"] = legs[1]["value"] * legs[1]["seconds"] * 1e9
     line = {"metric": "st-HOSVD GFLOP/s (Gram+eig+TTM)", "value": v, "unit": "GFLOP/s",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "n_gpus": args.gpus, "steps": 1, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "impl": "reference",
-            "config": workload_config(cfg, name, args.gpus, planned_flops(cfg)),
-            "cpu_baseline": {k: vals[-1][k] for k in ("kind", "cores", "sample")} | {"value": v, "unit": "GFLOP/s"},
+            "data": "synthetic", "impl": "reference", "config": conf,
+            "cpu_baseline": {"kind": "port", "cores": threads, "sample": sample, "value": v, "unit": "GFLOP/s",
+                             "sampled": sampled, "stage_s": stage, "legs": legs, "host": info,
+                             "method": f"{args.warmup} warm-up runs on a small sample, then one timed full run "
+                                       f"(harness.hpp:58-72); legs: median of K runs at all threads, 1 run at 1 thread"},
             "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -398,8 +547,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_sample(cfg, args.config, os.cpu_count() or 1)
-        cpu.pop("stage_s", None)
-        cpu.pop("seconds", None)
+        cpu["host"] = host_info()
 
     if rank == 0:
         line = {"metric": "st-HOSVD GFLOP/s (Gram+eig+TTM)", "value": value, "unit": "GFLOP/s",

@@ -28,6 +28,7 @@
 #include <random>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 namespace orc {
@@ -1060,10 +1061,24 @@ int or_sthosvd_f32_eig0(const float* x, const uint64_t* dims, int nd, const uint
         if (r0 < 1 || r0 > I) throw Err(E_RANK_EXCEEDS_DIM, "truncation invalid for mode 0");
         const uint64_t CH = std::max<uint64_t>(1, (uint64_t(1) << 27) / I);  // ~1 GB fp64 per chunk
         std::vector<double> buf(I * std::min(CH, J));
+        // fp32 -> fp64 chunk conversion on the same host threads as the BLAS
+        // (an artifact of streaming an fp32 input; the reference holds fp64)
+        const int nth = threads > 0 ? threads : 1;
+        auto widen = [&](uint64_t j0, uint64_t nc) {
+            const uint64_t tot = I * nc;
+            std::vector<std::thread> pool;
+            for (int t = 0; t < nth; ++t)
+                pool.emplace_back([&, t] {
+                    const uint64_t a = tot * t / nth, b = tot * (t + 1) / nth;
+                    for (uint64_t e = a; e < b; ++e) buf[e] = double(x[I * j0 + e]);
+                });
+            for (auto& th : pool) th.join();
+        };
+        auto t_gram = clk::now();
         Matrix s(I, I);
         for (uint64_t j0 = 0; j0 < J; j0 += CH) {
             const uint64_t nc = std::min(CH, J - j0);
-            for (uint64_t e = 0; e < I * nc; ++e) buf[e] = double(x[I * j0 + e]);
+            widen(j0, nc);
             gemm_raw(false, true, I, I, nc, buf.data(), I, buf.data(), I, s.v.data(), I, j0 ? 1.0 : 0.0);
         }
         record_gemm((long long)(I * I) * (long long)J);
@@ -1073,18 +1088,21 @@ int or_sthosvd_f32_eig0(const float* x, const uint64_t* dims, int nd, const uint
                 s(i, j) = v;
                 s(j, i) = v;
             }
-        EigPair e = sym_eig_top_r(s, r0);
+        g_t_gram += since(t_gram);
+        EigPair e = sym_eig_top_r(s, r0);  // times itself
+        auto t_ttm = clk::now();
         Tensor work;
         work.dims.assign(dims, dims + nd);
         work.dims[0] = r0;
         work.v.assign(r0 * J, 0.0);
         for (uint64_t j0 = 0; j0 < J; j0 += CH) {
             const uint64_t nc = std::min(CH, J - j0);
-            for (uint64_t q = 0; q < I * nc; ++q) buf[q] = double(x[I * j0 + q]);
+            widen(j0, nc);
             // Y(:, j0:j0+nc) = U^T X(:, j0:j0+nc)
             gemm_raw(true, false, r0, nc, I, e.vectors.v.data(), I, buf.data(), I, work.v.data() + r0 * j0, r0);
         }
         record_gemm(2LL * (long long)(r0 * J) * (long long)I);
+        g_t_ttm += since(t_ttm);
         // remaining modes: the reference loop on the shrunk tensor (mode 0 already done)
         std::vector<uint64_t> rk(ranks, ranks + nd);
         std::vector<Matrix> factors(nd);
