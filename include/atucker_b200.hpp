@@ -11,12 +11,14 @@
 // Containers are the reference's layout (column-major doubles).  `Strategy`
 // is any type with the reference's `decide(mode, i, r, j, params)` member
 // (so atucker::Strategy itself plugs in unchanged) or the local Strategy.
-// Errors come back as the reference's exception hierarchy (errors.hpp:9-25),
-// with sthosvd's "mode n: " prefix preserved (sthosvd.hpp:177-183).
+// Errors come back as the reference's exception hierarchy (errors.hpp:9-25) —
+// the reference's own types when its headers are on the include path (see
+// below) — with sthosvd's "mode n: " prefix preserved (sthosvd.hpp:177-183).
 #pragma once
 
 #include <cstdint>
 #include <cstdio>
+#include <array>
 #include <cstring>
 #include <functional>
 #include <stdexcept>
@@ -26,6 +28,49 @@
 
 #include "atk.h"
 
+// Reference types.  When the reference's Eigen-free headers are on the include
+// path (atucker/{errors,solver_kind,tensor,selector}.hpp), the drop-in uses
+// them directly: atucker::DenseTensor / DenseMatrix go in and come out,
+// failures throw atucker::NotSPD and friends, SolverKind is
+// atucker::SolverKind and the Adaptive strategy runs the reference's own
+// selector::predict.  Without them (the GPU box, a standalone build) the
+// same names are declared here with the reference's layout and semantics.
+// Define ATUCKER_B200_STANDALONE to force the local declarations.
+#if !defined(ATUCKER_B200_STANDALONE) && __has_include("atucker/tensor.hpp") && \
+    __has_include("atucker/selector.hpp")
+#define ATUCKER_B200_REFERENCE_TYPES 1
+#include "atucker/errors.hpp"
+#include "atucker/selector.hpp"
+#include "atucker/solver_kind.hpp"
+#include "atucker/tensor.hpp"
+
+namespace atucker_b200 {
+using atucker::DenseMatrix;
+using atucker::DenseTensor;
+using atucker::EmptyDataset;
+using atucker::Error;
+using atucker::FeatureVersionMismatch;
+using atucker::IoFailure;
+using atucker::ModeOutOfRange;
+using atucker::NoConvergence;
+using atucker::NotSPD;
+using atucker::NotSquare;
+using atucker::RankDeficient;
+using atucker::RankExceedsDim;
+using atucker::RankTooLarge;
+using atucker::SchemaMismatch;
+using atucker::ShapeMismatch;
+using atucker::SolverKind;
+using atucker::ZeroNormInput;
+using atucker::selector::CostModelParams;
+using atucker::selector::DecisionTreeModel;
+using atucker::selector::extract_features;
+using atucker::selector::FeatureVector;
+using atucker::selector::predict;
+struct DeviceError : Error { using Error::Error; };  // CUDA / NCCL / OOM (no CPU fallback)
+}  // namespace atucker_b200
+#else
+#define ATUCKER_B200_REFERENCE_TYPES 0
 namespace atucker_b200 {
 
 // ---------------------------------------------------------------- errors.hpp:9-25
@@ -44,6 +89,100 @@ struct FeatureVersionMismatch : Error { using Error::Error; };
 struct SchemaMismatch : Error { using Error::Error; };
 struct IoFailure : Error { using Error::Error; };
 struct DeviceError : Error { using Error::Error; };  // CUDA / NCCL / OOM (no CPU fallback)
+
+// ---------------------------------------------------------------- tensor.hpp:44-156
+struct DenseMatrix {
+    DenseMatrix() = default;
+    DenseMatrix(std::size_t r, std::size_t c) : rows_(r), cols_(c), data_(r * c, 0.0) {}
+    DenseMatrix(std::size_t r, std::size_t c, std::vector<double> d) : rows_(r), cols_(c), data_(std::move(d)) {
+        if (data_.size() != r * c) throw ShapeMismatch("matrix data length does not match rows*cols");
+    }
+    std::size_t rows() const { return rows_; }
+    std::size_t cols() const { return cols_; }
+    std::size_t size() const { return data_.size(); }
+    double operator()(std::size_t i, std::size_t j) const { return data_[i + rows_ * j]; }
+    double& operator()(std::size_t i, std::size_t j) { return data_[i + rows_ * j]; }
+    const double* data() const { return data_.data(); }
+    double* data() { return data_.data(); }
+    const std::vector<double>& values() const { return data_; }
+
+private:
+    std::size_t rows_ = 0, cols_ = 0;
+    std::vector<double> data_;
+};
+
+struct DenseTensor {
+    DenseTensor() = default;
+    explicit DenseTensor(std::vector<std::size_t> dims) : dims_(std::move(dims)) {
+        if (dims_.empty()) throw ShapeMismatch("tensor order must be at least 1");
+        std::size_t n = 1;
+        for (auto d : dims_) {
+            if (d == 0) throw ShapeMismatch("tensor dimensions must be positive");
+            n *= d;
+        }
+        data_.assign(n, 0.0);
+    }
+    DenseTensor(std::vector<std::size_t> dims, std::vector<double> d) : dims_(std::move(dims)), data_(std::move(d)) {
+        std::size_t n = 1;
+        for (auto x : dims_) n *= x;
+        if (dims_.empty() || n == 0) throw ShapeMismatch("tensor dimensions must be positive");
+        if (data_.size() != n) throw ShapeMismatch("tensor data length does not match the product of dims");
+    }
+    std::size_t order() const { return dims_.size(); }
+    const std::vector<std::size_t>& dims() const { return dims_; }
+    std::size_t dim(std::size_t m) const { return dims_.at(m); }
+    std::size_t size() const { return data_.size(); }
+    const double* data() const { return data_.data(); }
+    double* data() { return data_.data(); }
+    const std::vector<double>& values() const { return data_; }
+
+private:
+    std::vector<std::size_t> dims_;
+    std::vector<double> data_;
+};
+
+enum class SolverKind { Eig = 0, Als = 1, Svd = 2 };  // solver_kind.hpp:11
+
+struct CostModelParams { int num_iters = 5; };  // selector.hpp:31-33
+
+// selector.hpp:19-29, 60-104: the ten shape features and the trained tree's
+// deterministic root-to-leaf descent (the tree payload comes from the
+// reference's trainer / selector_io; this side only evaluates it).
+constexpr int kFeatureOrderVersion = 1;
+using FeatureVector = std::array<double, 10>;
+inline FeatureVector extract_features(double i, double r, double j) {
+    return {i, r, j, i * i, r * r, i * r, r * r / i, r * r / j, i / j, r / j};
+}
+struct DecisionTreeModel {
+    struct Node {
+        bool leaf = false;
+        int feature_index = -1;
+        double threshold = 0.0;
+        int left = -1, right = -1, label = 0;
+        std::array<long long, 2> class_counts{0, 0};
+    };
+    std::vector<Node> nodes;
+    int root = -1;
+    int feature_order_version = kFeatureOrderVersion;
+};
+inline SolverKind predict(const DecisionTreeModel& m, const FeatureVector& f) {
+    if (m.feature_order_version != kFeatureOrderVersion)
+        throw FeatureVersionMismatch("model was trained with feature order version " +
+                                     std::to_string(m.feature_order_version));
+    if (m.root < 0 || m.root >= int(m.nodes.size())) throw SchemaMismatch("decision tree has no valid root");
+    int id = m.root;
+    for (std::size_t steps = 0; steps <= m.nodes.size(); ++steps) {
+        const auto& nd = m.nodes[std::size_t(id)];
+        if (nd.leaf) return nd.label == 0 ? SolverKind::Eig : SolverKind::Als;
+        id = f[std::size_t(nd.feature_index)] <= nd.threshold ? nd.left : nd.right;
+        if (id < 0 || id >= int(m.nodes.size())) throw SchemaMismatch("decision tree child id out of range");
+    }
+    throw SchemaMismatch("decision tree descent did not reach a leaf");
+}
+}  // namespace atucker_b200
+#endif
+
+namespace atucker_b200 {
 
 inline void check(atk_status s) {
     if (s == ATK_OK) return;
@@ -67,63 +206,32 @@ inline void check(atk_status s) {
     }
 }
 
-// ---------------------------------------------------------------- tensor.hpp:44-156
-struct DenseMatrix {
-    std::size_t rows_ = 0, cols_ = 0;
-    std::vector<double> data_;
-    DenseMatrix() = default;
-    DenseMatrix(std::size_t r, std::size_t c) : rows_(r), cols_(c), data_(r * c, 0.0) {}
-    DenseMatrix(std::size_t r, std::size_t c, std::vector<double> d) : rows_(r), cols_(c), data_(std::move(d)) {
-        if (data_.size() != r * c) throw ShapeMismatch("matrix data length does not match rows*cols");
-    }
-    std::size_t rows() const { return rows_; }
-    std::size_t cols() const { return cols_; }
-    std::size_t size() const { return data_.size(); }
-    double operator()(std::size_t i, std::size_t j) const { return data_[i + rows_ * j]; }
-    double& operator()(std::size_t i, std::size_t j) { return data_[i + rows_ * j]; }
-    const double* data() const { return data_.data(); }
-    double* data() { return data_.data(); }
-};
-
-struct DenseTensor {
-    std::vector<std::size_t> dims_;
-    std::vector<double> data_;
-    DenseTensor() = default;
-    explicit DenseTensor(std::vector<std::size_t> dims) : dims_(std::move(dims)) {
-        std::size_t n = 1;
-        for (auto d : dims_) n *= d;
-        data_.assign(n, 0.0);
-    }
-    DenseTensor(std::vector<std::size_t> dims, std::vector<double> d) : dims_(std::move(dims)), data_(std::move(d)) {}
-    std::size_t order() const { return dims_.size(); }
-    const std::vector<std::size_t>& dims() const { return dims_; }
-    std::size_t dim(std::size_t m) const { return dims_.at(m); }
-    std::size_t size() const { return data_.size(); }
-    const double* data() const { return data_.data(); }
-    double* data() { return data_.data(); }
-};
-
-enum class SolverKind { Eig = 0, Als = 1, Svd = 2 };  // solver_kind.hpp:11
-
 struct AlsOptions {  // solvers.hpp:18-22
     int num_iters = 5;
     double rel_tol = 0.0;
     std::uint64_t seed = 0;
 };
 
-struct CostModelParams { int num_iters = 5; };  // selector.hpp:31-33
-
-// Local Strategy (sthosvd.hpp:39-107 without the trained-tree payload): a
-// fixed choice, a manual list, the flop cost model, or any callable hook.
+// Local Strategy (sthosvd.hpp:39-107): the trained tree (Adaptive), the flop
+// cost model, a fixed choice, a manual list, the B200 roofline model, or any
+// callable hook.  `decide` forwards the caller's CostModelParams (sthosvd
+// passes {opts.num_iters}, as sthosvd.hpp:160 does).
 class Strategy {
 public:
-    using Hook = std::function<SolverKind(std::size_t, std::size_t, std::size_t, std::size_t)>;
+    using Hook = std::function<SolverKind(std::size_t, std::size_t, std::size_t, std::size_t, const CostModelParams&)>;
+    static Strategy adaptive(DecisionTreeModel model) {
+        return Strategy([m = std::move(model)](std::size_t, std::size_t i, std::size_t r, std::size_t j,
+                                               const CostModelParams&) {
+            return predict(m, extract_features(double(i), double(r), double(j)));
+        });
+    }
     static Strategy fixed_eig() { return Strategy([](auto...) { return SolverKind::Eig; }); }
     static Strategy fixed_als() { return Strategy([](auto...) { return SolverKind::Als; }); }
     static Strategy fixed_svd() { return Strategy([](auto...) { return SolverKind::Svd; }); }
-    static Strategy cost_model() {
-        return Strategy([](std::size_t, std::size_t i, std::size_t r, std::size_t j) {
-            return atk_cost_eig(double(i), double(r), double(j)) <= atk_cost_als(double(i), double(r), double(j), 5)
+    static Strategy cost_model() {  // selector.hpp:52-58, ties go to EIG
+        return Strategy([](std::size_t, std::size_t i, std::size_t r, std::size_t j, const CostModelParams& p) {
+            return atk_cost_eig(double(i), double(r), double(j)) <=
+                           atk_cost_als(double(i), double(r), double(j), p.num_iters)
                        ? SolverKind::Eig : SolverKind::Als;
         });
     }
@@ -132,7 +240,7 @@ public:
     static Strategy roofline(atk_dtype dtype = ATK_F32, int num_iters = 5) {
         atk_roofline_params p;
         atk_roofline_params_default(&p, int(dtype), num_iters);
-        return Strategy([p](std::size_t mode, std::size_t i, std::size_t r, std::size_t j) {
+        return Strategy([p](std::size_t mode, std::size_t i, std::size_t r, std::size_t j, const CostModelParams&) {
             auto q = p;
             return atk_roofline_selector(&q, int(mode), i, r, j) == ATK_SOLVER_EIG ? SolverKind::Eig
                                                                                     : SolverKind::Als;
@@ -140,11 +248,14 @@ public:
     }
     static Strategy manual(std::vector<SolverKind> c) {
         for (auto k : c) if (k == SolverKind::Svd) throw Error("manual strategies choose between eig and als");
-        return Strategy([c](std::size_t mode, std::size_t, std::size_t, std::size_t) { return c.at(mode); }, c.size());
+        return Strategy([c](std::size_t mode, std::size_t, std::size_t, std::size_t, const CostModelParams&) {
+            return c.at(mode);
+        }, c.size());
     }
     explicit Strategy(Hook h, std::size_t manual_len = 0) : hook_(std::move(h)), manual_len_(manual_len) {}
-    SolverKind decide(std::size_t mode, std::size_t i, std::size_t r, std::size_t j, const CostModelParams&) const {
-        return hook_(mode, i, r, j);
+    SolverKind decide(std::size_t mode, std::size_t i, std::size_t r, std::size_t j,
+                      const CostModelParams& params) const {
+        return hook_(mode, i, r, j, params);
     }
     std::size_t manual_len() const { return manual_len_; }
 
@@ -356,7 +467,7 @@ SthosvdResult sthosvd(const DenseTensor& x, const std::vector<std::size_t>& rank
 inline double relative_error(const DenseTensor& x, const TuckerDecomposition& t) {
     detail::Dev d(x), c(t.core);
     std::vector<double> flat;
-    for (const auto& f : t.factors) flat.insert(flat.end(), f.data_.begin(), f.data_.end());
+    for (const auto& f : t.factors) flat.insert(flat.end(), f.data(), f.data() + f.size());
     double out = 0.0;
     check(atk_relative_error(Engine::instance().ctx(), d.t, c.t, flat.data(), &out));
     return out;
@@ -365,7 +476,7 @@ inline double relative_error(const DenseTensor& x, const TuckerDecomposition& t)
 inline DenseTensor reconstruct(const TuckerDecomposition& t) {
     detail::Dev c(t.core), y;
     std::vector<double> flat;
-    for (const auto& f : t.factors) flat.insert(flat.end(), f.data_.begin(), f.data_.end());
+    for (const auto& f : t.factors) flat.insert(flat.end(), f.data(), f.data() + f.size());
     std::vector<uint64_t> od(t.original_dims.begin(), t.original_dims.end());
     check(atk_reconstruct(Engine::instance().ctx(), c.t, flat.data(), od.data(), &y.t));
     return y.host();
@@ -414,7 +525,7 @@ inline DenseTensor read_dten(const std::string& path) {
 inline DenseMatrix read_dten_matrix(const std::string& path) {
     DenseTensor t = read_dten(path);
     if (t.order() != 2) throw IoFailure(path + ": expected an order-2 .dten");
-    return DenseMatrix(t.dim(0), t.dim(1), std::move(t.data_));
+    return DenseMatrix(t.dim(0), t.dim(1), std::vector<double>(t.data(), t.data() + t.size()));
 }
 // Engine handle (caller frees with atk_tensor_free).
 inline atk_tensor* read_dten_device(const std::string& path, atk_dtype dtype = ATK_F32) {
