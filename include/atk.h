@@ -186,6 +186,18 @@ typedef struct atk_host_collectives {
 } atk_host_collectives;
 atk_status atk_comm_init_host(atk_ctx* ctx, const atk_host_collectives* coll, int rank, int world);
 
+/* Collective accounting of this rank since the last reset (either backend):
+ * allreduces (the sizes exchange, the packed Gram triangle per sharded EIG
+ * mode, YR and GR per sharded ALS iteration) and the last-mode all-gather /
+ * broadcasts, with their payload bytes.  No reference counterpart (the
+ * reference is single-process); it backs the SURVEY §8(e) schedule tests. */
+typedef struct atk_comm_stats {
+    uint64_t allreduce_calls, allreduce_bytes;
+    uint64_t gather_calls, gather_bytes;
+} atk_comm_stats;
+atk_status atk_comm_get_stats(const atk_ctx* ctx, atk_comm_stats* out);
+atk_status atk_comm_reset_stats(atk_ctx* ctx);
+
 /* ------------------------------------------------------------ tensors */
 /* DenseTensor(dims) (tensor.hpp:103-107) — device allocation, NOT zero-filled. */
 atk_status atk_tensor_create(atk_ctx* ctx, atk_dtype dtype, int order, const uint64_t* dims,

@@ -78,6 +78,8 @@ _SIGS = {
     "atk_tensor_read_dten": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int, C.POINTER(C.c_void_p)]),
     "atk_tensor_write_dten": (C.c_int, [C.c_void_p, C.c_void_p, C.c_char_p]),
     "atk_comm_init_host": (C.c_int, [C.c_void_p, C.POINTER(HostCollectives), C.c_int, C.c_int]),
+    "atk_comm_get_stats": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64 * 4)]),
+    "atk_comm_reset_stats": (C.c_int, [C.c_void_p]),
     "atk_tensor_create": (C.c_int, [C.c_void_p, C.c_int, C.c_int, u64ptr, C.POINTER(C.c_void_p)]),
     "atk_tensor_wrap": (C.c_int, [C.c_void_p, C.c_int, C.c_int, u64ptr, C.c_void_p, C.POINTER(C.c_void_p)]),
     "atk_tensor_from_host": (C.c_int, [C.c_void_p, C.c_int, C.c_int, u64ptr, C.c_void_p, C.POINTER(C.c_void_p)]),

@@ -115,6 +115,14 @@ class Context:
         self._host_coll = coll  # the C side keeps raw callback pointers
         _lib.check(self.lib.atk_comm_init_host(self.h, C.byref(coll), int(rank), int(world)))
 
+    def comm_stats(self, reset: bool = False) -> dict:
+        """Collectives this rank issued (atk_comm_get_stats): counts and payload bytes."""
+        buf = (C.c_uint64 * 4)()
+        _lib.check(self.lib.atk_comm_get_stats(self.h, C.byref(buf)))
+        if reset:
+            _lib.check(self.lib.atk_comm_reset_stats(self.h))
+        return {"allreduce_calls": buf[0], "allreduce_bytes": buf[1], "gather_calls": buf[2], "gather_bytes": buf[3]}
+
     @staticmethod
     def nccl_unique_id() -> bytes:
         Context._nccl_hint()

@@ -260,6 +260,20 @@ atk_status atk_comm_init_host(atk_ctx* ctx, const atk_host_collectives* coll, in
     });
 }
 
+atk_status atk_comm_get_stats(const atk_ctx* ctx, atk_comm_stats* out) {
+    return guard([&] {
+        if (!ctx || !out) fail(ATK_INVALID_ARGUMENT, "null argument");
+        comm_stats(ctx, out);
+    });
+}
+
+atk_status atk_comm_reset_stats(atk_ctx* ctx) {
+    return guard([&] {
+        if (!ctx) fail(ATK_INVALID_ARGUMENT, "null context");
+        comm_stats_reset(ctx);
+    });
+}
+
 atk_status atk_dten_info(const char* path, int* order, uint64_t* dims) {
     return guard([&] {
         const DtenHeader h = dten_header(path);

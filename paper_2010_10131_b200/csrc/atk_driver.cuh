@@ -116,5 +116,9 @@ void allreduce_sum(atk_ctx* ctx, double* buf, uint64_t count, double* comm_ms);
 void allreduce_sum2(atk_ctx* ctx, double* a, uint64_t na, double* b, uint64_t nb, double* comm_ms);
 atk_tensor* allgather_last_mode(atk_ctx* ctx, const atk_tensor* local);
 uint64_t comm_global_last(atk_ctx* ctx, const atk_tensor* local);
+void allreduce_sym(atk_ctx* ctx, double* s, uint64_t n, double* comm_ms);  // packed upper triangle
+void comm_end_call(atk_ctx* ctx);
+void comm_stats(const atk_ctx* ctx, atk_comm_stats* out);
+void comm_stats_reset(atk_ctx* ctx);
 
 }  // namespace atk

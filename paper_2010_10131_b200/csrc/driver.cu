@@ -88,7 +88,7 @@ ModeOut eig_mode(atk_ctx* ctx, const atk_tensor* y, int mode, uint64_t r, int so
     if (!gram_pre) {
         tm.start();
         contract_ttt(ctx, y, y, mode, S.get(), true);
-        if (ctx->comm && !ctx->replicated) allreduce_sum(ctx, S.get(), I * I, &out.times.comm_ms);
+        if (ctx->comm && !ctx->replicated) allreduce_sym(ctx, S.get(), I, &out.times.comm_ms);
         out.times.gram_ms = tm.stop_ms();
         Sg = S.get();
     } else {
@@ -367,11 +367,17 @@ atk_tensor* sthosvd(atk_ctx* ctx, const atk_tensor* x, const uint64_t* ranks, at
                     atk_mode_report* reports, const ModeZeroPre* pre) {
     check_tensor(x, "sthosvd input");
     const int order = x->order;
-    for (int n = 0; n < order; ++n)
-        if (ranks[n] < 1 || ranks[n] > x->dims[n])
+    // sharded input: the last mode's GLOBAL size, from one collective up front
+    // (every rank reaches it, so a bad rank fails on all ranks alike); the
+    // global J of every sharded mode follows from it without further exchange
+    const uint64_t g_last = ctx->comm ? comm_global_last(ctx, x) : x->dims[order - 1];
+    for (int n = 0; n < order; ++n) {
+        const uint64_t dn = n == order - 1 ? g_last : x->dims[n];
+        if (ranks[n] < 1 || ranks[n] > dn)
             fail(ATK_RANK_EXCEEDS_DIM, "truncation " + std::to_string(ranks[n]) +
                                            " invalid for mode " + std::to_string(n) +
-                                           " of dimension " + std::to_string(x->dims[n]));
+                                           " of dimension " + std::to_string(dn));
+    }
     const atk_tensor* work = x;
     atk_tensor* owned = nullptr;
     size_t foff = 0;
@@ -389,7 +395,7 @@ atk_tensor* sthosvd(atk_ctx* ctx, const atk_tensor* x, const uint64_t* ranks, at
             }
             const uint64_t I = work->dims[n], r = ranks[n];
             uint64_t J = j_of(work, n);
-            if (ctx->comm && n < order - 1) J = J / work->dims[order - 1] * comm_global_last(ctx, work);
+            if (ctx->comm && n < order - 1) J = J / work->dims[order - 1] * g_last;
             atk_mode_report rep{};
             rep.mode = n;
             for (int m = 0; m < order; ++m) rep.dims_before[m] = work->dims[m];
@@ -433,10 +439,12 @@ atk_tensor* sthosvd(atk_ctx* ctx, const atk_tensor* x, const uint64_t* ranks, at
         }
     } catch (...) {
         ctx->replicated = false;
+        comm_end_call(ctx);
         if (owned) atk_tensor_free(owned);
         throw;
     }
     ctx->replicated = false;
+    comm_end_call(ctx);
     return owned;
 }
 

@@ -19,6 +19,9 @@ for p in $PARTS; do
     peaks) timeout 300 python profiles/measure_peaks.py gpurun_out/${TAG}_peaks.json > gpurun_out/${TAG}_peaks.log 2>&1; echo "peaks=$?"; tail -c 600 gpurun_out/${TAG}_peaks.json; echo;;
     bigeig) ATK_TRD_PROFILE=1 timeout 600 python profiles/eig_big_probe.py > gpurun_out/${TAG}_bigeig.log 2>&1; echo "bigeig=$?"; grep -E "dense eig|trd n|method=|Error|error" gpurun_out/${TAG}_bigeig.log | tail -30;;
     bigeigt) timeout 900 python -m pytest tests/test_gpu_eig_big.py -x -q -p no:hypothesispytest > gpurun_out/${TAG}_bigeigt.log 2>&1; echo "bigeigt=$? $(tail -1 gpurun_out/${TAG}_bigeigt.log)"; grep -E "Error|assert|FAIL" gpurun_out/${TAG}_bigeigt.log | head -20;;
+    c5ueig) ATK_TRACE=1 timeout 600 python profiles/c5u_eig_probe.py > gpurun_out/${TAG}_c5ueig.log 2>&1; echo "c5ueig=$?"; grep -E "^method|hand|dense|passes" gpurun_out/${TAG}_c5ueig.log | tail -30;;
+    dist) timeout 900 python -m pytest tests/test_gpu_dist.py -x -q -p no:hypothesispytest > gpurun_out/${TAG}_dist.log 2>&1; echo "dist=$? $(tail -1 gpurun_out/${TAG}_dist.log)"; grep -E "Error|assert" gpurun_out/${TAG}_dist.log | head -20;;
+    cpp) timeout 600 python -m pytest tests/test_gpu_cpp.py tests/test_cpp_types.py -x -q -p no:hypothesispytest > gpurun_out/${TAG}_cpp.log 2>&1; echo "cpp=$? $(tail -1 gpurun_out/${TAG}_cpp.log)";;
     fast) timeout 900 python -m pytest tests -m "gpu and not slow" -x -q -p no:hypothesispytest > gpurun_out/${TAG}_tests.log 2>&1; echo "fast=$? $(tail -1 gpurun_out/${TAG}_tests.log)";;
     bench) timeout 600 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err; echo "bench=$?"; head -c 400 gpurun_out/${TAG}_bench.json; echo;;
     ref) timeout 600 python bench.py --impl reference > gpurun_out/${TAG}_ref.json 2> gpurun_out/${TAG}_ref.err; echo "ref=$?"; head -c 300 gpurun_out/${TAG}_ref.json; echo;;

@@ -106,3 +106,86 @@ def test_two_ranks_one_gpu_host_collectives(dims, ranks, kinds, dtype, tol):
     assert abs(g - gr) / gr <= tol
     assert fd <= (1e-8 if dtype == np.float64 else 1e-3)
     assert comm_ms > 0.0
+
+
+def _schedule_worker(rank, world, port, dims, ranks, kinds, out):
+    import os
+    import sys
+    from pathlib import Path
+
+    sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2010_10131_b200 import atucker
+    from paper_2010_10131_b200.dist import init_host_comm_from_torch, shard_range
+    from paper_2010_10131_b200.errors import RankExceedsDim
+    from paper_2010_10131_b200.selector import SolverKind, Strategy
+
+    ctx = atucker.Context(0)
+    init_host_comm_from_torch(ctx)
+    lo, hi = shard_range(dims[-1], rank, world)
+    slab = list(dims[:-1]) + [hi - lo]
+    xl = atucker.DeviceTensor.uniform(slab, 3, np.float32, ctx=ctx, offset=lo * int(np.prod(dims[:-1])))
+    strat = Strategy.manual([SolverKind(k) for k in kinds])
+    ctx.comm_stats(reset=True)
+    res = atucker.sthosvd(xl, ranks, strat, atucker.AlsOptions(num_iters=3), ctx=ctx, global_dims=dims)
+    st = ctx.comm_stats()
+    # a rank above the global last dimension fails on every rank alike (no hang)
+    bad = list(ranks[:-1]) + [dims[-1] + 1]
+    try:
+        atucker.sthosvd(xl, bad, strat, ctx=ctx, global_dims=dims)
+        failed = False
+    except RankExceedsDim:
+        failed = True
+    out.put((rank, st, list(res.decomposition.core.shape), failed))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("dims,ranks,kinds", [
+    ([256, 256, 256], [16, 16, 16], [0, 0, 0]),  # C5-shaped at 1/512 of the size
+    ([96, 40, 33], [12, 8, 17], [0, 1, 0]),      # uneven slabs 16 / 17 and R_N = 17 > the smaller slab
+])
+def test_sharded_schedule_collectives(dims, ranks, kinds):
+    """SURVEY §8(e) schedule, counted on the host-staged backend (2 ranks on the one GPU):
+    one sizes exchange, ONE packed-triangle Gram allreduce per sharded EIG mode
+    (I(I+1)/2 doubles), two allreduces (YR, GR) per sharded ALS iteration, and the
+    last-mode all-gather (one broadcast per rank) — and nothing else."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    mpc = mp.get_context("spawn")
+    q = mpc.Queue()
+    procs = [mpc.Process(target=_schedule_worker, args=(r, 2, port, dims, ranks, kinds, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=300) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    n = len(dims)
+    ar_calls, ar_bytes, work = 1, 2 * 8, list(dims)
+    for m in range(n - 1):
+        i, r = work[m], ranks[m]
+        if kinds[m] == 0:
+            ar_calls += 1
+            ar_bytes += i * (i + 1) // 2 * 8
+        else:
+            ar_calls += 2 * 3
+            ar_bytes += 3 * (i * r + r * r) * 8
+        work[m] = r
+    gather_bytes = int(np.prod(work)) * 4  # the shrunk tensor before the last mode, fp32
+    for rank, st, shape, failed in got:
+        assert shape == list(ranks)
+        assert failed
+        assert st["allreduce_calls"] == ar_calls, st
+        assert st["allreduce_bytes"] == ar_bytes, st
+        assert st["gather_calls"] == 2, st
+        assert st["gather_bytes"] == gather_bytes, st
