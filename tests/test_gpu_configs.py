@@ -157,3 +157,22 @@ def lowrank_plus_noise(dims, ranks, seed, noise=1e-2, dtype=np.float32):
     x.axpy(noise, nz)       # x <- x + noise * uniform
     nz.free()
     return x
+
+
+def test_frobenius_norm_device_fp32_large():
+    """atk_frobenius_norm (tensor.hpp:158-168) on a 64M-element fp32 device tensor
+    (the counter-hash stream, bit-identical to the oracle's), accumulated in fp64."""
+    import sys
+    from pathlib import Path
+
+    from paper_2010_10131_b200 import atucker
+
+    sys.path.insert(0, str(Path(__file__).resolve().parent.parent / "oracle"))
+    import oracle as o
+
+    ctx = atucker.Context.default(0)
+    dims = [512, 512, 256]
+    x = atucker.DeviceTensor.uniform(dims, 21, np.float32, ctx=ctx)
+    ref = np.sqrt(o.norm2_f32(o.hash_uniform(21, int(np.prod(dims)))))
+    got = atucker.frobenius_norm(x, ctx=ctx)
+    assert abs(got - ref) <= 1e-12 * ref, (got, ref)

@@ -55,6 +55,27 @@ def rel(a, b):
     return float(np.abs(np.asarray(a) - np.asarray(b)).max() / max(1e-300, np.abs(b).max()))
 
 
+# ======================================================================= tensor
+def test_frobenius_norm_basics(impl):
+    """test_tensor.cpp:29-37 (tensor.hpp:158-168)."""
+    assert impl.frobenius_norm(np.zeros((2, 2, 2), order="F")) == 0.0
+    assert abs(impl.frobenius_norm(np.ones((2, 2, 2), order="F")) - np.sqrt(8.0)) <= 1e-12
+    iota = np.arange(1.0, 9.0).reshape((2, 2, 2), order="F")  # sum of squares 204
+    assert abs(impl.frobenius_norm(iota) - np.sqrt(204.0)) <= 1e-12
+
+
+def test_frobenius_norm_matches_every_unfolding(impl):
+    """test_tensor.cpp:39-51: the norm of every mode-n unfolding equals the tensor's."""
+    rng = np.random.default_rng(11)
+    for rep in range(20):
+        order = 2 + rep % 3
+        x = random_signed(rng_dims(rng, order, 2, 7), int(rng.integers(1 << 62)), "normal")
+        ref = impl.frobenius_norm(x)
+        assert abs(ref - np.sqrt((x * x).sum())) <= 1e-13 * ref
+        for n in range(order):
+            assert abs(impl.frobenius_norm(np.asfortranarray(unfold(x, n))) - ref) <= 1e-13 * ref
+
+
 # ======================================================================= kernels
 def test_ttm_identity_and_ones(impl):
     """test_kernels.cpp:34-49."""
