@@ -140,6 +140,8 @@ uint64_t atk_ctx_launch_count(const atk_ctx* ctx);
  *   "eig_method"   -1 auto (tridiagonal for n <= 200, else ChFSI handing over to the dense solver
  *                  after "eig_dense_passes" filter passes), 0 dense Jacobi (n <= 112; also the
  *                  Rayleigh-Ritz solver), 1 ChFSI only, 2 / 3 exact dense tridiagonal (any n <= 4096)
+ *   "svd_explicit"  1 = fp64 SVD modes on the explicit unfolding (Gram-preconditioned one-sided
+ *                  Jacobi; default), 0 = the Gram route (sigma = sqrt(lambda))
  *   "eig_dense_passes" ChFSI filter passes before the exact dense solver takes over (default 3;
  *                  -1 = never)
  *   "chfsi_tol"     relative Ritz-residual target of ChFSI (default 1e-12; fp32 Grams use >= 1e-9)

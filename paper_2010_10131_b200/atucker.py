@@ -537,7 +537,7 @@ def _reports(reps, order: int) -> list:
             predicted_cost_eig=rp.predicted_cost_eig, predicted_cost_als=rp.predicted_cost_als,
             dims_before=tuple(int(v) for v in rp.dims_before[:order]),
             dims_after=tuple(int(v) for v in rp.dims_after[:order]),
-            iterations_run=rp.iterations_run, eig_method={0: "jacobi", 1: "chfsi", 2: "tridiag", 3: "dense"}.get(rp.eig_method, "?"),
+            iterations_run=rp.iterations_run, eig_method={0: "jacobi", 1: "chfsi", 2: "tridiag", 3: "dense", 4: "svd-jacobi"}.get(rp.eig_method, "?"),
             times=StageTimes.from_c(rp.times)))
     return out
 

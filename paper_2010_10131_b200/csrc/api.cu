@@ -231,6 +231,7 @@ atk_status atk_ctx_set_option(atk_ctx* ctx, const char* key, double value) {
         else if (k == "trd_tiles") ctx->trd_tiles = int(value);
         else if (k == "chfsi_k") ctx->chfsi_k = int(value);
         else if (k == "eig_dense_passes") ctx->eig_dense_passes = int(value);
+        else if (k == "svd_explicit") ctx->svd_explicit = int(value);
         else if (k == "eig_assume_psd") ctx->eig_assume_psd = value != 0.0;
         else if (k == "tma_tf32") ctx->tma_tf32 = value != 0.0;
         else if (k == "gram_chunk_kb") ctx->gram_chunk_kb = int(value);

@@ -55,6 +55,9 @@ struct AlsOut {
     int iterations_run = 0;
     double comm_ms = 0.0;  // per-iteration YR/GR allreduce (sharded runs)
 };
+// svd.cu — svd_mode_solver on the explicit unfolding (fp64; one-sided Jacobi)
+bool svd_explicit_supported(atk_ctx* ctx, const atk_tensor* y, int mode);
+ModeOut svd_mode_explicit(atk_ctx* ctx, const atk_tensor* y, int mode, uint64_t r);
 void contract_ttt(atk_ctx* ctx, const atk_tensor* x, const atk_tensor* y, int mode, double* z_dev,
                   bool sym);
 // als_tc.cu — one ALS iteration's contractions in one pass over Y (mode 0, fp32, R <= 32)

@@ -56,6 +56,7 @@ struct atk_ctx {
     int force_simt = 0;        // option "simt": portable CUDA-core contractions
     int eig_method = -1;       // option "eig_method": -1 auto, 0 dense Jacobi, 1 ChFSI, 2 tridiagonal,
                                // 3 tridiagonal at every n (the grid-wide reduction above 200)
+    int svd_explicit = 1;      // option "svd_explicit": SVD mode on the explicit unfolding (fp64)
     int eig_dense_passes = 3;  // option "eig_dense_passes": ChFSI filter passes before the exact dense
                                // solver takes over (n > 200; -1 never)
     double chfsi_tol = 1e-12;  // option "chfsi_tol": relative Ritz residual target
@@ -250,7 +251,7 @@ void transpose(atk_ctx* ctx, const double* a, int rows, int cols, double* at);
 
 // eig.cu — sym_eig_top_r on device (linalg.hpp:101-123).
 struct EigInfo {
-    int method = 0;      // 0 dense Jacobi, 1 ChFSI
+    int method = 0;      // 0 dense Jacobi, 1 ChFSI, 2 tridiagonal, 3 dense (n > 200), 4 explicit SVD
     int iterations = 0;  // ChFSI outer iterations
     double residual = 0;
 };

@@ -80,6 +80,11 @@ ModeOut eig_mode(atk_ctx* ctx, const atk_tensor* y, int mode, uint64_t r, int so
     const uint64_t I = y->dims[mode], J = j_of(y, mode);
     if (solver_kind == ATK_SOLVER_SVD && r > std::min(I, J))
         fail(ATK_RANK_TOO_LARGE, "truncation exceeds the rank bound of the unfolding");
+    // the reference's SVD works on the explicit unfolding (solvers.hpp:142-162);
+    // fp32 data carries no more than the Gram route's precision (sqrt(eps64)
+    // relative sigma), sharded modes have J spread over the ranks: Gram route
+    if (solver_kind == ATK_SOLVER_SVD && !gram_pre && svd_explicit_supported(ctx, y, mode))
+        return svd_mode_explicit(ctx, y, mode, r);
     ModeOut out;
     out.solver = solver_kind;
     StageTimer tm(ctx);

@@ -831,7 +831,7 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
     bool have_bounds = false;
     double scale = 0.0;
     int it = 0;
-    double worst = 0.0;
+    double worst = 0.0, prev_worst = 0.0;
     for (;; ++it) {
         ritz_residual<<<r, 256, 0, st>>>(Wr.get(), Vr.get(), theta.get(), n, r, res.get());
         ATK_LAUNCHED(ctx);
@@ -848,6 +848,29 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
             mark("to-dense", it, worst / scale);
             return dense_big("ChFSI pass budget");
         }
+        // measured convergence: the residual reduction of the last pass predicts
+        // the passes still needed; hand over as soon as they would cost more than
+        // the dense solver (C5u: 2.2e-2 -> 1.8e-3 in the first pass, ~6 more
+        // passes of ~4.5 ms against ~19 ms dense; C2's flat modes gain >= 1e3
+        // per pass and stay)
+        if (ctx->eig_dense_passes >= 0 && it >= 1 && prev_worst > 0.0 && n <= kBigEigMax && n > kTridiagMax &&
+            ctx->eig_method == -1) {
+            const double rate = prev_worst / std::max(worst, 1e-300);
+            const double need = std::log(std::max(1.0, worst / (tol * scale)));
+            const double left = rate > 1.0 ? need / std::log(rate) : 1e9;
+            const double t_step = 4.0 + 2.0 * double(n) * n * k / 12e12 * 1e6;  // us
+            const double t_pass = 64.0 * t_step * 1e-3 + 0.6;                   // ms
+            const double fn = double(n) / 2048.0, fg = std::max(0.0, (n - 640.0) / 1408.0);
+            const double t_dense = 5.0 + 10.9 * fg * fg + 0.8 * fn + 2.3 * fn * fn;  // ms
+            if (trace)
+                std::fprintf(stderr, "[atk eig n=%d] pass rate %.3g, %.1f passes left (%.1f ms) vs dense %.1f ms\n",
+                             n, rate, left, left * t_pass, t_dense);
+            if (left * t_pass > t_dense) {
+                mark("to-dense", it, worst / scale);
+                return dense_big("predicted ChFSI passes");
+            }
+        }
+        prev_worst = worst;
         if (!have_bounds) {
             if (trace)
                 std::fprintf(stderr, "[atk eig n=%d r=%d k=%d] theta_1 %.6e theta_r %.6e theta_k %.6e\n", n, r, k,
