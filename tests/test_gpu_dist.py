@@ -139,7 +139,7 @@ def _schedule_worker(rank, world, port, dims, ranks, kinds, out):
         failed = False
     except RankExceedsDim:
         failed = True
-    out.put((rank, st, list(res.decomposition.core.shape), failed))
+    out.put((rank, st, list(res.decomposition.core.dims), failed))
     dist.barrier()
     dist.destroy_process_group()
 
