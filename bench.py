@@ -13,9 +13,10 @@ value : device-resident throughput (input already in HBM, > L2 so no flush
         needed), CUDA events on the engine stream, max over ranks.
 e2e   : the same through the host-buffer C-ABI entry atk_sthosvd_host: every
         step copies the input from pinned host memory and the core back.
-roofline : dominant kernel = the mode-1 Gram (gram_tf32_kernel + its split-K
-        reduction), I^2 J flops per launch / its event-timed duration, against
-        half the measured bf16 peak (tf32 rate).
+roofline : dominant kernel = the mode-1 Gram (gram_tf32_2cta_kernel K-launches
+        + the split-K reduction), I^2 J flops per launch / its event-timed
+        duration, against the measured sustained cuBLAS tf32 rate
+        (profiles/peaks_r2.json; the burst fraction is reported too).
 cpu_baseline : the CPU oracle (oracle/, reference port) on a bounded sample of
         the same workload (the leading slabs of the last mode, ~15 s), all host
         threads, with its per-stage split and the host's lscpu model / RAM.
@@ -71,16 +72,25 @@ def flops_of(dims, ranks, kinds, num_iters=5):
     return out
 
 
-FP64_TC_TFLOPS = 40.0  # B200 spec fp64 tensor (DMMA) rate; MEASURED_PEAKS.json has no fp64 figure
-
-
 def peaks():
+    """Roofline denominators: HBM and bf16 from the driver's MEASURED_PEAKS.json;
+    tf32 and fp64 (which it lacks) from profiles/peaks_r2.json, measured on a
+    B200 of this pool by profiles/measure_peaks.py (cuBLAS tf32 / DGEMM
+    8192^3, best single launch = burst, 4 s back to back = sustained)."""
+    out = {"hbm": 6650.0, "bf16": 1590.0, "bf16_sus": 1400.0, "src": "fallback"}
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
         d = json.loads(p.read_text())
-        return {"hbm": d["hbm_gbs"], "bf16": d["bf16_tflops"], "bf16_sus": d["bf16_tflops_sustained"],
-                "src": "measured"}
-    return {"hbm": 6650.0, "bf16": 1590.0, "bf16_sus": 1400.0, "src": "fallback"}
+        out.update(hbm=d["hbm_gbs"], bf16=d["bf16_tflops"], bf16_sus=d["bf16_tflops_sustained"], src="measured")
+    q = ROOT / "profiles" / "peaks_r2.json"
+    if q.exists():
+        d = json.loads(q.read_text())
+        out.update(tf32=d["tf32_tflops"], tf32_sus=d["tf32_tflops_sustained"], fp64=d["fp64_tflops"],
+                   fp64_sus=d["fp64_tflops_sustained"], tf_src=f"measured {d['when']} (profiles/peaks_r2.json)")
+    else:  # derived: tf32 = half the bf16 rate, fp64 = B200 DMMA spec
+        out.update(tf32=out["bf16"] / 2, tf32_sus=out["bf16_sus"] / 2, fp64=40.0, fp64_sus=40.0,
+                   tf_src="derived (tf32 = bf16 / 2, fp64 = 40 TF/s spec)")
+    return out
 
 
 class ClockSampler:
@@ -488,7 +498,9 @@ def main():
                        "ttm_gbs": round(4 * (np.prod(rp.dims_before) + np.prod(rp.dims_after)) /
                                         max(t.ttm_ms, 1e-9) / 1e6, 1)})
     pk = peaks()
-    tf32_peak = pk["bf16_sus"] / 2.0
+    # the Gram runs inside a long step (back-to-back st-HOSVDs): the sustained
+    # tf32 rate is its denominator; the burst fraction is reported beside it
+    tf32_peak = pk["tf32_sus"]
     g0 = reports[-1][0]
     gram_flops = fl[0].get("gram", 0)
     achieved = gram_flops / (g0.times.gram_ms * 1e-3) / 1e12 if g0.times.gram_ms > 0 else None
@@ -499,12 +511,17 @@ def main():
     roofline = {"kernel": "gram_tf32_2cta_kernel (+gram2_reduce), mode 1 (n = 0)",
                 "bound": "tensor", "achieved": achieved, "peak": tf32_peak, "unit": "TFLOP/s",
                 "frac": (achieved / tf32_peak) if achieved else None, "traffic": traffic,
-                "peak_note": f"tf32 = 1/2 of the {pk['src']} sustained bf16 {pk['bf16_sus']} TF/s",
-                "algorithmic_flops_per_launch": gram_flops}
+                "peak_burst": pk["tf32"], "frac_burst": (achieved / pk["tf32"]) if achieved else None,
+                "peak_note": f"tf32 sustained (cuBLAS tf32 8192^3, 4 s back to back), {pk['tf_src']}; "
+                             f"frac_burst against its best single launch",
+                "algorithmic_flops_per_launch": gram_flops,
+                "algorithmic_bytes_per_launch": 4 * int(np.prod(gdims)),
+                "traffic_note": "dram read+write of the same logical Gram (16 K-launches + reduce), "
+                                "ncu --metrics, profiles/gram_traffic.json"}
 
     # SURVEY 8(d) pipeline fraction: sum over stages of max(F / P, B / BW) against
     # the measured step (eig excluded from the bound, included in the step)
-    P = (tf32_peak if cfg["dtype"] == "f32" else FP64_TC_TFLOPS) * 1e12
+    P = (tf32_peak if cfg["dtype"] == "f32" else pk["fp64_sus"]) * 1e12
     BW = pk["hbm"] * 1e9
     es = 4 if cfg["dtype"] == "f32" else 8
     t_bound = 0.0
@@ -519,7 +536,8 @@ def main():
         work[n] = r
     pipeline = {"t_bound_ms": t_bound * 1e3, "frac": t_bound * 1e3 / ms,
                 "note": "sum of max(flops/peak, bytes/HBM) over Gram/TTM (ALS: HBM bytes); eig not in the bound"
-                        + ("" if cfg["dtype"] == "f32" else f"; fp64 peak {FP64_TC_TFLOPS} TF/s (B200 spec DMMA)")}
+                        + (f"; tf32 peak {tf32_peak:.1f} TF/s" if cfg["dtype"] == "f32"
+                           else f"; fp64 peak {pk['fp64_sus']:.1f} TF/s (measured DGEMM)")}
 
     # e2e through the host-buffer C ABI (pinned host input, core back)
     e2e = None
