@@ -121,9 +121,18 @@ StageTimer::~StageTimer() {
     if (a) cudaEventDestroy(a);
     if (b) cudaEventDestroy(b);
 }
-void StageTimer::start() { ATK_CUDA(cudaEventRecord(a, ctx->stream)); }
-double StageTimer::stop_ms() {
+void StageTimer::start() {
+    if (!a) ATK_CUDA(cudaEventCreate(&a));
+    if (!b) ATK_CUDA(cudaEventCreate(&b));
+    ATK_CUDA(cudaEventRecord(a, ctx->stream));
+}
+double StageTimer::stop_ms(int field) {
     ATK_CUDA(cudaEventRecord(b, ctx->stream));
+    if (ctx->defer_timing && field >= 0) {
+        ctx->deferred.push_back({a, b, ctx->timing_mode, field});
+        a = b = nullptr;
+        return 0.0;
+    }
     ATK_CUDA(cudaEventSynchronize(b));
     float ms = 0;
     ATK_CUDA(cudaEventElapsedTime(&ms, a, b));
@@ -527,6 +536,7 @@ atk_status atk_eig_mode(atk_ctx* ctx, const atk_tensor* y, int mode, uint64_t r,
         bind(ctx);
         check_tensor(y, "atk_eig_mode");
         ModeOut mo = eig_mode(ctx, y, mode, r, ATK_SOLVER_EIG);
+        factor_to_host(ctx, mo, y->dims[mode] * r);
         std::memcpy(factor_out, mo.factor.data(), mo.factor.size() * sizeof(double));
         *shrunk_out = mo.shrunk;
         copy_times(times, mo.times);
@@ -539,6 +549,7 @@ atk_status atk_svd_mode(atk_ctx* ctx, const atk_tensor* y, int mode, uint64_t r,
         bind(ctx);
         check_tensor(y, "atk_svd_mode");
         ModeOut mo = eig_mode(ctx, y, mode, r, ATK_SOLVER_SVD);
+        factor_to_host(ctx, mo, y->dims[mode] * r);
         std::memcpy(factor_out, mo.factor.data(), mo.factor.size() * sizeof(double));
         *shrunk_out = mo.shrunk;
         copy_times(times, mo.times);

@@ -42,7 +42,8 @@ void tc_ttm(atk_ctx* ctx, const atk_tensor* x, const double* u_dev, uint64_t R, 
 
 // driver.cu
 struct ModeOut {
-    std::vector<double> factor;  // I x r host
+    std::vector<double> factor;  // I x r host (filled by factor_to_host, or by the ALS path)
+    DevBuf<double> factor_dev;   // I x r device: EIG / SVD factors stay resident until the caller needs them
     atk_tensor* shrunk = nullptr;
     int iterations = 0;
     int solver = ATK_SOLVER_EIG;
@@ -55,6 +56,8 @@ struct AlsOut {
     int iterations_run = 0;
     double comm_ms = 0.0;  // per-iteration YR/GR allreduce (sharded runs)
 };
+// Host copy of a mode's factor (one D2H + sync; no-op when already on the host).
+void factor_to_host(atk_ctx* ctx, ModeOut& m, uint64_t count);
 // svd.cu — svd_mode_solver on the explicit unfolding (fp64; one-sided Jacobi)
 bool svd_explicit_supported(atk_ctx* ctx, const atk_tensor* y, int mode);
 ModeOut svd_mode_explicit(atk_ctx* ctx, const atk_tensor* y, int mode, uint64_t r);

@@ -47,8 +47,18 @@ struct Comm;  // dist.cu
 
 }  // namespace atk
 
+namespace atk {
+struct DeferredTiming {
+    cudaEvent_t a, b;
+    int mode, field;
+};
+}  // namespace atk
+
 struct atk_ctx {
     int device = 0;
+    bool defer_timing = false;  // StageTimer hands its events to `deferred` (sthosvd)
+    int timing_mode = 0;
+    std::vector<atk::DeferredTiming> deferred;
     int num_sms = 148;
     cudaStream_t stream = nullptr;
     cudaStream_t own_stream = nullptr;
@@ -160,13 +170,19 @@ void check_mode(int order, int mode);
 void record_gemm(long long charge);
 
 // ------------------------------------------------------------------ timing
+// Per-stage device time.  stop_ms(field) synchronizes on the stop event,
+// unless the context defers timing (sthosvd does): then the event pair is
+// handed to ctx->deferred and resolved after the call's final sync, so no
+// stage boundary blocks the host (the next stage is enqueued while the GPU
+// still runs this one).
+enum StageField { kStageGram = 0, kStageEig = 1, kStageTtm = 2, kStageAls = 3, kStageComm = 4 };
 struct StageTimer {
     atk_ctx* ctx;
     cudaEvent_t a = nullptr, b = nullptr;
     explicit StageTimer(atk_ctx* c);
     ~StageTimer();
     void start();
-    double stop_ms();  // synchronizes on the stop event
+    double stop_ms(int field = -1);
 };
 
 // ------------------------------------------------------------------ kernels

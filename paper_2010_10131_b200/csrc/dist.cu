@@ -214,7 +214,7 @@ void allreduce_sum(atk_ctx* ctx, double* buf, uint64_t n, double* comm_ms) {
                    "ncclAllReduce");
         nccl_poll(ctx->comm, "ncclAllReduce");
     }
-    const double ms = t.stop_ms();
+    const double ms = t.stop_ms(kStageComm);
     if (comm_ms) *comm_ms += ms;
 }
 
@@ -250,7 +250,7 @@ void allreduce_sum2(atk_ctx* ctx, double* a, uint64_t na, double* b, uint64_t nb
         nccl_check(nccl().GroupEnd(), "ncclGroupEnd");
         nccl_poll(ctx->comm, "ncclAllReduce(YR, GR)");
     }
-    const double ms = t.stop_ms();
+    const double ms = t.stop_ms(kStageComm);
     if (comm_ms) *comm_ms += ms;
 }
 

@@ -94,7 +94,7 @@ ModeOut eig_mode(atk_ctx* ctx, const atk_tensor* y, int mode, uint64_t r, int so
         tm.start();
         contract_ttt(ctx, y, y, mode, S.get(), true);
         if (ctx->comm && !ctx->replicated) allreduce_sym(ctx, S.get(), I, &out.times.comm_ms);
-        out.times.gram_ms = tm.stop_ms();
+        out.times.gram_ms = tm.stop_ms(kStageGram);
         Sg = S.get();
     } else {
         out.times.gram_ms = gram_pre_ms;
@@ -111,19 +111,26 @@ ModeOut eig_mode(atk_ctx* ctx, const atk_tensor* y, int mode, uint64_t r, int so
                             // the engine's Grams are mirrored (bitwise symmetric); an allreduce
                             // may sum (i, j) and (j, i) in different orders, so sharded modes symmetrise
                             /*exact_sym=*/!ctx->comm || ctx->replicated);
-    out.times.eig_ms = tm.stop_ms();
+    out.times.eig_ms = tm.stop_ms(kStageEig);
 
     tm.start();
     transpose(ctx, vecs.get(), int(I), int(r), ut.get());  // U^T : r x I
     out.shrunk = contract_ttm(ctx, y, ut.get(), r, mode);
     record_gemm(2LL * (long long)(r * J) * (long long)I);
-    out.times.ttm_ms = tm.stop_ms();
-    out.factor.resize(I * r);
-    ATK_CUDA(cudaMemcpyAsync(out.factor.data(), vecs.get(), I * r * sizeof(double),
-                             cudaMemcpyDeviceToHost, ctx->stream));
-    ATK_CUDA(cudaStreamSynchronize(ctx->stream));
+    out.times.ttm_ms = tm.stop_ms(kStageTtm);
+    // the factor stays on the device: sthosvd downloads all of them once at the
+    // end, so no host round trip sits between one mode and the next
+    out.factor_dev = std::move(vecs);
     out.times.total_ms = out.times.gram_ms + out.times.eig_ms + out.times.ttm_ms;
     return out;
+}
+
+void factor_to_host(atk_ctx* ctx, ModeOut& m, uint64_t count) {
+    if (!m.factor.empty() || !m.factor_dev.get()) return;
+    m.factor.resize(count);
+    ATK_CUDA(cudaMemcpyAsync(m.factor.data(), m.factor_dev.get(), count * sizeof(double), cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    ATK_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
 // ------------------------------------------------------------------ ALS
@@ -353,7 +360,7 @@ ModeOut als_mode(atk_ctx* ctx, const atk_tensor* y, int mode, uint64_t r, const 
     ATK_CUDA(cudaMemcpyAsync(out.factor.data(), Q.get(), I * r * sizeof(double),
                              cudaMemcpyDeviceToHost, ctx->stream));
     ATK_CUDA(cudaStreamSynchronize(ctx->stream));
-    out.times.als_ms = tm.stop_ms();
+    out.times.als_ms = tm.stop_ms(kStageAls);
     out.times.comm_ms = it.comm_ms;
     out.times.total_ms = out.times.als_ms;
     out.iterations = it.iterations_run;
@@ -386,8 +393,27 @@ atk_tensor* sthosvd(atk_ctx* ctx, const atk_tensor* x, const uint64_t* ranks, at
     const atk_tensor* work = x;
     atk_tensor* owned = nullptr;
     size_t foff = 0;
+    size_t ftotal = 0;
+    for (int n = 0; n < order; ++n) ftotal += (n == order - 1 ? g_last : x->dims[n]) * ranks[n];
+    DevBuf<double> fdev(ctx, ftotal);  // every device-resident factor, downloaded once at the end
+    std::vector<std::pair<size_t, size_t>> dev_segs;
+    // stage times are resolved from their events after the final sync
+    struct DeferScope {
+        atk_ctx* c;
+        explicit DeferScope(atk_ctx* cc) : c(cc) {
+            for (auto& d : c->deferred) { cudaEventDestroy(d.a); cudaEventDestroy(d.b); }
+            c->deferred.clear();
+            c->defer_timing = true;
+        }
+        ~DeferScope() {
+            c->defer_timing = false;
+            for (auto& d : c->deferred) { cudaEventDestroy(d.a); cudaEventDestroy(d.b); }
+            c->deferred.clear();
+        }
+    } defer_scope(ctx);
     try {
         for (int n = 0; n < order; ++n) {
+            ctx->timing_mode = n;
             // after the all-gather the last mode runs on the full (replicated)
             // tensor: its Gram / YR / GR are complete on every rank, no allreduce
             ctx->replicated = ctx->comm && n == order - 1;
@@ -434,8 +460,15 @@ atk_tensor* sthosvd(atk_ctx* ctx, const atk_tensor* x, const uint64_t* ranks, at
             rep.iterations_run = mo.iterations;
             rep.eig_method = mo.eig.method;
             rep.times = mo.times;
-            std::copy(mo.factor.begin(), mo.factor.end(), factors_out + foff);
-            foff += mo.factor.size();
+            const uint64_t fcount = work->dims[n] * r;
+            if (mo.factor_dev.get()) {
+                ATK_CUDA(cudaMemcpyAsync(fdev.get() + foff, mo.factor_dev.get(), fcount * sizeof(double),
+                                         cudaMemcpyDeviceToDevice, ctx->stream));
+                dev_segs.push_back({foff, fcount});
+            } else {
+                std::copy(mo.factor.begin(), mo.factor.end(), factors_out + foff);  // ALS: already on the host
+            }
+            foff += fcount;
             if (owned) atk_tensor_free(owned);
             owned = mo.shrunk;
             work = owned;
@@ -450,6 +483,24 @@ atk_tensor* sthosvd(atk_ctx* ctx, const atk_tensor* x, const uint64_t* ranks, at
     }
     ctx->replicated = false;
     comm_end_call(ctx);
+    std::vector<double> h(dev_segs.empty() ? 0 : ftotal);
+    if (!dev_segs.empty())
+        ATK_CUDA(cudaMemcpyAsync(h.data(), fdev.get(), ftotal * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    ATK_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (const auto& sg : dev_segs) std::copy(h.begin() + sg.first, h.begin() + sg.first + sg.second, factors_out + sg.first);
+    if (reports) {
+        for (const auto& d : ctx->deferred) {
+            float ms = 0.f;
+            ATK_CUDA(cudaEventElapsedTime(&ms, d.a, d.b));
+            atk_stage_times& t = reports[d.mode].times;
+            double* f[] = {&t.gram_ms, &t.eig_ms, &t.ttm_ms, &t.als_ms, &t.comm_ms};
+            *f[d.field] += double(ms);
+        }
+        for (int n = 0; n < order; ++n) {
+            atk_stage_times& t = reports[n].times;
+            t.total_ms = t.gram_ms + t.eig_ms + t.ttm_ms + t.als_ms;
+        }
+    }
     return owned;
 }
 

@@ -182,7 +182,7 @@ ModeOut svd_mode_explicit(atk_ctx* ctx, const atk_tensor* y, int mode, uint64_t 
     tm.start();
     DevBuf<double> S(ctx, I * I), vals(ctx, I), Q(ctx, I * I), Qt(ctx, I * I);
     contract_ttt(ctx, y, y, mode, S.get(), true);
-    out.times.gram_ms = tm.stop_ms();
+    out.times.gram_ms = tm.stop_ms(kStageGram);
     record_gemm((long long)(I * I) * (long long)J);
     tm.start();
     if (I <= uint64_t(kTridiagMax))
@@ -231,7 +231,7 @@ ModeOut svd_mode_explicit(atk_ctx* ctx, const atk_tensor* y, int mode, uint64_t 
     ATK_CUDA(cudaMemcpyAsync(dperm.get(), perm.data(), r * sizeof(int), cudaMemcpyHostToDevice, st));
     gather_left<<<unsigned(r), kSvdThreads, 0, st>>>(Q.get(), int(I), dperm.get(), U.get(), sign.get());
     ATK_LAUNCHED(ctx);
-    out.times.eig_ms = tm.stop_ms();
+    out.times.eig_ms = tm.stop_ms(kStageEig);
     tm.start();
     uint64_t od[ATK_MAX_ORDER];
     for (int m = 0; m < y->order; ++m) od[m] = y->dims[m];
@@ -240,10 +240,8 @@ ModeOut svd_mode_explicit(atk_ctx* ctx, const atk_tensor* y, int mode, uint64_t 
     tensorize_rows<<<grid_for(ctx, s.P * r * s.O), 256, 0, st>>>(M.get(), s.P, s.O, int(r), dperm.get(), sign.get(),
                                                                  static_cast<double*>(out.shrunk->data));
     ATK_LAUNCHED(ctx);
-    out.times.ttm_ms = tm.stop_ms();
-    out.factor.resize(I * r);
-    ATK_CUDA(cudaMemcpyAsync(out.factor.data(), U.get(), I * r * sizeof(double), cudaMemcpyDeviceToHost, st));
-    ATK_CUDA(cudaStreamSynchronize(st));
+    out.times.ttm_ms = tm.stop_ms(kStageTtm);
+    out.factor_dev = std::move(U);
     out.eig.method = 4;
     out.eig.iterations = sweeps + 1;  // Jacobi sweeps
     out.times.total_ms = out.times.gram_ms + out.times.eig_ms + out.times.ttm_ms;
