@@ -695,25 +695,58 @@ __device__ void invit_member(const double* __restrict__ d, const double* __restr
     if (fabs(di) < tiny) di = copysign(tiny, di);
     dd[(n - 1) * st] = 1.0 / di;
     for (int i = 0; i < n; ++i) x[i * xs] = hash_unit(uint64_t(m) * 1000003ULL + i);
+    // The solves are serial recurrences over rows; their operands are loaded
+    // kCh rows at a time into registers first (x[j] is read before it is
+    // overwritten in both sweeps, so the early loads are exact), which keeps
+    // kCh loads in flight instead of one memory round trip per row.
+    constexpr int kCh = 16;
     for (int it = 0; it < 3; ++it) {
         double cr = x[0];
-        for (int i = 0; i + 1 < n; ++i) {
-            const double nx = x[(i + 1) * xs];
-            if (pv[i * st] != 0.0) {
-                x[i * xs] = nx;
-                cr = fma(-dl[i * st], nx, cr);
-            } else {
-                x[i * xs] = cr;
-                cr = fma(-dl[i * st], cr, nx);
-            }
+        for (int i0 = 0; i0 + 1 < n; i0 += kCh) {
+            const int cnt = min(kCh, n - 1 - i0);
+            double pvr[kCh], dlr[kCh], nxr[kCh];
+#pragma unroll
+            for (int q = 0; q < kCh; ++q)
+                if (q < cnt) {
+                    pvr[q] = pv[(i0 + q) * st];
+                    dlr[q] = dl[(i0 + q) * st];
+                    nxr[q] = x[(i0 + q + 1) * xs];
+                }
+#pragma unroll
+            for (int q = 0; q < kCh; ++q)
+                if (q < cnt) {
+                    const double nx = nxr[q];
+                    if (pvr[q] != 0.0) {
+                        x[(i0 + q) * xs] = nx;
+                        cr = fma(-dlr[q], nx, cr);
+                    } else {
+                        x[(i0 + q) * xs] = cr;
+                        cr = fma(-dlr[q], cr, nx);
+                    }
+                }
         }
         double x2 = 0.0, x1 = cr * dd[(n - 1) * st];
         x[(n - 1) * xs] = x1;
-        for (int i = n - 2; i >= 0; --i) {
-            const double xi = (x[i * xs] - du[i * st] * x1 - du2[i * st] * x2) * dd[i * st];
-            x[i * xs] = xi;
-            x2 = x1;
-            x1 = xi;
+        for (int i1 = n - 2; i1 >= 0; i1 -= kCh) {
+            const int cnt = min(kCh, i1 + 1);
+            double xr[kCh], ur[kCh], u2r[kCh], dr[kCh];
+#pragma unroll
+            for (int q = 0; q < kCh; ++q)
+                if (q < cnt) {
+                    const int i = i1 - q;
+                    xr[q] = x[i * xs];
+                    ur[q] = du[i * st];
+                    u2r[q] = du2[i * st];
+                    dr[q] = dd[i * st];
+                }
+#pragma unroll
+            for (int q = 0; q < kCh; ++q)
+                if (q < cnt) {
+                    const double xi = (xr[q] - ur[q] * x1 - u2r[q] * x2) * dr[q];
+                    x[(i1 - q) * xs] = xi;
+                    x2 = x1;
+                    x1 = xi;
+                }
         }
         double mx = 0.0;
         for (int i = 0; i < n; ++i) mx = fmax(mx, fabs(x[i * xs]));
@@ -745,6 +778,19 @@ __global__ void __launch_bounds__(kIpT) invit_par_kernel(const double* __restric
     double* xw = wk + size_t(5) * n * st + m;
     invit_member(d, e, n, lam, m, tnsh, wk + m, st, xw, st);
     for (int i = 0; i < n; ++i) X[size_t(m) * n + i] = xw[size_t(i) * st];
+}
+
+__global__ void any_cluster(const double* __restrict__ d, const double* __restrict__ e, int n,
+                            const double* __restrict__ lam, int nw, int* __restrict__ out) {
+    __shared__ TNorm tnsh;
+    if (threadIdx.x < 32) {
+        const TNorm t = tnorm_warp(d, e, n);
+        if (threadIdx.x == 0) tnsh = t;
+    }
+    __syncthreads();
+    int c = 0;
+    for (int m = threadIdx.x + 1; m < nw; m += blockDim.x) c |= (lam[m - 1] - lam[m] <= 1e-3 * tnsh.norm);
+    if (__syncthreads_or(c) && threadIdx.x == 0) *out = 1;
 }
 
 // emax = max |G - I| (G: nw x nw), as the bit pattern of a non-negative double
@@ -791,6 +837,14 @@ __global__ void __launch_bounds__(kIbT) invit_block_small_kernel(const double* _
     }
     __syncthreads();
     const TNorm tn = tnsh;
+    // no dstein cluster among the wanted values: nothing to orthogonalise, the
+    // one-warp-per-member kernel is the cheaper one
+    int clustered = 0;
+    for (int m = t + 1; m < nw; m += kIbT) clustered |= (lam[m - 1] - lam[m] <= 1e-3 * tn.norm);
+    if (!__syncthreads_or(clustered)) {
+        if (t == 0) *ok = 0;
+        return;
+    }
     for (int m = t; m < nw; m += kIbT) invit_member(d, e, n, lam, m, tn, wk + m, size_t(nw), X + m, size_t(nw));
     for (int step = 0; step < 2; ++step) {
         __syncthreads();
@@ -1397,6 +1451,16 @@ static bool invit_block(atk_ctx* ctx, const double* d, const double* e, int n, c
                         double* X) {
     if (nw < 2 || std::getenv("ATK_INVIT_SEQ")) return false;
     cudaStream_t st = ctx->stream;
+    {  // any dstein cluster among the wanted values?  (else one CTA per member is cheaper)
+        DevBuf<int> cl(ctx, 1);
+        ATK_CUDA(cudaMemsetAsync(cl.get(), 0, sizeof(int), st));
+        any_cluster<<<1, 256, 0, st>>>(d, e, n, values, nw, cl.get());
+        ATK_LAUNCHED(ctx);
+        int h = 0;
+        ATK_CUDA(cudaMemcpyAsync(&h, cl.get(), sizeof(int), cudaMemcpyDeviceToHost, st));
+        ATK_CUDA(cudaStreamSynchronize(st));
+        if (!h) return false;
+    }
     DevBuf<double> wk(ctx, size_t(6) * n * nw), G(ctx, size_t(nw) * nw), C(ctx, size_t(nw) * nw),
         X2(ctx, size_t(n) * nw);
     DevBuf<unsigned long long> em(ctx, 1);
