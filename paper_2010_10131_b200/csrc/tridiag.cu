@@ -789,8 +789,8 @@ __global__ void any_cluster(const double* __restrict__ d, const double* __restri
     }
     __syncthreads();
     int c = 0;
-    for (int m = threadIdx.x + 1; m < nw; m += blockDim.x) c |= (lam[m - 1] - lam[m] <= 1e-3 * tnsh.norm);
-    if (__syncthreads_or(c) && threadIdx.x == 0) *out = 1;
+    for (int m = threadIdx.x + 1; m < nw; m += blockDim.x) c += (lam[m - 1] - lam[m] <= 1e-3 * tnsh.norm);
+    atomicAdd(out, c);  // clustered neighbour pairs
 }
 
 // emax = max |G - I| (G: nw x nw), as the bit pattern of a non-negative double
@@ -818,6 +818,7 @@ __global__ void lowdin_coeff(const double* __restrict__ g, int nw, double* __res
 // defect > 1e-3 it leaves *fallback = 1 and invit_kernel (launched right
 // after with `skip` = !fallback) redoes the block sequentially.
 constexpr int kIbSmall = 6400;
+constexpr int kIbMinPairs = 8;  // clustered neighbour pairs before the block path pays
 constexpr int kIbT = 256;
 __global__ void __launch_bounds__(kIbT) invit_block_small_kernel(const double* __restrict__ d,
                                                                  const double* __restrict__ e, int n,
@@ -837,11 +838,12 @@ __global__ void __launch_bounds__(kIbT) invit_block_small_kernel(const double* _
     }
     __syncthreads();
     const TNorm tn = tnsh;
-    // no dstein cluster among the wanted values: nothing to orthogonalise, the
-    // one-warp-per-member kernel is the cheaper one
+    // few dstein-clustered neighbours among the wanted values (C5's signal
+    // Ritz values): the one-warp-per-cluster kernel is the cheaper one (its
+    // short Gram-Schmidt chains cost less than this kernel's block steps)
     int clustered = 0;
-    for (int m = t + 1; m < nw; m += kIbT) clustered |= (lam[m - 1] - lam[m] <= 1e-3 * tn.norm);
-    if (!__syncthreads_or(clustered)) {
+    for (int m = t + 1; m < nw; m += kIbT) clustered += (lam[m - 1] - lam[m] <= 1e-3 * tn.norm);
+    if (__syncthreads_count(clustered) < kIbMinPairs) {  // nw <= 80 < kIbT: one pair per thread
         if (t == 0) *ok = 0;
         return;
     }
@@ -1459,7 +1461,7 @@ static bool invit_block(atk_ctx* ctx, const double* d, const double* e, int n, c
         int h = 0;
         ATK_CUDA(cudaMemcpyAsync(&h, cl.get(), sizeof(int), cudaMemcpyDeviceToHost, st));
         ATK_CUDA(cudaStreamSynchronize(st));
-        if (!h) return false;
+        if (h < kIbMinPairs) return false;
     }
     DevBuf<double> wk(ctx, size_t(6) * n * nw), G(ctx, size_t(nw) * nw), C(ctx, size_t(nw) * nw),
         X2(ctx, size_t(n) * nw);
