@@ -35,17 +35,25 @@
 namespace atk {
 namespace {
 
-constexpr int TM2 = 256, TN2 = 256, HALF = 128, BK = 32, STAGES2 = 6, THREADS = 192;
-constexpr uint32_t A_BYTES = HALF * BK * 4, B_BYTES = HALF * BK * 4, STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr size_t SMEM2 = STAGES2 * STAGE_BYTES + 1024 + 256;
+constexpr int TM2 = 256, TN2 = 256, HALF = 128, BK = 32, THREADS = 192;
+constexpr uint32_t A_BYTES = HALF * BK * 4, B_BYTES = HALF * BK * 4;
+// narrow unit: one 256 x 256 tile, 6 stages of A + B halves (32 KB);
+// wide unit: two tiles of one tile row sharing A, 4 stages of A + B0 + B1 (48 KB)
+template <bool WIDE>
+struct Cfg {
+    static constexpr int STAGES = WIDE ? 4 : 6;
+    static constexpr uint32_t STAGE_BYTES = A_BYTES + (WIDE ? 2 : 1) * B_BYTES;
+    static constexpr size_t SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+    static constexpr int NBUF = WIDE ? 1 : 2;  // accumulator buffers in TMEM (2 x 256 columns either way)
+};
 
 struct Gram2Params {
-    const int4* units;  // {tile_m, tile_n, kb_begin, kb_end} in 256-tiles
+    const int4* units;  // {tile_m, tile_n0 | tile_n1 << 16 (0xffff: none), kb_begin, kb_end} in 256-tiles
     int num_units;      // units are dealt to clusters round-robin
     int chunk_kb;
     int kmajor;
     int nkb_p;
-    double* acc;        // [unit][TN2][TM2] fp64 partial tiles
+    float* acc;         // [slot][TN2][TM2] fp32 partial tiles; unit u owns slots 2u (, 2u + 1)
     int accumulate;     // 1: add into acc (a later K-launch of the same Gram)
 };
 
@@ -110,8 +118,12 @@ __device__ __forceinline__ void mma2_commit_mc(uint64_t* bar) {
         : "memory");
 }
 
+template <bool WIDE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     gram_tf32_2cta_kernel(const __grid_constant__ CUtensorMap tma_x, const Gram2Params p) {
+    constexpr int STAGES2 = Cfg<WIDE>::STAGES;
+    constexpr uint32_t STAGE_BYTES = Cfg<WIDE>::STAGE_BYTES;
+    constexpr int NBUF = Cfg<WIDE>::NBUF;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES2 * STAGE_BYTES);
@@ -154,22 +166,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             uint32_t phase = 0;
             for (int u = pair; u < p.num_units; u += npairs) {
                 const int4 un = p.units[u];
-                const int arow = un.x * TM2 + int(crank) * HALF, brow = un.y * TN2 + int(crank) * HALF;
+                const int tn0 = un.y & 0xffff, tn1 = un.y >> 16;
+                const bool two = WIDE && tn1 != 0xffff;
+                const int arow = un.x * TM2 + int(crank) * HALF, brow = tn0 * TN2 + int(crank) * HALF;
+                const int brow1 = two ? tn1 * TN2 + int(crank) * HALF : 0;
+                const uint32_t bytes = 2 * (A_BYTES + (two ? 2 : 1) * B_BYTES);  // both CTAs of the pair
                 for (int kb = un.z; kb < un.w; ++kb) {
                     tc::mbar_wait(&empty[stage], phase ^ 1);
-                    if (leader) tc::mbar_arrive_expect_tx(&full[stage], 2 * STAGE_BYTES);
+                    if (leader) tc::mbar_arrive_expect_tx(&full[stage], bytes);
                     uint8_t* a = smem + stage * STAGE_BYTES;
                     uint8_t* b = a + A_BYTES;
+                    uint8_t* b1 = b + B_BYTES;
                     if (!p.kmajor) {
                         const int k0 = kb * BK;
 #pragma unroll
                         for (int q = 0; q < HALF / 32; ++q) tma2_load_2d(a + q * 4096, &tma_x, &full[stage], arow + q * 32, k0);
 #pragma unroll
                         for (int q = 0; q < HALF / 32; ++q) tma2_load_2d(b + q * 4096, &tma_x, &full[stage], brow + q * 32, k0);
+                        if (two) {
+#pragma unroll
+                            for (int q = 0; q < HALF / 32; ++q)
+                                tma2_load_2d(b1 + q * 4096, &tma_x, &full[stage], brow1 + q * 32, k0);
+                        }
                     } else {
                         const int p0 = (kb % p.nkb_p) * BK, o0 = kb / p.nkb_p;
                         tma2_load_3d(a, &tma_x, &full[stage], p0, o0, arow);
                         tma2_load_3d(b, &tma_x, &full[stage], p0, o0, brow);
+                        if (two) tma2_load_3d(b1, &tma_x, &full[stage], p0, o0, brow1);
                     }
                     if (++stage == STAGES2) { stage = 0; phase ^= 1; }
                 }
@@ -183,11 +206,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             uint32_t phase = 0, aphase = 0;
             for (int u = pair; u < p.num_units; u += npairs) {
                 const int4 un = p.units[u];
+                const bool two = WIDE && (un.y >> 16) != 0xffff;
                 for (int c0 = un.z; c0 < un.w; c0 += p.chunk_kb) {
                     const int c1 = min(un.w, c0 + p.chunk_kb);
                     tc::mbar_wait(&tempty[abuf], aphase ^ 1);
                     tc::tc_fence_after();
-                    const uint32_t d = tmem_base + uint32_t(abuf * TN2);
+                    const uint32_t d = tmem_base + uint32_t(abuf * TN2);  // WIDE: tile 0 at 0, tile 1 at 256
                     for (int kb = c0; kb < c1; ++kb) {
                         tc::mbar_wait(&full[stage], phase);
                         tc::tc_fence_after();
@@ -195,21 +219,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                         const uint32_t b_base = a_base + A_BYTES;
 #pragma unroll
                         for (int k = 0; k < BK / 8; ++k) {
-                            uint64_t ad, bd;
+                            uint64_t ad, bd, bd1 = 0;
                             if (!p.kmajor) {
                                 ad = tc::smem_desc(a_base + k * 1024, 4096, 512, 1);
                                 bd = tc::smem_desc(b_base + k * 1024, 4096, 512, 1);
+                                if (two) bd1 = tc::smem_desc(b_base + B_BYTES + k * 1024, 4096, 512, 1);
                             } else {
                                 ad = tc::smem_desc_sw128(a_base + k * 32, 16, 1024);
                                 bd = tc::smem_desc_sw128(b_base + k * 32, 16, 1024);
+                                if (two) bd1 = tc::smem_desc_sw128(b_base + B_BYTES + k * 32, 16, 1024);
                             }
-                            mma2_tf32(d, ad, bd, idesc, (kb > c0 || k > 0) ? 1u : 0u);
+                            const uint32_t acc = (kb > c0 || k > 0) ? 1u : 0u;
+                            mma2_tf32(d, ad, bd, idesc, acc);
+                            if (two) mma2_tf32(d + uint32_t(TN2), ad, bd1, idesc, acc);  // A reused from smem
                         }
                         mma2_commit_mc(&empty[stage]);
                         if (++stage == STAGES2) { stage = 0; phase ^= 1; }
                     }
                     mma2_commit_mc(&tfull[abuf]);
-                    if (++abuf == 2) { abuf = 0; aphase ^= 1; }
+                    if (++abuf == NBUF) { abuf = 0; aphase ^= 1; }
                 }
             }
         }
@@ -223,29 +251,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         uint32_t aphase = 0;
         for (int u = pair; u < p.num_units; u += npairs) {
             const int4 un = p.units[u];
-            double* tile = p.acc + size_t(u) * TM2 * TN2;
+            const int ntile = (WIDE && (un.y >> 16) != 0xffff) ? 2 : 1;
+            float* tile = p.acc + size_t(2 * u) * TM2 * TN2;
             for (int c0 = un.z; c0 < un.w; c0 += p.chunk_kb) {
                 tc::mbar_wait(&tfull[abuf], aphase);
                 tc::tc_fence_after();
                 const bool first = !p.accumulate && (c0 == un.z);
 #pragma unroll 1
-                for (int cc = 0; cc < TN2 / 32; ++cc) {
+                for (int cc = 0; cc < ntile * (TN2 / 32); ++cc) {  // WIDE: tile 1's columns follow tile 0's
                     uint32_t r[32];
                     tc::tmem_ld_32x32b_x32(tmem_base + (uint32_t(q * 32) << 16) + uint32_t(abuf * TN2 + cc * 32), r);
                     tc::tmem_ld_wait();
-                    double* dst = tile + size_t(cc * 32) * TM2 + row;
+                    float* dst = tile + size_t(cc * 32) * TM2 + row;  // slot 2u + cc / 8 continues contiguously
                     if (first) {
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) dst[size_t(j) * TM2] = double(__uint_as_float(r[j]));
+                        for (int j = 0; j < 32; ++j) dst[size_t(j) * TM2] = __uint_as_float(r[j]);
                     } else {
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) dst[size_t(j) * TM2] += double(__uint_as_float(r[j]));
+                        for (int j = 0; j < 32; ++j) dst[size_t(j) * TM2] += __uint_as_float(r[j]);
                     }
                 }
                 tc::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive_cluster(abuf ? tempty_leader1 : tempty_leader0);
-                if (++abuf == 2) { abuf = 0; aphase ^= 1; }
+                if (++abuf == NBUF) { abuf = 0; aphase ^= 1; }
             }
         }
     }
@@ -260,9 +289,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 // S = fixed-order sum of the split partials, mirrored: one 32 x 32 block
 // (bi <= bj) per CTA iteration, the mirror written through a shared-memory
 // transpose so both stores are coalesced (the direct mirror store was a
-// 2048-stride scatter: 33 us per C5 Gram).
-__global__ void __launch_bounds__(256) gram2_reduce(const double* __restrict__ acc, const int* __restrict__ tile_unit,
-                                                    int splits, int ntn, int I, double* __restrict__ s) {
+// 2048-stride scatter: 33 us per C5 Gram).  Tile (ti, tj), ti <= tj, is the sum
+// of slots tslots[(ti nt + tj) smax + k] (k < count, -1 terminated); a tile
+// computed transposed (as (tj, ti), to keep every tile row's count even for the
+// wide units) is read transposed.
+__global__ void __launch_bounds__(256) gram2_reduce(const float* __restrict__ acc, const int* __restrict__ tslots,
+                                                    const int* __restrict__ ttrans, int smax, int nt, int I,
+                                                    double* __restrict__ s) {
     __shared__ double tb[32][33];
     const int nb = (I + 31) / 32, nblk = nb * (nb + 1) / 2;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
@@ -275,9 +308,10 @@ __global__ void __launch_bounds__(256) gram2_reduce(const double* __restrict__ a
             const int i = 32 * bi + tx, j = 32 * bj + r;  // column j, row i (i fastest)
             double v = 0.0;
             if (i < I && j < I && i <= j) {
-                const int u0 = tile_unit[(i / TM2) * ntn + (j / TN2)];
-                const size_t off = size_t(j % TN2) * TM2 + (i % TM2);
-                for (int k = 0; k < splits; ++k) v += acc[size_t(u0 + k) * TM2 * TN2 + off];
+                const int t = (i / TM2) * nt + (j / TN2);
+                const int* sl = tslots + size_t(t) * smax;
+                const size_t off = ttrans[t] ? size_t(i % TM2) * TM2 + (j % TN2) : size_t(j % TN2) * TM2 + (i % TM2);
+                for (int k = 0; k < smax && sl[k] >= 0; ++k) v += double(acc[size_t(sl[k]) * TM2 * TN2 + off]);
                 s[size_t(i) + size_t(I) * j] = v;
             }
             tb[r][tx] = v;  // tb[j - 32 bj][i - 32 bi]
@@ -326,25 +360,63 @@ void tc_gram2(atk_ctx* ctx, const atk_tensor* x, int mode, double* s_dev) {
         nkb = uint64_t(nkb_p) * s.O;
     }
     const int nt = (I + TM2 - 1) / TM2;
-    std::vector<int> tiles_m, tiles_n;
-    for (int tn = 0; tn < nt; ++tn)
-        for (int tmi = 0; tmi <= tn; ++tmi) {
-            tiles_m.push_back(tmi);
-            tiles_n.push_back(tn);
+    const bool wide = ctx->gram_wide != 0;
+    // tile rows: the upper triangle (ti <= tj).  Wide units pair two tiles of one
+    // row (A staged once, two N = 256 MMAs); a row with an odd count hands one
+    // tile (a, b) to another odd row b as its transpose (b, a), so (for an even
+    // tile count) every unit is wide.
+    std::vector<std::vector<int>> row_tiles(nt);
+    std::vector<int> trans(size_t(nt) * nt, 0);
+    for (int ti = 0; ti < nt; ++ti)
+        for (int tj = ti; tj < nt; ++tj) row_tiles[ti].push_back(tj);
+    if (wide) {
+        int pend = -1;
+        for (int ti = 0; ti < nt; ++ti) {
+            if (row_tiles[ti].size() % 2 == 0) continue;
+            if (pend < 0) {
+                pend = ti;
+            } else {  // move tile (pend, ti) to row ti as (ti, pend)
+                auto& rp = row_tiles[pend];
+                rp.erase(std::find(rp.begin(), rp.end(), ti));
+                row_tiles[ti].push_back(pend);
+                trans[size_t(pend) * nt + ti] = 1;
+                pend = -1;
+            }
         }
-    const int ntiles = int(tiles_m.size());
-    static bool attr = false;
-    if (!attr) {
-        ATK_CUDA(cudaFuncSetAttribute(gram_tf32_2cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM2)));
-        attr = true;
+    }
+    struct WUnit {
+        int tm, tn0, tn1;
+    };
+    std::vector<WUnit> wu;
+    for (int ti = 0; ti < nt; ++ti) {
+        const auto& rt = row_tiles[ti];
+        for (size_t q = 0; q < rt.size(); q += wide ? 2 : 1)
+            wu.push_back({ti, rt[q], (wide && q + 1 < rt.size()) ? rt[q + 1] : 0xffff});
+    }
+    const int nwu = int(wu.size());
+    if (wide) {
+        static bool attr_w = false;
+        if (!attr_w) {
+            ATK_CUDA(cudaFuncSetAttribute(gram_tf32_2cta_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          int(Cfg<true>::SMEM)));
+            attr_w = true;
+        }
+    } else {
+        static bool attr_n = false;
+        if (!attr_n) {
+            ATK_CUDA(cudaFuncSetAttribute(gram_tf32_2cta_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          int(Cfg<false>::SMEM)));
+            attr_n = true;
+        }
     }
     // CTA pairs that are co-resident (GPCs with an odd SM count leave SMs unused)
-    static int pairs_resident = 0;
-    if (!pairs_resident) {
+    static int pairs_resident[2] = {0, 0};
+    int& pr = pairs_resident[wide ? 1 : 0];
+    if (!pr) {
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(2 * (ctx->num_sms / 2), 1, 1);
         cfg.blockDim = dim3(THREADS, 1, 1);
-        cfg.dynamicSmemBytes = SMEM2;
+        cfg.dynamicSmemBytes = wide ? Cfg<true>::SMEM : Cfg<false>::SMEM;
         cudaLaunchAttribute at{};
         at.id = cudaLaunchAttributeClusterDimension;
         at.val.clusterDim.x = 2;
@@ -353,36 +425,47 @@ void tc_gram2(atk_ctx* ctx, const atk_tensor* x, int mode, double* s_dev) {
         cfg.attrs = &at;
         cfg.numAttrs = 1;
         int nc = 0;
-        if (cudaOccupancyMaxActiveClusters(&nc, gram_tf32_2cta_kernel, &cfg) != cudaSuccess || nc <= 0) {
+        const cudaError_t e = wide ? cudaOccupancyMaxActiveClusters(&nc, gram_tf32_2cta_kernel<true>, &cfg)
+                                   : cudaOccupancyMaxActiveClusters(&nc, gram_tf32_2cta_kernel<false>, &cfg);
+        if (e != cudaSuccess || nc <= 0) {
             cudaGetLastError();
             nc = ctx->num_sms / 2;
         }
-        pairs_resident = std::min(nc, ctx->num_sms / 2);
+        pr = std::min(nc, ctx->num_sms / 2);
     }
-    const int pairs_avail = pairs_resident;
-    int splits = std::max(1, pairs_avail / ntiles);  // floor: units <= CTA pairs (one wave)
+    const int pairs_avail = pr;
+    // split-K: every unit into the same number of K pieces, as many as keep one wave
+    int splits = std::max(1, pairs_avail / nwu);
     splits = int(std::min<uint64_t>(uint64_t(splits), std::max<uint64_t>(1, nkb / 8)));
     const int chunk_kb = ctx->gram_chunk_kb > 0 ? ctx->gram_chunk_kb : 512;
     std::vector<int4> units;
-    std::vector<int> tile_unit(size_t(nt) * nt, 0);
-    for (int t = 0; t < ntiles; ++t) {
-        tile_unit[size_t(tiles_m[t]) * nt + tiles_n[t]] = int(units.size());
+    const int smax = splits;
+    std::vector<int> tslots(size_t(nt) * nt * smax, -1);
+    for (int w = 0; w < nwu; ++w) {
         for (int sp = 0; sp < splits; ++sp) {
             const int kb0 = int(nkb * sp / splits), kb1 = int(nkb * (sp + 1) / splits);
-            units.push_back(make_int4(tiles_m[t], tiles_n[t], kb0, std::max(kb0 + 1, kb1)));
+            const int u = int(units.size());
+            units.push_back(make_int4(wu[w].tm, wu[w].tn0 | (wu[w].tn1 << 16), kb0, std::max(kb0 + 1, kb1)));
+            for (int t = 0; t < (wu[w].tn1 != 0xffff ? 2 : 1); ++t) {
+                const int tn = t ? wu[w].tn1 : wu[w].tn0;
+                const int a = std::min(wu[w].tm, tn), b = std::max(wu[w].tm, tn);  // upper-triangle tile id
+                tslots[(size_t(a) * nt + b) * smax + sp] = 2 * u + t;
+            }
         }
     }
     DevBuf<int4> du(ctx, units.size());
-    DevBuf<int> dtu(ctx, tile_unit.size());
-    DevBuf<double> acc(ctx, units.size() * size_t(TM2) * TN2);
+    DevBuf<int> dts(ctx, tslots.size()), dtr(ctx, trans.size());
+    DevBuf<float> acc(ctx, units.size() * 2 * size_t(TM2) * TN2);
     ATK_CUDA(cudaMemcpyAsync(du.get(), units.data(), units.size() * sizeof(int4), cudaMemcpyHostToDevice, ctx->stream));
-    ATK_CUDA(cudaMemcpyAsync(dtu.get(), tile_unit.data(), tile_unit.size() * sizeof(int), cudaMemcpyHostToDevice,
+    ATK_CUDA(cudaMemcpyAsync(dts.get(), tslots.data(), tslots.size() * sizeof(int), cudaMemcpyHostToDevice,
                              ctx->stream));
+    ATK_CUDA(cudaMemcpyAsync(dtr.get(), trans.data(), trans.size() * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
     const int npairs = std::min<int>(int(units.size()), pairs_avail);
     Gram2Params prm{du.get(), int(units.size()), chunk_kb, kmajor ? 1 : 0, nkb_p, acc.get(), 0};
     // K-launches: unit u's K range [kb0, kb1) is walked in slices of launch_kb
     // K-blocks, one launch per slice index (all units advance together)
-    const int launch_kb = ctx->gram_launch_kb > 0 ? ctx->gram_launch_kb : (1 << 30);
+    int launch_kb = ctx->gram_launch_kb > 0 ? ctx->gram_launch_kb : (1 << 30);
+    if (wide && ctx->gram_launch_kb > 0) launch_kb = std::max(1, launch_kb / 2);  // same bytes per launch
     int max_len = 0;
     for (const int4& u : units) max_len = std::max(max_len, u.w - u.z);
     const int nlaunch = (max_len + launch_kb - 1) / launch_kb;
@@ -403,13 +486,15 @@ void tc_gram2(atk_ctx* ctx, const atk_tensor* x, int mode, double* s_dev) {
             prm.units = dlu.get() + size_t(L) * units.size();
             prm.accumulate = L > 0 ? 1 : 0;
         }
-        gram_tf32_2cta_kernel<<<2 * npairs, THREADS, SMEM2, ctx->stream>>>(tm, prm);
+        if (wide)
+            gram_tf32_2cta_kernel<true><<<2 * npairs, THREADS, Cfg<true>::SMEM, ctx->stream>>>(tm, prm);
+        else
+            gram_tf32_2cta_kernel<false><<<2 * npairs, THREADS, Cfg<false>::SMEM, ctx->stream>>>(tm, prm);
         ATK_LAUNCHED(ctx);
     }
-    const size_t n = size_t(I) * I;
     const int nb32 = (I + 31) / 32;
     gram2_reduce<<<unsigned(std::min(nb32 * (nb32 + 1) / 2, ctx->num_sms * 8)), 256, 0, ctx->stream>>>(
-        acc.get(), dtu.get(), splits, nt, I, s_dev);
+        acc.get(), dts.get(), dtr.get(), smax, nt, I, s_dev);
     ATK_LAUNCHED(ctx);
 }
 

@@ -146,3 +146,30 @@ def test_tc_gram_2cta_k_launches(dims, mode):
     # only the fp32 chain boundaries differ (64 vs 512 K-blocks per chain):
     # measured 5.5e-5 on the diagonal, the tf32 accumulation level
     assert np.abs(sk - s1).max() / scale <= 1e-4
+
+
+@pytest.mark.parametrize("dims,mode", [
+    ((512, 3000), 0), ((768, 2000), 0), ((1280, 900), 0), ((2048, 700), 0),  # nt = 2, 3, 5, 8 tile rows
+    ((64, 768, 40), 1), ((32, 1280, 30), 1),                                # K-major panels
+])
+def test_tc_gram_wide_units(dims, mode):
+    """The wide 2-CTA Gram (two tiles of one tile row per unit, A staged once;
+    odd rows hand a tile over as its transpose) against the one-tile-per-unit
+    kernel and the fp64 reference, at the tf32 level; exactly symmetric."""
+    from paper_2010_10131_b200 import atucker
+
+    ctx = atucker.Context.default(0)
+    xd = atucker.DeviceTensor.uniform(list(dims), 41, np.float32)
+    ref = gram_np(xd.to_numpy().astype(np.float64), mode)
+    try:
+        ctx.set_option("gram_wide", 0)
+        sn = atucker.gram(xd, mode)
+        ctx.set_option("gram_wide", 1)
+        sw = atucker.gram(xd, mode)
+    finally:
+        ctx.set_option("gram_wide", 1)
+    scale = np.abs(ref).max()
+    assert np.array_equal(sw, sw.T)
+    assert np.abs(sw - ref).max() / scale <= 1e-4
+    # same tf32 products, same chunking: only the split-K boundaries differ
+    assert np.abs(sw - sn).max() / scale <= 1e-4
