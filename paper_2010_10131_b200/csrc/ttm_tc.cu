@@ -15,6 +15,7 @@
 // warp 0 TMA, warp 1 MMA, warps 2-5 epilogue.  HBM-bound by design
 // (arithmetic intensity R/2 flop/B for fp32).
 #include <algorithm>
+#include <cstdlib>
 
 #include "atk_driver.cuh"
 #include "tc_common.cuh"
@@ -29,9 +30,12 @@ struct TtmParams {
     uint64_t P;       // inner size (MN-major layout)
     int R, NB;        // rank and padded N (multiple of 32)
     int nkb;          // K-blocks (ceil(I / 32))
+    int ks;           // K pieces per M tile (split-K when the tiles alone underfill the GPU)
+    int box4;         // MN-major A: one 4-D TMA box per stage ({32 p, 32 i, p-blocks, o}) instead of 8
+    int pb, ob;       // 4-D box: 32-row p blocks and o slabs per 256-row tile
     int stages;
     uint32_t stage_bytes, a_bytes;
-    float* y;
+    float* y;         // the output, or ks partial outputs (piece q at y + q M R) when ks > 1
 };
 
 template <bool KMAJOR_A>
@@ -74,9 +78,11 @@ __global__ void __launch_bounds__(THREADS, 1)
             int stage = 0;
             uint32_t phase = 0;
             const uint64_t pblk = p.P / 32;
-            for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            for (uint64_t it = blockIdx.x; it < ntiles * p.ks; it += gridDim.x) {
+                const uint64_t t = it / p.ks;
+                const int q = int(it % p.ks);
                 const uint64_t m0 = t * MT;
-                for (int kb = 0; kb < p.nkb; ++kb) {
+                for (int kb = p.nkb * q / p.ks; kb < p.nkb * (q + 1) / p.ks; ++kb) {
                     tc::mbar_wait(&empty[stage], phase ^ 1);
                     tc::mbar_arrive_expect_tx(&full[stage], p.stage_bytes);
                     uint8_t* a = smem + size_t(stage) * p.stage_bytes;
@@ -85,6 +91,9 @@ __global__ void __launch_bounds__(THREADS, 1)
                     if (KMAJOR_A) {
                         tc::tma_load_2d(a, &tma_x, &full[stage], k0, int(m0));
                         tc::tma_load_2d(a + 16384, &tma_x, &full[stage], k0, int(m0 + 128));
+                    } else if (p.box4) {
+                        // {32 p_lo, 32 i, pb p_hi, ob o}: lands as the 8 MN-major 4 KB groups in order
+                        tc::tma_load_4d(a, &tma_x, &full[stage], 0, k0, int((m0 % p.P) / 32), int(m0 / p.P));
                     } else {
 #pragma unroll
                         for (int g = 0; g < MT / 32; ++g) {
@@ -104,11 +113,13 @@ __global__ void __launch_bounds__(THREADS, 1)
             const uint32_t idesc = tc::idesc_tf32(128, p.NB, !KMAJOR_A, false);
             int stage = 0, abuf = 0;
             uint32_t phase = 0, aphase = 0;
-            for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            for (uint64_t it = blockIdx.x; it < ntiles * p.ks; it += gridDim.x) {
+                const int q = int(it % p.ks);
+                const int kb0 = p.nkb * q / p.ks;
                 tc::mbar_wait(&tempty[abuf], aphase ^ 1);
                 tc::tc_fence_after();
                 const uint32_t d0 = tmem_base + uint32_t(abuf * 2 * p.NB);
-                for (int kb = 0; kb < p.nkb; ++kb) {
+                for (int kb = kb0; kb < p.nkb * (q + 1) / p.ks; ++kb) {
                     tc::mbar_wait(&full[stage], phase);
                     tc::tc_fence_after();
                     const uint32_t a_base = tc::smem_u32(smem + size_t(stage) * p.stage_bytes);
@@ -121,7 +132,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                             uint64_t ad;
                             if (KMAJOR_A) ad = tc::smem_desc(a_base + h * 16384 + k * 32, 16, 1024, 2);
                             else ad = tc::smem_desc(a_base + h * 16384 + k * 1024, 4096, 512, 1);
-                            tc::mma_tf32(d0 + uint32_t(h * p.NB), ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+                            tc::mma_tf32(d0 + uint32_t(h * p.NB), ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
                         }
                     }
                     tc::mma_commit(&empty[stage]);
@@ -136,7 +147,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int q = warp & 3;
         int abuf = 0;
         uint32_t aphase = 0;
-        for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        for (uint64_t it = blockIdx.x; it < ntiles * p.ks; it += gridDim.x) {
+            const uint64_t t = it / p.ks;
+            float* const yq = p.y + uint64_t(it % p.ks) * p.M * uint64_t(p.R);
             tc::mbar_wait(&tfull[abuf], aphase);
             tc::tc_fence_after();
 #pragma unroll 1
@@ -151,7 +164,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                     if (!ok) continue;
                     const int nc = min(32, p.R - c);
                     if (KMAJOR_A) {
-                        float* dst = p.y + m * uint64_t(p.R) + c;
+                        float* dst = yq + m * uint64_t(p.R) + c;
                         if (nc == 32 && (p.R % 4) == 0) {
 #pragma unroll
                             for (int j = 0; j < 32; j += 4)
@@ -163,7 +176,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                         }
                     } else {
                         const uint64_t pp = m % p.P, o = m / p.P;
-                        float* dst = p.y + pp + p.P * (uint64_t(c) + uint64_t(p.R) * o);
+                        float* dst = yq + pp + p.P * (uint64_t(c) + uint64_t(p.R) * o);
 #pragma unroll
                         for (int j = 0; j < 32; ++j)
                             if (j < nc) dst[uint64_t(j) * p.P] = __uint_as_float(r[j]);
@@ -180,6 +193,15 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (warp == 1) {
         tc::tc_fence_after();
         tc::tmem_dealloc(tmem_base, tcols);
+    }
+}
+
+// y = the ks split-K partials summed in a fixed order (fp32, as the accumulators)
+__global__ void ttm_reduce(const float* __restrict__ part, uint64_t n, int ks, float* __restrict__ y) {
+    for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += uint64_t(gridDim.x) * blockDim.x) {
+        float v = part[e];
+        for (int q = 1; q < ks; ++q) v += part[uint64_t(q) * n + e];
+        y[e] = v;
     }
 }
 
@@ -229,12 +251,27 @@ void tc_ttm(atk_ctx* ctx, const atk_tensor* x, const double* u_dev, uint64_t R, 
         p.M = s.O;
         p.P = 1;
     } else {
-        const uint64_t dims[3] = {s.P, s.I, s.O};
-        const uint64_t str[2] = {s.P * 4, s.P * s.I * 4};
-        const uint32_t box[3] = {32, BK, 1};
-        if (encode_tensor_map(&tx, dt, 3, x->data, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) !=
-            CUDA_SUCCESS)
-            fail(ATK_CUDA_ERROR, "ttm: tensor map (MN-major) encoding failed");
+        // one 4-D box per stage when a 256-row tile is whole p blocks of whole o slabs
+        // (P | 256) or whole p blocks of one o slab (256 | P): map {32 p_lo, I, P/32 p_hi, O}
+        const bool box4 = !std::getenv("ATK_TTM_BOX3") && ((MT % s.P == 0) || (s.P % MT == 0));
+        if (box4) {
+            const uint64_t dims[4] = {32, s.I, s.P / 32, s.O};
+            const uint64_t str[3] = {s.P * 4, 32 * 4, s.P * s.I * 4};
+            p.pb = int(std::min<uint64_t>(s.P / 32, MT / 32));
+            p.ob = int(MT / 32 / p.pb);
+            const uint32_t box[4] = {32, BK, uint32_t(p.pb), uint32_t(p.ob)};
+            if (encode_tensor_map(&tx, dt, 4, x->data, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) !=
+                CUDA_SUCCESS)
+                fail(ATK_CUDA_ERROR, "ttm: tensor map (MN-major, 4-D) encoding failed");
+            p.box4 = 1;
+        } else {
+            const uint64_t dims[3] = {s.P, s.I, s.O};
+            const uint64_t str[2] = {s.P * 4, s.P * s.I * 4};
+            const uint32_t box[3] = {32, BK, 1};
+            if (encode_tensor_map(&tx, dt, 3, x->data, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) !=
+                CUDA_SUCCESS)
+                fail(ATK_CUDA_ERROR, "ttm: tensor map (MN-major) encoding failed");
+        }
         p.M = s.P * s.O;
         p.P = s.P;
     }
@@ -249,9 +286,22 @@ void tc_ttm(atk_ctx* ctx, const atk_tensor* x, const double* u_dev, uint64_t R, 
     auto kern = kmajor ? ttm_tf32_kernel<true> : ttm_tf32_kernel<false>;
     ATK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     const uint64_t ntiles = (p.M + MT - 1) / MT;
-    const int grid = int(std::min<uint64_t>(ntiles, uint64_t(ctx->num_sms)));
+    // split-K over I when the M tiles alone leave most SMs idle (C5's last
+    // mode: 16 tiles of 4096 x 64 over K = 2048); pieces of >= 8 K-blocks
+    p.ks = 1;
+    if (ntiles * 2 <= uint64_t(ctx->num_sms) && !std::getenv("ATK_TTM_NOSPLIT"))
+        p.ks = int(std::max<uint64_t>(1, std::min<uint64_t>(uint64_t(ctx->num_sms) / ntiles, uint64_t(p.nkb / 8))));
+    DevBuf<float> part(ctx, p.ks > 1 ? size_t(p.ks) * p.M * R : 0);
+    if (p.ks > 1) p.y = part.get();
+    const int grid = int(std::min<uint64_t>(ntiles * p.ks, uint64_t(ctx->num_sms)));
     kern<<<grid, THREADS, smem, ctx->stream>>>(tx, tf, p);
     ATK_LAUNCHED(ctx);
+    if (p.ks > 1) {
+        const uint64_t n = p.M * R;
+        ttm_reduce<<<unsigned(std::min<uint64_t>((n + 255) / 256, uint64_t(ctx->num_sms) * 8)), 256, 0,
+                     ctx->stream>>>(part.get(), n, p.ks, static_cast<float*>(y->data));
+        ATK_LAUNCHED(ctx);
+    }
 }
 
 }  // namespace atk

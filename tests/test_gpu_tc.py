@@ -74,6 +74,8 @@ def test_tc_gram_long_k_chunked():
 @pytest.mark.parametrize("dims,mode,r", [
     ((256, 1000), 0, 64), ((300, 64, 7), 0, 20), ((2048, 777), 0, 128), ((96, 40, 3), 0, 33),  # K-major A
     ((64, 256, 9), 1, 64), ((32, 128, 5), 1, 32), ((4096, 96), 1, 16), ((64, 64, 64), 2, 64),  # MN-major A
+    ((64, 64, 2048), 2, 64), ((64, 2048, 100), 1, 64), ((96, 128, 40), 1, 24),  # 4-D / 3-D boxes, split-K
+    ((128, 512, 2), 1, 32),
 ])
 def test_tc_ttm_vs_oracle(dims, mode, r, capsys):
     from paper_2010_10131_b200 import atucker
@@ -92,7 +94,7 @@ def test_tc_ttm_vs_oracle(dims, mode, r, capsys):
     with capsys.disabled():
         print(f"\nTTM dims={dims} mode={mode} r={r} launches={n_launch} maxrel={err:.2e} normrel={nrm:.2e}")
     assert err <= 4e-3 and nrm <= 1e-4
-    assert n_launch == 2  # factor cast + ttm_tf32_kernel
+    assert n_launch in (2, 3)  # factor cast + ttm_tf32_kernel (+ the split-K reduction)
 
 
 @pytest.mark.parametrize("dims,mode", [
