@@ -15,8 +15,8 @@ e2e   : the same through the host-buffer C-ABI entry atk_sthosvd_host: every
         step copies the input from pinned host memory and the core back.
 roofline : dominant kernel = the mode-1 Gram (gram_tf32_2cta_kernel K-launches
         + the split-K reduction), I^2 J flops per launch / its event-timed
-        duration, against the measured sustained cuBLAS tf32 rate
-        (profiles/peaks_r2.json; the burst fraction is reported too).
+        duration, against the measured cuBLAS tf32 burst rate
+        (profiles/peaks_r2.json; the sustained fraction is reported too).
 cpu_baseline : the CPU oracle (oracle/, reference port) on a bounded sample of
         the same workload (the leading slabs of the last mode, ~15 s), all host
         threads, with its per-stage split and the host's lscpu model / RAM.
@@ -498,9 +498,11 @@ def main():
                        "ttm_gbs": round(4 * (np.prod(rp.dims_before) + np.prod(rp.dims_after)) /
                                         max(t.ttm_ms, 1e-9) / 1e6, 1)})
     pk = peaks()
-    # the Gram runs inside a long step (back-to-back st-HOSVDs): the sustained
-    # tf32 rate is its denominator; the burst fraction is reported beside it
-    tf32_peak = pk["tf32_sus"]
+    # denominator: the measured cuBLAS tf32 burst rate (best single 8192^3
+    # launch).  Its 4 s sustained rate is lower (cuBLAS throttles to ~1.1 GHz
+    # under the power cap) and the Gram, which holds ~1.9 GHz, runs above it,
+    # so the sustained figure is reported beside it, not used as a ceiling.
+    tf32_peak = pk["tf32"]
     g0 = reports[-1][0]
     gram_flops = fl[0].get("gram", 0)
     achieved = gram_flops / (g0.times.gram_ms * 1e-3) / 1e12 if g0.times.gram_ms > 0 else None
@@ -511,9 +513,10 @@ def main():
     roofline = {"kernel": "gram_tf32_2cta_kernel (+gram2_reduce), mode 1 (n = 0)",
                 "bound": "tensor", "achieved": achieved, "peak": tf32_peak, "unit": "TFLOP/s",
                 "frac": (achieved / tf32_peak) if achieved else None, "traffic": traffic,
-                "peak_burst": pk["tf32"], "frac_burst": (achieved / pk["tf32"]) if achieved else None,
-                "peak_note": f"tf32 sustained (cuBLAS tf32 8192^3, 4 s back to back), {pk['tf_src']}; "
-                             f"frac_burst against its best single launch",
+                "peak_sustained": pk["tf32_sus"],
+                "frac_sustained": (achieved / pk["tf32_sus"]) if achieved else None,
+                "peak_note": f"tf32 burst = cuBLAS tf32 8192^3 best single launch, {pk['tf_src']}; "
+                             f"peak_sustained = 4 s back to back (cuBLAS at ~1.1 GHz under the power cap)",
                 "algorithmic_flops_per_launch": gram_flops,
                 "algorithmic_bytes_per_launch": 4 * int(np.prod(gdims)),
                 "traffic_note": "dram read+write of the same logical Gram (16 K-launches + reduce), "
