@@ -548,7 +548,10 @@ void svqb(atk_ctx* ctx, const double* Y, int n, int k, double* V, Ws& ws) {
 // Shifted CholeskyQR3 (three GEMM-based passes, the first with a diagonal
 // shift so a moderately ill-conditioned Y cannot break it down; Fukaya et al.).
 // Returns false if a Cholesky pivot still failed (V is then unusable).
-bool cholqr3(atk_ctx* ctx, const double* Y, int n, int k, double* V, Ws& ws) {
+// cholqr3_async enqueues the passes and leaves the pivot status of each in
+// ws.info[0..2] for the caller's next synchronisation (ChFSI reads it with its
+// residuals: no host round trip of its own).
+void cholqr3_async(atk_ctx* ctx, const double* Y, int n, int k, double* V, Ws& ws) {
     const double* src = Y;
     double* bufs[2] = {V, ws.tmp.get()};
     for (int pass = 0; pass < 3; ++pass) {
@@ -574,6 +577,10 @@ bool cholqr3(atk_ctx* ctx, const double* Y, int n, int k, double* V, Ws& ws) {
         src = dst;
     }
     // result of pass 2 is in bufs[0] == V
+}
+
+bool cholqr3(atk_ctx* ctx, const double* Y, int n, int k, double* V, Ws& ws) {
+    cholqr3_async(ctx, Y, n, k, V, ws);
     int h[3] = {0, 0, 0};
     ATK_CUDA(cudaMemcpyAsync(h, ws.info.get(), 3 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     ATK_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -811,7 +818,14 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
     ATK_LAUNCHED(ctx);
     dgemm(ctx, false, false, n, k, n, 1.0, Sp, n, Yb.get(), n, 0.0, Ya.get(), n);
     dgemm(ctx, false, false, n, k, n, 1.0, Sp, n, Ya.get(), n, 0.0, Yb.get(), n);
-    orthonormalize(ctx, Yb.get(), n, k, V.get(), ws);
+    // CholeskyQR3 without a host round trip: its status is read with the
+    // residuals below, and a failed pass is redone by SVQB from the same input
+    struct {
+        const double* src;
+        double* dst;
+        int ka;
+    } qr_job{Yb.get(), V.get(), k};
+    cholqr3_async(ctx, Yb.get(), n, k, V.get(), ws);
     mark("qr0");
     // Ritz vectors formed: the top r; all k once locking has started (the
     // active block is then Vk(:, nc:k)).  Forming all k from the start cost
@@ -837,7 +851,18 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
         ATK_LAUNCHED(ctx);
         ATK_CUDA(cudaMemcpyAsync(hth.data(), theta.get(), k * sizeof(double), cudaMemcpyDeviceToHost, st));
         ATK_CUDA(cudaMemcpyAsync(hres.data(), res.get(), r * sizeof(double), cudaMemcpyDeviceToHost, st));
+        int qinfo[3] = {0, 0, 0};
+        if (qr_job.src) ATK_CUDA(cudaMemcpyAsync(qinfo, ws.info.get(), sizeof(qinfo), cudaMemcpyDeviceToHost, st));
         ATK_CUDA(cudaStreamSynchronize(st));
+        if (qr_job.src && (qinfo[0] || qinfo[1] || qinfo[2])) {  // CholeskyQR broke down: SVQB, same Rayleigh-Ritz
+            svqb(ctx, qr_job.src, n, qr_job.ka, qr_job.dst, ws);
+            qr_job.src = nullptr;
+            rayleigh_ritz(ctx, Sp, n, k, r, nv, V.get(), W.get(), T.get(), Z.get(), theta.get(), Vr.get(), Wr.get(),
+                          sweeps.get(), psd);
+            --it;
+            continue;
+        }
+        qr_job.src = nullptr;
         scale = std::max(scale, std::fabs(hth[0]));
         worst = 0.0;
         for (int j = 0; j < r; ++j) worst = std::max(worst, hres[j]);
@@ -976,11 +1001,13 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
                 dgemm(ctx, true, false, nc, ka, n, 1.0, Vr.get(), n, ycur, n, 0.0, P, nc);
                 dgemm(ctx, false, false, n, ka, nc, -1.0, Vr.get(), n, P, nc, 1.0, ycur, n);
             }
-            orthonormalize(ctx, ycur, n, ka, V.get() + size_t(n) * nc, ws);
+            qr_job = {ycur, V.get() + size_t(n) * nc, ka};
+            cholqr3_async(ctx, ycur, n, ka, V.get() + size_t(n) * nc, ws);
             ATK_CUDA(cudaMemcpyAsync(V.get(), Vr.get(), size_t(n) * nc * sizeof(double), cudaMemcpyDeviceToDevice,
                                      st));
         } else {
-            orthonormalize(ctx, ycur, n, k, V.get(), ws);
+            qr_job = {ycur, V.get(), k};
+            cholqr3_async(ctx, ycur, n, k, V.get(), ws);
         }
         mark("qr", nc);
         rayleigh_ritz(ctx, Sp, n, k, r, nv, V.get(), W.get(), T.get(), Z.get(), theta.get(), Vr.get(), Wr.get(),

@@ -25,6 +25,7 @@ for p in $PARTS; do
     eigall) timeout 1200 python -m pytest tests/test_gpu_eig.py tests/test_gpu_eig_big.py tests/test_gpu_tridiag.py tests/test_gpu_svd.py -q -p no:hypothesispytest > gpurun_out/${TAG}_eigall.log 2>&1; echo "eigall=$? $(tail -1 gpurun_out/${TAG}_eigall.log)"; grep -E "^FAILED|Error" gpurun_out/${TAG}_eigall.log | head -20;;
     full) timeout 2400 python -m pytest tests/test_gpu_fullsize.py -q -s -p no:hypothesispytest > gpurun_out/${TAG}_full.log 2>&1; echo "full=$? $(tail -1 gpurun_out/${TAG}_full.log)"; grep -E "full:|FAILED" gpurun_out/${TAG}_full.log;;
     eigc5) timeout 600 python profiles/eig_c5_probe.py > gpurun_out/${TAG}_eigc5.log 2>&1; echo "eigc5=$?"; tail -30 gpurun_out/${TAG}_eigc5.log;;
+    eigtrace) timeout 600 python profiles/eig_c5_trace.py > gpurun_out/${TAG}_eigtrace.log 2>&1; echo "eigtrace=$?"; tail -40 gpurun_out/${TAG}_eigtrace.log;;
     fast) timeout 900 python -m pytest tests -m "gpu and not slow" -x -q -p no:hypothesispytest > gpurun_out/${TAG}_tests.log 2>&1; echo "fast=$? $(tail -1 gpurun_out/${TAG}_tests.log)";;
     bench) timeout 600 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err; echo "bench=$?"; head -c 400 gpurun_out/${TAG}_bench.json; echo;;
     ref) timeout 600 python bench.py --impl reference > gpurun_out/${TAG}_ref.json 2> gpurun_out/${TAG}_ref.err; echo "ref=$?"; head -c 300 gpurun_out/${TAG}_ref.json; echo;;
