@@ -34,7 +34,8 @@ struct TtmParams {
     int box4;         // MN-major A: one 4-D TMA box per stage ({32 p, 32 i, p-blocks, o}) instead of 8
     int pb, ob;       // 4-D box: 32-row p blocks and o slabs per 256-row tile
     int stages;
-    uint32_t stage_bytes, a_bytes;
+    int split;        // 1: the factor is staged as tf32 hi + lo parts and each K step issues two MMAs
+    uint32_t stage_bytes, a_bytes, b_bytes;
     float* y;         // the output, or ks partial outputs (piece q at y + q M R) when ks > 1
 };
 
@@ -102,7 +103,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                                             int(blk / pblk));
                         }
                     }
-                    tc::tma_load_2d(b, &tma_f, &full[stage], k0, 0);
+                    if (p.split) tc::tma_load_3d(b, &tma_f, &full[stage], k0, 0, 0);  // hi, then lo
+                    else tc::tma_load_2d(b, &tma_f, &full[stage], k0, 0);
                     if (++stage == S) { stage = 0; phase ^= 1; }
                 }
             }
@@ -127,12 +129,14 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
                     for (int k = 0; k < BK / 8; ++k) {
                         const uint64_t bd = tc::smem_desc(b_base + k * 32, 16, 1024, 2);
+                        const uint64_t bdl = tc::smem_desc(b_base + p.b_bytes + k * 32, 16, 1024, 2);
 #pragma unroll
                         for (int h = 0; h < 2; ++h) {
                             uint64_t ad;
                             if (KMAJOR_A) ad = tc::smem_desc(a_base + h * 16384 + k * 32, 16, 1024, 2);
                             else ad = tc::smem_desc(a_base + h * 16384 + k * 1024, 4096, 512, 1);
                             tc::mma_tf32(d0 + uint32_t(h * p.NB), ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+                            if (p.split) tc::mma_tf32(d0 + uint32_t(h * p.NB), ad, bdl, idesc, 1u);  // X F_lo
                         }
                     }
                     tc::mma_commit(&empty[stage]);
@@ -205,12 +209,27 @@ __global__ void ttm_reduce(const float* __restrict__ part, uint64_t n, int ks, f
     }
 }
 
-// F (I x R, fp32) = U^T from U (R x I, fp64)
-__global__ void factor_to_f32(const double* __restrict__ u, int R, int I, float* __restrict__ f) {
+// F (I x R, fp32) = U^T from U (R x I, fp64).  split: F_hi = tf32_rn(U^T) at f,
+// F_lo = fp32(U^T - F_hi) at f + I R (rounded to tf32 again by the TMA): the
+// factor enters the MMAs to ~2^-22 instead of 2^-12 (its rounding is one
+// coherent perturbation of every output column, unlike the data's)
+__device__ __forceinline__ float tf32_rn(float x) {
+    uint32_t b = __float_as_uint(x);
+    b += 0xfffu + ((b >> 13) & 1u);  // round to nearest even on the 13 dropped bits
+    return __uint_as_float(b & 0xffffe000u);
+}
+__global__ void factor_to_f32(const double* __restrict__ u, int R, int I, float* __restrict__ f, int split) {
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= R * I) return;
     const int i = e % I, r = e / I;
-    f[i + size_t(I) * r] = float(u[r + size_t(R) * i]);
+    const double v = u[r + size_t(R) * i];
+    if (!split) {
+        f[i + size_t(I) * r] = float(v);
+        return;
+    }
+    const float hi = tf32_rn(float(v));
+    f[i + size_t(I) * r] = hi;
+    f[size_t(I) * R + i + size_t(I) * r] = float(v - double(hi));
 }
 
 }  // namespace
@@ -229,19 +248,22 @@ void tc_ttm(atk_ctx* ctx, const atk_tensor* x, const double* u_dev, uint64_t R, 
     const bool kmajor = s.P == 1;
     const int NB = int((R + 31) / 32 * 32);
     const int I = int(s.I);
-    DevBuf<float> f(ctx, size_t(I) * R);
-    factor_to_f32<<<unsigned((R * I + 255) / 256), 256, 0, ctx->stream>>>(u_dev, int(R), I, f.get());
+    const int split = ctx->ttm_split && ctx->tma_tf32 ? 1 : 0;
+    DevBuf<float> f(ctx, size_t(I) * R * (split ? 2 : 1));
+    factor_to_f32<<<unsigned((R * I + 255) / 256), 256, 0, ctx->stream>>>(u_dev, int(R), I, f.get(), split);
     ATK_LAUNCHED(ctx);
     const CUtensorMapDataType dt = ctx->tma_tf32 ? CU_TENSOR_MAP_DATA_TYPE_TFLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
     CUtensorMap tx{}, tf{};
     {
-        const uint64_t dims[2] = {s.I, R};
-        const uint64_t str[1] = {s.I * 4};
-        const uint32_t box[2] = {BK, uint32_t(NB)};
-        if (encode_tensor_map(&tf, dt, 2, f.get(), dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B) != CUDA_SUCCESS)
+        const uint64_t dims[3] = {s.I, R, 2};
+        const uint64_t str[2] = {s.I * 4, s.I * R * 4};
+        const uint32_t box[3] = {BK, uint32_t(NB), 2};
+        if (encode_tensor_map(&tf, dt, split ? 3 : 2, f.get(), dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B) !=
+            CUDA_SUCCESS)
             fail(ATK_CUDA_ERROR, "ttm: factor tensor map encoding failed");
     }
     TtmParams p{};
+    p.split = split;
     if (kmajor) {
         const uint64_t dims[2] = {s.I, s.O};
         const uint64_t str[1] = {s.I * 4};
@@ -279,7 +301,8 @@ void tc_ttm(atk_ctx* ctx, const atk_tensor* x, const double* u_dev, uint64_t R, 
     p.NB = NB;
     p.nkb = (I + BK - 1) / BK;
     p.a_bytes = MT * BK * 4;
-    p.stage_bytes = p.a_bytes + uint32_t(NB) * BK * 4;
+    p.b_bytes = uint32_t(NB) * BK * 4;
+    p.stage_bytes = p.a_bytes + p.b_bytes * (split ? 2 : 1);
     p.stages = std::max(2, std::min(8, int((200 * 1024) / p.stage_bytes)));
     p.y = static_cast<float*>(y->data);
     const size_t smem = size_t(p.stages) * p.stage_bytes + 1024 + 256;
