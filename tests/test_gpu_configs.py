@@ -175,4 +175,6 @@ def test_frobenius_norm_device_fp32_large():
     x = atucker.DeviceTensor.uniform(dims, 21, np.float32, ctx=ctx)
     ref = np.sqrt(o.norm2_f32(o.hash_uniform(21, int(np.prod(dims)))))
     got = atucker.frobenius_norm(x, ctx=ctx)
-    assert abs(got - ref) <= 1e-12 * ref, (got, ref)
+    # the oracle sums 64M squares serially in fp64 (its own error ~sqrt(n) eps ~ 1e-12);
+    # an fp32 accumulation would be off by ~1e-4
+    assert abs(got - ref) <= 1e-10 * ref, (got, ref)
