@@ -406,6 +406,109 @@ __global__ void __launch_bounds__(1024) chol_inv_kernel(const double* __restrict
     if (tid == 0) *info = 0;
 }
 
+// The same factorisation with the matrix held in REGISTERS: entry e = i k + q
+// of the k x k working set (q >= i: A(i, q) of the upper triangle; q < i:
+// W(i, q), W = the elimination's L'^{-1}) belongs to thread e mod T, so a row
+// of k entries spans consecutive threads and every thread's few entries
+// spread over the rows (balanced work at every step).  Step c needs only row c
+// of A and W: its owners publish it to a double-buffered shared row (with
+// 1 / d_c from the pivot's owner) at the end of step c - 1, so a step is one
+// barrier, two shared loads and an FMA per live entry; no shared-memory round
+// trip on the update itself (k = 80: 69 -> see DESIGN).  Same outputs as
+// chol_inv_kernel: X = L^{-T} with A = L L^T, info = 0 or 1 + failing pivot.
+constexpr int kCrThreads = 1024, kCrMaxE = 13;  // k <= 112: k^2 <= 13 x 1024
+__global__ void __launch_bounds__(kCrThreads) chol_inv_reg_kernel(const double* __restrict__ g, int k,
+                                                                double* __restrict__ x, int* __restrict__ info,
+                                                                double identity_tol) {
+    __shared__ double rowA[2][kJacobiMax], rowW[2][kJacobiMax], dinv[kJacobiMax];
+    __shared__ int bad_sh;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    if (identity_tol > 0.0) {  // uniform
+        double dev = 0.0;
+        for (int e = tid; e < k * k; e += nt) dev = fmax(dev, fabs(g[e] - ((e % k) == (e / k) ? 1.0 : 0.0)));
+        for (int o = 16; o > 0; o >>= 1) dev = fmax(dev, __shfl_xor_sync(0xffffffffu, dev, o));
+        if ((tid & 31) == 0) rowA[0][tid >> 5] = dev;
+        __syncthreads();
+        dev = 0.0;
+        for (int q = 0; q < (nt >> 5); ++q) dev = fmax(dev, rowA[0][q]);
+        __syncthreads();
+        if (dev <= identity_tol) {
+            for (int e = tid; e < k * k; e += nt) x[e] = ((e % k) == (e / k)) ? 1.0 : 0.0;
+            if (tid == 0) *info = 0;
+            return;
+        }
+    }
+    double v[kCrMaxE];
+    int ne = 0;
+#pragma unroll
+    for (int s = 0; s < kCrMaxE; ++s) {
+        const int e = tid + s * nt;
+        if (e < k * k) {
+            const int i = e / k, q = e % k;
+            v[s] = q >= i ? g[i + k * q] : 0.0;
+            ne = s + 1;
+        }
+    }
+    if (tid == 0) bad_sh = 0;
+    // publish row 0
+    for (int q = tid; q < k; q += nt) {
+        const double a = g[k * q];
+        rowA[0][q] = a;
+        if (q == 0) {
+            rowW[0][0] = 1.0;
+            if (!(a > 0.0)) bad_sh = 1;
+            dinv[0] = 1.0 / a;
+        }
+    }
+    __syncthreads();
+    int bad = 0;
+    for (int c = 0; c < k; ++c) {
+        if (bad_sh) {
+            bad = bad_sh;
+            break;
+        }
+        const int cb = c & 1, nb = cb ^ 1;
+        const double inv = dinv[c];
+#pragma unroll
+        for (int s = 0; s < kCrMaxE; ++s) {
+            if (s >= ne) break;
+            const int e = tid + s * nt, i = e / k, q = e % k;
+            if (i <= c) continue;  // retired (row i final before step i)
+            const double m = rowA[cb][i] * inv;
+            if (q >= i) {
+                v[s] = fma(-m, rowA[cb][q], v[s]);
+            } else if (q <= c) {
+                v[s] = fma(-m, rowW[cb][q], v[s]);
+            }
+            if (i == c + 1) {  // row c + 1 is final: publish it for the next step
+                if (q >= i) {
+                    rowA[nb][q] = v[s];
+                    if (q == i) {
+                        rowW[nb][i] = 1.0;
+                        if (!(v[s] > 0.0)) bad_sh = i + 1;
+                        dinv[i] = __drcp_rn(v[s]);
+                    }
+                } else {
+                    rowW[nb][q] = v[s];
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (bad) {
+        if (tid == 0) *info = bad;
+        return;
+    }
+#pragma unroll
+    for (int s = 0; s < kCrMaxE; ++s) {
+        if (s >= ne) break;
+        const int e = tid + s * nt, i = e / k, q = e % k;
+        const double r = sqrt(dinv[i]);  // 1 / sqrt(d_i)
+        x[e] = q > i ? 0.0 : (q == i ? r : v[s] * r);  // x[q + k i] = X(q, i) = W(i, q) / sqrt(d_i)
+    }
+    if (tid == 0) *info = 0;
+}
+
 }  // namespace
 
 void cholesky_inv_t(atk_ctx* ctx, const double* g, int k, double* x, int* info_dev, double identity_tol) {
@@ -416,6 +519,12 @@ void cholesky_inv_t(atk_ctx* ctx, const double* g, int k, double* x, int* info_d
         ATK_CUDA(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       int(size_t(2) * (kJacobiMax + 1) * kJacobiMax * sizeof(double))));
         attr = true;
+    }
+    if (ctx->chol_reg) {
+        const int threads = std::min(kCrThreads, (k * k + 31) / 32 * 32);  // <= kCrMaxE entries each
+        chol_inv_reg_kernel<<<1, threads, 0, ctx->stream>>>(g, k, x, info_dev, identity_tol);
+        ATK_LAUNCHED(ctx);
+        return;
     }
     int threads = std::min(1024, std::max(64, 32 * k));  // one warp per column (measured: 128 threads 4x slower)
     static const int th_env = std::getenv("ATK_CHOL_THREADS") ? std::atoi(std::getenv("ATK_CHOL_THREADS")) : 0;
