@@ -328,7 +328,7 @@ double atk_cost_als(double i, double r, double j, int num_iters);
  * (s = element bytes, P = tf32 or fp64 tensor rate).  Times in seconds. */
 typedef struct atk_roofline_params {
     double hbm_gbs;              /* measured copy bandwidth (MEASURED_PEAKS.json hbm_gbs) */
-    double tf32_tflops;          /* 1/2 of the measured sustained bf16 rate */
+    double tf32_tflops;          /* measured sustained tf32 rate (profiles/peaks_r2.json) */
     double fp64_tflops;          /* effective DMMA fp64 contraction rate */
     double eig_small_ms;         /* dense tridiagonal eig, I <= 200 */
     double eig_large_ms;         /* ChFSI eig, I > 200 (gapped Gram spectra) */
@@ -337,6 +337,7 @@ typedef struct atk_roofline_params {
     int num_iters;               /* AlsOptions::num_iters */
     double als_fused_factor;     /* one-pass ALS (mode 0, fp32, R <= 32): measured time / (s I J / BW) */
     double als_fused_overhead_ms; /* its per-iteration fixed cost */
+    int num_sms;                 /* SMs of the run's device: the one-pass ALS shape gate (per-CTA columns) */
 } atk_roofline_params;
 void atk_roofline_params_default(atk_roofline_params* p, int dtype, int num_iters);
 double atk_roofline_time_eig(const atk_roofline_params* p, double i, double r, double j);

@@ -36,7 +36,8 @@ class RooflineParams(C.Structure):
     _fields_ = [("hbm_gbs", C.c_double), ("tf32_tflops", C.c_double), ("fp64_tflops", C.c_double),
                 ("eig_small_ms", C.c_double), ("eig_large_ms", C.c_double),
                 ("als_iter_overhead_ms", C.c_double), ("dtype", C.c_int), ("num_iters", C.c_int),
-                ("als_fused_factor", C.c_double), ("als_fused_overhead_ms", C.c_double)]
+                ("als_fused_factor", C.c_double), ("als_fused_overhead_ms", C.c_double),
+                ("num_sms", C.c_int)]
 
 
 class AlsOpts(C.Structure):

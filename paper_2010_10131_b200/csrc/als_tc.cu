@@ -332,13 +332,10 @@ __global__ void m_to_f32(const double* __restrict__ m, int R, int I, float* __re
 }  // namespace
 
 bool als_fused_supported(atk_ctx* ctx, const atk_tensor* y, int mode, uint64_t R) {
+    static_assert(NB == 32 && JT == 128, "als_fused_shape_ok (atk_driver.cuh) mirrors NB / JT");
     if (!ctx->als_fused || ctx->force_simt || y->dtype != ATK_F32 || mode != 0) return false;
     const Split s = loop_split(y->dims, y->order, mode);
-    if (s.P != 1 || R < 1 || R > uint64_t(NB) || s.I % 128 != 0 || s.I > 1024 || s.I < 128) return false;
-    if ((2 + s.I / 128) * NB > 512) return false;
-    // per-CTA fp32 chains of at most 16K columns (the other kernels' drain bound)
-    const uint64_t per_cta = (s.O + uint64_t(ctx->num_sms) - 1) / uint64_t(ctx->num_sms);
-    return s.O >= uint64_t(JT) && per_cta <= 16384 && s.O < (1ull << 31);
+    return s.P == 1 && als_fused_shape_ok(s.I, R, s.O, ctx->num_sms);
 }
 
 // One ALS iteration's contractions on mode 0: M (R x I, fp64 device) = (L^T L)^{-1} L^T;

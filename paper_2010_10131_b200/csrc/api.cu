@@ -675,8 +675,8 @@ double atk_cost_als(double i, double r, double j, int num_iters) { return cost_a
 // ---------------------------------------------------------------- roofline selector
 void atk_roofline_params_default(atk_roofline_params* p, int dtype, int num_iters) {
     if (!p) return;
-    p->hbm_gbs = 6535.1;        // MEASURED_PEAKS.json (B200 copy bandwidth)
-    p->tf32_tflops = 690.2;     // 1/2 x measured sustained bf16 1380.4 TF/s
+    p->hbm_gbs = 6632.0;        // profiles/peaks_r2.json: measured copy bandwidth
+    p->tf32_tflops = 618.0;     // profiles/peaks_r2.json: measured sustained cuBLAS tf32
     p->fp64_tflops = 10.0;      // measured: C3 mode-1 DMMA Gram
     p->eig_small_ms = 1.0;      // measured: C1 n = 200 (tridiag.cu)
     p->eig_large_ms = 1.5;      // measured: ChFSI 1.35-1.42 ms on gapped Grams (n = 2048); flat spectra cost more
@@ -685,6 +685,13 @@ void atk_roofline_params_default(atk_roofline_params* p, int dtype, int num_iter
     p->num_iters = num_iters > 0 ? num_iters : 5;
     p->als_fused_factor = 1.75;     // measured: C2 mode 0, 1.16 ms per pass vs 0.66 ms of HBM time
     p->als_fused_overhead_ms = 0.1;
+    p->num_sms = 148;
+    int dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && sms > 0)
+        p->num_sms = sms;
+    else
+        cudaGetLastError();  // no device: keep the B200's 148
 }
 
 static double rf_rate(const atk_roofline_params* p) {
@@ -709,8 +716,11 @@ double atk_roofline_time_als(const atk_roofline_params* p, double i, double r, d
 
 double atk_roofline_time_als_mode(const atk_roofline_params* p, int mode, double i, double r, double j) {
     if (!p) return 0.0;
-    const bool fused = mode == 0 && p->dtype == ATK_F32 && r <= 32 && std::fmod(i, 128.0) == 0.0 && i >= 128 &&
-                       i <= 1024 && p->als_fused_factor > 0.0;
+    // the kernel's own gate (atk_driver.cuh), so a shape the one-pass kernel refuses is priced
+    // as the two-pass schedule it will actually run
+    const bool fused = mode == 0 && p->dtype == ATK_F32 && p->als_fused_factor > 0.0 && r >= 1 && i >= 1 &&
+                       j >= 1 && i < 9.2e18 && j < 9.2e18 &&
+                       als_fused_shape_ok(uint64_t(i), uint64_t(r), uint64_t(j), p->num_sms > 0 ? p->num_sms : 148);
     if (!fused) return atk_roofline_time_als(p, i, r, j);
     const double bw = p->hbm_gbs * 1e9;
     return p->num_iters * (p->als_fused_factor * 4.0 * i * j / bw + p->als_fused_overhead_ms * 1e-3);

@@ -64,6 +64,16 @@ ModeOut svd_mode_explicit(atk_ctx* ctx, const atk_tensor* y, int mode, uint64_t 
 void contract_ttt(atk_ctx* ctx, const atk_tensor* x, const atk_tensor* y, int mode, double* z_dev,
                   bool sym);
 // als_tc.cu — one ALS iteration's contractions in one pass over Y (mode 0, fp32, R <= 32)
+// Shape gate of the one-pass kernel (I x J unfolding, rank R, num_sms CTAs), shared with the
+// roofline selector (api.cu) so the selector prices exactly the schedule that will run.
+inline bool als_fused_shape_ok(uint64_t I, uint64_t R, uint64_t J, int num_sms) {
+    constexpr uint64_t kNB = 32, kJT = 128;  // als_tc.cu NB / JT
+    if (R < 1 || R > kNB || I % 128 != 0 || I > 1024 || I < 128) return false;
+    if ((2 + I / 128) * kNB > 512) return false;  // TMEM columns
+    // per-CTA fp32 chains of at most 16K columns (the other kernels' drain bound)
+    const uint64_t per_cta = (J + uint64_t(num_sms) - 1) / uint64_t(num_sms);
+    return J >= kJT && per_cta <= 16384 && J < (1ull << 31);
+}
 bool als_fused_supported(atk_ctx* ctx, const atk_tensor* y, int mode, uint64_t R);
 void als_fused_pass(atk_ctx* ctx, const atk_tensor* y, const double* m_dev, uint64_t R, double* yr_dev,
                     double* gr_dev, atk_tensor* rfac_out);

@@ -14,7 +14,9 @@
 //      I/2 disjoint row pairs per launch, one CTA per pair, fp64 dot products
 //      in a fixed order; each rotation is also applied to the columns of
 //      W (= Q at the start), so Y_(n) = W M throughout.  With the Q start only
-//      the small-sigma clusters still rotate: 2-4 sweeps.
+//      the small-sigma clusters still rotate: 2-4 sweeps.  A tall unfolding
+//      (I > J, e.g. a last mode after the others shrank) is the mirror image:
+//      V from S' = Y^T Y, the J columns of M = Y V rotated, U = column / sigma.
 //   4. sigma_k = |row k of M| (rows are sigma_k v_k^T once orthogonal),
 //      sorted descending; U = the matching columns of W with the reference's
 //      sign rule (largest |u_i| positive, first on ties; linalg.hpp:34-50),
@@ -152,6 +154,45 @@ __global__ void tensorize_rows(const double* __restrict__ m, uint64_t P, uint64_
     }
 }
 
+// Tall unfoldings (I > J): the J columns of M = Q^T Y_(n) are rotated instead
+// (I - J rows of M cannot become mutually orthogonal without vanishing
+// exactly).  A[j * I + i] = B[p + P (i + I o)], j = p + P o.
+__global__ void unfold_cols(const double* __restrict__ b, uint64_t P, uint64_t I, uint64_t O,
+                            double* __restrict__ a) {
+    const uint64_t tot = P * I * O;
+    for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < tot; e += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t p = e % P, t = e / P, i = t % I, o = t / I;
+        a[(p + P * o) * I + i] = b[e];
+    }
+}
+
+// T(:, k) = M(:, perm[k]) / sigma_perm[k]  (M: I x n column-major), the left vectors of a
+// column-rotated tall unfolding.
+__global__ void scale_cols(const double* __restrict__ m, int I, const int* __restrict__ perm,
+                           const double* __restrict__ sig, int r, double* __restrict__ t) {
+    for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < uint64_t(I) * r;
+         e += uint64_t(gridDim.x) * blockDim.x) {
+        const int i = int(e % I), k = int(e / I);
+        const double sg = sig[perm[k]];
+        t[e] = sg > 0.0 ? m[uint64_t(perm[k]) * I + i] / sg : 0.0;
+    }
+}
+
+// shrunk[p + P (k + r o)] = sign_k sigma_k W(p + P o, perm[k]), W (J x J) column-major
+__global__ void tensorize_cols(const double* __restrict__ w, uint64_t P, uint64_t O, int r,
+                               const int* __restrict__ perm, const double* __restrict__ sign,
+                               const double* __restrict__ sig, double* __restrict__ out) {
+    const uint64_t J = P * O, tot = P * uint64_t(r) * O;
+    for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < tot; e += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t p = e % P, t = e / P, k = t % r, o = t / r;
+        out[e] = sign[k] * sig[perm[k]] * w[uint64_t(perm[k]) * J + p + P * o];
+    }
+}
+
+__global__ void iota_fill(int* __restrict__ v, int n) {
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) v[e] = e;
+}
+
 int grid_for(atk_ctx* ctx, uint64_t n) {
     return int(std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, uint64_t(ctx->num_sms) * 16)));
 }
@@ -178,36 +219,61 @@ ModeOut svd_mode_explicit(atk_ctx* ctx, const atk_tensor* y, int mode, uint64_t 
     ModeOut out;
     out.solver = ATK_SOLVER_SVD;
     StageTimer tm(ctx);
-    // 1. Gram and all of its eigenvectors (the preconditioner)
+    // Wide (I <= J): precondition with the eigenvectors Q of S = Y Y^T (I x I), rotate the I
+    // rows of M = Q^T Y (row-graded: rows ~ sigma_k v_k^T), accumulating W = Q.
+    // Tall (I > J): precondition with the eigenvectors V of S' = Y^T Y (J x J), rotate the J
+    // columns of M = Y V (column-graded: columns ~ sigma_k u_k), accumulating W = V.  Either
+    // way one-sided Jacobi sees a graded matrix and resolves each sigma to ~eps relative to
+    // itself; I - J rows could never become mutually orthogonal without vanishing exactly.
+    const bool tall = I > J;
+    const uint64_t nrot = tall ? J : I, len = tall ? I : J;  // rotated vectors and their length
+    DevBuf<double> M(ctx, I * J), W(ctx, nrot * nrot);
     tm.start();
-    DevBuf<double> S(ctx, I * I), vals(ctx, I), Q(ctx, I * I), Qt(ctx, I * I);
-    contract_ttt(ctx, y, y, mode, S.get(), true);
-    out.times.gram_ms = tm.stop_ms(kStageGram);
-    record_gemm((long long)(I * I) * (long long)J);
-    tm.start();
-    if (I <= uint64_t(kTridiagMax))
-        tridiag_eig(ctx, S.get(), int(I), int(I), int(I), vals.get(), Q.get(), int(I));
-    else
-        dense_eig_big(ctx, S.get(), int(I), int(I), int(I), vals.get(), Q.get(), int(I), true);
-    S.reset();
-    transpose(ctx, Q.get(), int(I), int(I), Qt.get());
-    // 2. M = Q^T Y_(n), row-major
-    atk_tensor* B = contract_ttm(ctx, y, Qt.get(), I, mode);
-    Qt.reset();
-    DevBuf<double> M(ctx, I * J);
-    unfold_rows<<<grid_for(ctx, I * J), 256, 0, st>>>(static_cast<const double*>(B->data), s.P, I, s.O, M.get());
-    ATK_LAUNCHED(ctx);
-    atk_tensor_free(B);
-    // 3. one-sided Jacobi on the rows
-    const int N = int(I + (I & 1));
-    const double tol = 2.220446049250313e-16 * std::max(1.0, std::sqrt(double(J)));
+    {
+        DevBuf<double> S(ctx, nrot * nrot), vals(ctx, nrot);
+        if (tall) {
+            // M <- Y_(n) column-major (I x J); S' = M^T M; W = V; M <- M V
+            unfold_cols<<<grid_for(ctx, I * J), 256, 0, st>>>(static_cast<const double*>(y->data), s.P, I, s.O,
+                                                              M.get());
+            ATK_LAUNCHED(ctx);
+            dgemm(ctx, true, false, int(J), int(J), int(I), 1.0, M.get(), int(I), M.get(), int(I), 0.0, S.get(),
+                  int(J));
+            symmetrize(ctx, S.get(), int(J));
+        } else {
+            contract_ttt(ctx, y, y, mode, S.get(), true);
+        }
+        out.times.gram_ms = tm.stop_ms(kStageGram);
+        record_gemm((long long)(I * I) * (long long)J);
+        tm.start();
+        if (nrot <= uint64_t(kTridiagMax))
+            tridiag_eig(ctx, S.get(), int(nrot), int(nrot), int(nrot), vals.get(), W.get(), int(nrot));
+        else
+            dense_eig_big(ctx, S.get(), int(nrot), int(nrot), int(nrot), vals.get(), W.get(), int(nrot), true);
+    }
+    if (tall) {
+        DevBuf<double> MV(ctx, I * J);
+        dgemm(ctx, false, false, int(I), int(J), int(J), 1.0, M.get(), int(I), W.get(), int(J), 0.0, MV.get(), int(I));
+        M = std::move(MV);
+    } else {
+        // M = Q^T Y_(n), row-major (row i contiguous over j = p + P o)
+        DevBuf<double> Qt(ctx, I * I);
+        transpose(ctx, W.get(), int(I), int(I), Qt.get());
+        atk_tensor* B = contract_ttm(ctx, y, Qt.get(), I, mode);
+        Qt.reset();
+        unfold_rows<<<grid_for(ctx, I * J), 256, 0, st>>>(static_cast<const double*>(B->data), s.P, I, s.O, M.get());
+        ATK_LAUNCHED(ctx);
+        atk_tensor_free(B);
+    }
+    // one-sided Jacobi on the nrot contiguous vectors of M
+    const int N = int(nrot + (nrot & 1));
+    const double tol = 2.220446049250313e-16 * std::max(1.0, std::sqrt(double(len)));
     DevBuf<int> rot(ctx, 1);
     int sweeps = 0, last = -1;
     const int max_sweeps = 30;
     for (; sweeps < max_sweeps; ++sweeps) {
         ATK_CUDA(cudaMemsetAsync(rot.get(), 0, sizeof(int), st));
         for (int t = 0; t < N - 1; ++t) {
-            jacobi_rows_round<<<N / 2, kSvdThreads, 0, st>>>(M.get(), J, Q.get(), int(I), N, t, tol, rot.get());
+            jacobi_rows_round<<<N / 2, kSvdThreads, 0, st>>>(M.get(), len, W.get(), int(nrot), N, t, tol, rot.get());
             ATK_LAUNCHED(ctx);
         }
         ATK_CUDA(cudaMemcpyAsync(&last, rot.get(), sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -215,30 +281,46 @@ ModeOut svd_mode_explicit(atk_ctx* ctx, const atk_tensor* y, int mode, uint64_t 
         if (last == 0) break;
     }
     if (last != 0) fail(ATK_NO_CONVERGENCE, "singular value decomposition failed");
-    // 4. sigma, order, U with the sign rule, shrunk = diag(sigma) V^T rows
-    DevBuf<double> sig(ctx, I);
-    row_norms<<<unsigned(I), kSvdThreads, 0, st>>>(M.get(), J, sig.get());
+    // sigma, order, U with the sign rule, shrunk = diag(sigma) V^T rows
+    DevBuf<double> sig(ctx, nrot);
+    row_norms<<<unsigned(nrot), kSvdThreads, 0, st>>>(M.get(), len, sig.get());
     ATK_LAUNCHED(ctx);
-    std::vector<double> hs(I);
-    ATK_CUDA(cudaMemcpyAsync(hs.data(), sig.get(), I * sizeof(double), cudaMemcpyDeviceToHost, st));
+    std::vector<double> hs(nrot);
+    ATK_CUDA(cudaMemcpyAsync(hs.data(), sig.get(), nrot * sizeof(double), cudaMemcpyDeviceToHost, st));
     ATK_CUDA(cudaStreamSynchronize(st));
-    std::vector<int> perm(I);
+    std::vector<int> perm(nrot);
     std::iota(perm.begin(), perm.end(), 0);
     std::stable_sort(perm.begin(), perm.end(), [&](int a, int b) { return hs[a] > hs[b]; });
     perm.resize(r);
     DevBuf<int> dperm(ctx, r);
     DevBuf<double> U(ctx, I * r), sign(ctx, r);
     ATK_CUDA(cudaMemcpyAsync(dperm.get(), perm.data(), r * sizeof(int), cudaMemcpyHostToDevice, st));
-    gather_left<<<unsigned(r), kSvdThreads, 0, st>>>(Q.get(), int(I), dperm.get(), U.get(), sign.get());
-    ATK_LAUNCHED(ctx);
+    if (tall) {
+        DevBuf<double> T(ctx, I * r);
+        DevBuf<int> ident(ctx, r);
+        scale_cols<<<grid_for(ctx, I * r), 256, 0, st>>>(M.get(), int(I), dperm.get(), sig.get(), int(r), T.get());
+        ATK_LAUNCHED(ctx);
+        iota_fill<<<1, 256, 0, st>>>(ident.get(), int(r));
+        ATK_LAUNCHED(ctx);
+        gather_left<<<unsigned(r), kSvdThreads, 0, st>>>(T.get(), int(I), ident.get(), U.get(), sign.get());
+        ATK_LAUNCHED(ctx);
+    } else {
+        gather_left<<<unsigned(r), kSvdThreads, 0, st>>>(W.get(), int(I), dperm.get(), U.get(), sign.get());
+        ATK_LAUNCHED(ctx);
+    }
     out.times.eig_ms = tm.stop_ms(kStageEig);
     tm.start();
     uint64_t od[ATK_MAX_ORDER];
     for (int m = 0; m < y->order; ++m) od[m] = y->dims[m];
     od[mode] = r;
     out.shrunk = new_tensor(ctx, ATK_F64, y->order, od);
-    tensorize_rows<<<grid_for(ctx, s.P * r * s.O), 256, 0, st>>>(M.get(), s.P, s.O, int(r), dperm.get(), sign.get(),
-                                                                 static_cast<double*>(out.shrunk->data));
+    if (tall)
+        tensorize_cols<<<grid_for(ctx, s.P * r * s.O), 256, 0, st>>>(W.get(), s.P, s.O, int(r), dperm.get(),
+                                                                     sign.get(), sig.get(),
+                                                                     static_cast<double*>(out.shrunk->data));
+    else
+        tensorize_rows<<<grid_for(ctx, s.P * r * s.O), 256, 0, st>>>(M.get(), s.P, s.O, int(r), dperm.get(),
+                                                                     sign.get(), static_cast<double*>(out.shrunk->data));
     ATK_LAUNCHED(ctx);
     out.times.ttm_ms = tm.stop_ms(kStageTtm);
     out.factor_dev = std::move(U);

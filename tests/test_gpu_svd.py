@@ -40,7 +40,9 @@ def sctx():
     ctx.set_option("svd_explicit", 1)
 
 
-@pytest.mark.parametrize("dims,mode,r", [([40, 30, 20], 0, 30), ([24, 40, 25], 1, 30), ([16, 12, 60], 2, 50)])
+@pytest.mark.parametrize("dims,mode,r", [([40, 30, 20], 0, 30), ([24, 40, 25], 1, 30), ([16, 12, 60], 2, 50),
+                                         # tall unfoldings (I > J): the column-rotated mirror path
+                                         ([60, 4, 5], 0, 15), ([3, 90, 8], 1, 20), ([4, 5, 300], 2, 20)])
 def test_svd_mode_ill_conditioned(sctx, oracle, dims, mode, r):
     from paper_2010_10131_b200 import atucker
 
@@ -90,3 +92,17 @@ def test_sthosvd_fixed_svd_explicit(sctx, oracle):
     for a, b in zip(res.decomposition.factors, ref.factors):
         assert np.abs(a - b).max() <= 1e-9
     assert all(rp.eig_method == "svd-jacobi" for rp in res.reports)
+
+
+def test_svd_mode_tall_rank_deficient_matches_oracle(sctx, oracle):
+    """test_sthosvd.cpp:39-52 on the SVD route: the last mode of a [20, 30, 40] exact-rank
+    tensor shrunk to 5 x 6 is a 40 x 30 unfolding of rank 7 (I > J)."""
+    from paper_2010_10131_b200 import atucker
+    from paper_2010_10131_b200.selector import Strategy
+
+    x = oracle.synth_lowrank([20, 30, 40], [5, 6, 7], 2024)
+    res = atucker.sthosvd(x, [5, 6, 7], Strategy.fixed_svd(), ctx=sctx)
+    ref = oracle.sthosvd(x, [5, 6, 7], lambda m, i, r, j: 2)
+    assert atucker.relative_error(x, res.decomposition, ctx=sctx) <= 1e-8
+    for a, b in zip(res.decomposition.factors, ref.factors):
+        assert principal_angle(a, b) <= 1e-8

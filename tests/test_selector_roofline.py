@@ -95,3 +95,13 @@ def test_one_pass_als_is_priced_on_mode_0():
     # not eligible: R > 32 or I not a multiple of 128
     assert s.roofline_times(1000, r, j, mode=0)[1] == pytest.approx(s.roofline_times(1000, r, j)[1], rel=1e-12)
     assert s.roofline_times(i, 48, j, mode=0)[1] == pytest.approx(s.roofline_times(i, 48, j)[1], rel=1e-12)
+    # the kernel's per-CTA column bound (als_fused_shape_ok): J above 16384 columns per SM runs
+    # the two-pass schedule, so it is priced as such (512 x 2048 x 2048 on mode 0: J = 4M)
+    sms = p.num_sms
+    assert sms > 0
+    j_big = 16384 * sms + 1
+    assert s.roofline_times(512, r, j_big, mode=0)[1] == pytest.approx(s.roofline_times(512, r, j_big)[1], rel=1e-12)
+    j_ok = 16384 * sms
+    assert s.roofline_times(512, r, j_ok, mode=0)[1] < s.roofline_times(512, r, j_ok)[1]
+    # and J below one 128-column tile
+    assert s.roofline_times(i, r, 100, mode=0)[1] == pytest.approx(s.roofline_times(i, r, 100)[1], rel=1e-12)
