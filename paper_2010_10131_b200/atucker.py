@@ -423,7 +423,7 @@ def eig_mode_solver(y, mode: int, r: int, ctx: Context | None = None) -> ModeRes
 
 
 def svd_mode_solver(y, mode: int, r: int, ctx: Context | None = None) -> ModeResult:
-    """svd_mode_solver (solvers.hpp:142-162), device route via the Gram eigenproblem."""
+    """svd_mode_solver (solvers.hpp:142-162): fp64 on the explicit unfolding (csrc/svd.cu), else the Gram route."""
     t, tmp, factor, h, times = _mode_call("svd", y, mode, r, ctx)
     _lib.check(t.ctx.lib.atk_svd_mode(t.ctx.h, t.h, int(mode), int(r), _dptr(factor), C.byref(h),
                                       C.byref(times)))

@@ -1,0 +1,65 @@
+"""Small invocations of the synchronisation-heavy kernels, for compute-sanitizer
+(memcheck / racecheck / synccheck; profiles/sanitize.sh).  Not a bench, not a test.
+
+Cases (argv[1]):
+  gram2   fp32 512 x 16 x 16 mode 0: gram_tf32_2cta_kernel (CTA pairs, peer TMA, mbarriers) + gram2_reduce
+  gram1   fp32 256 x 8 x 32 modes 0/1: gram_tf32_kernel (1-CTA), ttm_tf32_kernel, ttt
+  als     fp32 256 x 64 x 64, ALS mode 0: als_pass_kernel (one-pass ALS) + als_reduce_rows, chol_reg
+  chfsi   n = 400 flat PSD Gram: ChFSI (cheb_resident_kernel / cheb_filter_kernel, lanczos_tiles when
+          indefinite), CholeskyQR chol_inv, trd_small, bisect / invit / backtr
+  trd     n = 120 and 190: trd_small_kernel, trd_tile_kernel, trd_kernel
+  big     n = 320 dense: the grid-wide Householder reduction (trd_big.cu) + its cluster tail
+  svd     fp64 SVD mode on wide and tall unfoldings (svd.cu)
+"""
+import sys
+from pathlib import Path
+
+import numpy as np
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+from paper_2010_10131_b200 import atucker  # noqa: E402
+from paper_2010_10131_b200.selector import SolverKind, Strategy  # noqa: E402
+
+case = sys.argv[1] if len(sys.argv) > 1 else "gram2"
+ctx = atucker.Context.default(0)
+rng = np.random.default_rng(1)
+
+
+def sym(n, kind):
+    q = np.linalg.qr(rng.standard_normal((n, n)))[0]
+    lam = np.sort(1.0 + 0.06 * rng.standard_normal(n))[::-1] if kind == "flat" else np.linspace(n, 1, n)
+    return (q * lam) @ q.T
+
+
+if case == "gram2":
+    x = atucker.DeviceTensor.uniform([512, 16, 16], 3, np.float32, ctx=ctx)
+    res = atucker.sthosvd(x, [16, 8, 8], Strategy.fixed_eig(), ctx=ctx)
+elif case == "gram1":
+    x = atucker.DeviceTensor.uniform([256, 8, 32], 3, np.float32, ctx=ctx)
+    res = atucker.sthosvd(x, [32, 4, 8], Strategy.fixed_eig(), ctx=ctx)
+elif case == "als":
+    x = atucker.DeviceTensor.uniform([256, 64, 64], 5, np.float32, ctx=ctx)
+    res = atucker.sthosvd(x, [16, 16, 16], Strategy.manual([SolverKind.Als, SolverKind.Eig, SolverKind.Eig]),
+                          atucker.AlsOptions(num_iters=2, seed=3), ctx=ctx)
+elif case == "chfsi":
+    ctx.set_option("eig_assume_psd", 1.0)
+    ctx.set_option("eig_method", 1)
+    p = atucker.sym_eig_top_r(sym(400, "flat"), 24, ctx=ctx)
+    ctx.set_option("eig_assume_psd", 0.0)
+    p = atucker.sym_eig_top_r(sym(400, "lin") - 100.0 * np.eye(400), 24, ctx=ctx)
+    ctx.set_option("eig_method", -1)
+elif case == "trd":
+    for n in (120, 190):
+        p = atucker.sym_eig_top_r(sym(n, "lin"), 16, ctx=ctx)
+elif case == "big":
+    ctx.set_option("eig_method", 3)
+    p = atucker.sym_eig_top_r(sym(320, "flat"), 20, ctx=ctx)
+    ctx.set_option("eig_method", -1)
+elif case == "svd":
+    for dims, mode, r in (([24, 10, 12], 0, 8), ([40, 3, 4], 0, 6)):
+        y = np.asfortranarray(rng.standard_normal(dims))
+        atucker.svd_mode_solver(y, mode, r, ctx=ctx)
+else:
+    raise SystemExit(f"unknown case {case}")
+ctx.synchronize()
+print("ok", case)
