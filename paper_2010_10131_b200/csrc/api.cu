@@ -48,6 +48,25 @@ void dev_free(atk_ctx* ctx, void* p) {
     if (p) cudaFreeAsync(p, ctx->stream);
 }
 
+void* pinned_host(atk_ctx* ctx, size_t bytes) {
+    if (bytes > ctx->pinned_bytes) {
+        if (ctx->pinned) {
+            ATK_CUDA(cudaStreamSynchronize(ctx->stream));
+            cudaFreeHost(ctx->pinned);
+            ctx->pinned = nullptr;
+            ctx->pinned_bytes = 0;
+        }
+        const size_t want = std::max<size_t>(bytes, 4u << 20);
+        if (cudaMallocHost(&ctx->pinned, want) != cudaSuccess) {
+            cudaGetLastError();
+            ctx->pinned = nullptr;
+            fail(ATK_OOM, "pinned host staging of " + std::to_string(want) + " bytes");
+        }
+        ctx->pinned_bytes = want;
+    }
+    return ctx->pinned;
+}
+
 // ------------------------------------------------ AllocTracker (instrumentation.hpp:39-150)
 // Live device tensor payloads (the analogue of DenseTensor/DenseMatrix buffers)
 // while enabled; allocations made before enable() are invisible, as in the
@@ -204,6 +223,7 @@ atk_status atk_ctx_destroy(atk_ctx* ctx) {
             cudaStreamSynchronize(ctx->own_stream);
             cudaStreamDestroy(ctx->own_stream);
         }
+        if (ctx->pinned) cudaFreeHost(ctx->pinned);
         delete ctx;
     });
 }

@@ -95,6 +95,8 @@ struct atk_ctx {
                                // (off: lockstep hot-spots L2 slices, 45 ms vs 34 ms at C5, r1)
     atk::Comm* comm = nullptr;
     cudaEvent_t ev[8] = {};
+    void* pinned = nullptr;    // page-locked staging for the end-of-call factor download (grown on demand)
+    size_t pinned_bytes = 0;
 };
 
 struct atk_tensor {
@@ -121,6 +123,9 @@ namespace atk {
 // Stream-ordered allocations from the device's default pool; the pool keeps
 // freed blocks (release threshold = max) so repeated sthosvd calls reuse them.
 void* dev_alloc(atk_ctx* ctx, size_t bytes);
+// The context's page-locked host staging buffer, at least `bytes` long (kept across calls: a
+// fresh pageable vector cost ~1.4 ms of page faults per C5 sthosvd with the GPU idle).
+void* pinned_host(atk_ctx* ctx, size_t bytes);
 void dev_free(atk_ctx* ctx, void* p);
 
 template <class T>

@@ -483,11 +483,10 @@ atk_tensor* sthosvd(atk_ctx* ctx, const atk_tensor* x, const uint64_t* ranks, at
     }
     ctx->replicated = false;
     comm_end_call(ctx);
-    std::vector<double> h(dev_segs.empty() ? 0 : ftotal);
-    if (!dev_segs.empty())
-        ATK_CUDA(cudaMemcpyAsync(h.data(), fdev.get(), ftotal * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    double* h = dev_segs.empty() ? nullptr : static_cast<double*>(pinned_host(ctx, ftotal * sizeof(double)));
+    if (h) ATK_CUDA(cudaMemcpyAsync(h, fdev.get(), ftotal * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     ATK_CUDA(cudaStreamSynchronize(ctx->stream));
-    for (const auto& sg : dev_segs) std::copy(h.begin() + sg.first, h.begin() + sg.first + sg.second, factors_out + sg.first);
+    for (const auto& sg : dev_segs) std::copy(h + sg.first, h + sg.first + sg.second, factors_out + sg.first);
     if (reports) {
         for (const auto& d : ctx->deferred) {
             float ms = 0.f;
