@@ -162,9 +162,11 @@ uint64_t atk_ctx_launch_count(const atk_ctx* ctx);
  *   "eig_assume_psd" 1 = atk_sym_eig_top_r inputs are Grams (Cholesky-preconditioned Jacobi)
  *   "tma_tf32"      1 = round-to-nearest tf32 operand loads (default), 0 = hardware truncation
  *   "gram_2cta"     1 = CTA-pair (cta_group::2) Gram where supported (default)
+ *   "invit_smem"    1 = inverse iteration (n <= 128) with its iterates and LU factors in shared
+ *                  memory, one warp per CTA (default); 0 = the global-memory kernel
  *   "chol_reg"      1 = the k <= 112 Cholesky + inverse (CholeskyQR, ALS solves) with the matrix in
- *                  registers, one barrier per pivot; 0 = shared-memory column kernel (default:
- *                  measured 69 vs 136 us at k = 80)
+ *                  register tiles, one barrier per pivot (default; 40 us at k = 80); 0 = the
+ *                  shared-memory column kernel (67 us)
  *   "ttm_split"     1 = the TTM factor enters the tensor cores as tf32 hi + lo parts (two MMAs per
  *                  K step, ~2^-22 instead of 2^-12; the TTM stays HBM-bound; default), 0 = one tf32 part
  *   "gram_wide"     1 = 2-CTA Gram units of two 256 x 256 tiles of one tile row sharing the staged A

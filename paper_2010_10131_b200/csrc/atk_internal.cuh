@@ -86,8 +86,10 @@ struct atk_ctx {
                                // (the MMA itself truncates: measured 6e-4 bias vs 1e-6, test_gpu_tc.py)
     int gram_chunk_kb = 0;     // option "gram_chunk_kb": K-blocks per fp64 drain (0 = default)
     int gram_2cta = 1;         // option "gram_2cta": 256x256 Gram tiles on CTA pairs (cta_group::2)
-    int chol_reg = 0;          // option "chol_reg": register-resident Cholesky + inverse (k <= 112); measured
-                               // slower (C5 k = 80: 136 vs 69 us per call under ncu, r2)
+    int invit_smem = 1;        // option "invit_smem": inverse iteration with its iterates and LU factors in
+                               // shared memory (n <= 128); 0 = the global-memory kernel
+    int chol_reg = 1;          // option "chol_reg": register-tile Cholesky + inverse (k <= 112): C5's k = 80
+                               // in 40 us per call against 67 us for the shared-memory column kernel
     int ttm_split = 1;         // option "ttm_split": TTM factor as tf32 hi + lo (two MMAs per K step)
     int gram_wide = 1;         // option "gram_wide": 2-CTA Gram units of two tiles sharing the A operand
     int gram_lockstep = 0;     // option "gram_lockstep": bound CTA drift so X streams from HBM once

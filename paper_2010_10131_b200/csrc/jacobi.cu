@@ -406,31 +406,74 @@ __global__ void __launch_bounds__(1024) chol_inv_kernel(const double* __restrict
     if (tid == 0) *info = 0;
 }
 
-// The same factorisation with the matrix held in REGISTERS: entry e = i k + q
-// of the k x k working set (q >= i: A(i, q) of the upper triangle; q < i:
-// W(i, q), W = the elimination's L'^{-1}) belongs to thread e mod T, so a row
-// of k entries spans consecutive threads and every thread's few entries
-// spread over the rows (balanced work at every step).  Step c needs only row c
-// of A and W: its owners publish it to a double-buffered shared row (with
-// 1 / d_c from the pivot's owner) at the end of step c - 1, so a step is one
-// barrier, two shared loads and an FMA per live entry; no shared-memory round
-// trip on the update itself (k = 80: 69 -> see DESIGN).  Same outputs as
-// chol_inv_kernel: X = L^{-T} with A = L L^T, info = 0 or 1 + failing pivot.
-constexpr int kCrThreads = 1024, kCrMaxE = 13;  // k <= 112: k^2 <= 13 x 1024
-__global__ void __launch_bounds__(kCrThreads) chol_inv_reg_kernel(const double* __restrict__ g, int k,
-                                                                double* __restrict__ x, int* __restrict__ info,
-                                                                double identity_tol) {
-    __shared__ double rowA[2][kJacobiMax], rowW[2][kJacobiMax], dinv[kJacobiMax];
+// The same factorisation with the working set in REGISTERS, at compile-time
+// positions: thread (warp w of 8, lane l) owns entries (i, j), i = l + 32 m
+// (m < MR), j = w + 8 n (n < NC).  G is first scaled to unit diagonal
+// (G' = D^-1/2 G D^-1/2, so every pivot d_c lies in (0, 1]).  Position (i, j)
+// holds C = A + W, the Gauss-Jordan pair [A | W] superimposed: A's eliminated
+// columns are 0 and W (= L'^{-1}, unit lower) is 0 above its diagonal, so the
+// row operation row_i -= mult_i row_c is ONE uniform update of every entry,
+// C(i, :) -= mult_i C(c, :), mult_i = A(c, i) / d_c for rows i > c (0 for
+// finished rows): no per-entry predicates.  The published row c carries
+// d_c + 1 at its diagonal (A(c, c) + W(c, c)), which turns column c into
+// W(i, c) = -mult_i (error <= ~3 eps relative since d_c <= 1).  Rows are
+// processed in groups of 32 with the group index a template parameter, so row
+// c + 1's owners (lane (c + 1) mod 32 of every warp) publish their registers
+// without run-time register selection: one barrier per step.  (A first layout
+// with 32 warps and per-entry live-range predicates issued ~500 instructions
+// per warp per step: 120 us at k = 80, slower than the shared-memory column
+// kernel.)  Same outputs as chol_inv_kernel: X = L^{-T} with A = L L^T,
+// info = 0 or 1 + the failing pivot (a non-positive diagonal entry of G is
+// reported as its own pivot).
+constexpr int kCtWarps = 8;
+
+template <int MR, int NC, int MM>
+__device__ __forceinline__ void chol_tile_step(double (&v)[MR][NC], int c, int k, int lane, int w,
+                                               double (*row)[128], double* dinv, double* dpiv, int* bad_sh) {
+    const int cb = c & 1, nb = cb ^ 1;
+    const double inv = dinv[c];
+    double mult[MR], rv[NC];
+#pragma unroll
+    for (int m = 0; m < MR; ++m) {
+        const int i = lane + 32 * m;
+        mult[m] = i > c ? row[cb][i] * inv : 0.0;  // A(i, c) = A(c, i); the row is 0 beyond k
+    }
+#pragma unroll
+    for (int n = 0; n < NC; ++n) rv[n] = row[cb][w + kCtWarps * n];
+#pragma unroll
+    for (int m = 0; m < MR; ++m)
+#pragma unroll
+        for (int n = 0; n < NC; ++n) v[m][n] = fma(-mult[m], rv[n], v[m][n]);
+    const int r1 = c + 1;
+    if (r1 < k && lane == (r1 & 31)) {  // publish row c + 1 (final after this step): register row MM
+#pragma unroll
+        for (int n = 0; n < NC; ++n) row[nb][w + kCtWarps * n] = v[MM][n];
+        if (w == (r1 & (kCtWarps - 1))) {  // the diagonal's owner
+            const double d = row[nb][r1];   // its own store
+            row[nb][r1] = d + 1.0;
+            dpiv[r1] = d;
+            dinv[r1] = 1.0 / d;
+            if (!(d > 0.0)) *bad_sh = r1 + 1;
+        }
+    }
+    __syncthreads();
+}
+
+template <int MR, int NC>
+__global__ void __launch_bounds__(kCtWarps * 32, 1)
+    chol_inv_tile_kernel(const double* __restrict__ g, int k, double* __restrict__ x, int* __restrict__ info,
+                         double identity_tol) {
+    __shared__ double row[2][128], dinv[128], dpiv[128], sdiag[128];
     __shared__ int bad_sh;
-    const int tid = threadIdx.x, nt = blockDim.x;
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, w = tid >> 5;
     if (identity_tol > 0.0) {  // uniform
         double dev = 0.0;
         for (int e = tid; e < k * k; e += nt) dev = fmax(dev, fabs(g[e] - ((e % k) == (e / k) ? 1.0 : 0.0)));
         for (int o = 16; o > 0; o >>= 1) dev = fmax(dev, __shfl_xor_sync(0xffffffffu, dev, o));
-        if ((tid & 31) == 0) rowA[0][tid >> 5] = dev;
+        if (lane == 0) row[0][w] = dev;
         __syncthreads();
         dev = 0.0;
-        for (int q = 0; q < (nt >> 5); ++q) dev = fmax(dev, rowA[0][q]);
+        for (int q = 0; q < (nt >> 5); ++q) dev = fmax(dev, row[0][q]);
         __syncthreads();
         if (dev <= identity_tol) {
             for (int e = tid; e < k * k; e += nt) x[e] = ((e % k) == (e / k)) ? 1.0 : 0.0;
@@ -438,73 +481,72 @@ __global__ void __launch_bounds__(kCrThreads) chol_inv_reg_kernel(const double* 
             return;
         }
     }
-    double v[kCrMaxE];
-    int ne = 0;
-#pragma unroll
-    for (int s = 0; s < kCrMaxE; ++s) {
-        const int e = tid + s * nt;
-        if (e < k * k) {
-            const int i = e / k, q = e % k;
-            v[s] = q >= i ? g[i + k * q] : 0.0;
-            ne = s + 1;
-        }
+    if (tid == 0) bad_sh = 0x7fffffff;
+    __syncthreads();
+    for (int j = tid; j < 128; j += nt) {
+        row[0][j] = row[1][j] = 0.0;
+        const double gd = j < k ? g[j + size_t(k) * j] : 1.0;
+        if (!(gd > 0.0)) atomicMin(&bad_sh, j + 1);  // the first non-positive diagonal entry
+        sdiag[j] = gd > 0.0 ? rsqrt(gd) : 0.0;
     }
+    __syncthreads();
+    if (bad_sh != 0x7fffffff) {  // uniform
+        if (tid == 0) *info = bad_sh;
+        return;
+    }
+    __syncthreads();
     if (tid == 0) bad_sh = 0;
-    // publish row 0
-    for (int q = tid; q < k; q += nt) {
-        const double a = g[k * q];
-        rowA[0][q] = a;
-        if (q == 0) {
-            rowW[0][0] = 1.0;
-            if (!(a > 0.0)) bad_sh = 1;
-            dinv[0] = 1.0 / a;
+    double v[MR][NC];
+#pragma unroll
+    for (int m = 0; m < MR; ++m)
+#pragma unroll
+        for (int n = 0; n < NC; ++n) {
+            const int i = lane + 32 * m, j = w + kCtWarps * n;
+            v[m][n] = (i < k && j < k) ? g[i + size_t(k) * j] * sdiag[i] * sdiag[j] : 0.0;  // both triangles
+        }
+    if (lane == 0) {  // row 0 (register row 0)
+#pragma unroll
+        for (int n = 0; n < NC; ++n) row[0][w + kCtWarps * n] = v[0][n];
+        if (w == 0) {
+            const double d = v[0][0];
+            row[0][0] = d + 1.0;
+            dpiv[0] = d;
+            dinv[0] = 1.0 / d;
         }
     }
     __syncthreads();
+    // steps c whose next row c + 1 lies in register row MM: c in [32 MM - 1, 32 MM + 31)
     int bad = 0;
-    for (int c = 0; c < k; ++c) {
-        if (bad_sh) {
-            bad = bad_sh;
-            break;
-        }
-        const int cb = c & 1, nb = cb ^ 1;
-        const double inv = dinv[c];
 #pragma unroll
-        for (int s = 0; s < kCrMaxE; ++s) {
-            if (s >= ne) break;
-            const int e = tid + s * nt, i = e / k, q = e % k;
-            if (i <= c) continue;  // retired (row i final before step i)
-            const double m = rowA[cb][i] * inv;
-            if (q >= i) {
-                v[s] = fma(-m, rowA[cb][q], v[s]);
-            } else if (q <= c) {
-                v[s] = fma(-m, rowW[cb][q], v[s]);
+    for (int mm = 0; mm < MR; ++mm) {
+        const int c_lo = mm == 0 ? 0 : 32 * mm - 1, c_hi = min(k, 32 * mm + 31);
+        for (int c = c_lo; c < c_hi && !bad; ++c) {
+            if (bad_sh) {  // uniform (read after the barrier that published it)
+                bad = bad_sh;
+                break;
             }
-            if (i == c + 1) {  // row c + 1 is final: publish it for the next step
-                if (q >= i) {
-                    rowA[nb][q] = v[s];
-                    if (q == i) {
-                        rowW[nb][i] = 1.0;
-                        if (!(v[s] > 0.0)) bad_sh = i + 1;
-                        dinv[i] = __drcp_rn(v[s]);
-                    }
-                } else {
-                    rowW[nb][q] = v[s];
-                }
-            }
+            if (mm == 0) chol_tile_step<MR, NC, 0>(v, c, k, lane, w, row, dinv, dpiv, &bad_sh);
+            else if (mm == 1) chol_tile_step<MR, NC, (MR > 1 ? 1 : 0)>(v, c, k, lane, w, row, dinv, dpiv, &bad_sh);
+            else if (mm == 2) chol_tile_step<MR, NC, (MR > 2 ? 2 : 0)>(v, c, k, lane, w, row, dinv, dpiv, &bad_sh);
+            else chol_tile_step<MR, NC, (MR > 3 ? 3 : 0)>(v, c, k, lane, w, row, dinv, dpiv, &bad_sh);
         }
-        __syncthreads();
     }
+    if (!bad && bad_sh) bad = bad_sh;  // the last published pivot
     if (bad) {
         if (tid == 0) *info = bad;
         return;
     }
+    // X(j, i) = W(i, j) / sqrt(d_i) / sqrt(g_jj), W(i, i) = 1, W(i, j) = C(i, j) for j < i
 #pragma unroll
-    for (int s = 0; s < kCrMaxE; ++s) {
-        if (s >= ne) break;
-        const int e = tid + s * nt, i = e / k, q = e % k;
-        const double r = sqrt(dinv[i]);  // 1 / sqrt(d_i)
-        x[e] = q > i ? 0.0 : (q == i ? r : v[s] * r);  // x[q + k i] = X(q, i) = W(i, q) / sqrt(d_i)
+    for (int m = 0; m < MR; ++m) {
+        const int i = lane + 32 * m;
+        if (i >= k) continue;
+        const double r = rsqrt(dpiv[i]);
+#pragma unroll
+        for (int n = 0; n < NC; ++n) {
+            const int j = w + kCtWarps * n;
+            if (j < k) x[j + size_t(k) * i] = j > i ? 0.0 : (j == i ? r : v[m][n] * r) * sdiag[j];
+        }
     }
     if (tid == 0) *info = 0;
 }
@@ -521,8 +563,12 @@ void cholesky_inv_t(atk_ctx* ctx, const double* g, int k, double* x, int* info_d
         attr = true;
     }
     if (ctx->chol_reg) {
-        const int threads = std::min(kCrThreads, (k * k + 31) / 32 * 32);  // <= kCrMaxE entries each
-        chol_inv_reg_kernel<<<1, threads, 0, ctx->stream>>>(g, k, x, info_dev, identity_tol);
+        // 8 warps: warp w owns columns w + 8 n, lanes own rows (chol_inv_tile_kernel)
+        constexpr int T = kCtWarps * 32;
+        if (k <= 32) chol_inv_tile_kernel<1, 4><<<1, T, 0, ctx->stream>>>(g, k, x, info_dev, identity_tol);
+        else if (k <= 64) chol_inv_tile_kernel<2, 8><<<1, T, 0, ctx->stream>>>(g, k, x, info_dev, identity_tol);
+        else if (k <= 96) chol_inv_tile_kernel<3, 12><<<1, T, 0, ctx->stream>>>(g, k, x, info_dev, identity_tol);
+        else chol_inv_tile_kernel<4, 14><<<1, T, 0, ctx->stream>>>(g, k, x, info_dev, identity_tol);
         ATK_LAUNCHED(ctx);
         return;
     }

@@ -488,6 +488,134 @@ __global__ void __launch_bounds__(256) invit_kernel(const double* __restrict__ d
     }
 }
 
+// invit_kernel with the working set in SHARED memory (n <= kIvSmemMax): one
+// warp per CTA (CTA j = wanted vector j; non-leaders exit), the chunk's
+// iterates x and their tridiagonal LU factors interleaved by member (lane) at
+// stride 32.  Same arithmetic and order as invit_kernel.  The global-memory
+// version's solve loops were a chain of L2 round trips (a store to x[i] then a
+// dependent load of x[i + 1], factors re-read from L2): 70 us for C5's
+// Rayleigh-Ritz block (n = 80, 64 vectors).
+constexpr int kIvSmemMax = 128;  // 6 n x 32 doubles = 192 KB
+__global__ void __launch_bounds__(32) invit_smem_kernel(const double* __restrict__ d, const double* __restrict__ e,
+                                                         int n, const double* __restrict__ lam, int nwant,
+                                                         double* __restrict__ X, const int* __restrict__ skip) {
+    extern __shared__ double sm[];
+    const int j = blockIdx.x;
+    const int lane = threadIdx.x & 31;
+    if (j >= nwant || (skip && *skip)) return;
+    const TNorm tn = tnorm_warp(d, e, n);
+    const double ortol = 1e-3 * tn.norm;
+    if (j > 0 && lam[j - 1] - lam[j] <= ortol) return;  // not a cluster leader
+    int end = j + 1;
+    while (end < nwant && lam[end - 1] - lam[end] <= ortol) ++end;
+    const double pertol = 10.0 * DBL_EPSILON * fmax(tn.norm, DBL_MIN);
+    const double tiny = tn.norm > 0.0 ? DBL_EPSILON * tn.norm : 1.0;  // pivot floor
+    constexpr int st = 32;
+    double* xs = sm;  // member c of the chunk: xs[i st + c]
+    double* x = xs + lane;
+    double* dl = sm + size_t(n) * st + lane;  // L multipliers
+    double* dd = dl + size_t(n) * st;         // 1 / U(i, i)
+    double* du = dd + size_t(n) * st;
+    double* du2 = du + size_t(n) * st;
+    double* pv = du2 + size_t(n) * st;  // 1.0 where rows i, i + 1 were interchanged
+    for (int cb = j; cb < end; cb += 32) {
+        const int mm = cb + lane;
+        const bool mine = mm < end;
+        if (mine) {
+            // shift, kept >= pertol below the previous member (dstein)
+            double sh = lam[j];
+            for (int q = j + 1; q <= mm; ++q) sh = fmin(lam[q], sh - pertol);
+            // dgttrf on T - sh I (one division per row: f = l * (1 / pivot))
+            double di = d[0] - sh, ui = n > 1 ? e[0] : 0.0;
+            for (int i = 0; i + 1 < n; ++i) {
+                const double li = e[i], dn = d[i + 1] - sh, un = i + 2 < n ? e[i + 1] : 0.0;
+                if (fabs(di) >= fabs(li)) {
+                    if (fabs(di) < tiny) di = copysign(tiny, di);
+                    const double r = 1.0 / di;
+                    const double f = li * r;
+                    dl[i * st] = f;
+                    dd[i * st] = r;
+                    du[i * st] = ui;
+                    du2[i * st] = 0.0;
+                    pv[i * st] = 0.0;
+                    di = fma(-f, ui, dn);
+                    ui = un;
+                } else {
+                    const double r = 1.0 / li;
+                    const double f = di * r;
+                    dl[i * st] = f;
+                    dd[i * st] = r;
+                    du[i * st] = dn;
+                    du2[i * st] = un;
+                    pv[i * st] = 1.0;
+                    di = fma(-f, dn, ui);
+                    ui = -f * un;
+                }
+            }
+            if (fabs(di) < tiny) di = copysign(tiny, di);
+            dd[(n - 1) * st] = 1.0 / di;
+            for (int i = 0; i < n; ++i) x[i * st] = hash_unit(uint64_t(mm) * 1000003ULL + i);
+        }
+        const int cend = min(end, cb + 32);
+        for (int it = 0; it < 3; ++it) {
+            if (mine) {
+                double cr = x[0];
+                for (int i = 0; i + 1 < n; ++i) {
+                    const double nx = x[(i + 1) * st];
+                    if (pv[i * st] != 0.0) {
+                        x[i * st] = nx;
+                        cr = fma(-dl[i * st], nx, cr);
+                    } else {
+                        x[i * st] = cr;
+                        cr = fma(-dl[i * st], cr, nx);
+                    }
+                }
+                x[(n - 1) * st] = cr;
+                double x2 = 0.0, x1 = x[(n - 1) * st] * dd[(n - 1) * st];
+                x[(n - 1) * st] = x1;
+                for (int i = n - 2; i >= 0; --i) {
+                    const double xi = (x[i * st] - du[i * st] * x1 - du2[i * st] * x2) * dd[i * st];
+                    x[i * st] = xi;
+                    x2 = x1;
+                    x1 = xi;
+                }
+            }
+            __syncwarp();
+            // Gram-Schmidt of the chunk's members in order against every earlier
+            // member of the cluster (earlier chunks: final, in X), then normalise
+            for (int q = cb; q < cend; ++q) {
+                double* xq = xs + (q - cb);
+                double mx = 0.0;
+                for (int i = lane; i < n; i += 32) mx = fmax(mx, fabs(xq[i * st]));
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                const double sc = mx > 0.0 ? 1.0 / mx : 1.0;  // pre-scale: the solve grows x by ~1/eps
+                for (int i = lane; i < n; i += 32) xq[i * st] *= sc;
+                __syncwarp();
+                for (int u = j; u < q; ++u) {
+                    const bool here = u >= cb;
+                    const double* xu = here ? xs + (u - cb) : X + size_t(n) * u;
+                    const int su = here ? st : 1;
+                    double dt = 0.0;
+                    for (int i = lane; i < n; i += 32) dt = fma(xu[i * su], xq[i * st], dt);
+                    dt = warp_sum(dt);
+                    for (int i = lane; i < n; i += 32) xq[i * st] = fma(-dt, xu[i * su], xq[i * st]);
+                    __syncwarp();
+                }
+                double nr = 0.0;
+                for (int i = lane; i < n; i += 32) nr = fma(xq[i * st], xq[i * st], nr);
+                nr = warp_sum(nr);
+                const double inv = nr > 0.0 ? 1.0 / sqrt(nr) : 0.0;
+                for (int i = lane; i < n; i += 32) xq[i * st] *= inv;
+                __syncwarp();
+            }
+        }
+        for (int q = cb; q < cend; ++q)  // the chunk's vectors out
+            for (int i = lane; i < n; i += 32) X[size_t(n) * q + i] = xs[i * st + (q - cb)];
+        __syncwarp();
+    }
+}
+
 // The same inverse iteration for large n (the dense path of trd_big.cu): ONE CTA
 // per cluster.  Members are solved in parallel (one thread each, factors
 // interleaved by member so a warp's loads are contiguous), then the whole CTA
@@ -1519,6 +1647,27 @@ void tridiag_tail(atk_ctx* ctx, const double* d, const double* e, int n, int nva
     }
 }
 
+// One warp per cluster leader: the shared-memory variant for n <= kIvSmemMax
+// (option "invit_smem", default 1), else the global-memory kernel.
+static void invit_warp(atk_ctx* ctx, const double* d, const double* e, int n, const double* values, int nwant,
+                       double* X, double* wk, const int* skip) {
+    if (ctx->invit_smem && n <= kIvSmemMax) {
+        const size_t smem = size_t(6) * n * 32 * sizeof(double);
+        static bool attr = false;
+        if (!attr) {
+            ATK_CUDA(cudaFuncSetAttribute(invit_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          int(size_t(6) * kIvSmemMax * 32 * sizeof(double))));
+            attr = true;
+        }
+        invit_smem_kernel<<<unsigned(nwant), 32, smem, ctx->stream>>>(d, e, n, values, nwant, X, skip);
+        ATK_LAUNCHED(ctx);
+        return;
+    }
+    const int wpb = 8;
+    invit_kernel<<<unsigned((nwant + wpb - 1) / wpb), 32 * wpb, 0, ctx->stream>>>(d, e, n, values, nwant, X, wk, skip);
+    ATK_LAUNCHED(ctx);
+}
+
 void tridiag_eig(atk_ctx* ctx, const double* a, int n, int lda, int nwant, double* values, double* vectors,
                  int ldv, int nvals) {
     if (n < 1 || n > kTridiagMax) fail(ATK_UNSUPPORTED, "tridiag_eig: n out of range");
@@ -1552,11 +1701,9 @@ void tridiag_eig(atk_ctx* ctx, const double* a, int n, int lda, int nwant, doubl
         DevBuf<int> ok(ctx, 1);
         invit_block_small_kernel<<<1, kIbT, smem, st>>>(d, e, n, values, nwant, X, wk, ok.get());
         ATK_LAUNCHED(ctx);
-        invit_kernel<<<unsigned((nwant + wpb - 1) / wpb), 32 * wpb, 0, st>>>(d, e, n, values, nwant, X, wk, ok.get());
-        ATK_LAUNCHED(ctx);
+        invit_warp(ctx, d, e, n, values, nwant, X, wk, ok.get());
     } else {
-        invit_kernel<<<unsigned((nwant + wpb - 1) / wpb), 32 * wpb, 0, st>>>(d, e, n, values, nwant, X, wk);
-        ATK_LAUNCHED(ctx);
+        invit_warp(ctx, d, e, n, values, nwant, X, wk, nullptr);
     }
     trd_backtr(ctx, false, nullptr, n, 0, hh, d, e, tau, scal, X, nwant, vectors, ldv);
 }

@@ -3,6 +3,7 @@ torch.profiler's CUPTI activity trace, which records every kernel in the process
 library's included.  Prints per-kernel device time, the idle gaps between consecutive
 kernels, and the span.  Usage: python profiles/timeline_probe.py [eig|step] [out.json]"""
 import json
+import os
 import sys
 from collections import defaultdict
 from pathlib import Path
@@ -19,6 +20,9 @@ what = sys.argv[1] if len(sys.argv) > 1 else "eig"
 out = sys.argv[2] if len(sys.argv) > 2 else "gpurun_out/timeline.json"
 torch.cuda.init()
 ctx = atucker.Context.default(0)
+for kv in filter(None, os.environ.get("ATK_OPTS", "").split(",")):  # e.g. ATK_OPTS=chol_reg=0
+    k, v = kv.split("=")
+    ctx.set_option(k, float(v))
 cfg = bench.CONFIGS["c5"]
 x = bench.make_input(atucker, cfg, bench.SEEDS["c5"], ctx)
 if what == "eig":

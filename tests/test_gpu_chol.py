@@ -1,4 +1,4 @@
-"""The register-resident Cholesky + inverse (jacobi.cu chol_inv_reg_kernel,
+"""The register-tile Cholesky + inverse (jacobi.cu chol_inv_tile_kernel,
 option chol_reg) against the shared-memory kernel it replaces and LAPACK:
 through thin_qr (CholeskyQR3, linalg.hpp:126-149) and the ALS SPD solves
 (solvers.hpp:104,109; NotSPD on a non-positive pivot)."""
@@ -48,3 +48,28 @@ def test_als_matches_with_both_cholesky_kernels(cctx):
     assert np.abs(res[0].factor - res[1].factor).max() <= 1e-11
     assert np.abs(np.asarray(res[0].shrunk) - np.asarray(res[1].shrunk)).max() <= 1e-10 * np.abs(
         np.asarray(res[0].shrunk)).max()
+
+
+@pytest.mark.parametrize("k", [5, 40, 80, 112])
+def test_thin_qr_graded_columns_both_kernels(cctx, k):
+    """CholeskyQR3 on columns graded over 1e-7 (the Gram's diagonal spans 1e-14, which the tile
+    kernel's unit-diagonal scaling absorbs) and a rank-deficient block (RankDeficient floor,
+    linalg.hpp:143-147) with both Cholesky kernels."""
+    from paper_2010_10131_b200 import atucker
+    from paper_2010_10131_b200.errors import RankDeficient
+
+    rng = np.random.default_rng(k)
+    a = np.asfortranarray(rng.standard_normal((3000, k)) * np.logspace(0, -7, k))
+    q0, r0 = np.linalg.qr(a)
+    sg = np.sign(np.diag(r0))
+    q0 = q0 * sg
+    for reg in (0, 1):
+        cctx.set_option("chol_reg", reg)
+        p = atucker.thin_qr(a, ctx=cctx)
+        assert np.abs(p.q - q0).max() <= 1e-8
+        assert np.abs(p.q.T @ p.q - np.eye(k)).max() <= 1e-13
+        if k > 1:
+            bad = a.copy()
+            bad[:, -1] = bad[:, 0]
+            with pytest.raises(RankDeficient):
+                atucker.thin_qr(bad, ctx=cctx)

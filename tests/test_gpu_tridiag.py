@@ -166,3 +166,33 @@ def test_reduction_kernels(variant, n):
     finally:
         ctx.set_option("trd_tiles", 1)
         ctx.set_option("eig_method", -1)
+
+
+@pytest.mark.parametrize("n,kind", [(80, "gram"), (80, "flat"), (128, "flat"), (48, "degenerate")])
+def test_invit_shared_memory_variant_bit_identical(n, kind):
+    """Inverse iteration with its working set in shared memory (option invit_smem, the default for
+    n <= 128) does the same arithmetic in the same order as the global-memory kernel: the vectors are
+    bit-identical, including clusters of more than 32 members (the flat spectra: one chunk of 32
+    in shared memory, earlier chunks read back from the output)."""
+    from paper_2010_10131_b200 import atucker
+
+    rng = np.random.default_rng(n)
+    if kind == "gram":
+        a = rng.standard_normal((n, 3 * n))
+        s = a @ a.T
+    elif kind == "flat":
+        s = _spectrum_matrix(n, 1.0 + 1e-9 * rng.standard_normal(n), n)
+    else:
+        s = _spectrum_matrix(n, np.repeat([3.0, 2.0, 1.0], [20, 20, n - 40]), n)
+    ctx = atucker.Context(0)
+    ctx.set_option("eig_method", 2)
+    out = {}
+    try:
+        for v in (1, 0):
+            ctx.set_option("invit_smem", v)
+            out[v] = atucker.sym_eig_top_r(s, n - 4, ctx=ctx)
+    finally:
+        ctx.set_option("invit_smem", 1)
+    np.testing.assert_array_equal(out[0].values, out[1].values)
+    np.testing.assert_array_equal(out[0].vectors, out[1].vectors)
+    _check(s, n - 4, out[1])
