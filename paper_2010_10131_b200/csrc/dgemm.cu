@@ -501,6 +501,139 @@ void dgemm_launch(atk_ctx* ctx, bool ta, bool tb, int m, int n, int k, double al
 
 }  // namespace
 
+// ------------------------------------------------------------------ SYRK
+// The fp64 first / last-mode Gram (kernels.hpp:127-138, the unfolding is a
+// plain column-major matrix) as a SYRK: C = op(A) op(A)^T, n <= 160.  A K-slice
+// of the n-row panel is staged ONCE in shared memory (cp.async ring) and serves
+// as both operands.  The upper 32 x 32 blocks (nb = ceil(n / 32), U = nb (nb + 1)
+// / 2 of them) are cut into 32 x 16 halves, ONE per warp (2U warps, a 4 x 2 grid
+// of DMMA m8n8k4 fragments each), so no warp waits on another's second block.
+// Split-K over CTAs, fixed-order partial sums; the reduction writes both
+// triangles.  At n = 128 (C3 mode 0): 10 of the 16 blocks a GEMM computes,
+// from half the staged bytes.
+constexpr int kSyBK = 16, kSyStages = 4, kSyMaxN = 160;  // 2U <= 30 warps
+
+__global__ void __launch_bounds__(1024) syrk_panel_kernel(bool ta, int n, int k, int kchunk,
+                                                          const double* __restrict__ a, int lda,
+                                                          double* __restrict__ part) {
+    extern __shared__ __align__(16) double ps[];
+    const int nb = (n + 31) / 32;
+    const int ldp = nb * 32 + 4;  // = 4 (mod 16): conflict-free fragment loads
+    const int stage = kSyBK * ldp;
+    const int tid = threadIdx.x, nt_ = blockDim.x, warp = tid >> 5, lane = tid & 31;
+    const int r = lane & 3, c = lane >> 2;
+    const int kb = blockIdx.x * kchunk, ke = min(k, kb + kchunk);
+    // half-block warp -> (row block, column block, half), row-major over the upper blocks
+    int rb = 0, cb = 0;
+    {
+        int t = warp >> 1;
+        for (int i = 0; i < nb; ++i) {
+            if (t < nb - i) {
+                rb = i;
+                cb = i + t;
+                break;
+            }
+            t -= nb - i;
+        }
+    }
+    const int c0 = cb * 32 + (warp & 1) * 16;
+    double acc[4][2][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    auto issue = [&](int st, int k0) {
+        double* P = ps + st * stage;
+        for (int e = tid; e < kSyBK * n; e += nt_) {
+            int kk, mm;
+            if (!ta) { mm = e % n; kk = e / n; } else { kk = e % kSyBK; mm = e / kSyBK; }
+            const int gk = k0 + kk;
+            const bool ok = gk < ke;
+            cp_async8(P + kk * ldp + mm, ok ? (ta ? a + gk + size_t(lda) * mm : a + mm + size_t(lda) * gk) : a, ok);
+        }
+    };
+    const int nt = (ke > kb) ? (ke - kb + kSyBK - 1) / kSyBK : 0;
+    // rows n .. 32 nb - 1 of every stage stay 0
+    for (int e = tid; e < kSyStages * stage; e += nt_)
+        if ((e % ldp) >= n) ps[e] = 0.0;
+#pragma unroll
+    for (int s = 0; s < kSyStages - 1; ++s) {
+        if (s < nt) issue(s, kb + s * kSyBK);
+        cp_async_commit();
+    }
+    const int aoff = r * ldp + rb * 32 + c, boff = r * ldp + c0 + c;
+    for (int t = 0; t < nt; ++t) {
+        cp_async_wait<kSyStages - 2>();
+        __syncthreads();
+        const int tn = t + kSyStages - 1;
+        if (tn < nt) issue(tn % kSyStages, kb + tn * kSyBK);
+        cp_async_commit();
+        const double* P = ps + (t % kSyStages) * stage;
+#pragma unroll
+        for (int kk = 0; kk < kSyBK; kk += 4) {
+            double av[4], bv[2];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) av[i] = P[aoff + kk * ldp + i * 8];
+#pragma unroll
+            for (int j = 0; j < 2; ++j) bv[j] = P[boff + kk * ldp + j * 8];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 2; ++j) dmma::mma_8x8x4(acc[i][j][0], acc[i][j][1], av[i], bv[j]);
+        }
+    }
+    cp_async_wait<0>();
+    double* o = part + size_t(blockIdx.x) * size_t(n) * n;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+                const int gm = rb * 32 + i * 8 + c, gn = c0 + j * 8 + 2 * r + t;
+                if (gm < n && gn < n) o[gm + size_t(n) * gn] = acc[i][j][t];
+            }
+}
+
+// C(i, j) = C(j, i) = alpha sum_z part[z](min, max): the upper triangle of the partials,
+// summed in split order, written to both triangles
+__global__ void syrk_reduce_kernel(const double* __restrict__ part, int splits, int n, double alpha,
+                                   double* __restrict__ cout, int ldc) {
+    const size_t tot = size_t(n) * n;
+    for (size_t e = size_t(blockIdx.x) * blockDim.x + threadIdx.x; e < tot; e += size_t(gridDim.x) * blockDim.x) {
+        const int i = int(e % n), j = int(e / n);
+        const int u = min(i, j), v = max(i, j);
+        const size_t off = u + size_t(n) * v;
+        double sum = 0.0;
+        for (int z = 0; z < splits; ++z) sum += part[size_t(z) * tot + off];
+        cout[i + size_t(ldc) * j] = alpha * sum;
+    }
+}
+
+void dsyrk_upper(atk_ctx* ctx, bool ta, int n, int k, double alpha, const double* a, int lda, double* c, int ldc) {
+    if (n <= 0) return;
+    if (n > kSyMaxN) fail(ATK_UNSUPPORTED, "dsyrk_upper: n > 160");
+    const int nb = (n + 31) / 32, warps = nb * (nb + 1);  // two halves per upper block
+    const size_t smem = size_t(kSyStages) * kSyBK * (nb * 32 + 4) * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+        ATK_CUDA(cudaFuncSetAttribute(syrk_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(size_t(kSyStages) * kSyBK * (kSyMaxN + 4) * sizeof(double))));
+        attr = true;
+    }
+    // one or two CTAs per SM, K chunks of >= 256
+    int splits = std::max(1, std::min(2 * ctx->num_sms, (k + 255) / 256));
+    int kchunk = (k + splits - 1) / splits;
+    kchunk = (kchunk + kSyBK - 1) / kSyBK * kSyBK;
+    splits = std::max(1, (k + kchunk - 1) / kchunk);
+    DevBuf<double> part(ctx, size_t(splits) * n * n);
+    syrk_panel_kernel<<<splits, 32 * warps, smem, ctx->stream>>>(ta, n, k, kchunk, a, lda, part.get());
+    ATK_LAUNCHED(ctx);
+    syrk_reduce_kernel<<<unsigned(std::min<size_t>((size_t(n) * n + 255) / 256, size_t(ctx->num_sms) * 8)), 256, 0,
+                         ctx->stream>>>(part.get(), splits, n, alpha, c, ldc);
+    ATK_LAUNCHED(ctx);
+}
+
 void dgemm(atk_ctx* ctx, bool ta, bool tb, int m, int n, int k, double alpha, const double* a, int lda,
            const double* b, int ldb, double beta, double* c, int ldc) {
     if (m <= 0 || n <= 0) return;

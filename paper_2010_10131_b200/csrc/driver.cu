@@ -31,6 +31,11 @@ void contract_ttt(atk_ctx* ctx, const atk_tensor* x, const atk_tensor* y, int mo
         s.I <= 0x7fffffffULL && R <= 0x7fffffffULL && s.P * s.O <= 0x7fffffffULL) {
         const auto* xd = static_cast<const double*>(x->data);
         const auto* yd = static_cast<const double*>(y->data);
+        if (sym && x == y && s.I <= 160) {  // the Gram as a SYRK: upper blocks only, both triangles written
+            if (s.P == 1) dsyrk_upper(ctx, false, int(s.I), int(s.O), 1.0, xd, int(s.I), z_dev, int(s.I));
+            else dsyrk_upper(ctx, true, int(s.I), int(s.P), 1.0, xd, int(s.P), z_dev, int(s.I));
+            return;
+        }
         if (s.P == 1)  // Z = X(I x J) Y(R x J)^T
             dgemm(ctx, false, true, int(s.I), int(R), int(s.O), 1.0, xd, int(s.I), yd, int(R), 0.0, z_dev, int(s.I));
         else  // Z = X(P x I)^T Y(P x R)

@@ -178,3 +178,19 @@ def test_frobenius_norm_device_fp32_large():
     # the oracle sums 64M squares serially in fp64 (its own error ~sqrt(n) eps ~ 1e-12);
     # an fp32 accumulation would be off by ~1e-4
     assert abs(got - ref) <= 1e-10 * ref, (got, ref)
+
+
+@pytest.mark.parametrize("dims,mode", [([128, 40, 30], 0), ([31, 7, 9], 0), ([20, 30, 192], 2), ([6, 5, 97], 2),
+                                       ([64, 3000], 0), ([160, 50, 4], 0), ([200, 50, 4], 0)])
+def test_fp64_first_last_mode_gram_syrk(dims, mode):
+    """The fp64 first / last-mode Gram (kernels.hpp:127-138) runs as a SYRK on DMMA (dgemm.cu
+    syrk_panel_kernel, n <= 160; n = 200 keeps the GEMM): exactly symmetric, and equal to the
+    fp64 product to rounding."""
+    from paper_2010_10131_b200 import atucker
+
+    x = np.asfortranarray(np.random.default_rng(sum(dims)).standard_normal(dims))
+    g = atucker.gram(x, mode)
+    m = np.moveaxis(x, mode, 0).reshape(dims[mode], -1, order="F")
+    want = m @ m.T
+    np.testing.assert_array_equal(g, g.T)
+    assert np.abs(g - want).max() <= 1e-12 * np.abs(want).max()
