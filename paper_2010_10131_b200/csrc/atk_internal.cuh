@@ -226,6 +226,10 @@ void dgemm(atk_ctx* ctx, bool ta, bool tb, int m, int n, int k, double alpha, co
 // C (n x n, n <= 160) = alpha op(A) op(A)^T (op(A) n x k): the upper 32 x 32 blocks on DMMA from a
 // shared-memory panel that serves as both operands, both triangles written (dgemm.cu).
 void dsyrk_upper(atk_ctx* ctx, bool ta, int n, int k, double alpha, const double* a, int lda, double* c, int ldc);
+// C = op(A) op(B) (m x n, n = R <= 64, one pass over A, no split-K) for the fp64 first / last-mode
+// TTM; tout stores C^T (c[j + ldc i]).
+void dgemm_ttm(atk_ctx* ctx, bool ta, bool tb, int m, int n, int k, const double* a, int lda, const double* b,
+               int ldb, double* c, int ldc, bool tout);
 // Dense symmetric eigensolver for n <= kJacobiMax (one CTA, smem Jacobi):
 // all eigenpairs of A (n x n, lda), values descending, vectors n x n.  psd:
 // A is known positive semi-definite (Cholesky-preconditioned, vector-free path).

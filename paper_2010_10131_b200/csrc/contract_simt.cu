@@ -368,6 +368,19 @@ void ttt_simt(atk_ctx* ctx, const void* x, const void* y, atk_dtype dt, Split s,
 
 void ttm_simt(atk_ctx* ctx, const void* x, atk_dtype dt, Split s, const double* u_dev, uint64_t R, void* y) {
     const uint64_t M = s.P * s.O;
+    // fp64 first / last mode: the unfolding is a plain column-major matrix, so the pipelined
+    // DMMA GEMM applies (mode 0 writes Y = U X as (X^T U^T)^T; the last mode Y = X U^T directly)
+    if (dt == ATK_F64 && !ctx->force_simt && (s.P == 1 || s.O == 1) && R <= 64 && s.I < (1u << 30) &&
+        M < (1ull << 31)) {
+        const double* xd = static_cast<const double*>(x);
+        if (s.P == 1)
+            dgemm_ttm(ctx, true, true, int(s.O), int(R), int(s.I), xd, int(s.I), u_dev, int(R), (double*)y, int(R),
+                      true);
+        else
+            dgemm_ttm(ctx, false, true, int(s.P), int(R), int(s.I), xd, int(s.P), u_dev, int(R), (double*)y,
+                      int(s.P), false);
+        return;
+    }
     if (R <= 32 && s.I * R <= 6144 && s.P > 1 && M >= uint64_t(ctx->num_sms) * 256) {
         const unsigned blocks = unsigned((M + 255) / 256);
         const size_t smem = size_t(s.I) * R * sizeof(double);

@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 #include "atk_internal.cuh"
 #include "dmma.cuh"
@@ -92,7 +93,8 @@ __global__ void __launch_bounds__(NT) dgemm_tile(bool ta, bool tb, int m, int n,
                                                  const double* __restrict__ a, int lda,
                                                  const double* __restrict__ b, int ldb,
                                                  double* __restrict__ out, size_t out_split_stride,
-                                                 int ldo, double alpha, double beta, bool direct) {
+                                                 int ldo, double alpha, double beta, bool direct,
+                                                 bool tout = false) {
     extern __shared__ __align__(16) double dsm[];
     const int m0 = blockIdx.x * BM, n0 = blockIdx.y * Tile<FN_>::BN_;
     const int kb = blockIdx.z * kchunk, ke = min(k, kb + kchunk);
@@ -107,7 +109,7 @@ __global__ void __launch_bounds__(NT) dgemm_tile(bool ta, bool tb, int m, int n,
             for (int t = 0; t < 2; ++t) {
                 const int gm = m0 + dmma::row_of<WM, FM>(i), gn = n0 + dmma::col_of<WM, FN_>(j, t);
                 if (gm < m && gn < n) {
-                    double* cp = o + gm + size_t(ldo) * gn;
+                    double* cp = tout ? o + gn + size_t(ldo) * gm : o + gm + size_t(ldo) * gn;  // tout: C^T stored
                     const double v = acc.v[i][j][t];
                     if (direct) *cp = alpha * v + (beta == 0.0 ? 0.0 : beta * *cp);
                     else *cp = v;
@@ -632,6 +634,33 @@ void dsyrk_upper(atk_ctx* ctx, bool ta, int n, int k, double alpha, const double
     syrk_reduce_kernel<<<unsigned(std::min<size_t>((size_t(n) * n + 255) / 256, size_t(ctx->num_sms) * 8)), 256, 0,
                          ctx->stream>>>(part.get(), splits, n, alpha, c, ldc);
     ATK_LAUNCHED(ctx);
+}
+
+// C = op(A) op(B) for the fp64 first / last-mode TTM (kernels.hpp:88-118; the unfolding is a
+// plain column-major matrix): m = the long dimension (J or P), n = R <= 64, k = I, one pass over
+// A through the cp.async ring with a column tile of 16 ceil(R / 16), no split-K (m fills the
+// GPU).  tout: C^T is stored (c[j + ldc i]), the mode-0 output layout (R x J).
+void dgemm_ttm(atk_ctx* ctx, bool ta, bool tb, int m, int n, int k, const double* a, int lda, const double* b,
+               int ldb, double* c, int ldc, bool tout) {
+    if (m <= 0 || n <= 0) return;
+    if (n > 64) fail(ATK_UNSUPPORTED, "dgemm_ttm: n > 64");
+    auto go = [&](auto fnc) {
+        constexpr int FN_ = decltype(fnc)::value;
+        static bool attr = false;
+        if (!attr) {
+            ATK_CUDA(cudaFuncSetAttribute(dgemm_tile<FN_>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          int(Tile<FN_>::SMEM)));
+            attr = true;
+        }
+        dim3 grid{unsigned((m + BM - 1) / BM), unsigned((n + Tile<FN_>::BN_ - 1) / Tile<FN_>::BN_), 1u};
+        dgemm_tile<FN_><<<grid, NT, Tile<FN_>::SMEM, ctx->stream>>>(ta, tb, m, n, std::max(k, 0), std::max(k, BK), a,
+                                                                    lda, b, ldb, c, 0, ldc, 1.0, 0.0, true, tout);
+        ATK_LAUNCHED(ctx);
+    };
+    if (n <= 16) go(std::integral_constant<int, 1>{});
+    else if (n <= 32) go(std::integral_constant<int, 2>{});
+    else if (n <= 48) go(std::integral_constant<int, 3>{});
+    else go(std::integral_constant<int, 4>{});
 }
 
 void dgemm(atk_ctx* ctx, bool ta, bool tb, int m, int n, int k, double alpha, const double* a, int lda,

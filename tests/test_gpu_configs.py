@@ -194,3 +194,20 @@ def test_fp64_first_last_mode_gram_syrk(dims, mode):
     want = m @ m.T
     np.testing.assert_array_equal(g, g.T)
     assert np.abs(g - want).max() <= 1e-12 * np.abs(want).max()
+
+
+@pytest.mark.parametrize("dims,mode,r", [([128, 40, 30], 0, 16), ([31, 7, 9], 0, 5), ([20, 30, 40], 2, 33),
+                                         ([6, 5, 97], 2, 64), ([200, 500], 0, 20), ([64, 3000], 1, 1)])
+def test_fp64_first_last_mode_ttm_gemm(dims, mode, r):
+    """The fp64 first / last-mode TTM (kernels.hpp:88-118) on the pipelined DMMA GEMM (dgemm.cu
+    dgemm_ttm; mode 0 stores the transposed product): equal to the fp64 product to rounding."""
+    from paper_2010_10131_b200 import atucker
+
+    rng = np.random.default_rng(sum(dims) + r)
+    x = np.asfortranarray(rng.standard_normal(dims))
+    u = rng.standard_normal((r, dims[mode]))
+    y = atucker.ttm(x, u, mode)
+    y = y.to_numpy() if hasattr(y, "to_numpy") else np.asarray(y)
+    want = np.moveaxis(np.tensordot(u, x, axes=([1], [mode])), 0, mode)
+    assert y.shape == want.shape
+    assert np.abs(y - want).max() <= 1e-12 * np.abs(want).max()
