@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(1024) householder_qr_kernel(double* __restrict
                                                               double* __restrict__ q,
                                                               double* __restrict__ r) {
     __shared__ double sh[33];
-    __shared__ double dots[128];
+    extern __shared__ double dots[];  // n column dot products
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
     const int nw = nt >> 5;
     for (int k = 0; k < n; ++k) {
@@ -275,12 +275,12 @@ __global__ void __launch_bounds__(1024) householder_qr_kernel(double* __restrict
             double d = (lane == 0) ? cj[k] : 0.0;
             for (int i = k + 1 + lane; i < m; i += 32) d += col[i] * cj[i];
             for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-            if (lane == 0) dots[j & 127] = d;
+            if (lane == 0) dots[j] = d;
         }
         __syncthreads();
         for (int j = k + 1; j < n; ++j) {
             double* cj = w + size_t(m) * j;
-            const double f = t * dots[j & 127];
+            const double f = t * dots[j];
             if (f != 0.0) {
                 for (int i = k + tid; i < m; i += nt) cj[i] -= f * (i == k ? 1.0 : col[i]);
             }
@@ -305,12 +305,12 @@ __global__ void __launch_bounds__(1024) householder_qr_kernel(double* __restrict
             double d = (lane == 0) ? qj[k] : 0.0;
             for (int i = k + 1 + lane; i < m; i += 32) d += col[i] * qj[i];
             for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-            if (lane == 0) dots[j & 127] = d;
+            if (lane == 0) dots[j] = d;
         }
         __syncthreads();
         for (int j = k; j < n; ++j) {
             double* qj = q + size_t(m) * j;
-            const double f = t * dots[j & 127];
+            const double f = t * dots[j];
             if (f != 0.0)
                 for (int i = k + tid; i < m; i += nt) qj[i] -= f * (i == k ? 1.0 : col[i]);
         }
@@ -421,11 +421,18 @@ void cholesky_solve(atk_ctx* ctx, const double* l, int n, double* b, int nrhs) {
 }
 
 void householder_qr(atk_ctx* ctx, const double* a, int m, int n, double* q, double* r) {
-    if (n > 128) fail(ATK_UNSUPPORTED, "householder_qr: more than 128 columns");
+    // any n (the ALS factor QR for R > 112, where CholeskyQR's one-CTA Cholesky does not fit)
+    const size_t smem = size_t(std::max(n, 1)) * sizeof(double);
+    if (smem > smem_cap_bytes()) fail(ATK_UNSUPPORTED, "householder_qr: too many columns for one CTA");
+    static size_t attr = 48 * 1024;
+    if (smem > attr) {
+        ATK_CUDA(cudaFuncSetAttribute(householder_qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        attr = smem;
+    }
     DevBuf<double> w(ctx, size_t(m) * n + n);
     ATK_CUDA(cudaMemcpyAsync(w.get(), a, size_t(m) * n * sizeof(double), cudaMemcpyDeviceToDevice,
                              ctx->stream));
-    householder_qr_kernel<<<1, 1024, 0, ctx->stream>>>(w.get(), m, n, w.get() + size_t(m) * n, q, r);
+    householder_qr_kernel<<<1, 1024, smem, ctx->stream>>>(w.get(), m, n, w.get() + size_t(m) * n, q, r);
     ATK_LAUNCHED(ctx);
 }
 

@@ -211,3 +211,23 @@ def test_fp64_first_last_mode_ttm_gemm(dims, mode, r):
     want = np.moveaxis(np.tensordot(u, x, axes=([1], [mode])), 0, mode)
     assert y.shape == want.shape
     assert np.abs(y - want).max() <= 1e-12 * np.abs(want).max()
+
+
+def test_large_rank_als_and_thin_qr(oracle):
+    """Ranks beyond the one-CTA Cholesky (k <= 112): thin_qr of 200 columns through the Householder
+    kernel (linalg.hpp:126-149), and an ALS mode with R = 150 (solvers.hpp:88-138), against the
+    oracle / LAPACK."""
+    from paper_2010_10131_b200 import atucker
+
+    rng = np.random.default_rng(21)
+    a = np.asfortranarray(rng.standard_normal((600, 200)))
+    p = atucker.thin_qr(a)
+    q0, r0 = np.linalg.qr(a)
+    sg = np.sign(np.diag(r0))
+    assert np.abs(p.q - q0 * sg).max() <= 1e-10
+    assert np.abs(p.q.T @ p.q - np.eye(200)).max() <= 1e-12
+    y = np.asfortranarray(rng.standard_normal((300, 40, 40)))
+    res = atucker.als_mode_solver(y, 0, 150, atucker.AlsOptions(num_iters=3, seed=4))
+    ref = oracle.als_mode_solver(y, 0, 150, num_iters=3, seed=4)
+    assert principal_angle(res.factor, ref.factor) <= 1e-8
+    assert abs(np.linalg.norm(np.asarray(res.shrunk)) - np.linalg.norm(ref.shrunk)) <= 1e-10 * np.linalg.norm(ref.shrunk)
