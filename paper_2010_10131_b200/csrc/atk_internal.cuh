@@ -85,6 +85,8 @@ struct atk_ctx {
     int tma_tf32 = 1;          // option "tma_tf32": TMA converts fp32 -> tf32 with round-to-nearest
                                // (the MMA itself truncates: measured 6e-4 bias vs 1e-6, test_gpu_tc.py)
     int gram_chunk_kb = 0;     // option "gram_chunk_kb": K-blocks per fp64 drain (0 = default)
+    int gram_small = 1;        // option "gram_small": mode-0 Grams with I <= 128 stage one operand tile per
+                               // K-block (read as A and B) in a 12-deep ring; 0 = the general 4-stage ring
     int gram_2cta = 1;         // option "gram_2cta": 256x256 Gram tiles on CTA pairs (cta_group::2)
     int invit_smem = 1;        // option "invit_smem": inverse iteration with its iterates and LU factors in
                                // shared memory (n <= 128); 0 = the global-memory kernel

@@ -24,10 +24,20 @@
 namespace atk {
 namespace {
 
-constexpr int BM = 128, BN = 256, BK = 32, STAGES = 4;
-constexpr uint32_t A_BYTES = BM * BK * 4, B_BYTES = BN * BK * 4, STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int BM = 128, BN = 256, BK = 32;
+constexpr uint32_t A_BYTES = BM * BK * 4, B_BYTES = BN * BK * 4;
 constexpr int THREADS = 192;
-constexpr size_t SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+// Ring geometry.  Small mode (mode 0, I <= 128: C4's 48-wide first mode, the R x R Grams): the
+// single diagonal tile's A and B are the same rows, so ONE operand tile (ceil(I / 32) TMA boxes
+// of 4 KB) is staged per K-block and read as both A and B (N = I rounded up to 32): 12 stages
+// of 16 KB keep ~3x more bytes in flight than the general 4 x 48 KB ring, whose stages were
+// mostly zero fill at I = 48 (C4 mode 0 at 26 % of HBM).
+template <bool SMALL>
+struct Ring {
+    static constexpr int STAGES = SMALL ? 12 : 4;
+    static constexpr uint32_t STAGE_BYTES = SMALL ? A_BYTES : A_BYTES + B_BYTES;
+    static constexpr size_t SMEM = size_t(STAGES) * STAGE_BYTES + 1024 + 256;
+};
 
 struct GramParams {
     const int4* units;  // {tile_m, tile_n, kb_begin, kb_end}
@@ -40,11 +50,16 @@ struct GramParams {
     double* acc;        // [unit][BN][BM] fp64 partial tiles
     uint32_t* progress; // [gridDim.x] K-blocks issued per CTA (drift limiter), or null
     int slack_kb;       // allowed lead over the slowest CTA, in K-blocks
+    int small_boxes;    // small mode: 32-row TMA boxes per K-block (ceil(I / 32))
+    int small_n;        // small mode: MMA N (I rounded up to whole 32-element MN-major atoms)
 };
 
+template <bool SMALL>
 __global__ void __launch_bounds__(THREADS, 1)
     gram_tf32_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                      const GramParams p) {
+    constexpr int STAGES = Ring<SMALL>::STAGES;
+    constexpr uint32_t STAGE_BYTES = Ring<SMALL>::STAGE_BYTES;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
@@ -104,9 +119,14 @@ __global__ void __launch_bounds__(THREADS, 1)
                     // on/above the diagonal -> load and multiply just those
                     const int tm = un.x & 0xffff, half = un.x >> 16;
                     tc::mbar_wait(&empty[stage], phase ^ 1);
-                    tc::mbar_arrive_expect_tx(&full[stage], half ? A_BYTES + B_BYTES / 2 : STAGE_BYTES);
                     uint8_t* a = smem + stage * STAGE_BYTES;
                     uint8_t* b = a + A_BYTES;
+                    if (SMALL) {  // one operand tile, rows 0 .. 32 boxes - 1
+                        tc::mbar_arrive_expect_tx(&full[stage], uint32_t(p.small_boxes) * 4096u);
+                        for (int q = 0; q < p.small_boxes; ++q)
+                            tc::tma_load_2d(a + q * 4096, &tma_a, &full[stage], q * 32, kb * BK);
+                    } else {
+                    tc::mbar_arrive_expect_tx(&full[stage], half ? A_BYTES + B_BYTES / 2 : A_BYTES + B_BYTES);
                     if (!p.kmajor) {
                         const int k0 = kb * BK;
 #pragma unroll
@@ -130,6 +150,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                             else tc::tma_load_3d(b, &tma_b, &full[stage], p0, o0, un.y * BN);
                         }
                     }
+                    }
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
             }
@@ -140,8 +161,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     } else if (warp == 1) {
         // ------------------------------------------------ MMA issuer
         if (lane == 0) {
-            const uint32_t idesc_full = tc::idesc_tf32(BM, BN, !p.kmajor, !p.kmajor);
-            const uint32_t idesc_half = tc::idesc_tf32(BM, BN / 2, !p.kmajor, !p.kmajor);
+            const uint32_t idesc_full = SMALL ? tc::idesc_tf32(BM, p.small_n, true, true)
+                                              : tc::idesc_tf32(BM, BN, !p.kmajor, !p.kmajor);
+            const uint32_t idesc_half = SMALL ? idesc_full : tc::idesc_tf32(BM, BN / 2, !p.kmajor, !p.kmajor);
             int stage = 0, abuf = 0;
             uint32_t phase = 0, aphase = 0;
             for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
@@ -161,7 +183,10 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
                         for (int k = 0; k < BK / 8; ++k) {
                             uint64_t ad, bd;
-                            if (!p.kmajor) {
+                            if (SMALL) {  // A and B: the same staged rows
+                                ad = tc::smem_desc(a_base + k * 1024, 4096, 512, 1);
+                                bd = ad;
+                            } else if (!p.kmajor) {
                                 // MN-major tf32: 128B/32B-atom swizzle, 4-row K groups (SBO 512 B),
                                 // 32-element MN blocks one TMA box apart (LBO 4 KB)
                                 ad = tc::smem_desc(a_base + k * 1024, 4096, 512, 1);
@@ -200,7 +225,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                 tc::tc_fence_after();
                 const bool first = (c0 == un.z);
                 // half units: mode 1 fills columns 128..255, mode 2 columns 0..127
-                const int cc0 = (un.x >> 16) == 1 ? BN / 64 : 0, cc1 = (un.x >> 16) == 2 ? BN / 64 : BN / 32;
+                const int cc0 = SMALL ? 0 : ((un.x >> 16) == 1 ? BN / 64 : 0);
+                const int cc1 = SMALL ? (p.small_n + 31) / 32 : ((un.x >> 16) == 2 ? BN / 64 : BN / 32);
 #pragma unroll 1
                 for (int cc = cc0; cc < cc1; ++cc) {
                     uint32_t r[32];
@@ -394,14 +420,21 @@ void tc_gram(atk_ctx* ctx, const atk_tensor* x, int mode, double* s_dev) {
     // lockstep window well inside the 126 MB L2.
     const double kb_bytes = double(I) * BK * 4.0 * splits;
     const int slack = int(std::max(8.0, std::min(256.0, 32e6 / kb_bytes)));
+    const bool small = !kmajor && I <= 128 && ntiles == 1 && !ctx->gram_lockstep && ctx->gram_small;
     GramParams prm{du.get(), int(units.size()), chunk_kb, kmajor ? 1 : 0, nkb_p, panel, opb, acc.get(),
-                   ctx->gram_lockstep ? progress.get() : nullptr, slack};
+                   ctx->gram_lockstep ? progress.get() : nullptr, slack, (I + 31) / 32, (I + 31) / 32 * 32};
     static bool attr = false;
     if (!attr) {
-        ATK_CUDA(cudaFuncSetAttribute(gram_tf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES)));
+        ATK_CUDA(cudaFuncSetAttribute(gram_tf32_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(Ring<false>::SMEM)));
+        ATK_CUDA(cudaFuncSetAttribute(gram_tf32_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(Ring<true>::SMEM)));
         attr = true;
     }
-    gram_tf32_kernel<<<grid, THREADS, SMEM_BYTES, ctx->stream>>>(ta, tb, prm);
+    if (small)
+        gram_tf32_kernel<true><<<grid, THREADS, Ring<true>::SMEM, ctx->stream>>>(ta, tb, prm);
+    else
+        gram_tf32_kernel<false><<<grid, THREADS, Ring<false>::SMEM, ctx->stream>>>(ta, tb, prm);
     ATK_LAUNCHED(ctx);
     const size_t n = size_t(I) * I;
     if (I <= 256 && splits >= 8)

@@ -175,3 +175,24 @@ def test_tc_gram_wide_units(dims, mode):
     assert np.abs(sw - ref).max() / scale <= 1e-4
     # same tf32 products, same chunking: only the split-K boundaries differ
     assert np.abs(sw - sn).max() / scale <= 1e-4
+
+
+@pytest.mark.parametrize("dims", [(48, 9000), (100, 5000), (128, 3000), (8, 700), (33, 2000)])
+def test_tc_gram_small_ring_matches_general(dims):
+    """Mode-0 Grams with I <= 128 stage one operand tile per K-block and read it as both A and B
+    (option gram_small): the same products, the same fp32 chains and drains as the general ring,
+    so the result is bit-identical; and within the tf32 bound of the fp64 Gram."""
+    from paper_2010_10131_b200 import atucker
+
+    ctx = atucker.Context.default(0)
+    xd = atucker.DeviceTensor.uniform(list(dims), 5, np.float32)
+    out = {}
+    try:
+        for v in (0, 1):
+            ctx.set_option("gram_small", v)
+            out[v] = atucker.gram(xd, 0)
+    finally:
+        ctx.set_option("gram_small", 1)
+    np.testing.assert_array_equal(out[0], out[1])
+    ref = gram_np(xd.to_numpy().astype(np.float64), 0)
+    assert np.abs(out[1] - ref).max() / np.abs(ref).max() <= 4e-3
