@@ -27,7 +27,8 @@ namespace {
 constexpr int BM = 128, BN = 256, BK = 32;
 constexpr uint32_t A_BYTES = BM * BK * 4, B_BYTES = BN * BK * 4;
 constexpr int THREADS = 192;
-// Ring geometry.  Small mode (mode 0, I <= 128: C4's 48-wide first mode, the R x R Grams): the
+// Ring geometry.  Small mode (I <= 128, mode 0 or the P in {4, 8, 16} panels: C4's 48-wide modes,
+// the R x R Grams): the
 // single diagonal tile's A and B are the same rows, so ONE operand tile (ceil(I / 32) TMA boxes
 // of 4 KB) is staged per K-block and read as both A and B (N = I rounded up to 32): 12 stages
 // of 16 KB keep ~3x more bytes in flight than the general 4 x 48 KB ring, whose stages were
@@ -121,10 +122,15 @@ __global__ void __launch_bounds__(THREADS, 1)
                     tc::mbar_wait(&empty[stage], phase ^ 1);
                     uint8_t* a = smem + stage * STAGE_BYTES;
                     uint8_t* b = a + A_BYTES;
-                    if (SMALL) {  // one operand tile, rows 0 .. 32 boxes - 1
-                        tc::mbar_arrive_expect_tx(&full[stage], uint32_t(p.small_boxes) * 4096u);
-                        for (int q = 0; q < p.small_boxes; ++q)
-                            tc::tma_load_2d(a + q * 4096, &tma_a, &full[stage], q * 32, kb * BK);
+                    if (SMALL) {  // one operand tile
+                        if (!p.kmajor) {  // MN-major: rows 0 .. 32 boxes - 1
+                            tc::mbar_arrive_expect_tx(&full[stage], uint32_t(p.small_boxes) * 4096u);
+                            for (int q = 0; q < p.small_boxes; ++q)
+                                tc::tma_load_2d(a + q * 4096, &tma_a, &full[stage], q * 32, kb * BK);
+                        } else {  // 16-B panels: one 4-D box of BM rows (zero fill past I)
+                            tc::mbar_arrive_expect_tx(&full[stage], A_BYTES);
+                            tc::tma_load_4d(a, &tma_a, &full[stage], 0, 0, 0, kb * p.opb);
+                        }
                     } else {
                     tc::mbar_arrive_expect_tx(&full[stage], half ? A_BYTES + B_BYTES / 2 : A_BYTES + B_BYTES);
                     if (!p.kmajor) {
@@ -161,7 +167,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     } else if (warp == 1) {
         // ------------------------------------------------ MMA issuer
         if (lane == 0) {
-            const uint32_t idesc_full = SMALL ? tc::idesc_tf32(BM, p.small_n, true, true)
+            const uint32_t idesc_full = SMALL ? tc::idesc_tf32(BM, p.small_n, !p.kmajor, !p.kmajor)
                                               : tc::idesc_tf32(BM, BN, !p.kmajor, !p.kmajor);
             const uint32_t idesc_half = SMALL ? idesc_full : tc::idesc_tf32(BM, BN / 2, !p.kmajor, !p.kmajor);
             int stage = 0, abuf = 0;
@@ -184,7 +190,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                         for (int k = 0; k < BK / 8; ++k) {
                             uint64_t ad, bd;
                             if (SMALL) {  // A and B: the same staged rows
-                                ad = tc::smem_desc(a_base + k * 1024, 4096, 512, 1);
+                                ad = !p.kmajor ? tc::smem_desc(a_base + k * 1024, 4096, 512, 1)
+                                               : tc::smem_desc(a_base + k * 2 * (BM * 16), BM * 16, 128, 0);
                                 bd = ad;
                             } else if (!p.kmajor) {
                                 // MN-major tf32: 128B/32B-atom swizzle, 4-row K groups (SBO 512 B),
@@ -420,7 +427,7 @@ void tc_gram(atk_ctx* ctx, const atk_tensor* x, int mode, double* s_dev) {
     // lockstep window well inside the 126 MB L2.
     const double kb_bytes = double(I) * BK * 4.0 * splits;
     const int slack = int(std::max(8.0, std::min(256.0, 32e6 / kb_bytes)));
-    const bool small = !kmajor && I <= 128 && ntiles == 1 && !ctx->gram_lockstep && ctx->gram_small;
+    const bool small = (!kmajor || panel) && I <= 128 && ntiles == 1 && !ctx->gram_lockstep && ctx->gram_small;
     GramParams prm{du.get(), int(units.size()), chunk_kb, kmajor ? 1 : 0, nkb_p, panel, opb, acc.get(),
                    ctx->gram_lockstep ? progress.get() : nullptr, slack, (I + 31) / 32, (I + 31) / 32 * 32};
     static bool attr = false;

@@ -177,9 +177,10 @@ def test_tc_gram_wide_units(dims, mode):
     assert np.abs(sw - sn).max() / scale <= 1e-4
 
 
-@pytest.mark.parametrize("dims", [(48, 9000), (100, 5000), (128, 3000), (8, 700), (33, 2000)])
-def test_tc_gram_small_ring_matches_general(dims):
-    """Mode-0 Grams with I <= 128 stage one operand tile per K-block and read it as both A and B
+@pytest.mark.parametrize("dims,mode", [((48, 9000), 0), ((100, 5000), 0), ((128, 3000), 0), ((8, 700), 0),
+                                       ((33, 2000), 0), ((8, 48, 301), 1), ((16, 40, 77), 1), ((4, 64, 50, 3), 1)])
+def test_tc_gram_small_ring_matches_general(dims, mode):
+    """Single-tile Grams (I <= 128; mode 0 or 16-B panels) stage one operand tile per K-block and read it as both A and B
     (option gram_small): the same products, the same fp32 chains and drains as the general ring,
     so the result is bit-identical; and within the tf32 bound of the fp64 Gram."""
     from paper_2010_10131_b200 import atucker
@@ -190,9 +191,9 @@ def test_tc_gram_small_ring_matches_general(dims):
     try:
         for v in (0, 1):
             ctx.set_option("gram_small", v)
-            out[v] = atucker.gram(xd, 0)
+            out[v] = atucker.gram(xd, mode)
     finally:
         ctx.set_option("gram_small", 1)
     np.testing.assert_array_equal(out[0], out[1])
-    ref = gram_np(xd.to_numpy().astype(np.float64), 0)
+    ref = gram_np(xd.to_numpy().astype(np.float64), mode)
     assert np.abs(out[1] - ref).max() / np.abs(ref).max() <= 4e-3
