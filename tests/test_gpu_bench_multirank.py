@@ -33,3 +33,5 @@ def test_bench_two_ranks_shared_gpu():
     assert d["config"]["parallelism"] == "shard last mode x2"
     assert all(st["comm_ms"] > 0 for st in d["stages"][:-1])  # one Gram allreduce per sharded mode
     assert d["stages"][-1]["comm_ms"] == 0  # the last mode runs on the gathered tensor: no allreduce
+    # e2e at N > 1: each rank's slab from pinned host memory through the public sthosvd
+    assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] == 4 * 48 ** 5
