@@ -322,41 +322,107 @@ __device__ __forceinline__ int sturm_count(const double* __restrict__ d, const d
     return c;
 }
 
-// values[j] = the j-th largest eigenvalue of T, j < nwant.  One warp per j.
+// C Sturm counts at once (independent chains interleaved: the serial
+// rcp + Newton + fma chain of one count is latency-bound, so C counts cost
+// about one).  Same arithmetic per count as sturm_count.
+template <int C>
+__device__ __forceinline__ void sturm_count_multi(const double* __restrict__ d, const double* __restrict__ e2, int n,
+                                                  const double (&x)[C], double pivmin, int (&cnt)[C]) {
+    double q[C];
+    const double d0 = d[0];
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+        q[c] = d0 - x[c];
+        if (fabs(q[c]) < pivmin) q[c] = -pivmin;
+        cnt[c] = q[c] < 0.0;
+    }
+    for (int i = 1; i < n; ++i) {
+        const double di = d[i], e2i = e2[i - 1];
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            double r;
+            asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q[c]));
+            r = r * fma(-q[c], r, 2.0);
+            q[c] = fma(-e2i, r, di - x[c]);
+            if (fabs(q[c]) < pivmin) q[c] = -pivmin;
+            cnt[c] += q[c] < 0.0;
+        }
+    }
+}
+
+// values[j] = the j-th largest eigenvalue of T, j < nwant.  One warp per j:
+// multisection with 32 C shifts per pass (C chains per lane), d and e^2 in
+// shared memory.  A pass narrows the interval (32 C + 1)x.
+template <int kBisC>
 __global__ void __launch_bounds__(256) bisect_kernel(const double* __restrict__ d, const double* __restrict__ e,
                                                      int n, int nwant, double* __restrict__ values) {
-    extern __shared__ double e2s[];
-    for (int i = threadIdx.x; i + 1 < n; i += blockDim.x) e2s[i] = e[i] * e[i];
+    extern __shared__ double e2s[];  // e^2 (n - 1), then d (n)
+    double* ds = e2s + n;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        if (i + 1 < n) e2s[i] = e[i] * e[i];
+        ds[i] = d[i];
+    }
     __syncthreads();
     const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (j >= nwant) return;
-    const TNorm tn = tnorm_warp(d, e, n);
+    const TNorm tn = tnorm_warp(ds, e, n);
     double emax2 = 0.0;
-    for (int i = 0; i + 1 < n; ++i) emax2 = fmax(emax2, e2s[i]);
+    for (int i = lane; i + 1 < n; i += 32) emax2 = fmax(emax2, e2s[i]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) emax2 = fmax(emax2, __shfl_xor_sync(0xffffffffu, emax2, o));
     const double pivmin = DBL_MIN * fmax(1.0, emax2);
     const double eps = DBL_EPSILON;
     const double slack = 2.0 * eps * tn.norm * n + 2.0 * pivmin;
     double lo = tn.lo - slack, hi = tn.hi + slack;
     const int t = n - 1 - j;  // ascending index
     const double atol = 2.0 * eps * tn.norm;
+    constexpr int NS = 32 * kBisC;  // shifts per pass, s = c 32 + lane (increasing x)
     for (int it = 0; it < 64; ++it) {
         const double wdt = hi - lo;
         if (!(wdt > fmax(atol, 2.0 * eps * fmax(fabs(lo), fabs(hi))))) break;
-        const double x = lo + wdt * double(lane + 1) / 33.0;
-        const bool above = sturm_count(d, e2s, n, x, pivmin) >= t + 1;
-        const unsigned b = __ballot_sync(0xffffffffu, above);
-        const double xl = __shfl_sync(0xffffffffu, x, b ? __ffs(b) - 1 : 31);
-        const double xp = __shfl_sync(0xffffffffu, x, b ? max(__ffs(b) - 2, 0) : 31);
-        if (b) {
-            const int f = __ffs(b) - 1;
-            hi = xl;
-            if (f > 0) lo = xp;
+        double x[kBisC];
+        int cnt[kBisC];
+#pragma unroll
+        for (int c = 0; c < kBisC; ++c) x[c] = lo + wdt * double(c * 32 + lane + 1) / double(NS + 1);
+        sturm_count_multi<kBisC>(ds, e2s, n, x, pivmin, cnt);
+        int first = NS;  // the first shift with count >= t + 1
+#pragma unroll
+        for (int c = kBisC - 1; c >= 0; --c) {
+            const unsigned b = __ballot_sync(0xffffffffu, cnt[c] >= t + 1);
+            if (b) first = c * 32 + __ffs(b) - 1;
+        }
+        auto xs = [&](int s) { return lo + wdt * double(s + 1) / double(NS + 1); };
+        if (first < NS) {
+            const double nl = first > 0 ? xs(first - 1) : lo;
+            hi = xs(first);
+            lo = nl;
         } else {
-            lo = xl;
+            lo = xs(NS - 1);
         }
     }
     if (lane == 0) values[j] = tn.norm > 0.0 ? 0.5 * (lo + hi) : 0.0;  // T = 0: exactly zero
+}
+
+// d and e^2 staged in shared memory: 2 n doubles (n = 4096: 64 KB, above the default 48 KB)
+void bisect_launch(atk_ctx* ctx, const double* d, const double* e, int n, int nvals, double* values) {
+    // 2 warps per CTA (the wanted values spread over ~nvals / 2 SMs: the fp64 reciprocal pipe, not
+    // the chain latency, bounds 8 warps per SM) and 2 interleaved chains per lane (64 shifts per
+    // pass): C5's n = 80 block 41 -> 35 us, n = 2048 876 -> 707 us (profiles/bisect_sweep.sh)
+    static const int wpb = std::getenv("ATK_BIS_WPB") ? std::atoi(std::getenv("ATK_BIS_WPB")) : 2;  // probe knobs
+    static const int nc = std::getenv("ATK_BIS_C") ? std::atoi(std::getenv("ATK_BIS_C")) : 2;
+    const size_t smem = 2 * size_t(n) * sizeof(double);
+    static size_t attr = 48 * 1024;
+    if (smem > attr) {
+        ATK_CUDA(cudaFuncSetAttribute(bisect_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        ATK_CUDA(cudaFuncSetAttribute(bisect_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        ATK_CUDA(cudaFuncSetAttribute(bisect_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        attr = smem;
+    }
+    const dim3 g((nvals + wpb - 1) / wpb), b(32 * wpb);
+    if (nc == 1) bisect_kernel<1><<<g, b, smem, ctx->stream>>>(d, e, n, nvals, values);
+    else if (nc == 2) bisect_kernel<2><<<g, b, smem, ctx->stream>>>(d, e, n, nvals, values);
+    else bisect_kernel<4><<<g, b, smem, ctx->stream>>>(d, e, n, nvals, values);
 }
 
 __device__ __forceinline__ double hash_unit(uint64_t x) {  // splitmix64 -> (-1, 1)
@@ -1563,8 +1629,7 @@ void tridiag_extreme_eig(atk_ctx* ctx, const double* d, const double* e, int m, 
     if (m < 1 || m > kTridiagMax) fail(ATK_UNSUPPORTED, "tridiag_extreme_eig: m out of range");
     DevBuf<double> wk(ctx, 5 * size_t(m));
     const int wpb = 8;
-    bisect_kernel<<<unsigned((m + wpb - 1) / wpb), 32 * wpb, size_t(m) * sizeof(double), ctx->stream>>>(d, e, m, m,
-                                                                                                         values);
+    bisect_launch(ctx, d, e, m, m, values);
     ATK_LAUNCHED(ctx);
     // one vector per launch: a lone eigenvalue is its own cluster, so a near-
     // degenerate extreme pair costs no Gram-Schmidt (any vector of the pair's
@@ -1627,8 +1692,7 @@ void tridiag_tail(atk_ctx* ctx, const double* d, const double* e, int n, int nva
     if (trace)
         for (auto& x : ev) cudaEventCreate(&x);
     if (trace) cudaEventRecord(ev[0], ctx->stream);
-    bisect_kernel<<<unsigned((nvals + wpb - 1) / wpb), 32 * wpb, size_t(n) * sizeof(double), ctx->stream>>>(
-        d, e, n, nvals, values);
+    bisect_launch(ctx, d, e, n, nvals, values);
     ATK_LAUNCHED(ctx);
     if (trace) cudaEventRecord(ev[1], ctx->stream);
     if (nwant > 0 && !invit_block(ctx, d, e, n, values, nwant, X)) {
@@ -1685,8 +1749,7 @@ void tridiag_eig(atk_ctx* ctx, const double* a, int n, int lda, int nwant, doubl
     double* wk = X + size_t(n) * nwant;
     trd_backtr(ctx, true, a, n, lda, hh, d, e, tau, scal, nullptr, 0, nullptr, 0);
     const int wpb = 8;
-    bisect_kernel<<<unsigned((nvals + wpb - 1) / wpb), 32 * wpb, size_t(n) * sizeof(double), st>>>(d, e, n, nvals,
-                                                                                                  values);
+    bisect_launch(ctx, d, e, n, nvals, values);
     ATK_LAUNCHED(ctx);
     if (nwant == 0) return;
     if (nwant >= 2 && n * nwant <= kIbSmall && !std::getenv("ATK_INVIT_SEQ")) {
