@@ -1577,7 +1577,10 @@ void launch_trd_backtr(atk_ctx* ctx, bool trd, const double* a, int n, int lda, 
                          h[4] / double(NW), h[5] / double(NW));
         }
     } else {
-        const int bw = std::min(32, nwant);
+        // 4 vectors (warps) per CTA: the wanted vectors spread over nwant / 4 SMs instead of
+        // sharing two (C5's 64 Ritz vectors at n = 80: 36 -> 17 us, profiles/backtr_sweep.sh)
+        static const int bw_env = std::getenv("ATK_BACKTR_BW") ? std::atoi(std::getenv("ATK_BACKTR_BW")) : 4;
+        const int bw = std::max(1, std::min(bw_env, nwant));
         backtr_kernel<S><<<unsigned((nwant + bw - 1) / bw), 32 * bw, backtr_smem(n), ctx->stream>>>(
             hh, tau, scal, n, X, nwant, vout, ldv);
     }
