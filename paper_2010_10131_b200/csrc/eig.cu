@@ -849,11 +849,23 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
     for (;; ++it) {
         ritz_residual<<<r, 256, 0, st>>>(Wr.get(), Vr.get(), theta.get(), n, r, res.get());
         ATK_LAUNCHED(ctx);
-        ATK_CUDA(cudaMemcpyAsync(hth.data(), theta.get(), k * sizeof(double), cudaMemcpyDeviceToHost, st));
-        ATK_CUDA(cudaMemcpyAsync(hres.data(), res.get(), r * sizeof(double), cudaMemcpyDeviceToHost, st));
         int qinfo[3] = {0, 0, 0};
-        if (qr_job.src) ATK_CUDA(cudaMemcpyAsync(qinfo, ws.info.get(), sizeof(qinfo), cudaMemcpyDeviceToHost, st));
-        ATK_CUDA(cudaStreamSynchronize(st));
+        // one host round trip through the context's page-locked staging (pageable destinations made
+        // each copy a synchronous staged transfer: ~40 us of gaps per check)
+        {
+            auto* pin = static_cast<uint8_t*>(pinned_host(ctx, (size_t(k) + r) * sizeof(double) + 64));
+            double* pth = reinterpret_cast<double*>(pin);
+            double* pres = pth + k;
+            int* pq = reinterpret_cast<int*>(pres + r);
+            pq[0] = pq[1] = pq[2] = 0;
+            ATK_CUDA(cudaMemcpyAsync(pth, theta.get(), k * sizeof(double), cudaMemcpyDeviceToHost, st));
+            ATK_CUDA(cudaMemcpyAsync(pres, res.get(), r * sizeof(double), cudaMemcpyDeviceToHost, st));
+            if (qr_job.src) ATK_CUDA(cudaMemcpyAsync(pq, ws.info.get(), 3 * sizeof(int), cudaMemcpyDeviceToHost, st));
+            ATK_CUDA(cudaStreamSynchronize(st));
+            std::copy(pth, pth + k, hth.begin());
+            std::copy(pres, pres + r, hres.begin());
+            std::copy(pq, pq + 3, qinfo);
+        }
         if (qr_job.src && (qinfo[0] || qinfo[1] || qinfo[2])) {  // CholeskyQR broke down: SVQB, same Rayleigh-Ritz
             svqb(ctx, qr_job.src, n, qr_job.ka, qr_job.dst, ws);
             qr_job.src = nullptr;
