@@ -162,6 +162,8 @@ uint64_t atk_ctx_launch_count(const atk_ctx* ctx);
  *   "eig_assume_psd" 1 = atk_sym_eig_top_r inputs are Grams (Cholesky-preconditioned Jacobi)
  *   "tma_tf32"      1 = round-to-nearest tf32 operand loads (default), 0 = hardware truncation
  *   "gram_2cta"     1 = CTA-pair (cta_group::2) Gram where supported (default)
+ *   "als_gram"      1 = ALS iterations on the mode's Gram (YR = S M^T, GR = M S M^T; rfac formed
+ *                  once) when the roofline favours it, fp32 (default); 0 = passes over Y
  *   "gram_small"    1 = mode-0 fp32 Grams with I <= 128 stage one operand tile per K-block, read as
  *                  both operands, in a 12-deep ring (default); 0 = the general 4-stage ring
  *   "invit_smem"    1 = inverse iteration (n <= 128) with its iterates and LU factors in shared

@@ -271,6 +271,7 @@ atk_status atk_ctx_set_option(atk_ctx* ctx, const char* key, double value) {
         else if (k == "chol_reg") ctx->chol_reg = int(value);
         else if (k == "invit_smem") ctx->invit_smem = int(value);
         else if (k == "gram_small") ctx->gram_small = int(value);
+        else if (k == "als_gram") ctx->als_gram = int(value);
         else if (k == "gram_launch_kb") ctx->gram_launch_kb = int(value);
         else fail(ATK_INVALID_ARGUMENT, "unknown option: " + k);
     });

@@ -77,6 +77,8 @@ struct atk_ctx {
     int cheb_dataflow = 0;     // option "cheb_dataflow": resident Chebyshev steps synchronised by per-CTA ready
                                // flags instead of a grid barrier (measured slower: 14.0 vs 12.5 us per step)
     int lanczos_tiles = 1;     // option "lanczos_tiles": S resident in a 16-CTA cluster's smem for the bounds
+    int als_gram = 1;          // option "als_gram": ALS iterations on the mode's Gram when the roofline says
+                               // Gram + one TTM beats the iterations' passes over Y (fp32)
     int als_fused = 1;         // option "als_fused": one pass over Y per ALS iteration (mode 0, fp32)
     int trd_tiles = 1;         // option "trd_tiles": 32 x 32-tile tridiagonalisation for n <= 192
     int chfsi_k = 0;           // option "chfsi_k": ChFSI block size override (0 = r + max(16, r/4))

@@ -184,6 +184,24 @@ std::vector<double> als_initial_guess(uint64_t rows, uint64_t r, uint64_t seed, 
     return l0;
 }
 
+// The Gram route for ALS (see als_iterate): fp32 tensors whose Gram runs on tcgen05, 2 <= iters,
+// and the roofline says Gram + one TTM beats the iterations' passes over Y (the one-pass kernel
+// when it applies, else the two-pass TTM + TTT schedule).
+bool als_gram_route(atk_ctx* ctx, const atk_tensor* y, int mode, uint64_t r, int iters) {
+    if (!ctx->als_gram || ctx->force_simt || y->dtype != ATK_F32 || iters < 2) return false;
+    // sharded: the local J differs between ranks with uneven slabs, and every rank must take the
+    // same schedule (its collectives); the per-iteration allreduce path stays
+    if (ctx->comm && !ctx->replicated) return false;
+    const uint64_t I = y->dims[mode], J = j_of(y, mode);
+    if (I > 4096 || r > I || !tc_ttt_supported(ctx, y, y, mode, true)) return false;
+    atk_roofline_params p;
+    atk_roofline_params_default(&p, ATK_F32, iters);
+    const double bw = p.hbm_gbs * 1e9, P = p.tf32_tflops * 1e12;
+    const double t_gram = std::max(double(I) * I * J / P, 4.0 * I * J / bw) + 4.0 * (I + r) * J / bw;
+    const double t_als = atk_roofline_time_als_mode(&p, mode, double(I), double(r), double(J));
+    return t_gram < t_als;
+}
+
 // als_iterate (solvers.hpp:88-118).  L stays on the device; rfac is returned.
 AlsOut als_iterate(atk_ctx* ctx, const atk_tensor* y, int mode, const double* l0_host, uint64_t r,
                    const atk_als_opts& opts) {
@@ -217,7 +235,54 @@ AlsOut als_iterate(atk_ctx* ctx, const atk_tensor* y, int mode, const double* l0
         t_last = now;
     };
     mark("start", -1);
-    if (als_fused_supported(ctx, y, mode, r)) {
+    // ALS on the mode's Gram (option "als_gram"): with S = Y_(n) Y_(n)^T formed once, every
+    // iteration's contractions collapse to I x I x R products, YR = Y rfac^T = S M^T and
+    // GR = rfac rfac^T = M S M^T (M = (L^T L)^{-1} L^T, rfac = M Y_(n)), the same iterates in
+    // exact arithmetic (solvers.hpp:88-118); rfac itself is formed once, after the loop.  On
+    // B200 the Gram runs on the tensor cores while every ALS pass is HBM-bound, so this wins
+    // whenever I^2 J / P + s I J / BW (Gram + final TTM) < iters x (one-pass ALS time).
+    if (als_gram_route(ctx, y, mode, r, opts.num_iters)) {
+        DevBuf<double> S(ctx, I * I), M(ctx, I * r);
+        contract_ttt(ctx, y, y, mode, S.get(), true);
+        mark("gram", -1);
+        for (int k = 0; k < opts.num_iters; ++k) {
+            dgemm(ctx, true, false, int(r), int(r), int(I), 1.0, L.get(), int(I), L.get(), int(I), 0.0, GL.get(),
+                  int(r));
+            record_gemm(2LL * (long long)(r * r) * (long long)I);
+            spd_inverse(ctx, GL.get(), int(r), GLi.get(), infos.get() + 2 * k);
+            dgemm(ctx, false, true, int(r), int(I), int(r), 1.0, GLi.get(), int(r), L.get(), int(I), 0.0, M.get(),
+                  int(r));
+            // YR = S M^T (I x R), GR = M YR (R x R)
+            dgemm(ctx, false, true, int(I), int(r), int(I), 1.0, S.get(), int(I), M.get(), int(r), 0.0, YR.get(),
+                  int(I));
+            dgemm(ctx, false, false, int(r), int(r), int(I), 1.0, M.get(), int(r), YR.get(), int(I), 0.0, GR.get(),
+                  int(r));
+            symmetrize(ctx, GR.get(), int(r));
+            // the reference's logical contractions: W = ttm, rfac = ttm, YR = ttt, GR = ttt
+            record_gemm(2LL * (long long)(r * J) * (long long)I);
+            record_gemm(2LL * (long long)(r * J) * (long long)r);
+            record_gemm(2LL * (long long)(I * r) * (long long)J);
+            record_gemm(2LL * (long long)(r * r) * (long long)J);
+            spd_inverse(ctx, GR.get(), int(r), GRi.get(), infos.get() + 2 * k + 1);
+            dgemm(ctx, false, false, int(I), int(r), int(r), 1.0, YR.get(), int(I), GRi.get(), int(r), 0.0,
+                  nxt.get(), int(I));
+            record_gemm(2LL * (long long)(I * r) * (long long)r);
+            out.iterations_run = k + 1;
+            mark("iter", k);
+            double change = 0.0;
+            if (opts.rel_tol > 0.0) {
+                check_spd(k + 1);
+                const double diff = diff_norm2_sq(ctx, nxt.get(), L.get(), ATK_F64, I * r);
+                const double base = norm2_sq(ctx, L.get(), ATK_F64, I * r);
+                change = base > 0.0 ? std::sqrt(diff / base) : 0.0;
+            }
+            std::swap(L, nxt);
+            if (opts.rel_tol > 0.0 && change <= opts.rel_tol) break;
+        }
+        // rfac of the last iteration (its M): one pass over Y
+        out.rfac = contract_ttm(ctx, y, M.get(), r, mode);
+        mark("rfac", -1);
+    } else if (als_fused_supported(ctx, y, mode, r)) {
         // One pass over Y per iteration (als_tc.cu): rfac = M Y_(0) with
         // M = (L^T L)^{-1} L^T, and YR / GR, from the same streamed tiles.  The
         // update order, seeding, NotSPD checks and early stop are those below.
