@@ -740,7 +740,8 @@ double atk_roofline_time_als(const atk_roofline_params* p, double i, double r, d
 double atk_roofline_time_als_mode(const atk_roofline_params* p, int mode, double i, double r, double j) {
     if (!p) return 0.0;
     // the kernel's own gate (atk_driver.cuh), so a shape the one-pass kernel refuses is priced
-    // as the two-pass schedule it will actually run
+    // as the two-pass schedule.  The ALS-on-the-Gram route (option als_gram) is not priced here:
+    // it costs about EIG minus the eigensolve, so the hook errs toward EIG, the exact solver
     const bool fused = mode == 0 && p->dtype == ATK_F32 && p->als_fused_factor > 0.0 && r >= 1 && i >= 1 &&
                        j >= 1 && i < 9.2e18 && j < 9.2e18 &&
                        als_fused_shape_ok(uint64_t(i), uint64_t(r), uint64_t(j), p->num_sms > 0 ? p->num_sms : 148);
