@@ -709,7 +709,10 @@ void dense_eig_big(atk_ctx* ctx, const double* a, int n, int lda, int nwant, dou
     const int gslot = n - 1;
     const int qmax = (n - 1 + G - 1) / G;
     const int Sg = (n + kBT - 1) / kBT;
-    const int qm = qmax <= 8 ? 8 : qmax <= 16 ? 16 : 32;
+    // the launched instance (below) fixes QM, and with it the kernel's shared-memory layout
+    // beside the column slots: size for THAT QM (n > 2048 launches <8, 32> with qmax <= 16)
+    const int qm0 = qmax <= 8 ? 8 : qmax <= 16 ? 16 : 32;
+    const int qm = (Sg <= 2 && qm0 == 8) ? 8 : (Sg <= 4 && qm0 <= 16) ? 16 : 32;
     if (ks > 0 && (qmax > 32 || Sg > 8 || G > kMaxG)) fail(ATK_UNSUPPORTED, "dense_eig_big: n too large for this GPU");
     const size_t gextra = trd_extra(n, qm, false, gslot);
     const int nslots = int(std::min<size_t>(qmax, (cap - gextra) / (size_t(gslot) * sizeof(double))));
@@ -743,8 +746,8 @@ void dense_eig_big(atk_ctx* ctx, const double* a, int n, int lda, int nwant, dou
     if (ks > 0) {
         TrdArgs g{a, lda, n, exact_sym ? 1 : 0, 0, ks, wk, hand, hh, d, e, tau, pbuf, colbuf, sync.get(),
                   nslots, gslot, prof};
-        if (Sg <= 2 && qm == 8) launch_trd<2, 8, false>(ctx, g, gsmem);
-        else if (Sg <= 4 && qm <= 16) launch_trd<4, 16, false>(ctx, g, gsmem);
+        if (qm == 8) launch_trd<2, 8, false>(ctx, g, gsmem);
+        else if (qm == 16) launch_trd<4, 16, false>(ctx, g, gsmem);
         else launch_trd<8, 32, false>(ctx, g, gsmem);
     }
     if (trace) cudaEventRecord(ev[1], st);

@@ -138,3 +138,15 @@ def test_warp_backtransform_matches(dctx, monkeypatch):
     s = _sym(900, 13, "flat_gram")
     monkeypatch.setenv("ATK_BACKTR_WARP", "1")
     _check(s, 40, atucker.sym_eig_top_r(s, 40, ctx=dctx))
+
+
+@pytest.mark.parametrize("n,r", [(2049, 10), (2156, 300), (3000, 64)])
+def test_dense_above_2048(dctx, n, r):
+    """2048 < n <= 4096 (kBigEigMax): the grid phase runs its <8, 32> instance, whose shared-memory
+    layout beside the column slots is sized for 32 columns per CTA (an undersized layout wrote out
+    of bounds for every n > 2048 before round 2's fix)."""
+    from paper_2010_10131_b200 import atucker
+
+    dctx.set_option("eig_method", 3)
+    s = _sym(n, n, "indefinite")
+    _check(s, r, atucker.sym_eig_top_r(s, r, ctx=dctx))
