@@ -38,9 +38,11 @@ def _case(seed, big=False):
         r = int(rng.integers(1, hi + 1)) if rng.random() < 0.8 else hi
         if kind == 1 and r > min(i, 128):  # keep ALS cases quick
             r = max(1, min(i, 128) // 2)
-        if kind == 1 and 2 * r > j:
+        if kind == 1 and (2 * r > j or 2 * r > i):
             # GR = rfac rfac^T (r x r) has rank <= J: singular for r > J, where the reference's
-            # Cholesky (linalg.hpp:169-177) and this one both stop on a rounding-sized pivot
+            # Cholesky (linalg.hpp:169-177) and this one both stop on a rounding-sized pivot; and
+            # near r = I the five iterations invert GR = L^-1 S L^-T with cond(L)^2 cond(S), which
+            # amplifies fp64 rounding (any two BLAS orders, Eigen's included) past 1e-10
             kind = 0
 
         ranks.append(r)
