@@ -83,6 +83,7 @@ struct atk_ctx {
     int trd_tiles = 1;         // option "trd_tiles": 32 x 32-tile tridiagonalisation for n <= 192
     int chfsi_k = 0;           // option "chfsi_k": ChFSI block size override (0 = r + max(16, r/4))
     bool replicated = false;   // sthosvd's last mode under a comm: the work tensor is whole on every rank
+    uint64_t global_last = 0;  // sthosvd under a comm: the global size of the sharded (last) mode
     bool eig_assume_psd = false;  // option "eig_assume_psd": atk_sym_eig_top_r input is a Gram
     int tma_tf32 = 1;          // option "tma_tf32": TMA converts fp32 -> tf32 with round-to-nearest
                                // (the MMA itself truncates: measured 6e-4 bias vs 1e-6, test_gpu_tc.py)

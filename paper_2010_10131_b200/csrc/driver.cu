@@ -83,7 +83,12 @@ ModeOut eig_mode(atk_ctx* ctx, const atk_tensor* y, int mode, uint64_t r, int so
                  const double* gram_pre, double gram_pre_ms) {
     check_truncation(y, mode, r);
     const uint64_t I = y->dims[mode], J = j_of(y, mode);
-    if (solver_kind == ATK_SOLVER_SVD && r > std::min(I, J))
+    // the unfolding's column count: under a sharded sthosvd the local J scaled to the global last
+    // mode (every rank then checks the same bound and fails alike)
+    uint64_t Jg = J;
+    if (ctx->comm && !ctx->replicated && ctx->global_last && mode != y->order - 1)
+        Jg = J / y->dims[y->order - 1] * ctx->global_last;
+    if (solver_kind == ATK_SOLVER_SVD && r > std::min(I, Jg))
         fail(ATK_RANK_TOO_LARGE, "truncation exceeds the rank bound of the unfolding");
     // the reference's SVD works on the explicit unfolding (solvers.hpp:142-162);
     // fp32 data carries no more than the Gram route's precision (sqrt(eps64)
@@ -453,6 +458,11 @@ atk_tensor* sthosvd(atk_ctx* ctx, const atk_tensor* x, const uint64_t* ranks, at
     // (every rank reaches it, so a bad rank fails on all ranks alike); the
     // global J of every sharded mode follows from it without further exchange
     const uint64_t g_last = ctx->comm ? comm_global_last(ctx, x) : x->dims[order - 1];
+    struct GlobalLastScope {  // the mode solvers' view of the global last-mode size
+        atk_ctx* c;
+        GlobalLastScope(atk_ctx* cc, uint64_t g) : c(cc) { c->global_last = g; }
+        ~GlobalLastScope() { c->global_last = 0; }
+    } global_last_scope(ctx, ctx->comm ? g_last : 0);
     for (int n = 0; n < order; ++n) {
         const uint64_t dn = n == order - 1 ? g_last : x->dims[n];
         if (ranks[n] < 1 || ranks[n] > dn)

@@ -65,6 +65,7 @@ def _host_comm_worker(rank, world, port, dims, ranks, kinds, dtype, out):
     comm_ms = sum(r.times.comm_ms for r in res.reports)
     if rank == 0:
         plain = atucker.Context(0)
+        plain.set_option("als_gram", 0)  # the sharded run iterates over Y (the Gram route is single-GPU)
         ref = atucker.sthosvd(atucker.DeviceTensor.from_numpy(x, ctx=plain), ranks, strat, opts, ctx=plain)
         g, gr = np.linalg.norm(core), np.linalg.norm(ref.decomposition.core.to_numpy().astype(np.float64))
         fd = max(np.abs(a - b).max() for a, b in zip(facs, ref.decomposition.factors))
@@ -189,3 +190,86 @@ def test_sharded_schedule_collectives(dims, ranks, kinds):
         assert st["allreduce_bytes"] == ar_bytes, st
         assert st["gather_calls"] == 2, st
         assert st["gather_bytes"] == gather_bytes, st
+
+
+def _sweep_worker(rank, world, port, cases, out):
+    import os
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    sys.path.insert(0, str(root))
+    sys.path.insert(0, str(root / "tests"))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2010_10131_b200 import atucker
+    from paper_2010_10131_b200.dist import init_host_comm_from_torch, shard_range
+    from test_gpu_sweep import _PerMode
+
+    ctx = atucker.Context(0)
+    init_host_comm_from_torch(ctx)
+    plain = atucker.Context(0) if rank == 0 else None
+    if plain is not None:
+        plain.set_option("als_gram", 0)  # the sharded run iterates over Y (the Gram route is single-GPU)
+    for idx, (dims, ranks, kinds, dtype) in enumerate(cases):
+        x = np.asfortranarray(np.random.default_rng(idx).standard_normal(dims).astype(dtype))
+        lo, hi = shard_range(dims[-1], rank, world)
+        xl = atucker.DeviceTensor.from_numpy(np.asfortranarray(x[..., lo:hi]), ctx=ctx)
+        opts = atucker.AlsOptions(seed=idx)
+        res = atucker.sthosvd(xl, ranks, _PerMode(kinds), opts, ctx=ctx, global_dims=dims)
+        xl.free()
+        if rank == 0:
+            ref = atucker.sthosvd(x, ranks, _PerMode(kinds), opts, ctx=plain)
+            core = np.asarray(res.decomposition.core.to_numpy(), dtype=np.float64)
+            g = np.linalg.norm(core)
+            gr = np.linalg.norm(np.asarray(ref.decomposition.core, dtype=np.float64))
+            # the reconstruction error is basis-free: factors of rank-deficient modes (r > rank of
+            # the Gram) hold an arbitrary null-space basis in both runs
+            dec = atucker.TuckerDecomposition(core.astype(x.dtype), res.decomposition.factors, tuple(dims))
+            e = atucker.relative_error(x, dec, ctx=plain)
+            er = atucker.relative_error(x, ref.decomposition, ctx=plain)
+            out.put((idx, g, gr, abs(e - er)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sharded_sweep_three_ranks():
+    """World size 3 on the one GPU (host-staged collectives, uneven last-mode slabs): the seeded
+    sweep's small cases (tests/test_gpu_sweep.py) through the sharded schedule reproduce the
+    single-process st-HOSVD: core norm and relative reconstruction error to 1e-10 (fp64) / 1e-4
+    (fp32; fixed-order reductions in a different grouping)."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    from test_gpu_sweep import _case
+
+    cases = []
+    for s in range(400):
+        dims, ranks, kinds, dtype = _case(s)
+        if dims[-1] >= 3 and len(cases) < 40:
+            cases.append((dims, ranks, kinds, dtype))
+    for s in range(16):  # fp32 up to 40M elements: the tensor-core paths, sharded
+        dims, ranks, kinds, dtype = _case(s, True)
+        if dims[-1] >= 3 and len(cases) < 48:
+            cases.append((dims, ranks, kinds, dtype))
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    mpc = mp.get_context("spawn")
+    q = mpc.Queue()
+    procs = [mpc.Process(target=_sweep_worker, args=(r, 3, port, cases, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=300) for _ in cases]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for idx, g, gr, de in got:
+        dims, ranks, kinds, dtype = cases[idx]
+        tol = 1e-10 if dtype == np.float64 else 1e-4
+        assert abs(g - gr) <= tol * gr, (cases[idx], g, gr)
+        assert de <= tol, (cases[idx], de)
