@@ -10,6 +10,10 @@ Cases (argv[1]):
   trd     n = 120 and 190: trd_small_kernel, trd_tile_kernel, trd_kernel
   big     n = 320 dense: the grid-wide Householder reduction (trd_big.cu) + its cluster tail
   svd     fp64 SVD mode on wide and tall unfoldings (svd.cu)
+  small   fp32 single-tile Gram ring (mode 0 and 16-B panels), gram_tc.cu
+  f64     fp64 SYRK Gram and DMMA-GEMM TTM (dgemm.cu), first and last modes
+  alsgram ALS on the Gram (driver.cu), fp32 mode 0
+  bigeig  dense eigensolver above n = 2048 (the <8, 32> grid instance)
 """
 import sys
 from pathlib import Path
@@ -59,6 +63,21 @@ elif case == "svd":
     for dims, mode, r in (([24, 10, 12], 0, 8), ([40, 3, 4], 0, 6)):
         y = np.asfortranarray(rng.standard_normal(dims))
         atucker.svd_mode_solver(y, mode, r, ctx=ctx)
+elif case == "small":
+    for dims, mode in (([48, 2000], 0), ([8, 48, 301], 1), ([100, 700], 0)):
+        x = atucker.DeviceTensor.uniform(dims, 3, np.float32, ctx=ctx)
+        atucker.gram(x, mode, ctx=ctx)
+elif case == "f64":
+    x = np.asfortranarray(rng.standard_normal((128, 40, 30)))
+    res = atucker.sthosvd(x, [16, 8, 6], Strategy.fixed_eig(), ctx=ctx)
+elif case == "alsgram":
+    x = atucker.DeviceTensor.uniform([512, 64, 64], 5, np.float32, ctx=ctx)
+    atucker.als_mode_solver(x, 0, 16, atucker.AlsOptions(num_iters=2, seed=3), ctx=ctx)
+elif case == "bigeig":
+    ctx.set_option("eig_method", 3)
+    a = rng.standard_normal((2100, 2100))
+    p = atucker.sym_eig_top_r(0.5 * (a + a.T), 8, ctx=ctx)
+    ctx.set_option("eig_method", -1)
 else:
     raise SystemExit(f"unknown case {case}")
 ctx.synchronize()
