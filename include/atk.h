@@ -143,7 +143,8 @@ uint64_t atk_ctx_launch_count(const atk_ctx* ctx);
  *   "svd_explicit"  1 = fp64 SVD modes on the explicit unfolding (Gram-preconditioned one-sided
  *                  Jacobi; default), 0 = the Gram route (sigma = sqrt(lambda))
  *   "eig_dense_passes" ChFSI filter passes before the exact dense solver takes over (default 3;
- *                  -1 = never)
+ *                  skipped while the measured rate predicts convergence within ~2 more passes,
+ *                  always after twice the budget; -1 = never)
  *   "chfsi_tol"     relative Ritz-residual target of ChFSI (default 1e-12; fp32 Grams use >= 1e-9)
  *   "cheb_fused"    1 = each Chebyshev filter pass is one cooperative launch (default), 0 = per-step launches
  *   "als_head"      -1 = one-pass ALS: phase 1 and phase 2 of a tile in turn (default); k >= 0 interleaves
