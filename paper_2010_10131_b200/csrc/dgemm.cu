@@ -508,16 +508,20 @@ void dgemm_launch(atk_ctx* ctx, bool ta, bool tb, int m, int n, int k, double al
 // plain column-major matrix) as a SYRK: C = op(A) op(A)^T, n <= 160.  A K-slice
 // of the n-row panel is staged ONCE in shared memory (cp.async ring) and serves
 // as both operands.  The upper 32 x 32 blocks (nb = ceil(n / 32), U = nb (nb + 1)
-// / 2 of them) are cut into 32 x 16 halves, ONE per warp (2U warps, a 4 x 2 grid
-// of DMMA m8n8k4 fragments each), so no warp waits on another's second block.
+// / 2 of them) go ONE per warp (U warps, a 4 x 4 grid of DMMA m8n8k4 fragments
+// each: 16 independent accumulation chains), so no warp waits on another's
+// second block.
 // Split-K over CTAs, fixed-order partial sums; the reduction writes both
 // triangles.  At n = 128 (C3 mode 0): 10 of the 16 blocks a GEMM computes,
 // from half the staged bytes.
 constexpr int kSyBK = 16, kSyStages = 4, kSyMaxN = 160;  // 2U <= 30 warps
 
-__global__ void __launch_bounds__(1024) syrk_panel_kernel(bool ta, int n, int k, int kchunk,
+// FN: 8-column DMMA fragments per warp (2: a 32 x 16 half-block, 4: a whole 32 x 32 block)
+template <int FN>
+__global__ void __launch_bounds__(FN == 4 ? 512 : 1024) syrk_panel_kernel(bool ta, int n, int k, int kchunk,
                                                           const double* __restrict__ a, int lda,
                                                           double* __restrict__ part) {
+    constexpr int HB = 4 / FN;  // warps per 32 x 32 block
     extern __shared__ __align__(16) double ps[];
     const int nb = (n + 31) / 32;
     const int ldp = nb * 32 + 4;  // = 4 (mod 16): conflict-free fragment loads
@@ -525,10 +529,10 @@ __global__ void __launch_bounds__(1024) syrk_panel_kernel(bool ta, int n, int k,
     const int tid = threadIdx.x, nt_ = blockDim.x, warp = tid >> 5, lane = tid & 31;
     const int r = lane & 3, c = lane >> 2;
     const int kb = blockIdx.x * kchunk, ke = min(k, kb + kchunk);
-    // half-block warp -> (row block, column block, half), row-major over the upper blocks
+    // warp -> (row block, column block, part), row-major over the upper blocks
     int rb = 0, cb = 0;
     {
-        int t = warp >> 1;
+        int t = warp / HB;
         for (int i = 0; i < nb; ++i) {
             if (t < nb - i) {
                 rb = i;
@@ -538,12 +542,12 @@ __global__ void __launch_bounds__(1024) syrk_panel_kernel(bool ta, int n, int k,
             t -= nb - i;
         }
     }
-    const int c0 = cb * 32 + (warp & 1) * 16;
-    double acc[4][2][2];
+    const int c0 = cb * 32 + (warp % HB) * (8 * FN);
+    double acc[4][FN][2];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     auto issue = [&](int st, int k0) {
         double* P = ps + st * stage;
         for (int e = tid; e < kSyBK * n; e += nt_) {
@@ -573,15 +577,15 @@ __global__ void __launch_bounds__(1024) syrk_panel_kernel(bool ta, int n, int k,
         const double* P = ps + (t % kSyStages) * stage;
 #pragma unroll
         for (int kk = 0; kk < kSyBK; kk += 4) {
-            double av[4], bv[2];
+            double av[4], bv[FN];
 #pragma unroll
             for (int i = 0; i < 4; ++i) av[i] = P[aoff + kk * ldp + i * 8];
 #pragma unroll
-            for (int j = 0; j < 2; ++j) bv[j] = P[boff + kk * ldp + j * 8];
+            for (int j = 0; j < FN; ++j) bv[j] = P[boff + kk * ldp + j * 8];
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
-                for (int j = 0; j < 2; ++j) dmma::mma_8x8x4(acc[i][j][0], acc[i][j][1], av[i], bv[j]);
+                for (int j = 0; j < FN; ++j) dmma::mma_8x8x4(acc[i][j][0], acc[i][j][1], av[i], bv[j]);
         }
     }
     cp_async_wait<0>();
@@ -589,7 +593,7 @@ __global__ void __launch_bounds__(1024) syrk_panel_kernel(bool ta, int n, int k,
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 2; ++j)
+        for (int j = 0; j < FN; ++j)
 #pragma unroll
             for (int t = 0; t < 2; ++t) {
                 const int gm = rb * 32 + i * 8 + c, gn = c0 + j * 8 + 2 * r + t;
@@ -615,11 +619,16 @@ __global__ void syrk_reduce_kernel(const double* __restrict__ part, int splits, 
 void dsyrk_upper(atk_ctx* ctx, bool ta, int n, int k, double alpha, const double* a, int lda, double* c, int ldc) {
     if (n <= 0) return;
     if (n > kSyMaxN) fail(ATK_UNSUPPORTED, "dsyrk_upper: n > 160");
-    const int nb = (n + 31) / 32, warps = nb * (nb + 1);  // two halves per upper block
+    // one whole 32 x 32 block per warp (16 independent DMMA chains: C3 mode 0 2.09 -> 1.62 ms against
+    // 32 x 16 halves on twice the warps); ATK_SYRK_HALF: the half-block variant (probe knob)
+    static const bool full = std::getenv("ATK_SYRK_HALF") == nullptr;
+    const int nb = (n + 31) / 32, warps = full ? nb * (nb + 1) / 2 : nb * (nb + 1);
     const size_t smem = size_t(kSyStages) * kSyBK * (nb * 32 + 4) * sizeof(double);
     static bool attr = false;
     if (!attr) {
-        ATK_CUDA(cudaFuncSetAttribute(syrk_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        ATK_CUDA(cudaFuncSetAttribute(syrk_panel_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(size_t(kSyStages) * kSyBK * (kSyMaxN + 4) * sizeof(double))));
+        ATK_CUDA(cudaFuncSetAttribute(syrk_panel_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       int(size_t(kSyStages) * kSyBK * (kSyMaxN + 4) * sizeof(double))));
         attr = true;
     }
@@ -629,7 +638,8 @@ void dsyrk_upper(atk_ctx* ctx, bool ta, int n, int k, double alpha, const double
     kchunk = (kchunk + kSyBK - 1) / kSyBK * kSyBK;
     splits = std::max(1, (k + kchunk - 1) / kchunk);
     DevBuf<double> part(ctx, size_t(splits) * n * n);
-    syrk_panel_kernel<<<splits, 32 * warps, smem, ctx->stream>>>(ta, n, k, kchunk, a, lda, part.get());
+    if (full) syrk_panel_kernel<4><<<splits, 32 * warps, smem, ctx->stream>>>(ta, n, k, kchunk, a, lda, part.get());
+    else syrk_panel_kernel<2><<<splits, 32 * warps, smem, ctx->stream>>>(ta, n, k, kchunk, a, lda, part.get());
     ATK_LAUNCHED(ctx);
     syrk_reduce_kernel<<<unsigned(std::min<size_t>((size_t(n) * n + 255) / 256, size_t(ctx->num_sms) * 8)), 256, 0,
                          ctx->stream>>>(part.get(), splits, n, alpha, c, ldc);
