@@ -17,14 +17,15 @@ from paper_2010_10131_b200 import atucker  # noqa: E402
 from paper_2010_10131_b200.selector import Strategy  # noqa: E402
 
 what = sys.argv[1] if len(sys.argv) > 1 else "eig"
+cfg_name = os.environ.get("ATK_CFG", "c5")  # step mode: which bench config
 out = sys.argv[2] if len(sys.argv) > 2 else "gpurun_out/timeline.json"
 torch.cuda.init()
 ctx = atucker.Context.default(0)
 for kv in filter(None, os.environ.get("ATK_OPTS", "").split(",")):  # e.g. ATK_OPTS=chol_reg=0
     k, v = kv.split("=")
     ctx.set_option(k, float(v))
-cfg = bench.CONFIGS["c5"]
-x = bench.make_input(atucker, cfg, bench.SEEDS["c5"], ctx)
+cfg = bench.CONFIGS[cfg_name if what == "step" else "c5"]
+x = bench.make_input(atucker, cfg, bench.SEEDS[cfg_name if what == "step" else "c5"], ctx)
 if what == "eig":
     s0 = atucker.gram(x, 0, ctx=ctx)
     x.free()
