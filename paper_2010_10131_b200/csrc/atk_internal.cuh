@@ -299,5 +299,10 @@ struct EigInfo {
 // `exact_sym`: S is bitwise symmetric (the engine's mirrored Grams): no copy.
 EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* values_dev,
                       double* vectors_dev, bool psd = false, double tol = 0.0, bool exact_sym = false);
+// Power-of-two range scaling of an engine-owned symmetric S in place (only when max|S| lies
+// outside [2^-200, 2^200]; psd: the diagonal bounds every entry); fac_dev (2 doubles): the
+// eigenvalue factor and the applied scale.  eig_unscale_values multiplies eigenvalues back.
+void eig_scale(atk_ctx* ctx, double* s, int n, bool psd, double* fac_dev);
+void eig_unscale_values(atk_ctx* ctx, double* values, int count, const double* fac_dev);
 
 }  // namespace atk

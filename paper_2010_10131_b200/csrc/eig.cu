@@ -708,8 +708,80 @@ __global__ void scale_cols_shift(const double* __restrict__ l, const double* __r
 
 }  // namespace
 
+// ------------------------------------------------------------------ scaling
+// Eigen's SelfAdjointEigenSolver (linalg.hpp:108) divides the matrix by max|a_ij| before it
+// tridiagonalises, so squares of huge or tiny entries (Householder norms, Sturm counts, S^2
+// products) neither overflow nor underflow.  Here S is scaled in place by a power of two (exact)
+// only when max|S| lies outside [2^-200, 2^200], so ordinary inputs are untouched bit for bit;
+// fac[0] = the factor the eigenvalues are multiplied back by (1 when untouched).
+namespace {
+constexpr int kScT = 256;
+__global__ void __launch_bounds__(kScT) eig_maxabs_kernel(const double* __restrict__ s, int n, int diag_only,
+                                                          double* __restrict__ fac) {
+    __shared__ double red[kScT / 32];
+    double m = 0.0;
+    const size_t tot = diag_only ? size_t(n) : size_t(n) * n;
+    for (size_t e = threadIdx.x; e < tot; e += kScT)
+        m = fmax(m, fabs(diag_only ? s[e + size_t(n) * e] : s[e]));
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < kScT / 32; ++w) m = fmax(m, red[w]);
+        const bool safe = !(m > 0.0) || (m >= 0x1p-200 && m <= 0x1p200) || isinf(m) || isnan(m);
+        const int ex = safe ? 0 : ilogb(m);
+        fac[0] = ldexp(1.0, ex);   // eigenvalues x fac
+        fac[1] = ldexp(1.0, -ex);  // S x fac[1]
+    }
+}
+__global__ void eig_scale_kernel(double* __restrict__ s, size_t tot, const double* __restrict__ fac) {
+    const double f = fac[1];
+    if (f == 1.0) return;  // uniform: the common case writes nothing
+    for (size_t e = size_t(blockIdx.x) * blockDim.x + threadIdx.x; e < tot; e += size_t(gridDim.x) * blockDim.x)
+        s[e] *= f;
+}
+__global__ void eig_unscale_kernel(double* __restrict__ v, int count, const double* __restrict__ fac) {
+    const double f = fac[0];
+    if (f == 1.0) return;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < count; e += gridDim.x * blockDim.x) v[e] *= f;
+}
+}  // namespace
+
+void eig_scale(atk_ctx* ctx, double* s, int n, bool psd, double* fac_dev) {
+    // a PSD matrix's largest |entry| sits on its diagonal: n reads instead of n^2
+    eig_maxabs_kernel<<<1, kScT, 0, ctx->stream>>>(s, n, psd ? 1 : 0, fac_dev);
+    ATK_LAUNCHED(ctx);
+    const size_t tot = size_t(n) * n;
+    eig_scale_kernel<<<unsigned(std::max<size_t>(1, std::min<size_t>((tot + 255) / 256, size_t(ctx->num_sms) * 8))),
+                       256, 0, ctx->stream>>>(s, tot, fac_dev);
+    ATK_LAUNCHED(ctx);
+}
+
+void eig_unscale_values(atk_ctx* ctx, double* values, int count, const double* fac_dev) {
+    if (count <= 0) return;
+    eig_unscale_kernel<<<unsigned((count + 255) / 256), 256, 0, ctx->stream>>>(values, count, fac_dev);
+    ATK_LAUNCHED(ctx);
+}
+
+namespace {
+EigInfo sym_eig_top_r_impl(atk_ctx* ctx, const double* s_dev, int n, int r, double* values_dev, double* vectors_dev,
+                           bool psd, double tol, bool exact_sym);
+}
+
+// The inputs are the engine's own device buffers (a mode's Gram, the API's copy of the host
+// matrix): scaled in place when their range demands it (eig_scale).
 EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* values_dev, double* vectors_dev,
                       bool psd, double tol, bool exact_sym) {
+    DevBuf<double> fac(ctx, 2);
+    eig_scale(ctx, const_cast<double*>(s_dev), n, psd, fac.get());
+    EigInfo info = sym_eig_top_r_impl(ctx, s_dev, n, r, values_dev, vectors_dev, psd, tol, exact_sym);
+    eig_unscale_values(ctx, values_dev, r, fac.get());
+    return info;
+}
+
+namespace {
+EigInfo sym_eig_top_r_impl(atk_ctx* ctx, const double* s_dev, int n, int r, double* values_dev, double* vectors_dev,
+                           bool psd, double tol, bool exact_sym) {
     EigInfo info;
     cudaStream_t st = ctx->stream;
     if (n <= kTridiagMax && (ctx->eig_method == -1 || ctx->eig_method >= 2)) {
@@ -1054,6 +1126,7 @@ EigInfo sym_eig_top_r(atk_ctx* ctx, const double* s_dev, int n, int r, double* v
         fail(ATK_NO_CONVERGENCE, "symmetric eigendecomposition failed (ChFSI did not converge)");
     return info;
 }
+}  // namespace
 
 bool orthonormal_basis_cholqr(atk_ctx* ctx, const double* a, int m, int n, double* q) {
     if (n > kJacobiMax || m < n) return false;

@@ -62,7 +62,8 @@ __global__ void unfold_rows(const double* __restrict__ b, uint64_t P, uint64_t I
 // players >= I are byes).  Rotates rows (p, q) of M and columns (p, q) of W.
 __global__ void __launch_bounds__(kSvdThreads) jacobi_rows_round(double* __restrict__ m, uint64_t J,
                                                                   double* __restrict__ w, int I, int N, int t,
-                                                                  double tol, int* __restrict__ rotated) {
+                                                                  double tol, const double* __restrict__ negl,
+                                                                  int* __restrict__ rotated) {
     __shared__ double sh[kSvdThreads / 32];
     const int j = blockIdx.x;
     auto player = [&](int k) { return k == 0 ? 0 : (t + k - 1) % (N - 1) + 1; };
@@ -81,6 +82,10 @@ __global__ void __launch_bounds__(kSvdThreads) jacobi_rows_round(double* __restr
     a = block_sum(a, sh);
     b = block_sum(b, sh);
     c = block_sum(c, sh);
+    // a row at rounding level of the whole matrix (|row|^2 <= *negl) is converged as it is: rows
+    // that are exact multiples of one vector (a constant tensor's unfolding) would otherwise
+    // rotate forever, every rotation leaving an exactly parallel residue (dgesvj skips them too)
+    if (a <= *negl || b <= *negl) return;
     if (!(c != 0.0) || !(fabs(c) > tol * sqrt(a) * sqrt(b))) return;
     // rows made orthogonal: tan(2 theta) = 2c / (b - a), t = the small root
     const double zeta = (b - a) / (2.0 * c);
@@ -109,6 +114,16 @@ __global__ void __launch_bounds__(kSvdThreads) row_norms(const double* __restric
     for (uint64_t k = threadIdx.x; k < J; k += blockDim.x) s = fma(r[k], r[k], s);
     s = block_sum(s, sh);
     if (threadIdx.x == 0) out[blockIdx.x] = sqrt(s);
+}
+
+// negl = (16 eps)^2 sum_k |row k|^2 (= (16 eps ||M||_F)^2), one CTA
+__global__ void __launch_bounds__(kSvdThreads) negligible_threshold(const double* __restrict__ norms, int count,
+                                                                     double* __restrict__ negl) {
+    __shared__ double sh[kSvdThreads / 32];
+    double t = 0.0;
+    for (int k = threadIdx.x; k < count; k += blockDim.x) t = fma(norms[k], norms[k], t);
+    t = block_sum(t, sh);
+    if (threadIdx.x == 0) *negl = 256.0 * 2.220446049250313e-16 * 2.220446049250313e-16 * t;
 }
 
 // U(:, k) = sign_k W(:, perm[k]); sign_k makes the largest |entry| (first on
@@ -175,6 +190,63 @@ __global__ void scale_cols(const double* __restrict__ m, int I, const int* __res
         const int i = int(e % I), k = int(e / I);
         const double sg = sig[perm[k]];
         t[e] = sg > 0.0 ? m[uint64_t(perm[k]) * I + i] / sg : 0.0;
+    }
+}
+
+// Columns of T whose sigma is at rounding level (sigma^2 <= *negl: a rank-deficient tall unfolding)
+// carry no direction; replace each, in order, by the unit vector of e_j's component orthogonal to
+// the columns kept so far, j the row where that component is largest (>= (I - r) / I), twice
+// projected.  One CTA; the core slices they multiply are zero, so only orthonormality matters.
+__global__ void __launch_bounds__(kSvdThreads) complete_null_cols(double* __restrict__ t, int I, int r,
+                                                                   const int* __restrict__ perm,
+                                                                   const double* __restrict__ sig,
+                                                                   const double* __restrict__ negl) {
+    __shared__ double sh[kSvdThreads / 32];
+    __shared__ double sb[kSvdThreads / 32];
+    __shared__ int si[kSvdThreads / 32];
+    const double thr = *negl;
+    auto kept = [&](int c, int k) { return c < k || sig[perm[c]] * sig[perm[c]] > thr; };
+    for (int k = 0; k < r; ++k) {
+        if (sig[perm[k]] * sig[perm[k]] > thr) continue;
+        double* v = t + uint64_t(k) * I;
+        // pick j = argmax_j 1 - sum_{kept c} T(j, c)^2 (first on ties)
+        double best = -1.0;
+        int bj = 0;
+        for (int j = threadIdx.x; j < I; j += blockDim.x) {
+            double q = 1.0;
+            for (int c = 0; c < r; ++c)
+                if (c != k && kept(c, k)) q -= t[uint64_t(c) * I + j] * t[uint64_t(c) * I + j];
+            if (q > best) { best = q; bj = j; }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+            const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+            if (ob > best || (ob == best && oj < bj)) { best = ob; bj = oj; }
+        }
+        const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+        __syncthreads();
+        if (lane == 0) { sb[wp] = best; si[wp] = bj; }
+        __syncthreads();
+        if (threadIdx.x == 0)
+            for (int q = 1; q < int(blockDim.x >> 5); ++q)
+                if (sb[q] > sb[0] || (sb[q] == sb[0] && si[q] < si[0])) { sb[0] = sb[q]; si[0] = si[q]; }
+        __syncthreads();
+        const int j = si[0];
+        for (int i = threadIdx.x; i < I; i += blockDim.x) v[i] = i == j ? 1.0 : 0.0;
+        for (int pass = 0; pass < 2; ++pass)
+            for (int c = 0; c < r; ++c) {
+                if (c == k || !kept(c, k)) continue;
+                const double* u = t + uint64_t(c) * I;
+                double d = 0.0;
+                for (int i = threadIdx.x; i < I; i += blockDim.x) d = fma(u[i], v[i], d);
+                d = block_sum(d, sh);
+                for (int i = threadIdx.x; i < I; i += blockDim.x) v[i] = fma(-d, u[i], v[i]);
+            }
+        double n2 = 0.0;
+        for (int i = threadIdx.x; i < I; i += blockDim.x) n2 = fma(v[i], v[i], n2);
+        const double inv = 1.0 / sqrt(block_sum(n2, sh));
+        for (int i = threadIdx.x; i < I; i += blockDim.x) v[i] *= inv;
+        __syncthreads();
     }
 }
 
@@ -245,6 +317,8 @@ ModeOut svd_mode_explicit(atk_ctx* ctx, const atk_tensor* y, int mode, uint64_t 
         out.times.gram_ms = tm.stop_ms(kStageGram);
         record_gemm((long long)(I * I) * (long long)J);
         tm.start();
+        DevBuf<double> fac(ctx, 2);
+        eig_scale(ctx, S.get(), int(nrot), true, fac.get());  // huge / tiny data: the preconditioner's range
         if (nrot <= uint64_t(kTridiagMax))
             tridiag_eig(ctx, S.get(), int(nrot), int(nrot), int(nrot), vals.get(), W.get(), int(nrot));
         else
@@ -268,12 +342,18 @@ ModeOut svd_mode_explicit(atk_ctx* ctx, const atk_tensor* y, int mode, uint64_t 
     const int N = int(nrot + (nrot & 1));
     const double tol = 2.220446049250313e-16 * std::max(1.0, std::sqrt(double(len)));
     DevBuf<int> rot(ctx, 1);
+    DevBuf<double> negl(ctx, 1), norms0(ctx, nrot);
+    row_norms<<<unsigned(nrot), kSvdThreads, 0, st>>>(M.get(), len, norms0.get());
+    ATK_LAUNCHED(ctx);
+    negligible_threshold<<<1, kSvdThreads, 0, st>>>(norms0.get(), int(nrot), negl.get());
+    ATK_LAUNCHED(ctx);
     int sweeps = 0, last = -1;
     const int max_sweeps = 30;
     for (; sweeps < max_sweeps; ++sweeps) {
         ATK_CUDA(cudaMemsetAsync(rot.get(), 0, sizeof(int), st));
         for (int t = 0; t < N - 1; ++t) {
-            jacobi_rows_round<<<N / 2, kSvdThreads, 0, st>>>(M.get(), len, W.get(), int(nrot), N, t, tol, rot.get());
+            jacobi_rows_round<<<N / 2, kSvdThreads, 0, st>>>(M.get(), len, W.get(), int(nrot), N, t, tol, negl.get(),
+                                                             rot.get());
             ATK_LAUNCHED(ctx);
         }
         ATK_CUDA(cudaMemcpyAsync(&last, rot.get(), sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -300,6 +380,11 @@ ModeOut svd_mode_explicit(atk_ctx* ctx, const atk_tensor* y, int mode, uint64_t 
         DevBuf<int> ident(ctx, r);
         scale_cols<<<grid_for(ctx, I * r), 256, 0, st>>>(M.get(), int(I), dperm.get(), sig.get(), int(r), T.get());
         ATK_LAUNCHED(ctx);
+        if (hs[perm[r - 1]] * hs[perm[r - 1]] <= 256.0 * 4.93038065763132e-32 * std::accumulate(
+                hs.begin(), hs.end(), 0.0, [](double acc, double x) { return acc + x * x; }) * 2.0) {
+            complete_null_cols<<<1, kSvdThreads, 0, st>>>(T.get(), int(I), int(r), dperm.get(), sig.get(), negl.get());
+            ATK_LAUNCHED(ctx);
+        }
         iota_fill<<<1, 256, 0, st>>>(ident.get(), int(r));
         ATK_LAUNCHED(ctx);
         gather_left<<<unsigned(r), kSvdThreads, 0, st>>>(T.get(), int(I), ident.get(), U.get(), sign.get());

@@ -106,3 +106,21 @@ def test_svd_mode_tall_rank_deficient_matches_oracle(sctx, oracle):
     assert atucker.relative_error(x, res.decomposition, ctx=sctx) <= 1e-8
     for a, b in zip(res.decomposition.factors, ref.factors):
         assert principal_angle(a, b) <= 1e-8
+
+
+@pytest.mark.parametrize("rank", [0, 1, 4])
+def test_svd_mode_tall_rank_below_r_completes_basis(sctx, oracle, rank):
+    """A 40 x 12 (tall) unfolding of rank < r = 8: the columns whose sigma is at rounding level carry
+    no direction and are completed to an orthonormal basis (Eigen's JacobiSVD U is orthonormal for
+    zero singular values too, linalg.hpp:153-166); the rank-`rank` part matches the oracle."""
+    from paper_2010_10131_b200 import atucker
+
+    rng = np.random.default_rng(40 + rank)
+    y = np.asfortranarray(rng.standard_normal((40, rank)) @ rng.standard_normal((rank, 12)))
+    res = atucker.svd_mode_solver(y, 0, 8, ctx=sctx)
+    u = np.asarray(res.factor)
+    assert np.abs(u.T @ u - np.eye(8)).max() <= 1e-12
+    assert np.linalg.norm(y - u @ (u.T @ y)) <= 1e-12 * max(np.linalg.norm(y), 1e-300)
+    if rank:
+        ref = oracle.svd_mode_solver(y, 0, 8)
+        assert principal_angle(u[:, :rank], np.asarray(ref.factor)[:, :rank]) <= 1e-10
