@@ -48,6 +48,25 @@ void dev_free(atk_ctx* ctx, void* p) {
     if (p) cudaFreeAsync(p, ctx->stream);
 }
 
+ScratchScope::ScratchScope(atk_ctx* c, size_t bytes) : ctx(c) {
+    if (ctx->scratch_used) fail(ATK_ERROR, "internal: scratch scope already open");
+    if (bytes > ctx->scratch_bytes) {
+        if (ctx->scratch) dev_free(ctx, ctx->scratch);  // stream-ordered: earlier users finish first
+        ctx->scratch = nullptr;
+        ctx->scratch_bytes = 0;
+        ctx->scratch = static_cast<char*>(dev_alloc(ctx, bytes));
+        ctx->scratch_bytes = bytes;
+    }
+    ctx->scratch_used = 1;  // open (offsets start at 0; `used` is the next offset + 1)
+}
+
+void* ScratchScope::take(size_t bytes) {
+    const size_t off = ctx->scratch_used - 1, len = round(bytes);
+    if (off + len > ctx->scratch_bytes) fail(ATK_ERROR, "internal: scratch scope overrun");
+    ctx->scratch_used += len;
+    return ctx->scratch + off;
+}
+
 void* pinned_host(atk_ctx* ctx, size_t bytes) {
     if (bytes > ctx->pinned_bytes) {
         if (ctx->pinned) {
@@ -224,6 +243,9 @@ atk_status atk_ctx_destroy(atk_ctx* ctx) {
             cudaStreamDestroy(ctx->own_stream);
         }
         if (ctx->pinned) cudaFreeHost(ctx->pinned);
+        if (ctx->scratch) cudaFree(ctx->scratch);  // synchronous: every user has finished
+        for (cudaEvent_t e : ctx->ev)
+            if (e) cudaEventDestroy(e);
         delete ctx;
     });
 }

@@ -104,6 +104,10 @@ struct atk_ctx {
     cudaEvent_t ev[8] = {};
     void* pinned = nullptr;    // page-locked staging for the end-of-call factor download (grown on demand)
     size_t pinned_bytes = 0;
+    // device scratch kept across calls (atk::ScratchScope): the ChFSI block buffers, so a converged
+    // eigensolve returns without a burst of stream-ordered frees between its last check and the TTM
+    char* scratch = nullptr;
+    size_t scratch_bytes = 0, scratch_used = 0;
 };
 
 struct atk_tensor {
@@ -135,29 +139,49 @@ void* dev_alloc(atk_ctx* ctx, size_t bytes);
 void* pinned_host(atk_ctx* ctx, size_t bytes);
 void dev_free(atk_ctx* ctx, void* p);
 
+// ScratchScope: the context's persistent scratch, carved in 256-byte aligned pieces for the
+// scope's lifetime (one scope at a time; the context's stream orders every use).  Grown on
+// demand; released by atk_ctx_destroy.
+struct ScratchScope {
+    atk_ctx* ctx;
+    ScratchScope(atk_ctx* c, size_t bytes);
+    ~ScratchScope() { ctx->scratch_used = 0; }
+    ScratchScope(const ScratchScope&) = delete;
+    ScratchScope& operator=(const ScratchScope&) = delete;
+    void* take(size_t bytes);
+    static size_t round(size_t bytes) { return (bytes + 255) / 256 * 256; }
+};
+
 template <class T>
 struct DevBuf {
     atk_ctx* ctx = nullptr;
     T* p = nullptr;
     size_t n = 0;
+    bool own = true;
     DevBuf() = default;
     DevBuf(atk_ctx* c, size_t count) : ctx(c), n(count) {
         p = count ? static_cast<T*>(dev_alloc(c, count * sizeof(T))) : nullptr;
     }
+    // borrowed from a ScratchScope (not freed)
+    DevBuf(ScratchScope& s, size_t count) : ctx(s.ctx), n(count), own(false) {
+        p = count ? static_cast<T*>(s.take(count * sizeof(T))) : nullptr;
+    }
+    // a view of someone else's memory (not freed)
+    DevBuf(atk_ctx* c, T* borrowed, size_t count) : ctx(c), p(borrowed), n(count), own(false) {}
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
-    DevBuf(DevBuf&& o) noexcept : ctx(o.ctx), p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DevBuf(DevBuf&& o) noexcept : ctx(o.ctx), p(o.p), n(o.n), own(o.own) { o.p = nullptr; o.n = 0; }
     DevBuf& operator=(DevBuf&& o) noexcept {
         if (this != &o) {
             reset();
-            ctx = o.ctx; p = o.p; n = o.n;
+            ctx = o.ctx; p = o.p; n = o.n; own = o.own;
             o.p = nullptr; o.n = 0;
         }
         return *this;
     }
     ~DevBuf() { reset(); }
     void reset() {
-        if (p) dev_free(ctx, p);
+        if (p && own) dev_free(ctx, p);
         p = nullptr;
         n = 0;
     }

@@ -840,12 +840,20 @@ EigInfo sym_eig_top_r_impl(atk_ctx* ctx, const double* s_dev, int n, int r, doub
     const size_t nr = size_t(n) * r;
     // an exactly symmetric input (the engine's Grams are mirrored) is used in
     // place; anything else is copied and symmetrised first (linalg.hpp:104)
-    DevBuf<double> Sbuf(ctx, exact_sym ? 0 : nn), V(ctx, nk), W(ctx, nk), Ya(ctx, nk), Yb(ctx, nk), Yc(ctx, nk), T(ctx, kk), Z(ctx, kk),
-        theta(ctx, k), res(ctx, k), Vr(ctx, nk), Wr(ctx, nr);
+    // the block buffers come from the context's persistent scratch: no allocation or free
+    // sits between the converged check and the caller's next launch
+    auto rb = [](size_t count, size_t sz) { return ScratchScope::round(count * sz); };
+    ScratchScope scr(ctx, 7 * rb(nk, 8) + rb(nr, 8) + 5 * rb(kk, 8) + 4 * rb(k, 8) + 3 * rb(3, 4));
+    // the per-pass check reads theta (k), the residuals (r of k) and the CholeskyQR status words
+    // (3 ints) in ONE device-to-host copy: they sit back to back in `chk`
+    DevBuf<double> chk(scr, 2 * size_t(k) + 2);
+    DevBuf<double> Sbuf(ctx, exact_sym ? 0 : nn), V(scr, nk), W(scr, nk), Ya(scr, nk), Yb(scr, nk), Yc(scr, nk),
+        T(scr, kk), Z(scr, kk), theta(ctx, chk.get(), k), res(ctx, chk.get() + k, k), Vr(scr, nk), Wr(scr, nr);
     DevBuf<double> Sd(ctx, 0), Dm(ctx, 0);  // deflated copy of S, deflation term (allocated on first lock)
-    Ws ws{DevBuf<double>(ctx, kk), DevBuf<double>(ctx, kk), DevBuf<double>(ctx, k), DevBuf<double>(ctx, k),
-          DevBuf<double>(ctx, kk), DevBuf<double>(ctx, nk), DevBuf<int>(ctx, 1), DevBuf<int>(ctx, 3)};
-    DevBuf<int> sweeps(ctx, 1);
+    Ws ws{DevBuf<double>(scr, kk), DevBuf<double>(scr, kk), DevBuf<double>(scr, k), DevBuf<double>(scr, k),
+          DevBuf<double>(scr, kk), DevBuf<double>(scr, nk), DevBuf<int>(scr, 1),
+          DevBuf<int>(ctx, reinterpret_cast<int*>(chk.get() + 2 * size_t(k)), 3)};
+    DevBuf<int> sweeps(scr, 1);
     static const bool trace = std::getenv("ATK_TRACE") != nullptr;
     auto t_last = std::chrono::steady_clock::now();
     // ATK_TRACE=events: CUDA events instead of synchronising at every mark
@@ -921,19 +929,28 @@ EigInfo sym_eig_top_r_impl(atk_ctx* ctx, const double* s_dev, int n, int r, doub
     for (;; ++it) {
         ritz_residual<<<r, 256, 0, st>>>(Wr.get(), Vr.get(), theta.get(), n, r, res.get());
         ATK_LAUNCHED(ctx);
+        // the result as if this check passes, enqueued before the host waits on it (a later pass
+        // overwrites it): the GPU forms the output while the host reads the residuals
+        auto emit = [&] {
+            ATK_CUDA(cudaMemcpyAsync(values_dev, theta.get(), r * sizeof(double), cudaMemcpyDeviceToDevice, st));
+            ATK_CUDA(cudaMemcpyAsync(vectors_dev, Vr.get(), nr * sizeof(double), cudaMemcpyDeviceToDevice, st));
+            fix_signs(ctx, vectors_dev, n, r, n);
+        };
         int qinfo[3] = {0, 0, 0};
         // one host round trip through the context's page-locked staging (pageable destinations made
         // each copy a synchronous staged transfer: ~40 us of gaps per check)
         {
-            auto* pin = static_cast<uint8_t*>(pinned_host(ctx, (size_t(k) + r) * sizeof(double) + 64));
+            const size_t chk_bytes = (2 * size_t(k) + 2) * sizeof(double);
+            auto* pin = static_cast<uint8_t*>(pinned_host(ctx, chk_bytes));
             double* pth = reinterpret_cast<double*>(pin);
             double* pres = pth + k;
-            int* pq = reinterpret_cast<int*>(pres + r);
-            pq[0] = pq[1] = pq[2] = 0;
-            ATK_CUDA(cudaMemcpyAsync(pth, theta.get(), k * sizeof(double), cudaMemcpyDeviceToHost, st));
-            ATK_CUDA(cudaMemcpyAsync(pres, res.get(), r * sizeof(double), cudaMemcpyDeviceToHost, st));
-            if (qr_job.src) ATK_CUDA(cudaMemcpyAsync(pq, ws.info.get(), 3 * sizeof(int), cudaMemcpyDeviceToHost, st));
-            ATK_CUDA(cudaStreamSynchronize(st));
+            int* pq = reinterpret_cast<int*>(pth + 2 * size_t(k));
+            ATK_CUDA(cudaMemcpyAsync(pin, chk.get(), chk_bytes, cudaMemcpyDeviceToHost, st));
+            cudaEvent_t& got = ctx->ev[7];
+            if (!got) ATK_CUDA(cudaEventCreateWithFlags(&got, cudaEventDisableTiming));
+            ATK_CUDA(cudaEventRecord(got, st));
+            emit();
+            ATK_CUDA(cudaEventSynchronize(got));
             std::copy(pth, pth + k, hth.begin());
             std::copy(pres, pres + r, hres.begin());
             std::copy(pq, pq + 3, qinfo);
@@ -1116,9 +1133,7 @@ EigInfo sym_eig_top_r_impl(atk_ctx* ctx, const double* s_dev, int n, int r, doub
         }
         for (auto& x : evs) cudaEventDestroy(x.e);
     }
-    ATK_CUDA(cudaMemcpyAsync(values_dev, theta.get(), r * sizeof(double), cudaMemcpyDeviceToDevice, st));
-    ATK_CUDA(cudaMemcpyAsync(vectors_dev, Vr.get(), nr * sizeof(double), cudaMemcpyDeviceToDevice, st));
-    fix_signs(ctx, vectors_dev, n, r, n);
+    // values / vectors: already enqueued by the last check (emit above)
     info.method = 1;
     info.iterations = it;
     info.residual = scale > 0 ? worst / scale : 0.0;
