@@ -13,10 +13,11 @@ value : device-resident throughput (input already in HBM, > L2 so no flush
         needed), CUDA events on the engine stream, max over ranks.
 e2e   : the same through the host-buffer C-ABI entry atk_sthosvd_host: every
         step copies the input from pinned host memory and the core back.
-roofline : dominant kernel = the mode-1 Gram (gram_tf32_2cta_kernel K-launches
-        + the split-K reduction), I^2 J flops per launch / its event-timed
-        duration, against the measured cuBLAS tf32 burst rate
-        (profiles/peaks_r2.json; the sustained fraction is reported too).
+roofline : the step's dominant stage (dominant_roofline).  C5: the mode-1 Gram
+        (gram_tf32_2cta_kernel K-launches + the split-K reduction), I^2 J flops
+        per launch / its event-timed duration, against the measured cuBLAS tf32
+        burst rate (profiles/peaks_r2.json; the sustained fraction too); fp64
+        Grams against the measured DGEMM rate; TTM / ALS stages against HBM.
 cpu_baseline : the CPU oracle (oracle/, reference port) on a bounded sample of
         the same workload (the leading slabs of the last mode, ~15 s), all host
         threads, with its per-stage split and the host's lscpu model / RAM.
@@ -90,6 +91,65 @@ def peaks():
     else:  # derived: tf32 = half the bf16 rate, fp64 = B200 DMMA spec
         out.update(tf32=out["bf16"] / 2, tf32_sus=out["bf16_sus"] / 2, fp64=40.0, fp64_sus=40.0,
                    tf_src="derived (tf32 = bf16 / 2, fp64 = 40 TF/s spec)")
+    return out
+
+
+def dominant_roofline(cfg, gdims, reports, fl, pk):
+    """Roofline of the step's dominant kernel: the stage (Gram, TTM or ALS of one mode) with the
+    largest device time.  Gram: tensor-bound (tf32 tcgen05 for fp32, DMMA for fp64); TTM and
+    ALS passes: HBM-bound (bytes of the tensor read plus the shrunk tensor written).  `traffic`
+    is the ncu DRAM count of profiles/gram_traffic.json, given only for the C5-shaped Gram it
+    was captured on."""
+    f32 = cfg["dtype"] == "f32"
+    es = 4 if f32 else 8
+    best = None
+    for rp, f in zip(reports, fl):
+        t = rp.times
+        before, after = int(np.prod(rp.dims_before)), int(np.prod(rp.dims_after))
+        for stage, ms in (("gram", t.gram_ms), ("ttm", t.ttm_ms), ("als", t.als_ms)):
+            if ms > 0 and (best is None or ms > best[2]):
+                best = (rp, stage, ms, f, before, after)
+    if best is None:
+        return None
+    rp, stage, ms, f, before, after = best
+    n = rp.mode
+    if stage == "gram":
+        peak = pk["tf32"] if f32 else pk["fp64"]
+        achieved = f.get("gram", 0) / (ms * 1e-3) / 1e12
+        i = int(rp.dims_before[n])
+        kern = (("gram_tf32_2cta_kernel (+gram2_reduce)" if i >= 256 else "gram_tf32_kernel") if f32
+                else ("syrk_panel_kernel (DMMA, + syrk_reduce_kernel)" if n in (0, len(gdims) - 1)
+                      else "ttt DMMA (dgemm_tile)"))
+        out = {"kernel": f"{kern}, mode {n + 1} (n = {n}) Gram", "bound": "tensor", "achieved": achieved,
+               "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+               "algorithmic_flops_per_launch": f.get("gram", 0),
+               "algorithmic_bytes_per_launch": es * before}
+        if f32:
+            out.update(peak_sustained=pk["tf32_sus"], frac_sustained=achieved / pk["tf32_sus"],
+                       peak_note=f"tf32 burst = cuBLAS tf32 8192^3 best single launch, {pk['tf_src']}; "
+                                 "peak_sustained = 4 s back to back (cuBLAS at ~1.1 GHz under the power cap)")
+        else:
+            out.update(peak_sustained=pk["fp64_sus"], frac_sustained=achieved / pk["fp64_sus"],
+                       peak_note=f"fp64 = DGEMM 8192^3 best single launch, {pk['tf_src']}")
+    else:
+        nbytes = es * (before + after) if stage == "ttm" else None
+        if stage == "als":  # the fp32 route of the bench configs: ALS on the mode's Gram (option
+            # als_gram), i.e. one Gram pass and one TTM pass over Y; the I x I iterations are small
+            nbytes = es * (2 * before + after)
+        achieved = nbytes / (ms * 1e-3) / 1e9
+        kern = {"ttm": "ttm_tf32_kernel" if f32 else "dgemm_ttm / ttm DMMA", "als": "ALS on the mode's Gram (Gram + TTM passes)"}[stage]
+        out = {"kernel": f"{kern}, mode {n + 1} (n = {n}) {stage.upper()}", "bound": "hbm",
+               "achieved": achieved, "peak": pk["hbm"], "unit": "GB/s", "frac": achieved / pk["hbm"],
+               "algorithmic_bytes_per_launch": nbytes}
+    out["stage_ms"] = ms
+    traffic = None
+    prof = ROOT / "profiles" / "gram_traffic.json"
+    c5_gram = stage == "gram" and f32 and n == 0 and list(gdims) == [2048, 2048, 2048]
+    if c5_gram and prof.exists():
+        traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+        out["traffic_note"] = ("dram read+write of the same logical Gram (16 K-launches + reduce), "
+                               "ncu --metrics, profiles/gram_traffic.json")
+    out["traffic"] = traffic
     return out
 
 
@@ -503,24 +563,7 @@ def main():
     # under the power cap) and the Gram, which holds ~1.9 GHz, runs above it,
     # so the sustained figure is reported beside it, not used as a ceiling.
     tf32_peak = pk["tf32"]
-    g0 = reports[-1][0]
-    gram_flops = fl[0].get("gram", 0)
-    achieved = gram_flops / (g0.times.gram_ms * 1e-3) / 1e12 if g0.times.gram_ms > 0 else None
-    traffic = None
-    prof = ROOT / "profiles" / "gram_traffic.json"
-    if prof.exists():
-        traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
-    roofline = {"kernel": "gram_tf32_2cta_kernel (+gram2_reduce), mode 1 (n = 0)",
-                "bound": "tensor", "achieved": achieved, "peak": tf32_peak, "unit": "TFLOP/s",
-                "frac": (achieved / tf32_peak) if achieved else None, "traffic": traffic,
-                "peak_sustained": pk["tf32_sus"],
-                "frac_sustained": (achieved / pk["tf32_sus"]) if achieved else None,
-                "peak_note": f"tf32 burst = cuBLAS tf32 8192^3 best single launch, {pk['tf_src']}; "
-                             f"peak_sustained = 4 s back to back (cuBLAS at ~1.1 GHz under the power cap)",
-                "algorithmic_flops_per_launch": gram_flops,
-                "algorithmic_bytes_per_launch": 4 * int(np.prod(gdims)),
-                "traffic_note": "dram read+write of the same logical Gram (16 K-launches + reduce), "
-                                "ncu --metrics, profiles/gram_traffic.json"}
+    roofline = dominant_roofline(cfg, gdims, reports[-1], fl, pk)
 
     # SURVEY 8(d) pipeline fraction: sum over stages of max(F / P, B / BW) against
     # the measured step (eig excluded from the bound, included in the step)
