@@ -1189,6 +1189,23 @@ constexpr int kTileLd = 33, kTileDbl = 32 * kTileLd;
 
 __device__ __forceinline__ int tile_index(int I, int J) { return I * (I + 1) / 2 + J; }
 
+// NT = 7 covers 192 < n <= 200 (C1's n = 200): its last tile row holds at most 8 rows, stored
+// with a 9-row leading dimension (28 full tiles would need 236 KB of shared memory, this 211 KB)
+static_assert(kTridiagMax <= 6 * 32 + 8, "TileShape<7>: the short tile row holds 8 rows");
+template <int NT>
+struct TileShape {
+    static constexpr bool SHORT = NT == 7;
+    static constexpr int RP = 8, LDL = 9;  // rows of the short tile row, its leading dimension
+    static constexpr int NTILES = NT * (NT + 1) / 2;
+    static constexpr int NFULL = SHORT ? (NT - 1) * NT / 2 : NTILES;  // tiles stored 32 x 33
+    static constexpr int TDBL = NFULL * kTileDbl + (SHORT ? NT * 32 * LDL : 0);
+    __device__ static __forceinline__ bool last(int I) { return SHORT && I == NT - 1; }
+    __device__ static __forceinline__ int off(int I, int J) {
+        return last(I) ? NFULL * kTileDbl + J * 32 * LDL : tile_index(I, J) * kTileDbl;
+    }
+    __device__ static __forceinline__ int ld(int I) { return last(I) ? LDL : kTileLd; }
+};
+
 constexpr int kTileThreads = 256;  // 8 warps: 255 registers/thread (at 512 the CTA-id read was rematerialised per step)
 
 template <int NT>
@@ -1196,7 +1213,8 @@ __global__ void __launch_bounds__(kTileThreads, 1)
     trd_tile_kernel(const double* __restrict__ a, int n, int lda, double* __restrict__ hh, double* __restrict__ d,
                     double* __restrict__ e, double* __restrict__ tau_out, double* __restrict__ scal_out,
                     long long* __restrict__ prof) {
-    constexpr int NTILES = NT * (NT + 1) / 2, NR = 32 * NT, NWARP = kTileThreads / 32;
+    using TS = TileShape<NT>;
+    constexpr int NTILES = TS::NTILES, NR = 32 * NT, NWARP = kTileThreads / 32;
     long long t_mark = clock64(), t_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // ATK_TRD_PROFILE
     auto lap = [&](int ph) {
         if (prof) {
@@ -1206,8 +1224,8 @@ __global__ void __launch_bounds__(kTileThreads, 1)
         }
     };
     extern __shared__ double sm[];
-    double* T = sm;                       // NTILES x (32 x 33)
-    double* crow = T + NTILES * kTileDbl; // NTILES x 32: row parts
+    double* T = sm;                       // NTILES x (32 x 33) (TileShape: a short last tile row)
+    double* crow = T + TS::TDBL;          // NTILES x 32: row parts
     double* ccol = crow + NTILES * 32;    // NTILES x 32: column parts
     double* v = ccol + NTILES * 32;       // NR
     double* pb = v + NR;                  // NR
@@ -1217,10 +1235,10 @@ __global__ void __launch_bounds__(kTileThreads, 1)
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     auto at = [&](int i, int j) -> double& {  // i >= j or same diagonal tile
         const int I = i >> 5, J = j >> 5;
-        return T[tile_index(I, J) * kTileDbl + (i & 31) + kTileLd * (j & 31)];
+        return T[TS::off(I, J) + (i & 31) + TS::ld(I) * (j & 31)];
     };
     // load: symmetrised, zero padding
-    for (int q = tid; q < NTILES * kTileDbl; q += kTileThreads) T[q] = 0.0;
+    for (int q = tid; q < TS::TDBL; q += kTileThreads) T[q] = 0.0;
     __syncthreads();
     for (int q = tid; q < n * n; q += kTileThreads) {
         const int i = q % n, j = q / n;
@@ -1267,7 +1285,7 @@ __global__ void __launch_bounds__(kTileThreads, 1)
             int J = J0, rem = q;
             while (rem >= NT - J) { rem -= NT - J; ++J; }
             const int I = J + rem;
-            const double* B = T + tile_index(I, J) * kTileDbl;
+            const double* B = T + TS::off(I, J);
             const double* vJ = v + J * 32;
             const double* vI = v + I * 32;
             // 8 independent accumulators per walk: the fp64 FMA chains, not the loads,
@@ -1276,12 +1294,15 @@ __global__ void __launch_bounds__(kTileThreads, 1)
 #pragma unroll
             for (int u = 0; u < 8; ++u) ra[u] = ca[u] = 0.0;
             const bool off = I != J;
+            const bool lst = TS::last(I);
+            const int ld = TS::ld(I), rows = lst ? TS::RP : 32;  // stored rows of this tile
+            const bool lv = lane < rows;
 #pragma unroll
             for (int c = 0; c < 32; c += 8)
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
-                    ra[u] = fma(B[lane + kTileLd * (c + u)], vJ[c + u], ra[u]);
-                    if (off) ca[u] = fma(B[c + u + kTileLd * lane], vI[c + u], ca[u]);
+                    if (lv) ra[u] = fma(B[lane + ld * (c + u)], vJ[c + u], ra[u]);
+                    if (off && c < rows) ca[u] = fma(B[c + u + ld * lane], vI[c + u], ca[u]);
                 }
             crow[tile_index(I, J) * 32 + lane] = ((ra[0] + ra[1]) + (ra[2] + ra[3])) + ((ra[4] + ra[5]) + (ra[6] + ra[7]));
             if (off)
@@ -1314,7 +1335,9 @@ __global__ void __launch_bounds__(kTileThreads, 1)
             int J = J0, rem = q;
             while (rem >= NT - J) { rem -= NT - J; ++J; }
             const int I = J + rem;
-            double* B = T + tile_index(I, J) * kTileDbl;
+            double* B = T + TS::off(I, J);
+            const int ld = TS::ld(I);
+            if (TS::last(I) && lane >= TS::RP) continue;  // rows the short tile row does not store
             const double vr = v[I * 32 + lane];
             const double wr = fma(-K, vr, pb[I * 32 + lane]);
             const double* vJ = v + J * 32;
@@ -1325,14 +1348,14 @@ __global__ void __launch_bounds__(kTileThreads, 1)
                 double xs[8], vc[8], pc[8];
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
-                    xs[u] = B[lane + kTileLd * (c + u)];
+                    xs[u] = B[lane + ld * (c + u)];
                     vc[u] = vJ[c + u];
                     pc[u] = pJ[c + u];
                 }
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
                     const double wc = fma(-K, vc[u], pc[u]);
-                    B[lane + kTileLd * (c + u)] = fma(-vr, wc, fma(-wr, vc[u], xs[u]));
+                    B[lane + ld * (c + u)] = fma(-vr, wc, fma(-wr, vc[u], xs[u]));
                 }
             }
         }
@@ -1360,7 +1383,8 @@ __global__ void __launch_bounds__(kTileThreads, 1)
 
 size_t trd_tile_smem(int nt) {
     const int ntiles = nt * (nt + 1) / 2;
-    return (size_t(ntiles) * kTileDbl + size_t(ntiles) * 64 + 64 * size_t(nt) + 2) * sizeof(double);
+    const size_t tdbl = nt == 7 ? size_t(TileShape<7>::TDBL) : size_t(ntiles) * kTileDbl;
+    return (tdbl + size_t(ntiles) * 64 + 64 * size_t(nt) + 2) * sizeof(double);
 }
 
 // n <= 32 NW (NW <= 4): the same reduction (dsytd2 conventions, same outputs as
@@ -1601,14 +1625,15 @@ void trd_backtr(atk_ctx* ctx, bool trd, const double* a, int n, int lda, double*
         }
         return;
     }
-    if (trd && ctx->trd_tiles && n <= 192) {  // tile variant (fits shared memory up to 6 x 6 tiles)
+    if (trd && ctx->trd_tiles && n <= kTridiagMax) {  // tile variant (7 tile rows: a short last one)
         switch ((n + 31) / 32) {
             case 1: launch_trd_tile<1>(ctx, a, n, lda, hh, d, e, tau, scal); return;
             case 2: launch_trd_tile<2>(ctx, a, n, lda, hh, d, e, tau, scal); return;
             case 3: launch_trd_tile<3>(ctx, a, n, lda, hh, d, e, tau, scal); return;
             case 4: launch_trd_tile<4>(ctx, a, n, lda, hh, d, e, tau, scal); return;
             case 5: launch_trd_tile<5>(ctx, a, n, lda, hh, d, e, tau, scal); return;
-            default: launch_trd_tile<6>(ctx, a, n, lda, hh, d, e, tau, scal); return;
+            case 6: launch_trd_tile<6>(ctx, a, n, lda, hh, d, e, tau, scal); return;
+            default: launch_trd_tile<7>(ctx, a, n, lda, hh, d, e, tau, scal); return;
         }
     }
     switch ((n + 31) / 32) {

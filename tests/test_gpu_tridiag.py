@@ -55,7 +55,7 @@ def _check(s, r, res):
             assert principal_angle(v[:, j:j + 1], q[:, j:j + 1]) <= 1e-9
 
 
-@pytest.mark.parametrize("n", [1, 2, 3, 7, 31, 32, 33, 64, 96, 127, 160, 200])
+@pytest.mark.parametrize("n", [1, 2, 3, 7, 31, 32, 33, 64, 96, 127, 160, 192, 193, 197, 200])
 def test_random_symmetric(tctx, n):
     from paper_2010_10131_b200 import atucker
 
@@ -75,6 +75,25 @@ def test_flat_gram(tctx, n):
     a = rng.standard_normal((n, 40 * n))
     s = a @ a.T
     _check(s, n // 2, atucker.sym_eig_top_r(s, n // 2, ctx=tctx))
+
+
+@pytest.mark.parametrize("n", [193, 200])
+def test_short_tile_row_matches_column_kernel(tctx, n):
+    """192 < n <= 200 runs the tile reduction with a short 7th tile row (trd_tile_kernel<7>); the
+    column-slot kernel (option trd_tiles 0) is an independent implementation of the same dsytd2
+    reduction: same eigenvalues, same subspaces, on a graded spectrum."""
+    from paper_2010_10131_b200 import atucker
+
+    s = _spectrum_matrix(n, np.logspace(4, -4, n), 7)
+    r = n // 3
+    tiles = atucker.sym_eig_top_r(s, r, ctx=tctx)
+    ctx2 = atucker.Context(0)
+    ctx2.set_option("trd_tiles", 0)
+    cols = atucker.sym_eig_top_r(s, r, ctx=ctx2)
+    np.testing.assert_allclose(tiles.values, cols.values, rtol=1e-12, atol=1e-12 * abs(cols.values[0]))
+    _check(s, r, tiles)
+    for j in range(r):
+        assert principal_angle(tiles.vectors[:, j:j + 1], cols.vectors[:, j:j + 1]) <= 1e-9
 
 
 def test_all_wanted_flat_spectrum(tctx):
