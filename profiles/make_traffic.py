@@ -40,4 +40,5 @@ def main(src, dst, n_gram=16):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else "profiles/gram_traffic.json")
+    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else "profiles/gram_traffic.json",
+         int(sys.argv[3]) if len(sys.argv) > 3 else 16)

@@ -11,6 +11,10 @@ name = sys.argv[1] if len(sys.argv) > 1 else "c5"
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 cfg = bench.CONFIGS[name]
 ctx = atucker.Context(0)
+import os  # noqa: E402
+for kv in filter(None, os.environ.get("ATK_OPTS", "").split(",")):  # e.g. ATK_OPTS=gram_launch_kb=2048
+    k, v = kv.split("=")
+    ctx.set_option(k, float(v))
 x = bench.make_input(atucker, cfg, bench.SEEDS[name], ctx)
 for _ in range(steps):
     res = atucker.sthosvd(x, cfg["ranks"], Strategy.parse(cfg["strategy"]), ctx=ctx)
