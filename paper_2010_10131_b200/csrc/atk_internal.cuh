@@ -98,7 +98,9 @@ struct atk_ctx {
     int ttm_split = 1;         // option "ttm_split": TTM factor as tf32 hi + lo (two MMAs per K step)
     int gram_wide = 1;         // option "gram_wide": 2-CTA Gram units of two tiles sharing the A operand
     int gram_lockstep = 0;     // option "gram_lockstep": bound CTA drift so X streams from HBM once
-    int gram_launch_kb = 4096; // option "gram_launch_kb": 2-CTA Gram K-blocks per unit per launch (0 = one launch)
+    int gram_launch_kb = 1024; // option "gram_launch_kb": 2-CTA Gram K-blocks per unit per launch (0 = one launch);
+                               // C5 mode 0, ncu DRAM per Gram: 4096 -> 48.4 GB, 2048 -> 38.5, 1024 -> 36.8 (1.07x
+                               // the 34.4 GB of X), 512 -> 39.2; step time equal within noise (A/B, 3 x 10 steps)
                                // (off: lockstep hot-spots L2 slices, 45 ms vs 34 ms at C5, r1)
     atk::Comm* comm = nullptr;
     cudaEvent_t ev[8] = {};

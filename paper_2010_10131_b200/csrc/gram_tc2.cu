@@ -12,7 +12,7 @@
 // reads ~ 192 B/clk/SM > 128 B/clk/SM for 1-CTA tiles).
 //
 // K is cut into several launches (option "gram_launch_kb": K-blocks per unit
-// per launch, default 4096) that accumulate into the same fp64 partial tiles:
+// per launch, default 1024) that accumulate into the same fp32 partial tiles:
 // every launch boundary re-aligns the pairs, so their K fronts cannot drift
 // apart and each K-block of X is fetched from HBM ~once and served to the
 // other tiles from L2.  Measured at I = 2048 (profiles/gram_probe.cu): one

@@ -2,8 +2,8 @@
 
 Input: ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum
        -k regex:"gram_tf32_2cta|gram2_reduce" --csv (profiles/gpu_round.sh part `traffic`).
-The mode-1 Gram is the first 16 gram_tf32_2cta_kernel K-launches (4096 K-blocks
-per unit each) plus the first gram2_reduce: bench.py's roofline treats that
+The mode-1 Gram is every gram_tf32_2cta_kernel K-launch before the first
+gram2_reduce (64 at the default 1024 K-blocks per unit and launch) plus that reduce: bench.py's roofline treats that
 logical Gram (I^2 J flops) as one launch, so its traffic is their sum."""
 import csv
 import json
@@ -12,7 +12,7 @@ import sys
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3}
 
 
-def main(src, dst, n_gram=16):
+def main(src, dst, n_gram=0):
     rows, hdr = [], None
     for r in csv.reader(open(src)):
         if r and r[0] == "ID":
@@ -26,8 +26,12 @@ def main(src, dst, n_gram=16):
         launches.setdefault(key, {})[d["Metric Name"]] = float(d["Metric Value"].replace(",", "")) * UNIT.get(
             d["Metric Unit"], 1)
     order = sorted(launches, key=lambda k: int(k[0]))
-    gram = [launches[k] for k in order if "gram_tf32_2cta" in k[1]][:n_gram]
-    red = [launches[k] for k in order if "gram2_reduce" in k[1]][:1]
+    # the mode-1 Gram = every K-launch before the first reduction (n_gram <= 0), or the first n_gram
+    first_red = next(i for i, k in enumerate(order) if "gram2_reduce" in k[1])
+    gram = [launches[k] for k in order[:first_red] if "gram_tf32_2cta" in k[1]]
+    if n_gram > 0:
+        gram = gram[:n_gram]
+    red = [launches[order[first_red]]]
     sel = gram + red
     rd = sum(x["dram__bytes_read.sum"] for x in sel)
     wr = sum(x["dram__bytes_write.sum"] for x in sel)
@@ -41,4 +45,4 @@ def main(src, dst, n_gram=16):
 
 if __name__ == "__main__":
     main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else "profiles/gram_traffic.json",
-         int(sys.argv[3]) if len(sys.argv) > 3 else 16)
+         int(sys.argv[3]) if len(sys.argv) > 3 else 0)
