@@ -147,7 +147,7 @@ def dominant_roofline(cfg, gdims, reports, fl, pk):
     c5_gram = stage == "gram" and f32 and n == 0 and list(gdims) == [2048, 2048, 2048]
     if c5_gram and prof.exists():
         traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
-        out["traffic_note"] = ("dram read+write of the same logical Gram (16 K-launches + reduce), "
+        out["traffic_note"] = ("dram read+write of the same logical Gram (all its K-launches + reduce), "
                                "ncu --metrics, profiles/gram_traffic.json")
     out["traffic"] = traffic
     return out
