@@ -197,3 +197,22 @@ def test_tc_gram_small_ring_matches_general(dims, mode):
     np.testing.assert_array_equal(out[0], out[1])
     ref = gram_np(xd.to_numpy().astype(np.float64), mode)
     assert np.abs(out[1] - ref).max() / np.abs(ref).max() <= 4e-3
+
+
+@pytest.mark.parametrize("dims,r", [
+    ((128, 64, 33), 16), ((200, 40, 41), 20), ((2, 7, 5), 1), ((256, 9, 3), 32), ((130, 31), 8),
+    ((96, 1000), 24), ((127, 50, 2), 8),
+])
+def test_fp64_first_mode_ttm(dims, r):
+    """fp64 mode-0 TTM (dgemm_ttm: the pipelined DMMA GEMM on the raw tensor, C^T stored): against
+    numpy in fp64, odd and even I, R from 1 to 32, J not a multiple of the tile."""
+    from paper_2010_10131_b200 import atucker
+
+    ctx = atucker.Context.default(0)
+    xd = atucker.DeviceTensor.uniform(list(dims), 29, np.float64)
+    x = xd.to_numpy()
+    u = np.random.default_rng(7).standard_normal((r, dims[0]))
+    y = atucker.ttm(xd, u, 0, ctx=ctx).to_numpy()
+    ref = np.tensordot(u, x, axes=([1], [0]))
+    assert y.shape == ref.shape
+    np.testing.assert_allclose(y, ref, rtol=0, atol=1e-13 * np.abs(ref).max())
