@@ -130,7 +130,8 @@ const char* atk_version(void);
 const char* atk_last_error(void);
 atk_status atk_ctx_create(int device, atk_ctx** out);
 atk_status atk_ctx_destroy(atk_ctx* ctx);
-/* Run on a caller-provided cudaStream_t (0 = the context's own stream). */
+/* Run on a caller-provided cudaStream_t (0 = the context's own stream).  Switching streams
+   synchronises the previous one (the context's scratch is ordered by its stream). */
 atk_status atk_ctx_set_stream(atk_ctx* ctx, void* cuda_stream);
 atk_status atk_ctx_synchronize(atk_ctx* ctx);
 /* Kernels this context launched so far (for bench accounting). */

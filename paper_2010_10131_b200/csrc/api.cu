@@ -51,7 +51,7 @@ void dev_free(atk_ctx* ctx, void* p) {
 ScratchScope::ScratchScope(atk_ctx* c, size_t bytes) : ctx(c) {
     if (ctx->scratch_used) fail(ATK_ERROR, "internal: scratch scope already open");
     if (bytes > ctx->scratch_bytes) {
-        if (ctx->scratch) dev_free(ctx, ctx->scratch);  // stream-ordered: earlier users finish first
+        if (ctx->scratch) dev_free(ctx, ctx->scratch);  // stream-ordered: earlier users (same stream) finish first
         ctx->scratch = nullptr;
         ctx->scratch_bytes = 0;
         ctx->scratch = static_cast<char*>(dev_alloc(ctx, bytes));
@@ -253,7 +253,11 @@ atk_status atk_ctx_destroy(atk_ctx* ctx) {
 atk_status atk_ctx_set_stream(atk_ctx* ctx, void* s) {
     return guard([&] {
         bind(ctx);
-        ctx->stream = s ? static_cast<cudaStream_t>(s) : ctx->own_stream;
+        cudaStream_t next = s ? static_cast<cudaStream_t>(s) : ctx->own_stream;
+        // the context's persistent scratch (ScratchScope) is ordered by its stream: work still
+        // queued on the old stream finishes before the new one can reuse it
+        if (next != ctx->stream) ATK_CUDA(cudaStreamSynchronize(ctx->stream));
+        ctx->stream = next;
     });
 }
 

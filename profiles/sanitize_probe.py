@@ -7,7 +7,7 @@ Cases (argv[1]):
   als     fp32 256 x 64 x 64, ALS mode 0: als_pass_kernel (one-pass ALS) + als_reduce_rows, chol_reg
   chfsi   n = 400 flat PSD Gram: ChFSI (cheb_resident_kernel / cheb_filter_kernel, lanczos_tiles when
           indefinite), CholeskyQR chol_inv, trd_small, bisect / invit / backtr
-  trd     n = 120 and 190: trd_small_kernel, trd_tile_kernel, trd_kernel
+  trd     n = 120, 190, 193, 200: trd_small_kernel, trd_tile_kernel (193 / 200: the short 7th tile row)
   big     n = 320 dense: the grid-wide Householder reduction (trd_big.cu) + its cluster tail
   svd     fp64 SVD mode on wide and tall unfoldings (svd.cu)
   small   fp32 single-tile Gram ring (mode 0 and 16-B panels), gram_tc.cu
@@ -45,7 +45,7 @@ elif case == "als":
     x = atucker.DeviceTensor.uniform([256, 64, 64], 5, np.float32, ctx=ctx)
     res = atucker.sthosvd(x, [16, 16, 16], Strategy.manual([SolverKind.Als, SolverKind.Eig, SolverKind.Eig]),
                           atucker.AlsOptions(num_iters=2, seed=3), ctx=ctx)
-elif case == "chfsi":
+elif case == "chfsi":  # (also the persistent scratch and the early result enqueue)
     ctx.set_option("eig_assume_psd", 1.0)
     ctx.set_option("eig_method", 1)
     p = atucker.sym_eig_top_r(sym(400, "flat"), 24, ctx=ctx)
@@ -53,7 +53,7 @@ elif case == "chfsi":
     p = atucker.sym_eig_top_r(sym(400, "lin") - 100.0 * np.eye(400), 24, ctx=ctx)
     ctx.set_option("eig_method", -1)
 elif case == "trd":
-    for n in (120, 190):
+    for n in (120, 190, 193, 200):  # 193 / 200: the tile reduction's short 7th tile row
         p = atucker.sym_eig_top_r(sym(n, "lin"), 16, ctx=ctx)
 elif case == "big":
     ctx.set_option("eig_method", 3)
