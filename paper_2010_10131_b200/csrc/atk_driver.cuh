@@ -66,6 +66,10 @@ void contract_ttt(atk_ctx* ctx, const atk_tensor* x, const atk_tensor* y, int mo
 // als_tc.cu — one ALS iteration's contractions in one pass over Y (mode 0, fp32, R <= 32)
 // Shape gate of the one-pass kernel (I x J unfolding, rank R, num_sms CTAs), shared with the
 // roofline selector (api.cu) so the selector prices exactly the schedule that will run.
+// fp32 tensors below this many elements take the fp32 CUDA-core contractions instead of tcgen05's
+// tf32 operands: at that size every path is launch-bound, and full fp32 keeps tiny slowly-converging
+// ALS modes within the 1e-4 parity bar (sweep seed 5339: 22 x 10 x 7, 1.3e-4 on tf32, 2.5e-8 fp32)
+constexpr uint64_t kTcMinElems = 8192;
 inline bool als_fused_shape_ok(uint64_t I, uint64_t R, uint64_t J, int num_sms) {
     constexpr uint64_t kNB = 32, kJT = 128;  // als_tc.cu NB / JT
     if (R < 1 || R > kNB || I % 128 != 0 || I > 1024 || I < 128) return false;

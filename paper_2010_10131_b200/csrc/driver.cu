@@ -19,7 +19,7 @@ void contract_ttt(atk_ctx* ctx, const atk_tensor* x, const atk_tensor* y, int mo
     const Split s = loop_split(x->dims, x->order, mode);
     const uint64_t R = y->dims[mode];
     if (s.P * s.O == 0 || s.I == 0 || R == 0) return;
-    if (!ctx->force_simt && tc_ttt_supported(ctx, x, y, mode, sym)) {
+    if (!ctx->force_simt && x->numel() >= kTcMinElems && tc_ttt_supported(ctx, x, y, mode, sym)) {
         tc_ttt(ctx, x, y, mode, z_dev, sym);
         return;
     }
@@ -53,7 +53,7 @@ atk_tensor* contract_ttm(atk_ctx* ctx, const atk_tensor* x, const double* u_dev,
     od[mode] = R;
     atk_tensor* y = new_tensor(ctx, x->dtype, x->order, od);
     const Split s = loop_split(x->dims, x->order, mode);
-    if (!ctx->force_simt && tc_ttm_supported(ctx, x, R, mode)) {
+    if (!ctx->force_simt && x->numel() >= kTcMinElems && tc_ttm_supported(ctx, x, R, mode)) {
         tc_ttm(ctx, x, u_dev, R, mode, y);
     } else {
         ttm_simt(ctx, x->data, x->dtype, s, u_dev, R, y->data);
@@ -198,7 +198,7 @@ bool als_gram_route(atk_ctx* ctx, const atk_tensor* y, int mode, uint64_t r, int
     // same schedule (its collectives); the per-iteration allreduce path stays
     if (ctx->comm && !ctx->replicated) return false;
     const uint64_t I = y->dims[mode], J = j_of(y, mode);
-    if (I > 4096 || r > I || !tc_ttt_supported(ctx, y, y, mode, true)) return false;
+    if (I > 4096 || r > I || y->numel() < kTcMinElems || !tc_ttt_supported(ctx, y, y, mode, true)) return false;
     atk_roofline_params p;
     atk_roofline_params_default(&p, ATK_F32, iters);
     const double bw = p.hbm_gbs * 1e9, P = p.tf32_tflops * 1e12;

@@ -90,3 +90,10 @@ def test_sthosvd_sweep_vs_oracle(seed, big, oracle):
     # reconstructible input (er ~ 0) keeps a reconstruction floor of a few 2^-12
     floor = 0.0 if dtype == np.float64 else 4 * 2.0 ** -12
     assert abs(e - er) <= tol * max(1.0, er) + floor, (dims, ranks, kinds, dtype, e, er)
+
+
+def test_sweep_seed_5339_tiny_fp32_als(oracle):
+    """A probe-found case (fp32 22 x 1 x 10 x 1 x 7, ranks 8 x 1 x 7 x 1 x 3, ALS on the last mode,
+    whose 5-iteration iterate is first-order sensitive): on tf32 tensor-core operands it missed the
+    1e-4 core-norm bar (1.3e-4); tensors below kTcMinElems now take the fp32 CUDA-core path."""
+    test_sthosvd_sweep_vs_oracle(5339, False, oracle)
